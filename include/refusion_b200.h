@@ -1,0 +1,215 @@
+/*
+ * refusion_b200.h — C ABI of the B200-native ReFusion hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++/torch types.
+ * Each entry point replaces one interface of the CPU reference (`tsdfslam`,
+ * /root/reference/proj/include/tsdfslam); the reference symbol it replaces is
+ * cited beside it. Conventions shared by every call:
+ *
+ *  - Poses are 12 doubles, camera-to-world: rotation row-major (9) then
+ *    translation (3) — `Pose` (geometry.hpp:69-108).
+ *  - Images are dense row-major W*H: depth f32 metres (<= 0 or non-finite =
+ *    invalid, image.hpp:66-68), colour RGB8 (3 bytes/pixel), masks u8
+ *    (nonzero = excluded, image.hpp:71).
+ *  - A NULL mask means "no mask" (the reference's `const PixelMask* = nullptr`).
+ *  - Voxels are 8 bytes {f32 sdf, u8 weight, u8 r, u8 g, u8 b}
+ *    (tsdf_volume.hpp:32-37); a brick is 8^3 voxels, x fastest.
+ *  - Every call returns an rf_status; on failure rf_last_error() holds a
+ *    thread-local message. The C++ host layer rethrows RF_TRACKING_LOST as
+ *    TrackingLostError, RF_RESOURCE_LIMIT as ResourceLimitError and
+ *    RF_INVALID_ARGUMENT as std::invalid_argument (errors.hpp:9-21).
+ *  - Calls are synchronous like the reference (results are on the host when
+ *    they return). Handles are not thread-safe, matching the reference's
+ *    volume concurrency contract (tsdf_volume.hpp:64-66).
+ *  - block_side must be 8 (the reference default); other values return
+ *    RF_UNSUPPORTED.
+ */
+#ifndef REFUSION_B200_H
+#define REFUSION_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RF_OK = 0,
+    RF_INVALID_ARGUMENT = 1,
+    RF_TRACKING_LOST = 2,   /* TrackingLostError (errors.hpp:14) */
+    RF_RESOURCE_LIMIT = 3,  /* ResourceLimitError (errors.hpp:19) */
+    RF_CUDA_ERROR = 4,
+    RF_IO_ERROR = 5,
+    RF_UNSUPPORTED = 6
+} rf_status;
+
+enum { RF_MEMORY_HOST = 0, RF_MEMORY_DEVICE = 1 };
+
+/* CameraIntrinsics (geometry.hpp:11-38) */
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double depth_scale;
+} rf_intrinsics;
+
+/* VolumeConfig (tsdf_volume.hpp:14-29); hash_capacity 0 = next power of two
+ * >= 4/3 * max_blocks (the load bound of spatial_hash.hpp:51). */
+typedef struct {
+    double voxel_size, truncation;
+    int32_t block_side, max_weight, carve_weight, reserved0;
+    double min_depth, max_depth, carve_clip;
+    uint64_t max_blocks;
+    uint64_t hash_capacity;
+} rf_volume_config;
+
+/* RegistrationConfig (registration.hpp:13-23); `threads` is accepted and ignored */
+typedef struct {
+    double color_weight;
+    int32_t pyramid_levels, max_iterations;
+    double lm_lambda_init, lm_lambda_up, lm_lambda_down, convergence_eps;
+    int32_t min_valid_residuals, threads;
+} rf_registration_config;
+
+/* MaskConfig (dynamics_mask.hpp:10-17) */
+typedef struct {
+    double gamma, truncation, theta;
+    int32_t erode_radius, dilate_radius, connectivity, reserved0;
+} rf_mask_config;
+
+/* PipelineConfig (config.hpp:12-24) with RefinementConfig (depth_refinement.hpp:12-17) */
+typedef struct {
+    rf_volume_config volume;
+    rf_registration_config registration;
+    rf_mask_config mask;
+    int32_t refine_enabled, refine_window;
+    double far_value;
+    int32_t bisection_iterations, dynamics_enabled, threads, reserved0;
+} rf_pipeline_config;
+
+/* One RGB-D measurement, `Frame` (image.hpp:94-103). memory = RF_MEMORY_HOST
+ * (pointers are copied in, pinned memory is fastest) or RF_MEMORY_DEVICE
+ * (device pointers of the volume's GPU, read in place). rgb may be NULL. */
+typedef struct {
+    const float* depth;
+    const uint8_t* rgb;
+    rf_intrinsics intrinsics;
+    double timestamp;
+    int32_t memory;
+    int32_t reserved0;
+} rf_frame;
+
+/* FrameStats (pipeline.hpp:18-29) */
+typedef struct {
+    uint64_t frame_index;
+    double timestamp;
+    int32_t tracking_lost, converged, registrations, iterations;
+    uint64_t valid_residuals, masked_pixels;
+    double final_error, runtime_ms;
+} rf_frame_stats;
+
+/* RegistrationResult (registration.hpp:66-74); residual images are separate out-params */
+typedef struct {
+    double pose[12];
+    int32_t converged, iterations;
+    uint64_t valid_residuals;
+    double final_error;
+} rf_registration_result;
+
+/* LinearizeResult (registration.hpp:47-55) */
+typedef struct {
+    double H[36];
+    double b[6];
+    double depth_error, color_error, error;
+    uint64_t valid_count;
+    int32_t degenerate, reserved0;
+} rf_linearize_result;
+
+/* Per-frame work counters for the algorithmic-bytes model (not in the reference). */
+typedef struct {
+    uint64_t dda_visits, new_blocks, visible_bricks, num_blocks;
+    int32_t floodfill_rounds, overflow;
+} rf_frame_counters;
+
+typedef struct rf_volume rf_volume;
+typedef struct rf_pipeline rf_pipeline;
+
+const char* rf_last_error(void);
+const char* rf_version(void);
+
+/* ---- volume: TsdfVolume (tsdf_volume.hpp:67-134) ---------------------- */
+rf_status rf_volume_create(const rf_volume_config* cfg, int device, rf_volume** out);      /* TsdfVolume(VolumeConfig) */
+void rf_volume_destroy(rf_volume* v);
+rf_status rf_volume_num_blocks(const rf_volume* v, uint64_t* out);                         /* num_blocks() */
+rf_status rf_volume_hash_capacity(const rf_volume* v, uint64_t* out);
+rf_status rf_volume_allocate_blocks(rf_volume* v, const int32_t* coords, uint64_t n,
+                                    int32_t* created);                                     /* AllocateBlock (batched) */
+rf_status rf_volume_allocate_for_frame(rf_volume* v, const rf_frame* f, const double pose[12],
+                                       const uint8_t* mask);                               /* AllocateForFrame */
+rf_status rf_volume_integrate(rf_volume* v, const rf_frame* f, const double pose[12],
+                              const uint8_t* mask);                                        /* Integrate */
+rf_status rf_volume_carve(rf_volume* v, const rf_frame* f, const double pose[12]);         /* CarveFreeSpace */
+/* mode 0 SampleSdf, 1 SampleIntensity, 2 SampleSdfWithGradient,
+ * 3 SampleIntensityWithGradient, 4 SampleSdfGradient. grad may be NULL. */
+rf_status rf_volume_sample(const rf_volume* v, int32_t mode, const double* points, uint64_t n,
+                           double* value, double* grad, uint8_t* valid);
+rf_status rf_volume_get_voxels(const rf_volume* v, const int32_t* voxel_coords, uint64_t n,
+                               uint8_t* voxels, uint8_t* found);                          /* const VoxelHandle */
+rf_status rf_volume_set_voxels(rf_volume* v, const int32_t* voxel_coords, uint64_t n,
+                               const uint8_t* voxels, uint64_t* missing);                 /* mutable VoxelHandle */
+/* blocks() in pool (allocation) order; voxels may be NULL. capacity in blocks. */
+rf_status rf_volume_export_blocks(const rf_volume* v, int32_t* coords, uint8_t* voxels, uint64_t capacity,
+                                  uint64_t* count);
+rf_status rf_volume_hash_occupancy(const rf_volume* v, uint8_t* bitmap);                  /* hash_capacity bytes */
+rf_status rf_volume_reset(rf_volume* v);
+rf_status rf_volume_save(const rf_volume* v, const char* path);                           /* Save (TSDFVOL v1) */
+rf_status rf_volume_load(const char* path, int device, rf_volume** out);                  /* Load */
+
+/* ---- registration (registration.hpp:42-85) ----------------------------- */
+rf_status rf_linearize(const rf_volume* v, const rf_frame* f, const double pose[12],
+                       const rf_registration_config* cfg, const uint8_t* mask, rf_linearize_result* out);
+rf_status rf_evaluate_depth_error(const rf_volume* v, const rf_frame* f, const double pose[12],
+                                  const uint8_t* mask, double* error, float* res_sq, uint8_t* res_valid);
+rf_status rf_evaluate_color_error(const rf_volume* v, const rf_frame* f, const double pose[12],
+                                  const uint8_t* mask, double* error);
+rf_status rf_register(const rf_volume* v, const rf_frame* f, const double initial_pose[12], const uint8_t* mask,
+                      const rf_registration_config* cfg, rf_registration_result* out, float* res_sq,
+                      uint8_t* res_valid);                                                 /* Register */
+
+/* ---- dynamics mask (dynamics_mask.hpp:21-41) ----------------------------
+ * stages: bit0 ThresholdResiduals, bit1 Erode, bit2 FloodfillDepth, bit3 Dilate
+ * (15 = BuildMask). With bit0 clear, `res_valid` is read as the input mask. */
+rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const float* depth, int32_t width,
+                         int32_t height, const rf_mask_config* cfg, int32_t stages, int device, uint8_t* out,
+                         uint64_t* masked);
+
+/* ---- raycast (ray-march of RenderVirtualDepth, depth_refinement.cpp:32-79) */
+rf_status rf_raycast(const rf_volume* v, const double view_pose[12], const rf_intrinsics* k,
+                     int32_t bisection_iterations, float* out_depth);
+
+/* ---- pipeline (pipeline.hpp:51-96) ------------------------------------- */
+rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipeline** out);
+void rf_pipeline_destroy(rf_pipeline* p);
+rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_stats* stats,
+                                    double pose_out[12]);                                  /* ProcessFrame */
+rf_status rf_pipeline_finalize(rf_pipeline* p);                                            /* Finalize */
+rf_status rf_pipeline_volume(rf_pipeline* p, rf_volume** out);                             /* volume() (borrowed) */
+rf_status rf_pipeline_tracking_losses(const rf_pipeline* p, uint64_t* out);               /* tracking_losses() */
+rf_status rf_pipeline_trajectory(const rf_pipeline* p, double* timestamps, double* poses, uint64_t capacity,
+                                 uint64_t* count);                                         /* trajectory() */
+rf_status rf_pipeline_last_mask(const rf_pipeline* p, uint8_t* out, int32_t* has_mask);    /* FrameDebug::mask */
+rf_status rf_pipeline_last_residuals(const rf_pipeline* p, float* res_sq, uint8_t* res_valid); /* FrameDebug::residuals */
+rf_status rf_pipeline_last_counters(const rf_pipeline* p, rf_frame_counters* out);
+
+/* ---- memory helpers ------------------------------------------------------ */
+void* rf_host_alloc(size_t bytes);  /* pinned host memory (fast frame uploads) */
+void rf_host_free(void* p);
+void* rf_device_alloc(size_t bytes, int device);
+void rf_device_free(void* p);
+rf_status rf_copy_to_device(void* dst, const void* src, size_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* REFUSION_B200_H */

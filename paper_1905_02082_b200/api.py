@@ -1,0 +1,392 @@
+"""Python mirror of the reference's tracker / map interfaces
+(proj/include/tsdfslam) over the C ABI. Same names and argument meaning as the
+reference, snake_case; exceptions map onto TrackingLostError /
+ResourceLimitError / ValueError like errors.hpp. Images are numpy arrays
+(host, copied in) or CUDA torch tensors (device, read in place)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+VOXEL_DTYPE = np.dtype([("sdf", "<f4"), ("weight", "u1"), ("r", "u1"), ("g", "u1"), ("b", "u1")])
+IDENTITY = np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0], dtype=np.float64)
+
+
+def _lib():
+    return L.load()
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+# ------------------------------------------------------------------ configs
+def intrinsics(fx=525.0, fy=525.0, cx=319.5, cy=239.5, width=640, height=480, depth_scale=5000.0):
+    """CameraIntrinsics (geometry.hpp:11-38) with the reference defaults."""
+    return L.rf_intrinsics(fx, fy, cx, cy, width, height, depth_scale)
+
+
+def volume_config(**kw) -> L.rf_volume_config:
+    """VolumeConfig (tsdf_volume.hpp:14-29) defaults."""
+    c = L.rf_volume_config(0.01, 0.1, 8, 64, 1, 0, 0.1, 5.0, 4.0, 1000000, 0)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def registration_config(**kw) -> L.rf_registration_config:
+    """RegistrationConfig (registration.hpp:13-23) defaults."""
+    c = L.rf_registration_config(0.025, 3, 20, 1e-4, 10.0, 2.0, 1e-5, 100, 1)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def mask_config(**kw) -> L.rf_mask_config:
+    """MaskConfig (dynamics_mask.hpp:10-17) defaults."""
+    c = L.rf_mask_config(0.5, 0.1, 0.007, 2, 2, 4, 0)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def pipeline_config(refine=False, window=10, dynamics=True, threads=1, volume=None, registration=None, mask=None):
+    """PipelineConfig (config.hpp:12-24). refine defaults to False: the CUDA
+    path does not implement the depth-refinement window yet."""
+    v = volume or volume_config()
+    m = mask or mask_config()
+    m.truncation = v.truncation
+    return L.rf_pipeline_config(v, registration or registration_config(), m, int(refine), window, 8.0, 8,
+                                int(dynamics), threads, 0)
+
+
+# ------------------------------------------------------------------ frames
+@dataclass
+class Frame:
+    """One RGB-D measurement (image.hpp:94-103)."""
+    depth: object  # HxW float32 numpy array or CUDA tensor
+    rgb: object = None  # HxWx3 uint8 numpy array or CUDA tensor
+    intrinsics: L.rf_intrinsics = field(default_factory=intrinsics)
+    timestamp: float = 0.0
+
+    def c(self) -> L.rf_frame:
+        f = L.rf_frame()
+        f.intrinsics = self.intrinsics
+        f.timestamp = self.timestamp
+        dev = _is_cuda(self.depth)
+        f.memory = L.RF_MEMORY_DEVICE if dev else L.RF_MEMORY_HOST
+        if dev:
+            f.depth = self.depth.data_ptr()
+            f.rgb = None if self.rgb is None else self.rgb.data_ptr()
+            self._keep = ()
+        else:
+            d = np.ascontiguousarray(self.depth, dtype=np.float32)
+            rgb = None if self.rgb is None else np.ascontiguousarray(self.rgb, dtype=np.uint8)
+            self._keep = (d, rgb)
+            f.depth = d.ctypes.data
+            f.rgb = None if rgb is None else rgb.ctypes.data
+        return f
+
+
+def _is_cuda(x):
+    return hasattr(x, "is_cuda") and x.is_cuda
+
+
+def _mask_ptr(mask, frame: Frame):
+    if mask is None:
+        return None, None
+    if _is_cuda(frame.depth):
+        return C.c_void_p(mask.data_ptr()), mask
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    return C.c_void_p(m.ctypes.data), m
+
+
+# ------------------------------------------------------------------ volume
+class TsdfVolume:
+    """TsdfVolume (tsdf_volume.hpp:67-134) on the GPU."""
+
+    def __init__(self, config: L.rf_volume_config | None = None, device: int = 0, _handle=None, **kw):
+        self.config = config or volume_config(**kw)
+        self.device = device
+        if _handle is not None:
+            self.h = _handle
+            self._owned = False
+            return
+        h = C.c_void_p()
+        L.check(_lib().rf_volume_create(C.byref(self.config), device, C.byref(h)))
+        self.h = h
+        self._owned = True
+
+    def close(self):
+        if getattr(self, "_owned", False) and self.h:
+            _lib().rf_volume_destroy(self.h)
+            self.h = None
+            self._owned = False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def num_blocks(self) -> int:
+        out = C.c_uint64()
+        L.check(_lib().rf_volume_num_blocks(self.h, C.byref(out)))
+        return out.value
+
+    def hash_capacity(self) -> int:
+        out = C.c_uint64()
+        L.check(_lib().rf_volume_hash_capacity(self.h, C.byref(out)))
+        return out.value
+
+    def allocate_blocks(self, coords):
+        c = _i32(coords).reshape(-1, 3)
+        created = np.zeros(len(c), dtype=np.int32)
+        L.check(_lib().rf_volume_allocate_blocks(self.h, _p(c), C.c_uint64(len(c)), _p(created)))
+        return created
+
+    def allocate_block(self, coord) -> bool:  # AllocateBlock (tsdf_volume.cpp:64-77)
+        return bool(self.allocate_blocks([coord])[0] == 1)
+
+    def allocate_for_frame(self, frame: Frame, pose, mask=None):
+        f = frame.c()
+        mp, _keep = _mask_ptr(mask, frame)
+        L.check(_lib().rf_volume_allocate_for_frame(self.h, C.byref(f), _p(_f64(pose)), mp))
+
+    def integrate(self, frame: Frame, pose, mask=None):
+        f = frame.c()
+        mp, _keep = _mask_ptr(mask, frame)
+        L.check(_lib().rf_volume_integrate(self.h, C.byref(f), _p(_f64(pose)), mp))
+
+    def carve(self, frame: Frame, pose):  # CarveFreeSpace
+        f = frame.c()
+        L.check(_lib().rf_volume_carve(self.h, C.byref(f), _p(_f64(pose))))
+
+    def sample(self, points, mode=0):
+        pts = _f64(points).reshape(-1, 3)
+        n = len(pts)
+        val = np.zeros(n)
+        grad = np.zeros((n, 3))
+        valid = np.zeros(n, dtype=np.uint8)
+        L.check(_lib().rf_volume_sample(self.h, mode, _p(pts), C.c_uint64(n), _p(val), _p(grad), _p(valid)))
+        return val, grad, valid.astype(bool)
+
+    def get_voxels(self, coords):
+        c = _i32(coords).reshape(-1, 3)
+        vox = np.zeros(len(c), dtype=VOXEL_DTYPE)
+        found = np.zeros(len(c), dtype=np.uint8)
+        L.check(_lib().rf_volume_get_voxels(self.h, _p(c), C.c_uint64(len(c)), _p(vox), _p(found)))
+        return vox, found.astype(bool)
+
+    def set_voxels(self, coords, voxels) -> int:
+        c = _i32(coords).reshape(-1, 3)
+        v = np.ascontiguousarray(voxels, dtype=VOXEL_DTYPE)
+        missing = C.c_uint64()
+        L.check(_lib().rf_volume_set_voxels(self.h, _p(c), C.c_uint64(len(c)), _p(v), C.byref(missing)))
+        return missing.value
+
+    def export(self, with_voxels=True):
+        """blocks() in pool order: coords (n,3) i32 and voxels (n,512) VOXEL_DTYPE."""
+        cnt = C.c_uint64()
+        L.check(_lib().rf_volume_export_blocks(self.h, None, None, C.c_uint64(0), C.byref(cnt)))
+        n = cnt.value
+        coords = np.zeros((n, 3), dtype=np.int32)
+        vox = np.zeros((n, 512), dtype=VOXEL_DTYPE) if with_voxels else None
+        L.check(_lib().rf_volume_export_blocks(self.h, _p(coords), _p(vox), C.c_uint64(n), C.byref(cnt)))
+        return coords, vox
+
+    def hash_occupancy(self) -> np.ndarray:
+        bm = np.zeros(self.hash_capacity(), dtype=np.uint8)
+        L.check(_lib().rf_volume_hash_occupancy(self.h, _p(bm)))
+        return bm
+
+    def reset(self):
+        L.check(_lib().rf_volume_reset(self.h))
+
+    def save(self, path: str):
+        L.check(_lib().rf_volume_save(self.h, path.encode()))
+
+    @staticmethod
+    def load(path: str, device: int = 0) -> "TsdfVolume":
+        h = C.c_void_p()
+        L.check(_lib().rf_volume_load(path.encode(), device, C.byref(h)))
+        v = TsdfVolume.__new__(TsdfVolume)
+        v.h, v._owned, v.device = h, True, device
+        v.config = volume_config()  # header values are held by the handle
+        return v
+
+    # --- registration.hpp:42-85 --------------------------------------------
+    def linearize(self, frame: Frame, pose, config=None, mask=None):
+        cfg = config or registration_config()
+        f = frame.c()
+        mp, _keep = _mask_ptr(mask, frame)
+        out = L.rf_linearize_result()
+        L.check(_lib().rf_linearize(self.h, C.byref(f), _p(_f64(pose)), C.byref(cfg), mp, C.byref(out)))
+        return dict(H=np.array(out.H).reshape(6, 6), b=np.array(out.b), depth_error=out.depth_error,
+                    color_error=out.color_error, error=out.error, valid=out.valid_count)
+
+    def evaluate_depth_error(self, frame: Frame, pose, mask=None):
+        f = frame.c()
+        mp, _keep = _mask_ptr(mask, frame)
+        k = frame.intrinsics
+        sq = np.zeros((k.height, k.width), dtype=np.float32)
+        valid = np.zeros((k.height, k.width), dtype=np.uint8)
+        err = C.c_double()
+        L.check(_lib().rf_evaluate_depth_error(self.h, C.byref(f), _p(_f64(pose)), mp, C.byref(err), _p(sq),
+                                               _p(valid)))
+        return err.value, sq, valid
+
+    def evaluate_color_error(self, frame: Frame, pose, mask=None):
+        f = frame.c()
+        mp, _keep = _mask_ptr(mask, frame)
+        err = C.c_double()
+        L.check(_lib().rf_evaluate_color_error(self.h, C.byref(f), _p(_f64(pose)), mp, C.byref(err)))
+        return err.value
+
+    def register(self, frame: Frame, initial_pose, mask=None, config=None):
+        cfg = config or registration_config()
+        f = frame.c()
+        mp, _keep = _mask_ptr(mask, frame)
+        k = frame.intrinsics
+        out = L.rf_registration_result()
+        sq = np.zeros((k.height, k.width), dtype=np.float32)
+        rv = np.zeros((k.height, k.width), dtype=np.uint8)
+        L.check(_lib().rf_register(self.h, C.byref(f), _p(_f64(initial_pose)), mp, C.byref(cfg), C.byref(out),
+                                   _p(sq), _p(rv)))
+        return dict(pose=np.array(out.pose), converged=bool(out.converged), iterations=out.iterations,
+                    valid_residuals=out.valid_residuals, final_error=out.final_error, res_sq=sq, res_valid=rv)
+
+    def raycast(self, pose, k: L.rf_intrinsics, bisections=8):
+        out = np.zeros((k.height, k.width), dtype=np.float32)
+        L.check(_lib().rf_raycast(self.h, _p(_f64(pose)), C.byref(k), bisections, _p(out)))
+        return out
+
+
+# ------------------------------------------------------------------ mask
+def mask_stages(res_sq, res_valid, depth, config=None, stages=15, device=0):
+    """BuildMask (stages=15) or any subset of its stages (dynamics_mask.hpp:21-41)."""
+    cfg = config or mask_config()
+    rv = np.ascontiguousarray(res_valid, dtype=np.uint8)
+    h, w = rv.shape
+    sq = None if res_sq is None else np.ascontiguousarray(res_sq, dtype=np.float32)
+    d = np.ascontiguousarray(depth, dtype=np.float32)
+    out = np.zeros((h, w), dtype=np.uint8)
+    n = C.c_uint64()
+    L.check(_lib().rf_mask_stages(_p(sq), _p(rv), _p(d), w, h, C.byref(cfg), stages, device, _p(out), C.byref(n)))
+    return out
+
+
+def threshold_residuals(res_sq, res_valid, config=None):
+    return mask_stages(res_sq, res_valid, np.zeros_like(res_sq, dtype=np.float32), config, 1)
+
+
+def erode(mask, radius):
+    return mask_stages(None, mask, np.zeros(np.shape(mask), np.float32), mask_config(erode_radius=radius), 2)
+
+
+def dilate(mask, radius):
+    return mask_stages(None, mask, np.zeros(np.shape(mask), np.float32), mask_config(dilate_radius=radius), 8)
+
+
+def floodfill_depth(seeds, depth, theta, connectivity=4):
+    return mask_stages(None, seeds, depth, mask_config(theta=theta, connectivity=connectivity), 4)
+
+
+def build_mask(res_sq, res_valid, depth, config=None):
+    return mask_stages(res_sq, res_valid, depth, config, 15)
+
+
+# ------------------------------------------------------------------ pipeline
+class Pipeline:
+    """Pipeline (pipeline.hpp:51-86) with the whole ProcessFrame on the GPU."""
+
+    def __init__(self, config: L.rf_pipeline_config | None = None, device: int = 0):
+        self.config = config or pipeline_config()
+        h = C.c_void_p()
+        L.check(_lib().rf_pipeline_create(C.byref(self.config), device, C.byref(h)))
+        self.h = h
+        self.device = device
+        self.stats = []
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib().rf_pipeline_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def process_frame(self, frame: Frame):
+        f = frame.c()
+        st = L.rf_frame_stats()
+        pose = (C.c_double * 12)()
+        L.check(_lib().rf_pipeline_process_frame(self.h, C.byref(f), C.byref(st), pose))
+        s = {k: getattr(st, k) for k, _ in L.rf_frame_stats._fields_}
+        self.stats.append(s)
+        return s, np.array(pose)
+
+    def process_frame_raw(self, f: L.rf_frame, st: L.rf_frame_stats, pose):
+        """Minimal-overhead call for timing loops (no Python-side conversion)."""
+        return _lib().rf_pipeline_process_frame(self.h, C.byref(f), C.byref(st), pose)
+
+    def finalize(self):
+        L.check(_lib().rf_pipeline_finalize(self.h))
+
+    def volume(self) -> TsdfVolume:
+        h = C.c_void_p()
+        L.check(_lib().rf_pipeline_volume(self.h, C.byref(h)))
+        v = TsdfVolume(self.config.volume, self.device, _handle=h)
+        v._owner = self
+        return v
+
+    def tracking_losses(self) -> int:
+        out = C.c_uint64()
+        L.check(_lib().rf_pipeline_tracking_losses(self.h, C.byref(out)))
+        return out.value
+
+    def trajectory(self):
+        cnt = C.c_uint64()
+        L.check(_lib().rf_pipeline_trajectory(self.h, None, None, C.c_uint64(0), C.byref(cnt)))
+        ts = np.zeros(cnt.value)
+        poses = np.zeros((cnt.value, 12))
+        L.check(_lib().rf_pipeline_trajectory(self.h, _p(ts), _p(poses), cnt, C.byref(cnt)))
+        return ts, poses
+
+    def last_mask(self):
+        has = C.c_int32()
+        L.check(_lib().rf_pipeline_last_mask(self.h, None, C.byref(has)))
+        if not has.value:
+            return None
+        return has
+
+    def last_mask_image(self, k):
+        out = np.zeros((k.height, k.width), dtype=np.uint8)
+        has = C.c_int32()
+        L.check(_lib().rf_pipeline_last_mask(self.h, _p(out), C.byref(has)))
+        return out if has.value else None
+
+    def last_residuals(self, k):
+        sq = np.zeros((k.height, k.width), dtype=np.float32)
+        v = np.zeros((k.height, k.width), dtype=np.uint8)
+        L.check(_lib().rf_pipeline_last_residuals(self.h, _p(sq), _p(v)))
+        return sq, v
+
+    def last_counters(self):
+        c = L.rf_frame_counters()
+        L.check(_lib().rf_pipeline_last_counters(self.h, C.byref(c)))
+        return {k: getattr(c, k) for k, _ in L.rf_frame_counters._fields_}

@@ -1,0 +1,1107 @@
+// C ABI (include/refusion_b200.h) over the CUDA kernels: volume / pipeline
+// objects, device buffers, frame upload and the per-frame launch sequence.
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/refusion_b200.h"
+#include "rf_track.cuh"
+#include "rf_volume.cuh"
+
+namespace rfb {
+__global__ void k_track(TrackArgs a);
+__global__ void k_import(VolumeView V, const int* coords, uint32_t n, uint32_t base) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int x = coords[3 * i], y = coords[3 * i + 1], z = coords[3 * i + 2];
+    const unsigned long long key = pack_key(x, y, z);
+    uint32_t idx = hash_coord(x, y, z) & V.hash_mask;
+    while (atomicCAS(&V.slots[idx].key, kEmptyKey, key) != kEmptyKey) idx = (idx + 1) & V.hash_mask;
+    V.slots[idx].value = base + i;
+    V.coords[base + i] = make_int4(x, y, z, 0);
+}
+}  // namespace rfb
+
+using namespace rfb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error {
+    rf_status code;
+    std::string msg;
+};
+
+#define CK(x)                                                                                    \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess) throw Error{RF_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+    } while (0)
+
+template <class F>
+rf_status guard(F&& f) {
+    try {
+        f();
+        return RF_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return RF_CUDA_ERROR;
+    }
+}
+
+void require(bool ok, rf_status code, const std::string& msg) {
+    if (!ok) throw Error{code, msg};
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    void ensure(size_t bytes) {
+        if (bytes <= n) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        CK(cudaMalloc(&p, bytes));
+        n = bytes;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// Per-object scratch: stream, frame images, pyramid, grid-sync state.
+struct Workspace {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int track_grid = 0;
+    DevBuf depth, rgb, mask_in, pose, res_sq, res_valid, mwork, levels, gsync, partials, result, out, list;
+    TrackOut* h_out = nullptr;
+    uint32_t* h_counters = nullptr;
+    int W = 0, H = 0, L = 0;
+    size_t lvl_off_depth[kMaxLevels] = {}, lvl_off_inten[kMaxLevels] = {}, lvl_off_mask[kMaxLevels] = {};
+
+    void init(int dev) {
+        device = dev;
+        CK(cudaSetDevice(dev));
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        int sms = 0, per = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_track, kTrackThreads, 0));
+        require(per > 0, RF_CUDA_ERROR, "tracking kernel does not fit on an SM");
+        track_grid = sms * per;
+        gsync.ensure(sizeof(GridSync));
+        CK(cudaMemset(gsync.p, 0, sizeof(GridSync)));
+        partials.ensure(size_t(track_grid) * kRedStride * sizeof(double));
+        result.ensure(kRedStride * sizeof(double));
+        out.ensure(sizeof(TrackOut));
+        pose.ensure(12 * sizeof(double));
+        CK(cudaMallocHost(&h_out, sizeof(TrackOut)));
+        CK(cudaMallocHost(&h_counters, kNumCounters * sizeof(uint32_t)));
+    }
+    void destroy() {
+        for (DevBuf* b : {&depth, &rgb, &mask_in, &pose, &res_sq, &res_valid, &mwork, &levels, &gsync, &partials,
+                          &result, &out, &list})
+            b->release();
+        if (h_out) cudaFreeHost(h_out);
+        if (h_counters) cudaFreeHost(h_counters);
+        if (stream) cudaStreamDestroy(stream);
+        h_out = nullptr;
+        h_counters = nullptr;
+        stream = nullptr;
+    }
+    void ensure_frame(int w, int h, int levels_needed) {
+        if (w == W && h == H && levels_needed <= L) return;
+        const size_t n = size_t(w) * h;
+        depth.ensure(n * 4);
+        rgb.ensure(n * 3);
+        mask_in.ensure(n);
+        res_sq.ensure(n * 4);
+        res_valid.ensure(n);
+        mwork.ensure(3 * n);
+        size_t off = 0;
+        for (int l = 0; l < levels_needed; ++l) {
+            const size_t nl = size_t(w >> l) * (h >> l);
+            lvl_off_depth[l] = off;
+            off += (nl * 4 + 255) & ~size_t(255);
+            lvl_off_inten[l] = off;
+            off += (nl * 4 + 255) & ~size_t(255);
+            lvl_off_mask[l] = off;
+            off += (nl + 255) & ~size_t(255);
+        }
+        levels.ensure(off + 256);
+        W = w;
+        H = h;
+        L = levels_needed;
+    }
+    void sync() { CK(cudaStreamSynchronize(stream)); }
+};
+
+Intr level_intr(const rf_intrinsics& k, int l) {  // CameraIntrinsics::Scaled (geometry.hpp:27-37)
+    const double s = 1.0 / double(1 << l);
+    Intr r;
+    r.fx = k.fx * s;
+    r.fy = k.fy * s;
+    r.cx = k.cx * s;
+    r.cy = k.cy * s;
+    r.w = k.width >> l;
+    r.h = k.height >> l;
+    return r;
+}
+
+uint64_t next_pow2(uint64_t v) {
+    uint64_t c = 16;
+    while (c < v) c <<= 1;
+    return c;
+}
+
+void validate_volume_config(const rf_volume_config& c) {  // VolumeConfig::Validate (tsdf_volume.cpp:40-52)
+    require(c.voxel_size > 0, RF_INVALID_ARGUMENT, "voxel_size must be positive");
+    require(c.truncation >= c.voxel_size, RF_INVALID_ARGUMENT, "truncation must be at least one voxel_size");
+    require(c.block_side >= 2, RF_INVALID_ARGUMENT, "block_side must be at least 2");
+    require(c.max_weight >= 1 && c.max_weight <= 255, RF_INVALID_ARGUMENT, "max_weight must be in [1, 255]");
+    require(c.carve_weight >= 1 && c.carve_weight <= c.max_weight, RF_INVALID_ARGUMENT,
+            "carve_weight must be in [1, max_weight]");
+    require(c.min_depth > 0 && c.max_depth > c.min_depth, RF_INVALID_ARGUMENT, "need 0 < min_depth < max_depth");
+    require(c.carve_clip > 0, RF_INVALID_ARGUMENT, "carve_clip must be positive");
+    require(c.max_blocks > 0, RF_INVALID_ARGUMENT, "max_blocks must be positive");
+    require(c.block_side == kSide, RF_UNSUPPORTED, "the CUDA path supports block_side == 8 only");
+    require(c.max_blocks < (1ull << 30), RF_UNSUPPORTED, "max_blocks must be < 2^30");
+}
+
+void check_reg_config(const rf_registration_config& r) {
+    require(r.pyramid_levels >= 1, RF_INVALID_ARGUMENT, "pyramid_levels must be >= 1");
+    require(r.pyramid_levels <= kMaxLevels, RF_UNSUPPORTED, "pyramid_levels > 6");
+    require(r.max_iterations >= 1, RF_INVALID_ARGUMENT, "max_iterations must be >= 1");
+}
+
+}  // namespace
+
+struct rf_volume {
+    int device = 0;
+    rf_volume_config cfg{};
+    uint64_t cap = 0;
+    DevBuf slots, coords, voxels, counters;
+    VolumeView view{};
+    Workspace ws;
+
+    uint64_t num_blocks() {
+        uint32_t c = 0;
+        CK(cudaMemcpy(&c, view.counters + kNumBlocks, 4, cudaMemcpyDeviceToHost));
+        return std::min<uint64_t>(c, cfg.max_blocks);
+    }
+    uint32_t overflow() {
+        uint32_t c = 0;
+        CK(cudaMemcpy(&c, view.counters + kOverflow, 4, cudaMemcpyDeviceToHost));
+        return c;
+    }
+    // Uploads a frame's images into the workspace unless they already live on the device.
+    const float* depth_of(const rf_frame* f) {
+        const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
+        if (f->memory == RF_MEMORY_DEVICE) return f->depth;
+        CK(cudaMemcpyAsync(ws.depth.p, f->depth, n * 4, cudaMemcpyHostToDevice, ws.stream));
+        return ws.depth.as<float>();
+    }
+    const uint8_t* rgb_of(const rf_frame* f) {
+        if (!f->rgb) return nullptr;
+        const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
+        if (f->memory == RF_MEMORY_DEVICE) return f->rgb;
+        CK(cudaMemcpyAsync(ws.rgb.p, f->rgb, n * 3, cudaMemcpyHostToDevice, ws.stream));
+        return ws.rgb.as<uint8_t>();
+    }
+    const uint8_t* mask_of(const rf_frame* f, const uint8_t* mask, uint8_t* dst = nullptr) {
+        if (!mask) return nullptr;
+        const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
+        if (!dst) dst = ws.mask_in.as<uint8_t>();
+        if (f->memory == RF_MEMORY_DEVICE) {
+            if (dst == ws.mask_in.as<uint8_t>()) return mask;
+            CK(cudaMemcpyAsync(dst, mask, n, cudaMemcpyDeviceToDevice, ws.stream));
+        } else {
+            CK(cudaMemcpyAsync(dst, mask, n, cudaMemcpyHostToDevice, ws.stream));
+        }
+        return dst;
+    }
+    void upload_pose(const double pose[12]) {
+        CK(cudaMemcpyAsync(ws.pose.p, pose, 96, cudaMemcpyHostToDevice, ws.stream));
+    }
+    void prepare(const rf_frame* f, int levels = 1) {
+        require(f && f->depth, RF_INVALID_ARGUMENT, "frame has no depth");
+        require(f->intrinsics.width > 0 && f->intrinsics.height > 0, RF_INVALID_ARGUMENT, "bad image size");
+        CK(cudaSetDevice(device));
+        ws.ensure_frame(f->intrinsics.width, f->intrinsics.height, levels);
+    }
+    void reset_counter(int which) {
+        CK(cudaMemsetAsync(view.counters + which, 0, 4, ws.stream));
+    }
+    void fuse(const float* d, const uint8_t* rgb, const uint8_t* mask, const rf_intrinsics& k, const double* pose,
+              const int* lost, bool carve, bool integrate, bool carve_only_before) {
+        CullArgs ca{};
+        ca.V = view;
+        ca.K = level_intr(k, 0);
+        ca.pose = pose;
+        ca.lost = lost;
+        ca.list = ws.list.as<uint32_t>();
+        ca.do_carve = carve;
+        ca.do_integrate = integrate;
+        ca.carve_only_before = carve_only_before;
+        k_cull<<<4 * 148, 256, 0, ws.stream>>>(ca);
+        CK(cudaGetLastError());
+        FuseArgs fa{};
+        fa.V = view;
+        fa.depth = d;
+        fa.rgb = rgb;
+        fa.mask = mask;
+        fa.K = ca.K;
+        fa.pose = pose;
+        fa.lost = lost;
+        fa.list = ca.list;
+        k_fuse<<<4 * 148, kBrickVoxels, 0, ws.stream>>>(fa);
+        CK(cudaGetLastError());
+    }
+    void allocate(const float* d, const uint8_t* mask, const rf_intrinsics& k, const double* pose, const int* lost) {
+        AllocArgs aa{};
+        aa.V = view;
+        aa.depth = d;
+        aa.mask = mask;
+        aa.K = level_intr(k, 0);
+        aa.pose = pose;
+        aa.lost = lost;
+        const int n = k.width * k.height;
+        k_alloc<<<(n + 255) / 256, 256, 0, ws.stream>>>(aa);
+        CK(cudaGetLastError());
+    }
+    TrackArgs track_args(const rf_frame* f, const float* d, const uint8_t* rgb, int levels) {
+        TrackArgs a{};
+        a.V = view;
+        a.F.depth0 = d;
+        a.F.rgb0 = rgb;
+        uint8_t* base = ws.levels.as<uint8_t>();
+        for (int l = 0; l < levels; ++l) {
+            a.F.K[l] = level_intr(f->intrinsics, l);
+            a.F.depth[l] = reinterpret_cast<float*>(base + ws.lvl_off_depth[l]);
+            a.F.inten[l] = reinterpret_cast<float*>(base + ws.lvl_off_inten[l]);
+            a.F.mask[l] = base + ws.lvl_off_mask[l];
+        }
+        a.F.res_sq = ws.res_sq.as<float>();
+        a.F.res_valid = ws.res_valid.as<uint8_t>();
+        const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
+        for (int i = 0; i < 3; ++i) a.F.mwork[i] = ws.mwork.as<uint8_t>() + i * n;
+        a.grid.sync = ws.gsync.as<GridSync>();
+        a.grid.partials = ws.partials.as<double>();
+        a.grid.result = ws.result.as<double>();
+        a.pose_state = ws.pose.as<double>();
+        a.out = ws.out.as<TrackOut>();
+        a.reg.levels = levels;
+        return a;
+    }
+    void launch_track(TrackArgs& a) {
+        void* args[] = {&a};
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
+    }
+    TrackOut fetch_out() {
+        CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
+        ws.sync();
+        return *ws.h_out;
+    }
+};
+
+namespace {
+
+RegParams to_reg(const rf_registration_config& c, int levels) {
+    RegParams r;
+    r.color_weight = c.color_weight;
+    r.levels = levels;
+    r.max_iterations = c.max_iterations;
+    r.lambda_init = c.lm_lambda_init;
+    r.lambda_up = c.lm_lambda_up;
+    r.lambda_down = c.lm_lambda_down;
+    r.eps = c.convergence_eps;
+    r.min_valid = c.min_valid_residuals;
+    return r;
+}
+
+MaskParams to_mask(const rf_mask_config& c) {
+    MaskParams m;
+    m.gamma = c.gamma;
+    m.truncation = c.truncation;
+    m.theta = c.theta;
+    m.erode_radius = c.erode_radius;
+    m.dilate_radius = c.dilate_radius;
+    m.connectivity = c.connectivity;
+    return m;
+}
+
+void check_frame_dims(const rf_frame* f) {
+    require(f && f->depth, RF_INVALID_ARGUMENT, "frame has no depth");
+    require(f->intrinsics.width > 0 && f->intrinsics.height > 0, RF_INVALID_ARGUMENT, "bad image size");
+}
+
+void create_volume(const rf_volume_config* cfg, int device, rf_volume** out) {
+    require(cfg && out, RF_INVALID_ARGUMENT, "null argument");
+    validate_volume_config(*cfg);
+    CK(cudaSetDevice(device));
+    auto v = std::make_unique<rf_volume>();
+    v->device = device;
+    v->cfg = *cfg;
+    v->cap = cfg->hash_capacity ? cfg->hash_capacity : next_pow2((cfg->max_blocks * 4 + 2) / 3);
+    require((v->cap & (v->cap - 1)) == 0 && v->cap <= (1ull << 31), RF_INVALID_ARGUMENT,
+            "hash_capacity must be a power of two <= 2^31");
+    require(v->cap >= cfg->max_blocks, RF_INVALID_ARGUMENT, "hash_capacity must be >= max_blocks");
+    v->slots.ensure(v->cap * sizeof(HashSlot));
+    v->coords.ensure(cfg->max_blocks * sizeof(int4));
+    v->voxels.ensure(cfg->max_blocks * kBrickVoxels * sizeof(Voxel));
+    v->counters.ensure(kNumCounters * sizeof(uint32_t));
+    v->ws.init(device);
+    CK(cudaMemsetAsync(v->slots.p, 0xFF, v->cap * sizeof(HashSlot), v->ws.stream));
+    CK(cudaMemsetAsync(v->voxels.p, 0, cfg->max_blocks * kBrickVoxels * sizeof(Voxel), v->ws.stream));
+    CK(cudaMemsetAsync(v->counters.p, 0, kNumCounters * sizeof(uint32_t), v->ws.stream));
+    v->ws.list.ensure(cfg->max_blocks * sizeof(uint32_t));
+    VolumeView& V = v->view;
+    V.slots = v->slots.as<HashSlot>();
+    V.hash_mask = uint32_t(v->cap - 1);
+    V.max_blocks = uint32_t(cfg->max_blocks);
+    V.coords = v->coords.as<int4>();
+    V.voxels = v->voxels.as<Voxel>();
+    V.counters = v->counters.as<uint32_t>();
+    V.voxel_size = cfg->voxel_size;
+    V.truncation = cfg->truncation;
+    V.max_weight = cfg->max_weight;
+    V.carve_weight = cfg->carve_weight;
+    V.min_depth = cfg->min_depth;
+    V.max_depth = cfg->max_depth;
+    V.carve_clip = cfg->carve_clip;
+    v->ws.sync();
+    *out = v.release();
+}
+
+// Shared per-device workspace for the volume-less mask entry point.
+std::mutex g_ws_mu;
+std::map<int, Workspace*> g_ws;
+Workspace& device_ws(int device) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = g_ws.find(device);
+    if (it != g_ws.end()) return *it->second;
+    auto* w = new Workspace();
+    w->init(device);
+    g_ws[device] = w;
+    return *w;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rf_last_error(void) { return g_err.c_str(); }
+const char* rf_version(void) { return "refusion_b200 0.1 (sm_100a)"; }
+
+rf_status rf_volume_create(const rf_volume_config* cfg, int device, rf_volume** out) {
+    return guard([&] { create_volume(cfg, device, out); });
+}
+
+void rf_volume_destroy(rf_volume* v) {
+    if (!v) return;
+    cudaSetDevice(v->device);
+    cudaStreamSynchronize(v->ws.stream);
+    v->ws.destroy();
+    v->slots.release();
+    v->coords.release();
+    v->voxels.release();
+    v->counters.release();
+    delete v;
+}
+
+rf_status rf_volume_num_blocks(const rf_volume* v, uint64_t* out) {
+    return guard([&] {
+        require(v && out, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(v->device));
+        *out = const_cast<rf_volume*>(v)->num_blocks();
+    });
+}
+
+rf_status rf_volume_hash_capacity(const rf_volume* v, uint64_t* out) {
+    return guard([&] {
+        require(v && out, RF_INVALID_ARGUMENT, "null argument");
+        *out = v->cap;
+    });
+}
+
+rf_status rf_volume_allocate_blocks(rf_volume* v, const int32_t* coords, uint64_t n, int32_t* created) {
+    return guard([&] {
+        require(v && (coords || n == 0), RF_INVALID_ARGUMENT, "null argument");
+        if (n == 0) return;
+        CK(cudaSetDevice(v->device));
+        DevBuf dc, dr;
+        dc.ensure(n * 12);
+        dr.ensure(n * 4);
+        CK(cudaMemcpyAsync(dc.p, coords, n * 12, cudaMemcpyHostToDevice, v->ws.stream));
+        k_alloc_coords<<<unsigned((n + 255) / 256), 256, 0, v->ws.stream>>>(v->view, dc.as<int>(), int(n),
+                                                                             dr.as<int>());
+        CK(cudaGetLastError());
+        if (created) CK(cudaMemcpyAsync(created, dr.p, n * 4, cudaMemcpyDeviceToHost, v->ws.stream));
+        v->ws.sync();
+        dc.release();
+        dr.release();
+        require(v->overflow() == 0, RF_RESOURCE_LIMIT,
+                "voxel block budget exhausted (" + std::to_string(v->cfg.max_blocks) + " blocks)");
+    });
+}
+
+rf_status rf_volume_allocate_for_frame(rf_volume* v, const rf_frame* f, const double pose[12],
+                                       const uint8_t* mask) {
+    return guard([&] {
+        require(v && pose, RF_INVALID_ARGUMENT, "null argument");
+        v->prepare(f);
+        const float* d = v->depth_of(f);
+        const uint8_t* m = v->mask_of(f, mask);
+        v->upload_pose(pose);
+        v->reset_counter(kDdaVisits);
+        v->allocate(d, m, f->intrinsics, v->ws.pose.as<double>(), nullptr);
+        v->ws.sync();
+        require(v->overflow() == 0, RF_RESOURCE_LIMIT,
+                "voxel block budget exhausted (" + std::to_string(v->cfg.max_blocks) + " blocks)");
+    });
+}
+
+rf_status rf_volume_integrate(rf_volume* v, const rf_frame* f, const double pose[12], const uint8_t* mask) {
+    return guard([&] {
+        require(v && pose, RF_INVALID_ARGUMENT, "null argument");
+        v->prepare(f);
+        const float* d = v->depth_of(f);
+        const uint8_t* rgb = v->rgb_of(f);
+        const uint8_t* m = v->mask_of(f, mask);
+        v->upload_pose(pose);
+        v->reset_counter(kVisible);
+        v->fuse(d, rgb, m, f->intrinsics, v->ws.pose.as<double>(), nullptr, false, true, false);
+        v->ws.sync();
+    });
+}
+
+rf_status rf_volume_carve(rf_volume* v, const rf_frame* f, const double pose[12]) {
+    return guard([&] {
+        require(v && pose, RF_INVALID_ARGUMENT, "null argument");
+        v->prepare(f);
+        const float* d = v->depth_of(f);
+        v->upload_pose(pose);
+        v->reset_counter(kVisible);
+        v->fuse(d, nullptr, nullptr, f->intrinsics, v->ws.pose.as<double>(), nullptr, true, false, false);
+        v->ws.sync();
+    });
+}
+
+rf_status rf_volume_sample(const rf_volume* cv, int32_t mode, const double* points, uint64_t n, double* value,
+                           double* grad, uint8_t* valid) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && points && value && valid && mode >= 0 && mode <= 4, RF_INVALID_ARGUMENT, "bad argument");
+        if (n == 0) return;
+        CK(cudaSetDevice(v->device));
+        DevBuf dp, dv, dg, dk;
+        dp.ensure(n * 24);
+        dv.ensure(n * 8);
+        dg.ensure(n * 24);
+        dk.ensure(n);
+        CK(cudaMemcpyAsync(dp.p, points, n * 24, cudaMemcpyHostToDevice, v->ws.stream));
+        k_sample<<<unsigned((n + 127) / 128), 128, 0, v->ws.stream>>>(v->view, dp.as<double>(), int(n), mode,
+                                                                        dv.as<double>(), dg.as<double>(),
+                                                                        dk.as<uint8_t>());
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(value, dv.p, n * 8, cudaMemcpyDeviceToHost, v->ws.stream));
+        if (grad) CK(cudaMemcpyAsync(grad, dg.p, n * 24, cudaMemcpyDeviceToHost, v->ws.stream));
+        CK(cudaMemcpyAsync(valid, dk.p, n, cudaMemcpyDeviceToHost, v->ws.stream));
+        v->ws.sync();
+    });
+}
+
+static rf_status voxel_rw(const rf_volume* cv, const int32_t* vc, uint64_t n, uint8_t* io, uint8_t* found,
+                          uint64_t* missing, bool write) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && vc && io, RF_INVALID_ARGUMENT, "null argument");
+        if (n == 0) {
+            if (missing) *missing = 0;
+            return;
+        }
+        CK(cudaSetDevice(v->device));
+        DevBuf dc, dio, df;
+        dc.ensure(n * 12);
+        dio.ensure(n * 8);
+        df.ensure(n);
+        CK(cudaMemcpyAsync(dc.p, vc, n * 12, cudaMemcpyHostToDevice, v->ws.stream));
+        if (write) CK(cudaMemcpyAsync(dio.p, io, n * 8, cudaMemcpyHostToDevice, v->ws.stream));
+        k_voxel_rw<<<unsigned((n + 255) / 256), 256, 0, v->ws.stream>>>(v->view, dc.as<int>(), int(n),
+                                                                          dio.as<Voxel>(), df.as<uint8_t>(),
+                                                                          write ? 1 : 0);
+        CK(cudaGetLastError());
+        std::vector<uint8_t> hf(n);
+        if (!write) CK(cudaMemcpyAsync(io, dio.p, n * 8, cudaMemcpyDeviceToHost, v->ws.stream));
+        CK(cudaMemcpyAsync(hf.data(), df.p, n, cudaMemcpyDeviceToHost, v->ws.stream));
+        v->ws.sync();
+        uint64_t miss = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            if (!hf[i]) {
+                ++miss;
+                if (!write) std::memset(io + 8 * i, 0, 8);
+            }
+        }
+        if (found) std::memcpy(found, hf.data(), n);
+        if (missing) *missing = miss;
+    });
+}
+
+rf_status rf_volume_get_voxels(const rf_volume* v, const int32_t* vc, uint64_t n, uint8_t* voxels,
+                               uint8_t* found) {
+    return voxel_rw(v, vc, n, voxels, found, nullptr, false);
+}
+
+rf_status rf_volume_set_voxels(rf_volume* v, const int32_t* vc, uint64_t n, const uint8_t* voxels,
+                               uint64_t* missing) {
+    return voxel_rw(v, vc, n, const_cast<uint8_t*>(voxels), nullptr, missing, true);
+}
+
+rf_status rf_volume_export_blocks(const rf_volume* cv, int32_t* coords, uint8_t* voxels, uint64_t capacity,
+                                  uint64_t* count) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && count, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(v->device));
+        const uint64_t nb = v->num_blocks();
+        *count = nb;
+        if (!coords || capacity < nb || nb == 0) return;
+        std::vector<int4> c(nb);
+        CK(cudaMemcpy(c.data(), v->coords.p, nb * sizeof(int4), cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < nb; ++i) {
+            coords[3 * i] = c[i].x;
+            coords[3 * i + 1] = c[i].y;
+            coords[3 * i + 2] = c[i].z;
+        }
+        if (voxels) CK(cudaMemcpy(voxels, v->voxels.p, nb * kBrickVoxels * sizeof(Voxel), cudaMemcpyDeviceToHost));
+    });
+}
+
+rf_status rf_volume_hash_occupancy(const rf_volume* cv, uint8_t* bitmap) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && bitmap, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(v->device));
+        DevBuf b;
+        b.ensure(v->cap);
+        k_occupancy<<<1024, 256, 0, v->ws.stream>>>(v->view, b.as<uint8_t>());
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(bitmap, b.p, v->cap, cudaMemcpyDeviceToHost, v->ws.stream));
+        v->ws.sync();
+    });
+}
+
+rf_status rf_volume_reset(rf_volume* v) {
+    return guard([&] {
+        require(v, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(v->device));
+        const uint64_t nb = v->num_blocks();
+        CK(cudaMemsetAsync(v->slots.p, 0xFF, v->cap * sizeof(HashSlot), v->ws.stream));
+        CK(cudaMemsetAsync(v->voxels.p, 0, nb * kBrickVoxels * sizeof(Voxel), v->ws.stream));
+        CK(cudaMemsetAsync(v->counters.p, 0, kNumCounters * sizeof(uint32_t), v->ws.stream));
+        v->ws.sync();
+    });
+}
+
+// TsdfVolume::Save / Load (tsdf_volume.cpp:375-449): "TSDFVOL\0", u32 version 1,
+// config, u64 block count, then per block i32[3] + 512 voxels, little-endian.
+rf_status rf_volume_save(const rf_volume* cv, const char* path) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && path, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(v->device));
+        const uint64_t nb = v->num_blocks();
+        std::vector<int4> c(nb);
+        std::vector<Voxel> vox(nb * kBrickVoxels);
+        if (nb) {
+            CK(cudaMemcpy(c.data(), v->coords.p, nb * sizeof(int4), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(vox.data(), v->voxels.p, vox.size() * sizeof(Voxel), cudaMemcpyDeviceToHost));
+        }
+        std::ofstream out(path, std::ios::binary);
+        require(bool(out), RF_IO_ERROR, std::string("cannot open for writing: ") + path);
+        const char magic[8] = {'T', 'S', 'D', 'F', 'V', 'O', 'L', '\0'};
+        out.write(magic, 8);
+        auto w = [&](const auto& x) { out.write(reinterpret_cast<const char*>(&x), sizeof(x)); };
+        w(uint32_t(1));
+        w(v->cfg.voxel_size);
+        w(v->cfg.truncation);
+        w(int32_t(v->cfg.block_side));
+        w(int32_t(v->cfg.max_weight));
+        w(int32_t(v->cfg.carve_weight));
+        w(v->cfg.min_depth);
+        w(v->cfg.max_depth);
+        w(v->cfg.carve_clip);
+        w(uint64_t(v->cfg.max_blocks));
+        w(uint64_t(nb));
+        for (uint64_t i = 0; i < nb; ++i) {
+            const int32_t cc[3] = {c[i].x, c[i].y, c[i].z};
+            out.write(reinterpret_cast<const char*>(cc), 12);
+            out.write(reinterpret_cast<const char*>(&vox[i * kBrickVoxels]), kBrickVoxels * sizeof(Voxel));
+        }
+        require(bool(out), RF_IO_ERROR, std::string("write failed: ") + path);
+    });
+}
+
+rf_status rf_volume_load(const char* path, int device, rf_volume** out) {
+    return guard([&] {
+        require(path && out, RF_INVALID_ARGUMENT, "null argument");
+        std::ifstream in(path, std::ios::binary);
+        require(bool(in), RF_IO_ERROR, std::string("cannot open volume snapshot: ") + path);
+        char magic[8];
+        in.read(magic, 8);
+        require(bool(in) && std::memcmp(magic, "TSDFVOL\0", 8) == 0, RF_IO_ERROR,
+                std::string("not a volume snapshot: ") + path);
+        auto r = [&](auto& x) { in.read(reinterpret_cast<char*>(&x), sizeof(x)); };
+        uint32_t version = 0;
+        r(version);
+        require(version == 1, RF_IO_ERROR, std::string("unsupported volume snapshot version in ") + path);
+        rf_volume_config cfg{};
+        int32_t bs, mw, cw;
+        uint64_t mb, nb;
+        r(cfg.voxel_size);
+        r(cfg.truncation);
+        r(bs);
+        r(mw);
+        r(cw);
+        r(cfg.min_depth);
+        r(cfg.max_depth);
+        r(cfg.carve_clip);
+        r(mb);
+        r(nb);
+        require(bool(in), RF_IO_ERROR, std::string("truncated volume snapshot: ") + path);
+        cfg.block_side = bs;
+        cfg.max_weight = mw;
+        cfg.carve_weight = cw;
+        cfg.max_blocks = mb;
+        require(nb <= mb, RF_RESOURCE_LIMIT, "snapshot holds more blocks than max_blocks");
+        std::vector<int32_t> coords(nb * 3);
+        std::vector<Voxel> vox(nb * kBrickVoxels);
+        for (uint64_t i = 0; i < nb; ++i) {
+            in.read(reinterpret_cast<char*>(&coords[3 * i]), 12);
+            in.read(reinterpret_cast<char*>(&vox[i * kBrickVoxels]), kBrickVoxels * sizeof(Voxel));
+            require(bool(in), RF_IO_ERROR, std::string("truncated volume snapshot: ") + path);
+        }
+        rf_volume* v = nullptr;
+        create_volume(&cfg, device, &v);
+        std::unique_ptr<rf_volume, void (*)(rf_volume*)> hold(v, rf_volume_destroy);
+        if (nb) {
+            DevBuf dc;
+            dc.ensure(nb * 12);
+            CK(cudaMemcpy(dc.p, coords.data(), nb * 12, cudaMemcpyHostToDevice));
+            k_import<<<unsigned((nb + 255) / 256), 256, 0, v->ws.stream>>>(v->view, dc.as<int>(), uint32_t(nb), 0);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(v->voxels.p, vox.data(), vox.size() * sizeof(Voxel), cudaMemcpyHostToDevice,
+                               v->ws.stream));
+            const uint32_t cnt = uint32_t(nb);
+            CK(cudaMemcpyAsync(v->view.counters + kNumBlocks, &cnt, 4, cudaMemcpyHostToDevice, v->ws.stream));
+            v->ws.sync();
+        }
+        *out = hold.release();
+    });
+}
+
+// ---------------------------------------------------------------- registration
+static void run_pass(rf_volume* v, const rf_frame* f, const double pose[12], const uint8_t* mask, int mode,
+                     double cw, TrackOut& out) {
+    v->prepare(f);
+    const float* d = v->depth_of(f);
+    const uint8_t* rgb = v->rgb_of(f);
+    TrackArgs a = v->track_args(f, d, rgb, 1);
+    if (mask) {
+        v->mask_of(f, mask, a.F.mask[0]);
+        a.use_mask = 1;
+    }
+    v->upload_pose(pose);
+    a.mode = mode;
+    a.reg.color_weight = cw;
+    a.reg.levels = 1;
+    v->launch_track(a);
+    out = v->fetch_out();
+}
+
+rf_status rf_linearize(const rf_volume* cv, const rf_frame* f, const double pose[12],
+                       const rf_registration_config* cfg, const uint8_t* mask, rf_linearize_result* out) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && pose && cfg && out, RF_INVALID_ARGUMENT, "null argument");
+        TrackOut o;
+        run_pass(v, f, pose, mask, kModeLinearize, cfg->color_weight, o);
+        for (int i = 0, k = 0; i < 6; ++i)
+            for (int j = i; j < 6; ++j, ++k) out->H[6 * i + j] = out->H[6 * j + i] = o.acc[k];
+        for (int i = 0; i < 6; ++i) out->b[i] = o.acc[21 + i];
+        out->depth_error = o.acc[27];
+        out->color_error = o.acc[28];
+        out->error = o.acc[27] + cfg->color_weight * o.acc[28];
+        out->valid_count = uint64_t(o.acc[29]);
+        out->degenerate = 0;  // informational only; computed by the host layer
+    });
+}
+
+rf_status rf_evaluate_depth_error(const rf_volume* cv, const rf_frame* f, const double pose[12], const uint8_t* mask,
+                                  double* error, float* res_sq, uint8_t* res_valid) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && pose, RF_INVALID_ARGUMENT, "null argument");
+        TrackOut o;
+        run_pass(v, f, pose, mask, kModeEvalDepth, 0.0, o);
+        if (error) *error = o.acc[27];
+        const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
+        if (res_sq) CK(cudaMemcpy(res_sq, v->ws.res_sq.p, n * 4, cudaMemcpyDeviceToHost));
+        if (res_valid) CK(cudaMemcpy(res_valid, v->ws.res_valid.p, n, cudaMemcpyDeviceToHost));
+    });
+}
+
+rf_status rf_evaluate_color_error(const rf_volume* cv, const rf_frame* f, const double pose[12],
+                                  const uint8_t* mask, double* error) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && pose && error, RF_INVALID_ARGUMENT, "null argument");
+        TrackOut o;
+        run_pass(v, f, pose, mask, kModeEvalColor, 1.0, o);
+        *error = o.acc[28];
+    });
+}
+
+rf_status rf_register(const rf_volume* cv, const rf_frame* f, const double init[12], const uint8_t* mask,
+                      const rf_registration_config* cfg, rf_registration_result* out, float* res_sq,
+                      uint8_t* res_valid) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && init && cfg && out, RF_INVALID_ARGUMENT, "null argument");
+        check_reg_config(*cfg);
+        check_frame_dims(f);
+        for (int l = 1; l < cfg->pyramid_levels; ++l)
+            require((f->intrinsics.width >> l) >= 1 && (f->intrinsics.height >> l) >= 1, RF_INVALID_ARGUMENT,
+                    "image too small for pyramid level");
+        v->prepare(f, cfg->pyramid_levels);
+        const float* d = v->depth_of(f);
+        const uint8_t* rgb = v->rgb_of(f);
+        TrackArgs a = v->track_args(f, d, rgb, cfg->pyramid_levels);
+        if (mask) {
+            v->mask_of(f, mask, a.F.mask[0]);
+            a.use_mask = 1;
+        }
+        v->upload_pose(init);
+        a.mode = kModeRegister;
+        a.reg = to_reg(*cfg, cfg->pyramid_levels);
+        v->launch_track(a);
+        const TrackOut o = v->fetch_out();
+        require(!o.lost, RF_TRACKING_LOST, "too few valid residuals");
+        std::memcpy(out->pose, o.pose, sizeof(o.pose));
+        out->converged = o.converged;
+        out->iterations = o.iterations;
+        out->valid_residuals = o.valid;
+        out->final_error = o.final_error;
+        const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
+        if (res_sq) CK(cudaMemcpy(res_sq, v->ws.res_sq.p, n * 4, cudaMemcpyDeviceToHost));
+        if (res_valid) CK(cudaMemcpy(res_valid, v->ws.res_valid.p, n, cudaMemcpyDeviceToHost));
+    });
+}
+
+rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const float* depth, int32_t w, int32_t h,
+                         const rf_mask_config* cfg, int32_t stages, int device, uint8_t* out, uint64_t* masked) {
+    return guard([&] {
+        require(res_valid && depth && cfg && out && w > 0 && h > 0, RF_INVALID_ARGUMENT, "null argument");
+        require(!(stages & 1) || res_sq, RF_INVALID_ARGUMENT, "threshold stage needs residuals");
+        require(cfg->connectivity == 4 || cfg->connectivity == 8, RF_INVALID_ARGUMENT,
+                "connectivity must be 4 or 8");
+        CK(cudaSetDevice(device));
+        Workspace& ws = device_ws(device);
+        ws.ensure_frame(w, h, 1);
+        const size_t n = size_t(w) * h;
+        if (res_sq) CK(cudaMemcpyAsync(ws.res_sq.p, res_sq, n * 4, cudaMemcpyHostToDevice, ws.stream));
+        CK(cudaMemcpyAsync(ws.res_valid.p, res_valid, n, cudaMemcpyHostToDevice, ws.stream));
+        CK(cudaMemcpyAsync(ws.depth.p, depth, n * 4, cudaMemcpyHostToDevice, ws.stream));
+        if (!(stages & 1))
+            CK(cudaMemcpyAsync(ws.mwork.p, res_valid, n, cudaMemcpyHostToDevice, ws.stream));
+        TrackArgs a{};
+        a.mode = kModeMask;
+        a.mask_stages = stages;
+        a.mp = to_mask(*cfg);
+        a.F.depth0 = ws.depth.as<float>();
+        a.F.K[0].w = w;
+        a.F.K[0].h = h;
+        a.F.res_sq = ws.res_sq.as<float>();
+        a.F.res_valid = ws.res_valid.as<uint8_t>();
+        for (int i = 0; i < 3; ++i) a.F.mwork[i] = ws.mwork.as<uint8_t>() + i * n;
+        a.F.mask[0] = ws.mask_in.as<uint8_t>();
+        a.grid.sync = ws.gsync.as<GridSync>();
+        a.grid.partials = ws.partials.as<double>();
+        a.grid.result = ws.result.as<double>();
+        a.out = ws.out.as<TrackOut>();
+        void* args[] = {&a};
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
+        CK(cudaMemcpyAsync(out, ws.mask_in.p, n, cudaMemcpyDeviceToHost, ws.stream));
+        CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
+        ws.sync();
+        if (masked) *masked = ws.h_out->masked;
+    });
+}
+
+rf_status rf_raycast(const rf_volume* cv, const double view_pose[12], const rf_intrinsics* k,
+                     int32_t bisection_iterations, float* out_depth) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && view_pose && k && out_depth, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(v->device));
+        const size_t n = size_t(k->width) * k->height;
+        DevBuf o;
+        o.ensure(n * 4);
+        RaycastArgs a{};
+        a.V = v->view;
+        for (int i = 0; i < 9; ++i) a.view.R[i] = view_pose[i];
+        for (int i = 0; i < 3; ++i) a.view.t[i] = view_pose[9 + i];
+        a.K = level_intr(*k, 0);
+        a.bisections = bisection_iterations;
+        a.out = o.as<float>();
+        k_raycast<<<unsigned((n + 127) / 128), 128, 0, v->ws.stream>>>(a);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out_depth, o.p, n * 4, cudaMemcpyDeviceToHost, v->ws.stream));
+        v->ws.sync();
+    });
+}
+
+// ---------------------------------------------------------------- memory helpers
+void* rf_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+}
+void rf_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+void* rf_device_alloc(size_t bytes, int device) {
+    void* p = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    return p;
+}
+void rf_device_free(void* p) {
+    if (p) cudaFree(p);
+}
+rf_status rf_copy_to_device(void* dst, const void* src, size_t bytes) {
+    return guard([&] { CK(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice)); });
+}
+
+}  // extern "C"
+
+// ==================================================================== pipeline
+// Pipeline::ProcessFrame (pipeline.cpp:57-131) as a fixed launch sequence with
+// device-side control flow: k_track (pyramid, Register, BuildMask, masked
+// Register, pose update or hold), then AllocateForFrame, the frustum cull and
+// the fused CarveFreeSpace+Integrate, all gated by the device `lost` flag. The
+// host reads back one small struct per frame.
+struct rf_pipeline {
+    rf_pipeline_config cfg{};
+    rf_volume* vol = nullptr;
+    bool first = true;
+    uint64_t frame_count = 0, losses = 0;
+    std::vector<double> traj_t, traj_p;
+    TrackOut last{};
+    uint32_t last_counters[kNumCounters] = {};
+    bool has_mask = false;
+};
+
+namespace {
+
+void validate_pipeline_config(rf_pipeline_config c) {  // PipelineConfig::Sync (config.cpp:12-48)
+    c.mask.truncation = c.volume.truncation;
+    validate_volume_config(c.volume);
+    require(c.mask.gamma > 0, RF_INVALID_ARGUMENT, "gamma must be positive");
+    require(c.mask.theta > 0, RF_INVALID_ARGUMENT, "theta must be positive");
+    require(c.mask.erode_radius >= 0 && c.mask.dilate_radius >= 0, RF_INVALID_ARGUMENT,
+            "morphology radii must be non-negative");
+    require(c.mask.connectivity == 4 || c.mask.connectivity == 8, RF_INVALID_ARGUMENT,
+            "connectivity must be 4 or 8");
+    require(c.registration.color_weight >= 0, RF_INVALID_ARGUMENT, "color_weight must be non-negative");
+    check_reg_config(c.registration);
+    require(c.registration.lm_lambda_init > 0 && c.registration.lm_lambda_up > 1 && c.registration.lm_lambda_down > 1,
+            RF_INVALID_ARGUMENT, "invalid LM damping schedule");
+    require(c.registration.convergence_eps > 0, RF_INVALID_ARGUMENT, "convergence_eps must be positive");
+    require(c.registration.min_valid_residuals >= 1, RF_INVALID_ARGUMENT, "min_valid_residuals must be >= 1");
+    require(c.refine_window >= 1, RF_INVALID_ARGUMENT, "refine_window must be >= 1");
+    require(c.far_value > c.volume.max_depth, RF_INVALID_ARGUMENT, "far_value must exceed max_depth");
+    require(c.threads >= 1, RF_INVALID_ARGUMENT, "threads must be >= 1");
+    require(!c.refine_enabled, RF_UNSUPPORTED,
+            "depth refinement (RefinementConfig::enabled) is not on the CUDA path yet; set refine_enabled = 0");
+}
+
+bool intrinsics_valid(const rf_intrinsics& k) {  // CameraIntrinsics::Valid (geometry.hpp:20-24)
+    return k.fx > 0.0 && k.fy > 0.0 && k.width > 0 && k.height > 0 && k.cx > 0.0 && k.cx < double(k.width) &&
+           k.cy > 0.0 && k.cy < double(k.height) && k.depth_scale > 0.0;
+}
+
+}  // namespace
+
+extern "C" {
+
+rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipeline** out) {
+    return guard([&] {
+        require(cfg && out, RF_INVALID_ARGUMENT, "null argument");
+        validate_pipeline_config(*cfg);
+        auto p = std::make_unique<rf_pipeline>();
+        p->cfg = *cfg;
+        p->cfg.mask.truncation = cfg->volume.truncation;
+        create_volume(&p->cfg.volume, device, &p->vol);
+        *out = p.release();
+    });
+}
+
+void rf_pipeline_destroy(rf_pipeline* p) {
+    if (!p) return;
+    rf_volume_destroy(p->vol);
+    delete p;
+}
+
+rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_stats* stats, double pose_out[12]) {
+    return guard([&] {
+        require(p && f, RF_INVALID_ARGUMENT, "null argument");
+        require(intrinsics_valid(f->intrinsics) && f->depth && f->rgb, RF_INVALID_ARGUMENT,
+                "frame images do not match the intrinsics");
+        const auto t0 = std::chrono::steady_clock::now();
+        rf_volume* v = p->vol;
+        const int L = p->cfg.registration.pyramid_levels;
+        for (int l = 1; l < L; ++l)
+            require((f->intrinsics.width >> l) >= 1 && (f->intrinsics.height >> l) >= 1, RF_INVALID_ARGUMENT,
+                    "image too small for pyramid level");
+        v->prepare(f, L);
+        Workspace& ws = v->ws;
+        const float* d = v->depth_of(f);
+        const uint8_t* rgb = v->rgb_of(f);
+        rf_frame_stats st{};
+        st.frame_index = p->frame_count;
+        st.timestamp = f->timestamp;
+        double* pose_state = ws.pose.as<double>();
+        if (p->first) {  // bootstrap at the identity (pipeline.cpp:66-76)
+            static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+            CK(cudaMemcpyAsync(pose_state, kIdentity, 96, cudaMemcpyHostToDevice, ws.stream));
+            CK(cudaMemsetAsync(v->view.counters + kBlocksBefore, 0, 4 * 4, ws.stream));
+            v->allocate(d, nullptr, f->intrinsics, pose_state, nullptr);
+            v->fuse(d, rgb, nullptr, f->intrinsics, pose_state, nullptr, false, true, false);
+            CK(cudaMemcpyAsync(ws.h_counters, v->view.counters, kNumCounters * 4, cudaMemcpyDeviceToHost, ws.stream));
+            ws.sync();
+            st.converged = 1;
+            std::memcpy(p->last.pose, kIdentity, 96);
+            p->last.rounds = 0;
+            p->has_mask = false;
+        } else {
+            TrackArgs a = v->track_args(f, d, rgb, L);
+            a.mode = kModeFrame;
+            a.dynamics = p->cfg.dynamics_enabled;
+            a.reg = to_reg(p->cfg.registration, L);
+            a.mp = to_mask(p->cfg.mask);
+            a.vol_counters = v->view.counters;
+            v->launch_track(a);
+            const uint8_t* mask = p->cfg.dynamics_enabled ? a.F.mask[0] : nullptr;
+            const int* lost = &ws.out.as<TrackOut>()->lost;
+            v->allocate(d, mask, f->intrinsics, pose_state, lost);
+            v->fuse(d, rgb, mask, f->intrinsics, pose_state, lost, true, true, true);
+            CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
+            CK(cudaMemcpyAsync(ws.h_counters, v->view.counters, kNumCounters * 4, cudaMemcpyDeviceToHost, ws.stream));
+            ws.sync();
+            p->last = *ws.h_out;
+            const TrackOut& o = p->last;
+            st.tracking_lost = o.lost;
+            st.converged = o.converged;
+            st.registrations = o.registrations;
+            st.iterations = o.iterations;
+            st.valid_residuals = o.valid;
+            st.masked_pixels = o.masked;
+            st.final_error = o.final_error;
+            p->has_mask = !o.lost && p->cfg.dynamics_enabled;
+            if (o.lost) ++p->losses;
+        }
+        std::memcpy(p->last_counters, ws.h_counters, sizeof(p->last_counters));
+        p->traj_t.push_back(f->timestamp);
+        p->traj_p.insert(p->traj_p.end(), p->last.pose, p->last.pose + 12);
+        if (pose_out) std::memcpy(pose_out, p->last.pose, 96);
+        p->first = false;
+        require(ws.h_counters[kOverflow] == 0, RF_RESOURCE_LIMIT,
+                "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)");
+        st.runtime_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        ++p->frame_count;
+        if (stats) *stats = st;
+    });
+}
+
+rf_status rf_pipeline_finalize(rf_pipeline* p) {
+    return guard([&] { require(p, RF_INVALID_ARGUMENT, "null argument"); });
+}
+
+rf_status rf_pipeline_volume(rf_pipeline* p, rf_volume** out) {
+    return guard([&] {
+        require(p && out, RF_INVALID_ARGUMENT, "null argument");
+        *out = p->vol;
+    });
+}
+
+rf_status rf_pipeline_tracking_losses(const rf_pipeline* p, uint64_t* out) {
+    return guard([&] {
+        require(p && out, RF_INVALID_ARGUMENT, "null argument");
+        *out = p->losses;
+    });
+}
+
+rf_status rf_pipeline_trajectory(const rf_pipeline* p, double* ts, double* poses, uint64_t capacity,
+                                 uint64_t* count) {
+    return guard([&] {
+        require(p && count, RF_INVALID_ARGUMENT, "null argument");
+        *count = p->traj_t.size();
+        if (!ts || !poses || capacity < p->traj_t.size()) return;
+        std::memcpy(ts, p->traj_t.data(), p->traj_t.size() * 8);
+        std::memcpy(poses, p->traj_p.data(), p->traj_p.size() * 8);
+    });
+}
+
+rf_status rf_pipeline_last_mask(const rf_pipeline* p, uint8_t* out, int32_t* has_mask) {
+    return guard([&] {
+        require(p && has_mask, RF_INVALID_ARGUMENT, "null argument");
+        *has_mask = p->has_mask;
+        if (!p->has_mask || !out) return;
+        Workspace& ws = p->vol->ws;
+        CK(cudaSetDevice(p->vol->device));
+        CK(cudaMemcpy(out, ws.levels.as<uint8_t>() + ws.lvl_off_mask[0], size_t(ws.W) * ws.H, cudaMemcpyDeviceToHost));
+    });
+}
+
+rf_status rf_pipeline_last_residuals(const rf_pipeline* p, float* res_sq, uint8_t* res_valid) {
+    return guard([&] {
+        require(p, RF_INVALID_ARGUMENT, "null argument");
+        Workspace& ws = p->vol->ws;
+        CK(cudaSetDevice(p->vol->device));
+        const size_t n = size_t(ws.W) * ws.H;
+        if (res_sq) CK(cudaMemcpy(res_sq, ws.res_sq.p, n * 4, cudaMemcpyDeviceToHost));
+        if (res_valid) CK(cudaMemcpy(res_valid, ws.res_valid.p, n, cudaMemcpyDeviceToHost));
+    });
+}
+
+rf_status rf_pipeline_last_counters(const rf_pipeline* p, rf_frame_counters* out) {
+    return guard([&] {
+        require(p && out, RF_INVALID_ARGUMENT, "null argument");
+        const uint32_t* c = p->last_counters;
+        out->num_blocks = std::min<uint64_t>(c[kNumBlocks], p->cfg.volume.max_blocks);
+        out->dda_visits = c[kDdaVisits];
+        out->visible_bricks = c[kVisible];
+        out->new_blocks = out->num_blocks - std::min<uint64_t>(c[kBlocksBefore], out->num_blocks);
+        out->floodfill_rounds = p->last.rounds;
+        out->overflow = int32_t(c[kOverflow]);
+    });
+}
+
+}  // extern "C"

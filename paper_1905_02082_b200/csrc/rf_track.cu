@@ -1,0 +1,615 @@
+// Tracking + dynamics mask as one persistent cooperative kernel.
+//
+// One launch runs the whole coarse-to-fine Levenberg-Marquardt loop of
+// Register (registration.cpp:211-286) on the device: every pixel pass is a
+// grid-stride sweep over 16x16 pixel tiles whose per-thread normal equations
+// (21 H + 6 b + 2 errors + count, fp64) are folded warp -> CTA -> grid in a
+// fixed order, so results are deterministic run to run. Every CTA then runs
+// the same tiny LM state machine (6x6 LDLT, ExpMap) on the identical reduced
+// vector, so no host round trip or second barrier is needed per iteration.
+// In kModeFrame the kernel continues with BuildMask (dynamics_mask.cpp:98-104)
+// and the masked second registration (pipeline.cpp:81-99).
+#include "rf_track.cuh"
+
+namespace rfb {
+
+namespace {
+
+constexpr double kIntensityScale = 1.0 / 255.0;  // registration.cpp:22
+constexpr double kRelDecreaseTol = 1e-6;         // registration.cpp:26
+
+__device__ __forceinline__ int hidx(int i, int j) { return i * 6 - (i * (i - 1)) / 2 + (j - i); }
+
+struct RegState {
+    Pose pose, cand;
+    double lambda;
+    double cur[kAccN];
+    double trial[kAccN];
+    int total, converged, lost, ok, brk;
+};
+
+// ------------------------------------------------------------------ math
+__device__ void expmap(const double xi[6], Pose& out) {  // geometry.cpp:14-38
+    const double w0 = xi[3], w1 = xi[4], w2 = xi[5];
+    const double theta = sqrt((w0 * w0 + w1 * w1) + w2 * w2);
+    const double hat[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
+    double hat2[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            hat2[3 * i + j] = (hat[3 * i] * hat[j] + hat[3 * i + 1] * hat[3 + j]) + hat[3 * i + 2] * hat[6 + j];
+    double a, b, c;
+    const double t2 = theta * theta;
+    if (theta < 1e-6) {
+        a = 1.0 - t2 / 6.0;
+        b = 0.5 - t2 / 24.0;
+        c = 1.0 / 6.0 - t2 / 120.0;
+    } else {
+        a = sin(theta) / theta;
+        b = (1.0 - cos(theta)) / t2;
+        c = (theta - sin(theta)) / (t2 * theta);
+    }
+    double vm[9];
+    for (int i = 0; i < 9; ++i) {
+        const double id = (i % 4 == 0) ? 1.0 : 0.0;
+        out.R[i] = (id + a * hat[i]) + b * hat2[i];
+        vm[i] = (id + b * hat[i]) + c * hat2[i];
+    }
+    for (int i = 0; i < 3; ++i) out.t[i] = (vm[3 * i] * xi[0] + vm[3 * i + 1] * xi[1]) + vm[3 * i + 2] * xi[2];
+}
+
+// Eigen::LDLT<Matrix6d> (lower, diagonal pivoting) + solve, as the oracle.
+__device__ bool ldlt6_solve(const double A[36], const double rhs[6], double x[6]) {
+    double m[36];
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) m[6 * i + j] = (j <= i) ? A[6 * i + j] : A[6 * j + i];
+    int tr[6];
+    double temp[6];
+    bool found_zero = false, ret = true;
+    for (int k = 0; k < 6; ++k) {
+        int big = k;
+        double bigv = fabs(m[7 * k]);
+        for (int i = k + 1; i < 6; ++i)
+            if (fabs(m[7 * i]) > bigv) {
+                bigv = fabs(m[7 * i]);
+                big = i;
+            }
+        tr[k] = big;
+        if (k != big) {
+            for (int j = 0; j < k; ++j) {
+                const double t = m[6 * k + j];
+                m[6 * k + j] = m[6 * big + j];
+                m[6 * big + j] = t;
+            }
+            for (int i = big + 1; i < 6; ++i) {
+                const double t = m[6 * i + k];
+                m[6 * i + k] = m[6 * i + big];
+                m[6 * i + big] = t;
+            }
+            const double t = m[7 * k];
+            m[7 * k] = m[7 * big];
+            m[7 * big] = t;
+            for (int i = k + 1; i < big; ++i) {
+                const double u = m[6 * i + k];
+                m[6 * i + k] = m[6 * big + i];
+                m[6 * big + i] = u;
+            }
+        }
+        if (k > 0) {
+            for (int j = 0; j < k; ++j) temp[j] = m[7 * j] * m[6 * k + j];
+            double dot = 0.0;
+            for (int j = 0; j < k; ++j) dot += m[6 * k + j] * temp[j];
+            m[7 * k] -= dot;
+            for (int i = k + 1; i < 6; ++i) {
+                double s = 0.0;
+                for (int j = 0; j < k; ++j) s += m[6 * i + j] * temp[j];
+                m[6 * i + k] -= s;
+            }
+        }
+        const double akk = m[7 * k];
+        const bool valid = fabs(akk) > 0.0;
+        if (k == 0 && !valid) {
+            for (int j = 0; j < 6; ++j) {
+                tr[j] = j;
+                for (int i = j + 1; i < 6; ++i) m[6 * i + j] = 0.0;
+            }
+            break;
+        }
+        if (k < 5) {
+            if (valid) {
+                for (int i = k + 1; i < 6; ++i) m[6 * i + k] /= akk;
+            } else {
+                for (int i = k + 1; i < 6; ++i) ret = ret && (m[6 * i + k] == 0.0);
+            }
+        }
+        if (found_zero && valid) ret = false;
+        else if (!valid) found_zero = true;
+    }
+    if (!ret) return false;
+    for (int i = 0; i < 6; ++i) x[i] = rhs[i];
+    for (int k = 0; k < 6; ++k) {
+        const double t = x[k];
+        x[k] = x[tr[k]];
+        x[tr[k]] = t;
+    }
+    for (int j = 0; j < 6; ++j)
+        for (int i = j + 1; i < 6; ++i) x[i] -= m[6 * i + j] * x[j];
+    for (int i = 0; i < 6; ++i) {
+        if (fabs(m[7 * i]) > 2.2250738585072014e-308) x[i] /= m[7 * i];
+        else x[i] = 0.0;
+    }
+    for (int j = 5; j >= 0; --j)
+        for (int i = 0; i < j; ++i) x[i] -= m[6 * j + i] * x[j];
+    for (int k = 5; k >= 0; --k) {
+        const double t = x[k];
+        x[k] = x[tr[k]];
+        x[tr[k]] = t;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void full_h(const double* acc, double H[36]) {
+    for (int i = 0; i < 6; ++i)
+        for (int j = i; j < 6; ++j) H[6 * i + j] = H[6 * j + i] = acc[hidx(i, j)];
+}
+
+// ------------------------------------------------------------------ pyramid
+// BuildPyramid (registration.cpp:144-182), levels >= 1, one barrier per level.
+__device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
+    const FrameView& F = a.F;
+    const int stride = gridDim.x * blockDim.x;
+    for (int l = 1; l < a.reg.levels; ++l) {
+        const int w = F.K[l].w, h = F.K[l].h, pw = F.K[l - 1].w;
+        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) {
+            const int x = p % w, y = p / w;
+            float closest = 0.f, isum = 0.f;
+            uint8_t masked = 0;
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) {
+                    const int sp = (2 * y + dy) * pw + (2 * x + dx);
+                    if (images) {
+                        const float d = (l == 1) ? __ldg(F.depth0 + sp) : __ldcg(F.depth[l - 1] + sp);
+                        if (depth_valid(d) && (!depth_valid(closest) || d < closest)) closest = d;
+                        if (F.rgb0) {
+                            float iv;
+                            if (l == 1) {
+                                const uint8_t* c = F.rgb0 + 3 * size_t(sp);
+                                iv = float(luma(__ldg(c), __ldg(c + 1), __ldg(c + 2)));  // image.hpp:85-91
+                            } else {
+                                iv = __ldcg(F.inten[l - 1] + sp);
+                            }
+                            isum += iv;
+                        }
+                    }
+                    if (masks && __ldcg(F.mask[l - 1] + sp)) masked = 1;
+                }
+            if (images) {
+                F.depth[l][p] = closest;
+                if (F.rgb0) F.inten[l][p] = isum * 0.25f;
+            }
+            if (masks) F.mask[l][p] = masked;
+        }
+        grid_barrier(a.grid);
+    }
+}
+
+// ------------------------------------------------------------------ pixel pass
+// One Accumulate (registration.cpp:49-117) over pyramid level `level`.
+template <bool kJac, bool kColor>
+__device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
+                           double* scratch, double* blk, double* out) {
+    const FrameView& F = a.F;
+    const Intr K = F.K[level];
+    const double min_depth = a.V.min_depth, max_depth = a.V.max_depth;
+    double acc[kAccN];
+#pragma unroll
+    for (int i = 0; i < kAccN; ++i) acc[i] = 0.0;
+    const int ntx = (K.w + kTileW - 1) / kTileW, nty = (K.h + kTileH - 1) / kTileH;
+    const float* depth = level == 0 ? F.depth0 : F.depth[level];
+    const uint8_t* mask = use_mask ? F.mask[level] : nullptr;
+    for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
+        const int u = (t % ntx) * kTileW + (threadIdx.x % kTileW);
+        const int v = (t / ntx) * kTileH + (threadIdx.x / kTileW);
+        if (u >= K.w || v >= K.h) continue;
+        const int p = v * K.w + u;
+        const float d = level == 0 ? __ldg(depth + p) : __ldcg(depth + p);
+        float rs = 0.f;
+        uint8_t rv = 0;
+        if (depth_valid(d) && !(d < min_depth) && !(d > max_depth)) {
+            const bool masked = mask && __ldcg(mask + p) != 0;
+            if (!(masked && !write_res)) {
+                const double dd = double(d);
+                const double x0 = (double(u) - K.cx) / K.fx * dd;  // geometry.hpp:41-43
+                const double x1 = (double(v) - K.cy) / K.fy * dd;
+                double y[3];
+                pose_apply(P, x0, x1, dd, y);
+                CellSample cs;
+                if (sample_point<kJac, kColor>(a.V, y, cs)) {
+                    const double r_d = cs.sdf;
+                    double I = 0.0;
+                    if (kColor) {
+                        if (level == 0) {
+                            const uint8_t* c = F.rgb0 + 3 * size_t(p);
+                            I = double(float(luma(__ldg(c), __ldg(c + 1), __ldg(c + 2))));
+                        } else {
+                            I = double(__ldcg(F.inten[level] + p));
+                        }
+                    }
+                    if (kJac) {
+                        const double J[6] = {cs.gs[0], cs.gs[1], cs.gs[2], y[1] * cs.gs[2] - y[2] * cs.gs[1],
+                                             y[2] * cs.gs[0] - y[0] * cs.gs[2], y[0] * cs.gs[1] - y[1] * cs.gs[0]};
+#pragma unroll
+                        for (int i = 0; i < 6; ++i)
+#pragma unroll
+                            for (int j = i; j < 6; ++j) acc[hidx(i, j)] += J[i] * J[j];
+#pragma unroll
+                        for (int i = 0; i < 6; ++i) acc[21 + i] += J[i] * r_d;
+                        acc[27] += r_d * r_d;
+                        if (kColor) {
+                            const double r_c = (cs.inten - I) * kIntensityScale;
+                            const double Jc[6] = {cs.gi[0] * kIntensityScale, cs.gi[1] * kIntensityScale,
+                                                  cs.gi[2] * kIntensityScale,
+                                                  (y[1] * cs.gi[2] - y[2] * cs.gi[1]) * kIntensityScale,
+                                                  (y[2] * cs.gi[0] - y[0] * cs.gi[2]) * kIntensityScale,
+                                                  (y[0] * cs.gi[1] - y[1] * cs.gi[0]) * kIntensityScale};
+#pragma unroll
+                            for (int i = 0; i < 6; ++i)
+#pragma unroll
+                                for (int j = i; j < 6; ++j) acc[hidx(i, j)] += cw * (Jc[i] * Jc[j]);
+#pragma unroll
+                            for (int i = 0; i < 6; ++i) acc[21 + i] += cw * (Jc[i] * r_c);
+                            acc[28] += r_c * r_c;
+                        }
+                        acc[29] += 1.0;
+                    } else {
+                        rs = float(r_d * r_d);
+                        rv = 1;
+                        if (!masked) {
+                            acc[27] += r_d * r_d;
+                            if (kColor) {
+                                const double r_c = (cs.inten - I) * kIntensityScale;
+                                acc[28] += r_c * r_c;
+                            }
+                            acc[29] += 1.0;
+                        }
+                    }
+                }
+            }
+        }
+        if (!kJac && write_res) {
+            F.res_sq[p] = rs;
+            F.res_valid[p] = rv;
+        }
+    }
+    block_reduce<kAccN>(acc, scratch, blk);
+    grid_allreduce<kAccN>(a.grid, blk, out);
+}
+
+template <bool kJac>
+__device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res,
+                                     double cw, double* scratch, double* blk, double* out) {
+    const bool color = cw > 0.0 && a.F.rgb0 != nullptr;
+    if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
+    else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
+}
+
+// ------------------------------------------------------------------ Register
+// registration.cpp:211-286. All CTAs run the same state machine on the same
+// reduced vectors; thread 0 of each CTA updates the shared state.
+__device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask, RegState& st, double* scratch,
+                             double* blk) {
+    const RegParams& R = a.reg;
+    const double cw = R.color_weight;
+    if (threadIdx.x == 0) {
+        st.pose = init;
+        st.total = 0;
+        st.converged = 0;
+        st.lost = 0;
+    }
+    __syncthreads();
+    for (int l = R.levels - 1; l >= 0; --l) {
+        const long long mv = (long long)(max(R.min_valid, 1)) >> (2 * l);
+        const double min_valid = double(mv > 16 ? mv : 16);
+        pass<true>(a, l, st.pose, use_mask, false, cw, scratch, blk, st.cur);
+        if (st.cur[29] < min_valid) {
+            if (threadIdx.x == 0) st.lost = 1;
+            __syncthreads();
+            return;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            st.lambda = R.lambda_init;
+            st.converged = 0;
+        }
+        for (int it = 0; it < R.max_iterations; ++it) {
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                ++st.total;
+                double H[36];
+                full_h(st.cur, H);
+                double dmax = H[0];
+                for (int i = 1; i < 6; ++i) dmax = fmax(dmax, H[7 * i]);
+                const double floor_v = 1e-3 * dmax + 1e-12;
+                for (int i = 0; i < 6; ++i) H[7 * i] += st.lambda * fmax(H[7 * i], floor_v);
+                double negb[6], delta[6];
+                for (int i = 0; i < 6; ++i) negb[i] = -st.cur[21 + i];
+                bool ok = ldlt6_solve(H, negb, delta);
+                for (int i = 0; i < 6 && ok; ++i) ok = isfinite(delta[i]);
+                st.ok = ok;
+                if (!ok) {
+                    st.lambda = fmin(st.lambda * R.lambda_up, 1e12);
+                } else {
+                    Pose e;
+                    expmap(delta, e);
+                    st.cand = pose_mul(e, st.pose);
+                    double dn = 0.0;
+                    for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
+                    st.trial[0] = sqrt(dn);  // stash |delta| until the pass overwrites trial
+                }
+            }
+            __syncthreads();
+            if (!st.ok) continue;
+            const double dnorm = st.trial[0];
+            __syncthreads();
+            pass<true>(a, l, st.cand, use_mask, false, cw, scratch, blk, st.trial);
+            if (threadIdx.x == 0) {
+                const double cur_err = st.cur[27] + cw * st.cur[28];
+                const double trial_err = st.trial[27] + cw * st.trial[28];
+                st.brk = 0;
+                if (st.trial[29] >= min_valid && trial_err < cur_err) {
+                    const double decrease = cur_err - trial_err;
+                    st.pose = st.cand;
+                    for (int i = 0; i < kAccN; ++i) st.cur[i] = st.trial[i];
+                    st.lambda = fmax(st.lambda / R.lambda_down, 1e-12);
+                    if (dnorm < R.eps || decrease < kRelDecreaseTol * cur_err) {
+                        st.converged = 1;
+                        st.brk = 1;
+                    }
+                } else {
+                    st.lambda = fmin(st.lambda * R.lambda_up, 1e12);
+                    if (st.lambda >= 1e12) {
+                        st.converged = 1;
+                        st.brk = 1;
+                    }
+                }
+            }
+            __syncthreads();
+            if (st.brk) break;
+        }
+        __syncthreads();
+    }
+    // Full-resolution residual image at the final pose, mask ignored (:282-284).
+    pass<false>(a, 0, st.pose, false, true, 0.0, scratch, blk, st.trial);
+}
+
+// ------------------------------------------------------------------ mask
+// Separable square morphology (dynamics_mask.cpp:22-47): the square window
+// factors into a row pass and a column pass; out-of-image pixels are off.
+__device__ void morph_pass(const uint8_t* src, uint8_t* dst, int w, int h, int r, bool erode, bool rows) {
+    const int stride = gridDim.x * blockDim.x;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) {
+        const int x = p % w, y = p / w;
+        bool val = erode;
+        for (int o = -r; o <= r; ++o) {
+            const int nx = rows ? x + o : x, ny = rows ? y : y + o;
+            const bool on = nx >= 0 && nx < w && ny >= 0 && ny < h && __ldcg(src + ny * w + nx) != 0;
+            if (erode && !on) {
+                val = false;
+                break;
+            }
+            if (!erode && on) {
+                val = true;
+                break;
+            }
+        }
+        dst[p] = val ? 1 : 0;
+    }
+}
+
+constexpr int kFfW = 32, kFfH = 8;  // floodfill tile (256 threads, 1 px each)
+
+// FloodfillDepth (dynamics_mask.cpp:59-96) as the least fixpoint of the
+// growth rule: tile-local shared-memory sweeps until stable, global rounds
+// until no tile changes. Returns the number of global rounds.
+__device__ int floodfill(const TrackArgs& a, uint8_t* m, const float* depth, int w, int h, double theta, int conn,
+                         double* blk, double* red) {
+    __shared__ uint8_t sm[(kFfH + 2) * (kFfW + 2)];
+    __shared__ float sd[(kFfH + 2) * (kFfW + 2)];
+    const int ntx = (w + kFfW - 1) / kFfW, nty = (h + kFfH - 1) / kFfH;
+    const int lx = threadIdx.x % kFfW, ly = threadIdx.x / kFfW;
+    constexpr int SW = kFfW + 2;
+    const int me = (ly + 1) * SW + (lx + 1);
+    const int offs[8] = {1, -1, SW, -SW, SW + 1, -SW + 1, SW - 1, -SW - 1};  // kDx/kDy order
+    int rounds = 0;
+    while (true) {
+        int changed_cta = 0;
+        for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
+            const int x0 = (t % ntx) * kFfW - 1, y0 = (t / ntx) * kFfH - 1;
+            for (int i = threadIdx.x; i < (kFfH + 2) * SW; i += blockDim.x) {
+                const int gx = x0 + i % SW, gy = y0 + i / SW;
+                const bool in = gx >= 0 && gx < w && gy >= 0 && gy < h;
+                sm[i] = in ? __ldcg(m + gy * w + gx) : 0;
+                sd[i] = in ? __ldg(depth + gy * w + gx) : 0.f;
+            }
+            __syncthreads();
+            const int gx = x0 + 1 + lx, gy = y0 + 1 + ly;
+            const bool inb = gx < w && gy < h;
+            const uint8_t initial = sm[me];
+            const float dn = sd[me];
+            const bool cand = inb && depth_valid(dn);
+            while (true) {
+                int ch = 0;
+                if (cand && !sm[me]) {
+                    for (int k = 0; k < conn; ++k) {
+                        const int nb = me + offs[k];
+                        const float dp = sd[nb];
+                        if (sm[nb] && depth_valid(dp) && fabs(double(dp) - double(dn)) < theta * double(dp)) {
+                            sm[me] = 1;
+                            ch = 1;
+                            break;
+                        }
+                    }
+                }
+                if (!__syncthreads_or(ch)) break;
+            }
+            if (inb && sm[me] != initial) {
+                m[gy * w + gx] = 1;
+                changed_cta = 1;
+            }
+            __syncthreads();
+        }
+        const int any = __syncthreads_or(changed_cta);
+        if (threadIdx.x == 0) blk[0] = any ? 1.0 : 0.0;
+        __syncthreads();
+        grid_allreduce<1>(a.grid, blk, red);
+        ++rounds;
+        if (red[0] == 0.0) break;
+    }
+    return rounds;
+}
+
+// BuildMask (dynamics_mask.cpp:98-104) on the full-resolution residual image.
+// Stages: bit0 threshold, bit1 erode, bit2 floodfill, bit3 dilate. The result
+// lands in F.mask[0]; returns the masked-pixel count (CountMasked).
+__device__ double build_mask(const TrackArgs& a, int stages, double* blk, double* red, int* rounds) {
+    const FrameView& F = a.F;
+    const int w = F.K[0].w, h = F.K[0].h;
+    const int stride = gridDim.x * blockDim.x;
+    const MaskParams& M = a.mp;
+    uint8_t* cur = F.mwork[0];
+    if (stages & 1) {  // ThresholdResiduals (dynamics_mask.cpp:9-18)
+        const double thr = M.gamma * M.truncation * M.truncation;
+        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride)
+            cur[p] = (__ldcg(F.res_valid + p) && double(__ldcg(F.res_sq + p)) > thr) ? 1 : 0;
+        grid_barrier(a.grid);
+    }
+    if ((stages & 2) && M.erode_radius > 0) {
+        morph_pass(cur, F.mwork[1], w, h, M.erode_radius, true, true);
+        grid_barrier(a.grid);
+        morph_pass(F.mwork[1], F.mwork[2], w, h, M.erode_radius, true, false);
+        grid_barrier(a.grid);
+        cur = F.mwork[2];
+    }
+    *rounds = 0;
+    if (stages & 4) *rounds = floodfill(a, cur, F.depth0, w, h, M.theta, M.connectivity, blk, red);
+    if ((stages & 8) && M.dilate_radius > 0) {
+        uint8_t* tmp = (cur == F.mwork[1]) ? F.mwork[0] : F.mwork[1];
+        morph_pass(cur, tmp, w, h, M.dilate_radius, false, true);
+        grid_barrier(a.grid);
+        morph_pass(tmp, F.mask[0], w, h, M.dilate_radius, false, false);
+    } else {
+        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) F.mask[0][p] = __ldcg(cur + p);
+    }
+    grid_barrier(a.grid);
+    double cnt = 0.0;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) cnt += __ldcg(F.mask[0] + p) ? 1.0 : 0.0;
+    double v[1] = {cnt};
+    block_reduce<1>(v, blk + 8, blk);
+    grid_allreduce<1>(a.grid, blk, red);
+    return red[0];
+}
+
+__device__ void write_out(const TrackArgs& a, const RegState& st) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int i = 0; i < 9; ++i) a.out->pose[i] = st.pose.R[i];
+        for (int i = 0; i < 3; ++i) a.out->pose[9 + i] = st.pose.t[i];
+    }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kTrackThreads, 2) k_track(TrackArgs a) {
+    __shared__ RegState st;
+    __shared__ double scratch[(kTrackThreads / 32) * kAccN];
+    __shared__ double blk[kAccN + 2];
+    __shared__ double red[kAccN + 2];
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+
+    if (a.mode == kModeLinearize || a.mode == kModeEvalDepth || a.mode == kModeEvalColor) {
+        Pose P;
+        for (int i = 0; i < 9; ++i) P.R[i] = a.pose_state[i];
+        for (int i = 0; i < 3; ++i) P.t[i] = a.pose_state[9 + i];
+        if (a.mode == kModeLinearize)
+            pass<true>(a, 0, P, a.use_mask, false, a.reg.color_weight, scratch, blk, red);
+        else if (a.mode == kModeEvalDepth)
+            pass<false>(a, 0, P, a.use_mask, true, 0.0, scratch, blk, red);
+        else
+            pass<false>(a, 0, P, a.use_mask, false, 1.0, scratch, blk, red);
+        if (lead)
+            for (int i = 0; i < kAccN; ++i) a.out->acc[i] = red[i];
+        return;
+    }
+    if (a.mode == kModeMask) {
+        int rounds = 0;
+        const double cnt = build_mask(a, a.mask_stages, blk, red, &rounds);
+        if (lead) {
+            a.out->masked = (unsigned long long)cnt;
+            a.out->rounds = rounds;
+        }
+        return;
+    }
+
+    Pose init;
+    for (int i = 0; i < 9; ++i) init.R[i] = a.pose_state[i];
+    for (int i = 0; i < 3; ++i) init.t[i] = a.pose_state[9 + i];
+    const bool masked_reg = a.mode == kModeRegister && a.use_mask;
+    build_pyramid(a, true, masked_reg);
+    run_register(a, init, masked_reg, st, scratch, blk);
+
+    if (a.mode == kModeRegister) {
+        if (lead) {
+            a.out->lost = st.lost;
+            a.out->converged = st.converged;
+            a.out->iterations = st.total;
+            a.out->registrations = 1;
+            a.out->valid = (unsigned long long)st.cur[29];
+            a.out->final_error = st.cur[27] + a.reg.color_weight * st.cur[28];
+            for (int i = 0; i < kAccN; ++i) a.out->acc[i] = st.cur[i];
+        }
+        write_out(a, st);
+        return;
+    }
+
+    // kModeFrame: pipeline.cpp:79-122 (tracking part).
+    int registrations = 0, iterations = 0, rounds = 0;
+    double masked = 0.0;
+    if (!st.lost) {
+        registrations = 1;
+        iterations = st.total;
+        if (a.dynamics) {
+            masked = build_mask(a, 15, blk, red, &rounds);
+            if (masked > 0.0) {
+                Pose p1 = st.pose;
+                build_pyramid(a, false, true);
+                __syncthreads();
+                run_register(a, p1, true, st, scratch, blk);
+                if (!st.lost) {
+                    registrations = 2;
+                    iterations += st.total;
+                }
+            }
+        }
+    }
+    if (lead) {
+        TrackOut* o = a.out;
+        o->lost = st.lost;
+        o->registrations = registrations;
+        o->iterations = iterations;
+        o->masked = (unsigned long long)masked;
+        o->rounds = rounds;
+        o->converged = st.lost ? 0 : st.converged;
+        o->valid = st.lost ? 0ull : (unsigned long long)st.cur[29];
+        o->final_error = st.lost ? 0.0 : st.cur[27] + a.reg.color_weight * st.cur[28];
+        if (!st.lost) {  // hold the previous pose on loss (pipeline.cpp:117-122)
+            for (int i = 0; i < 9; ++i) a.pose_state[i] = st.pose.R[i];
+            for (int i = 0; i < 3; ++i) a.pose_state[9 + i] = st.pose.t[i];
+        }
+        for (int i = 0; i < 12; ++i) o->pose[i] = a.pose_state[i];
+        if (a.vol_counters) {  // frame bookkeeping for the allocate / cull / fuse launches that follow
+            a.vol_counters[kBlocksBefore] = a.vol_counters[kNumBlocks];
+            a.vol_counters[kVisible] = 0;
+            a.vol_counters[kDdaVisits] = 0;
+        }
+    }
+}
+
+}  // namespace rfb

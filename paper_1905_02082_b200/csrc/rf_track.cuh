@@ -1,0 +1,73 @@
+// Direct SDF + colour tracking (registration.cpp) and the dynamics mask
+// (dynamics_mask.cpp) as device phases of one persistent cooperative kernel.
+#pragma once
+
+#include "rf_grid.cuh"
+
+namespace rfb {
+
+constexpr int kMaxLevels = 6;
+constexpr int kTrackThreads = 256;
+constexpr int kTileW = 16, kTileH = 16;  // pixel tile per CTA step (256 px)
+
+struct RegParams {  // RegistrationConfig, registration.hpp:13-23
+    double color_weight;
+    int levels, max_iterations;
+    double lambda_init, lambda_up, lambda_down, eps;
+    int min_valid;
+};
+
+struct MaskParams {  // MaskConfig, dynamics_mask.hpp:10-17
+    double gamma, truncation, theta;
+    int erode_radius, dilate_radius, connectivity;
+};
+
+// Device images of one frame and its pyramid. Level 0 depth/rgb are the
+// inputs; coarser levels are built in-kernel.
+struct FrameView {
+    const float* depth0;
+    const uint8_t* rgb0;      // may be null (no colour)
+    float* depth[kMaxLevels]; // [0] unused
+    float* inten[kMaxLevels]; // [0] unused (computed from rgb0 on the fly)
+    uint8_t* mask[kMaxLevels];// [0] = mask used by masked registration
+    Intr K[kMaxLevels];
+    float* res_sq;            // full-resolution residual image
+    uint8_t* res_valid;
+    uint8_t* mwork[3];        // mask build scratch
+};
+
+struct TrackOut {
+    double pose[12];
+    int32_t lost, converged, registrations, iterations;
+    unsigned long long valid, masked;
+    double final_error;
+    double acc[kAccN];  // last accumulation (linearize/evaluate entry points)
+    int32_t rounds;     // floodfill rounds (diagnostic)
+    int32_t pad;
+};
+
+enum TrackMode : int {
+    kModeFrame = 0,      // pyramid, register, mask, register under mask (pipeline.cpp:81-99)
+    kModeRegister = 1,   // pyramid + one Register with optional mask
+    kModeLinearize = 2,  // one Jacobian pass at level 0 (Linearize)
+    kModeEvalDepth = 3,  // value pass at level 0 writing residuals (EvaluateDepthError)
+    kModeEvalColor = 4,  // value pass at level 0, colour error (EvaluateColorError)
+    kModeMask = 5,       // BuildMask stages on given residuals
+};
+
+struct TrackArgs {
+    int mode;
+    int use_mask;        // kModeRegister/Linearize/Eval: mask[0] is valid
+    int dynamics;        // kModeFrame: build mask + second registration
+    int mask_stages;     // kModeMask: bit0 threshold, bit1 erode, bit2 floodfill, bit3 dilate
+    VolumeView V;
+    FrameView F;
+    RegParams reg;
+    MaskParams mp;
+    GridCtx grid;
+    double* pose_state;  // in: initial pose; out: tracked pose (kModeFrame/Register)
+    TrackOut* out;
+    uint32_t* vol_counters;  // kModeFrame: snapshot kNumBlocks -> kBlocksBefore
+};
+
+}  // namespace rfb

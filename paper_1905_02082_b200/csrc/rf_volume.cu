@@ -1,0 +1,271 @@
+// Sparse-volume kernels: ray-segment brick allocation into the open-addressed
+// hash, frustum culling into a compacted visible-brick list, and one fused
+// carve+integrate sweep per visible 8^3 brick (one thread per voxel, the brick
+// read and written once, coalesced 8-byte voxels).
+#include "rf_volume.cuh"
+
+namespace rfb {
+
+// ---------------------------------------------------------------- allocation
+// AllocateForFrame + WalkGridSegment (tsdf_volume.cpp:93-113,
+// tsdf_volume.hpp:149-185), one thread per pixel, all cells inserted with
+// atomicCAS. The set of inserted keys, and so the occupied-slot set of the
+// linear-probing table, is independent of thread order.
+__global__ void k_alloc(AllocArgs a) {
+    if (a.lost && *a.lost) return;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const int w = a.K.w, h = a.K.h;
+    unsigned visits = 0;
+    if (p < w * h) {
+        const int u = p % w, v = p / w;
+        const float d = __ldg(a.depth + p);
+        const bool masked = a.mask && __ldg(a.mask + p);
+        if (depth_valid(d) && !(d < a.V.min_depth) && !(d > a.V.max_depth) && !masked) {
+            Pose P;
+            for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = __ldg(a.pose + i);
+            const double tau = a.V.truncation;
+            const double ext = double(kSide) * a.V.voxel_size;  // block_extent(), tsdf_volume.hpp:123
+            const double dir0 = (double(u) - a.K.cx) / a.K.fx, dir1 = (double(v) - a.K.cy) / a.K.fy;
+            const double z0 = fmax(double(d) - tau, 1e-4);
+            const double z1 = double(d) + tau;
+            double w0[3], w1[3];
+            pose_apply(P, z0 * dir0, z0 * dir1, z0 * 1.0, w0);
+            pose_apply(P, z1 * dir0, z1 * dir1, z1 * 1.0, w1);
+            const double p0[3] = {w0[0] / ext, w0[1] / ext, w0[2] / ext};
+            const double p1[3] = {w1[0] / ext, w1[1] / ext, w1[2] / ext};
+            int cell[3], end[3], step[3];
+            double tmax[3], tdel[3];
+            for (int i = 0; i < 3; ++i) {
+                const double dd = p1[i] - p0[i];
+                cell[i] = int(floor(p0[i]));
+                end[i] = int(floor(p1[i]));
+                step[i] = 0;
+                tmax[i] = tdel[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+                if (dd > 0) {
+                    step[i] = 1;
+                    tmax[i] = (floor(p0[i]) + 1.0 - p0[i]) / dd;
+                    tdel[i] = 1.0 / dd;
+                } else if (dd < 0) {
+                    step[i] = -1;
+                    tmax[i] = (p0[i] - floor(p0[i])) / -dd;
+                    tdel[i] = 1.0 / -dd;
+                }
+            }
+            const int max_steps = abs(end[0] - cell[0]) + abs(end[1] - cell[1]) + abs(end[2] - cell[2]) + 3;
+            hash_insert(a.V, cell[0], cell[1], cell[2]);
+            ++visits;
+            for (int n = 0; n < max_steps && (cell[0] != end[0] || cell[1] != end[1] || cell[2] != end[2]); ++n) {
+                int axis = 0;
+                if (tmax[1] < tmax[axis]) axis = 1;
+                if (tmax[2] < tmax[axis]) axis = 2;
+                if (tmax[axis] > 1.0) break;
+                tmax[axis] += tdel[axis];
+                cell[axis] += step[axis];
+                hash_insert(a.V, cell[0], cell[1], cell[2]);
+                ++visits;
+            }
+        }
+    }
+    // warp-aggregated visit counter (for the algorithmic-bytes model)
+    for (int o = 16; o > 0; o >>= 1) visits += __shfl_down_sync(0xffffffffu, visits, o);
+    if ((threadIdx.x & 31) == 0 && visits) atomicAdd(&a.V.counters[kDdaVisits], visits);
+}
+
+// Explicit AllocateBlock (tsdf_volume.cpp:64-77) for a batch of coordinates.
+__global__ void k_alloc_coords(VolumeView V, const int* coords, int n, int* created) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = hash_insert(V, coords[3 * i], coords[3 * i + 1], coords[3 * i + 2]);
+    if (created) created[i] = r;
+}
+
+// ---------------------------------------------------------------- culling
+// BlockOutsideFrustum (tsdf_volume.cpp:119-151) for every allocated brick,
+// evaluated once for the carve bound (carve_clip) and the integrate bound
+// (max_depth + truncation). Visible bricks are appended with their flags.
+__device__ __forceinline__ bool outside(const double cc[8][3], const Intr& K, double max_z) {
+    bool any_behind = false;
+    double min_z = __longlong_as_double(0x7ff0000000000000ll);
+    for (int c = 0; c < 8; ++c) {
+        if (cc[c][2] <= 1e-9) any_behind = true;
+        min_z = fmin(min_z, cc[c][2]);
+    }
+    if (min_z > max_z) return true;
+    if (any_behind) {
+        for (int c = 0; c < 8; ++c)
+            if (cc[c][2] > 1e-9) return false;
+        return true;
+    }
+    double min_u = __longlong_as_double(0x7ff0000000000000ll), max_u = -min_u, min_v = min_u, max_v = -min_u;
+    for (int c = 0; c < 8; ++c) {
+        const double pu = K.fx * cc[c][0] / cc[c][2] + K.cx;
+        const double pv = K.fy * cc[c][1] / cc[c][2] + K.cy;
+        min_u = fmin(min_u, pu);
+        max_u = fmax(max_u, pu);
+        min_v = fmin(min_v, pv);
+        max_v = fmax(max_v, pv);
+    }
+    return max_u < -0.5 || min_u > K.w - 0.5 || max_v < -0.5 || min_v > K.h - 0.5;
+}
+
+__global__ void k_cull(CullArgs a) {
+    if (a.lost && *a.lost) return;
+    const uint32_t nb = min(a.V.counters[kNumBlocks], a.V.max_blocks);
+    const uint32_t before = a.carve_only_before ? min(a.V.counters[kBlocksBefore], nb) : nb;
+    Pose P;
+    for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = __ldg(a.pose + i);
+    const Pose W = pose_inverse(P);
+    const double ext = double(kSide) * a.V.voxel_size;
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+        const int4 c = a.V.coords[b];
+        double cc[8][3];
+        for (int k = 0; k < 8; ++k) {
+            const double x = (double(c.x) + double(k & 1)) * ext;
+            const double y = (double(c.y) + double((k >> 1) & 1)) * ext;
+            const double z = (double(c.z) + double(k >> 2)) * ext;
+            pose_apply(W, x, y, z, cc[k]);
+        }
+        uint32_t flags = 0;
+        if (a.do_carve && b < before && !outside(cc, a.K, a.V.carve_clip)) flags |= kFlagCarve;
+        if (a.do_integrate && !outside(cc, a.K, a.V.max_depth + a.V.truncation)) flags |= kFlagIntegrate;
+        if (flags) {
+            const uint32_t slot = atomicAdd(&a.V.counters[kVisible], 1u);
+            a.list[slot] = b | flags;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- fusion
+// CarveFreeSpace (tsdf_volume.cpp:204-241) then Integrate (:155-202) applied
+// voxel by voxel inside one brick; the sdf is rounded to f32 between the two
+// updates exactly as the sequential reference stores it.
+__global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
+    if (a.lost && *a.lost) return;
+    __shared__ Pose W;
+    if (threadIdx.x == 0) {
+        Pose P;
+        for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = a.pose[i];
+        W = pose_inverse(P);
+    }
+    __syncthreads();
+    const uint32_t nvis = a.V.counters[kVisible];
+    const int x = threadIdx.x & 7, y = (threadIdx.x >> 3) & 7, z = threadIdx.x >> 6;
+    const double s = a.V.voxel_size, tau = a.V.truncation;
+    const int cw = a.V.carve_weight, mw = a.V.max_weight;
+    for (uint32_t i = blockIdx.x; i < nvis; i += gridDim.x) {
+        const uint32_t e = __ldcg(a.list + i);
+        const uint32_t b = e & kIndexMask;
+        const int4 c = a.V.coords[b];
+        const double cx = (double(c.x * kSide + x) + 0.5) * s;  // VoxelCenter, tsdf_volume.hpp:117-119
+        const double cy = (double(c.y * kSide + y) + 0.5) * s;
+        const double cz = (double(c.z * kSide + z) + 0.5) * s;
+        double pc[3];
+        pose_apply(W, cx, cy, cz, pc);
+        if (!(pc[2] <= 1e-9)) {
+            const double pu_d = a.K.fx * pc[0] / pc[2] + a.K.cx;  // Project, geometry.hpp:46-48
+            const double pv_d = a.K.fy * pc[1] / pc[2] + a.K.cy;
+            const long pu = lround(pu_d), pv = lround(pv_d);
+            if (pu >= 0 && pu < a.K.w && pv >= 0 && pv < a.K.h) {
+                const int pix = int(pv) * a.K.w + int(pu);
+                const float d = __ldg(a.depth + pix);
+                Voxel* vp = a.V.voxels + size_t(b) * kBrickVoxels + threadIdx.x;
+                uint2 raw = *reinterpret_cast<uint2*>(vp);
+                float sdf = __uint_as_float(raw.x);
+                uint32_t wgt = raw.y & 0xFFu, r = (raw.y >> 8) & 0xFFu, g = (raw.y >> 16) & 0xFFu,
+                         bl = raw.y >> 24;
+                bool dirty = false;
+                if ((e & kFlagCarve) && pc[2] < a.V.carve_clip && depth_valid(d) && !(pc[2] >= double(d) - tau)) {
+                    const double w = double(wgt);
+                    sdf = float((double(sdf) * w + tau * cw) / (w + cw));
+                    wgt = min(wgt + uint32_t(cw), uint32_t(mw));
+                    dirty = true;
+                }
+                if ((e & kFlagIntegrate) && !(a.mask && __ldg(a.mask + pix)) && depth_valid(d) &&
+                    !(d < a.V.min_depth) && !(d > a.V.max_depth)) {
+                    const double dist = double(d) - pc[2];
+                    if (!(dist <= -tau)) {
+                        const double clamped = fmin(dist, tau);
+                        const double w = double(wgt);
+                        sdf = float((double(sdf) * w + clamped) / (w + 1.0));
+                        if (fabs(dist) <= tau && a.rgb) {
+                            const uint8_t* col = a.rgb + 3 * size_t(pix);
+                            r = uint32_t(lround((double(r) * w + double(__ldg(col))) / (w + 1.0)));
+                            g = uint32_t(lround((double(g) * w + double(__ldg(col + 1))) / (w + 1.0)));
+                            bl = uint32_t(lround((double(bl) * w + double(__ldg(col + 2))) / (w + 1.0)));
+                        }
+                        wgt = min(wgt + 1u, uint32_t(mw));
+                        dirty = true;
+                    }
+                }
+                if (dirty) {
+                    raw.x = __float_as_uint(sdf);
+                    raw.y = (wgt & 0xFFu) | ((r & 0xFFu) << 8) | ((g & 0xFFu) << 16) | ((bl & 0xFFu) << 24);
+                    *reinterpret_cast<uint2*>(vp) = raw;
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- sampling
+// Batch of SampleSdf / SampleIntensity / *WithGradient / SampleSdfGradient.
+__global__ void k_sample(VolumeView V, const double* pts, int n, int mode, double* value, double* grad,
+                         uint8_t* valid) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    CellSample cs;
+    bool ok;
+    double val = 0.0, g[3] = {0, 0, 0};
+    if (mode == 4) {  // central differences, tsdf_volume.cpp:358-373
+        ok = true;
+        const double s = V.voxel_size;
+        for (int axis = 0; axis < 3 && ok; ++axis) {
+            double hi[3] = {p[0], p[1], p[2]}, lo[3] = {p[0], p[1], p[2]};
+            hi[axis] = p[axis] + s;
+            lo[axis] = p[axis] - s;
+            CellSample a, b;
+            ok = sample_point<false, false>(V, hi, a) && sample_point<false, false>(V, lo, b);
+            if (ok) g[axis] = (a.sdf - b.sdf) / (2.0 * s);
+        }
+        if (ok) {
+            sample_point<false, false>(V, p, cs);
+            val = cs.sdf;
+        }
+    } else if (mode >= 2) {
+        ok = sample_point<true, true>(V, p, cs);
+        if (ok) {
+            val = mode == 2 ? cs.sdf : cs.inten;
+            for (int k = 0; k < 3; ++k) g[k] = mode == 2 ? cs.gs[k] : cs.gi[k];
+        }
+    } else {
+        ok = sample_point<false, true>(V, p, cs);
+        if (ok) val = mode == 0 ? cs.sdf : cs.inten;
+    }
+    value[i] = ok ? val : 0.0;
+    if (grad)
+        for (int k = 0; k < 3; ++k) grad[3 * i + k] = ok ? g[k] : 0.0;
+    valid[i] = ok;
+}
+
+// ---------------------------------------------------------------- host mirror support
+// Voxel access through VoxelHandle semantics (tsdf_volume.cpp:79-87).
+__global__ void k_voxel_rw(VolumeView V, const int* vc, int n, Voxel* io, uint8_t* found, int write) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int x = vc[3 * i], y = vc[3 * i + 1], z = vc[3 * i + 2];
+    const uint32_t b = hash_find(V, x >> 3, y >> 3, z >> 3);
+    if (found) found[i] = b != kInvalid;
+    if (b == kInvalid) return;
+    Voxel* v = V.voxels + size_t(b) * kBrickVoxels + (((z & 7) * 8 + (y & 7)) * 8 + (x & 7));
+    if (write) *v = io[i];
+    else io[i] = *v;
+}
+
+// Occupied-slot bitmap (for bit-exact hash-occupancy parity).
+__global__ void k_occupancy(VolumeView V, uint8_t* bitmap) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= V.hash_mask; i += gridDim.x * blockDim.x)
+        bitmap[i] = V.slots[i].key != kEmptyKey;
+}
+
+}  // namespace rfb
