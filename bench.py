@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""bench.py — ReFusion per-frame hot path on B200.
+
+metric : frames/s of Pipeline::ProcessFrame (track + mask + carve + allocate +
+         integrate, pipeline.cpp:57-131) at 640x480 with 1 cm voxels.
+workload: BASELINE.json configs[1] ("C2"): the acceptance room with two moving
+         boxes, 200 frames at 30 Hz, replayed forwards then backwards (a
+         continuous ping-pong sequence) so any step count keeps tracking.
+         Frames are synthetic, rendered on the GPU before timing.
+One step = one ProcessFrame on one frame.
+
+Arms:
+  default          : our CUDA path through the C ABI. `value` = frames/s with
+                     the frames already resident in HBM (CUDA events on the
+                     pipeline's stream, max over ranks); `e2e` = the same through
+                     rf_pipeline_process_frame with pinned HOST buffers (H2D of
+                     depth+RGB and the D2H of stats+pose inside the timed loop).
+  --impl reference : the reference algorithm on the host CPU (the oracle
+                     restatement, all host threads; the C++ reference itself
+                     cannot be built here — DESIGN.md §Oracle).
+Multi-GPU (torchrun): independent sequences per GPU (replicas, no collective).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec (track+integrate, 640x480, 1cm voxels) per B200 + HBM roofline frac"
+UNIT = "frames/s"
+CONFIG = "C2"
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def seq_index(step, n):
+    """Ping-pong through the n rendered frames: 0..n-1, n-2..1, 0.."""
+    period = 2 * n - 2
+    i = step % period
+    return i if i < n else period - i
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 7:
+                for n, v in zip(names, r[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_1905_02082_b200 import _lib as L
+    from paper_1905_02082_b200 import api, scenes, synth
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = L.load()
+    cfgd = scenes.BENCH_CONFIGS[CONFIG]
+    seed = cfgd["seed"] + rank  # independent sequence per replica
+    scene = synth.parse(scenes.bench_script(dynamic=cfgd["dynamic"], frames=cfgd["frames"], seed=seed))
+    k = scene.intrinsics
+    H, W, F = k.height, k.width, len(scene)
+    depth = torch.empty((F, H, W), dtype=torch.float32, device="cuda")
+    rgb = torch.empty((F, H, W, 3), dtype=torch.uint8, device="cuda")
+    labels = torch.empty((F, H, W), dtype=torch.uint8, device="cuda")
+    for i in range(F):
+        synth.render(scene, i, depth[i], rgb[i], labels[i], device=local)
+    torch.cuda.synchronize()
+    depth_h = depth.cpu().pin_memory()
+    rgb_h = rgb.cpu().pin_memory()
+
+    cfg = api.pipeline_config(refine=False)
+
+    def make_frames(dev_resident):
+        frames = []
+        for i in range(F):
+            f = L.rf_frame()
+            f.intrinsics = k
+            if dev_resident:
+                f.depth, f.rgb, f.memory = depth[i].data_ptr(), rgb[i].data_ptr(), L.RF_MEMORY_DEVICE
+            else:
+                f.depth, f.rgb, f.memory = depth_h[i].data_ptr(), rgb_h[i].data_ptr(), L.RF_MEMORY_HOST
+            frames.append(f)
+        return frames
+
+    def run_steps(p, frames, start, n, stats, pose, record=None):
+        for s in range(start, start + n):
+            f = frames[seq_index(s, F)]
+            f.timestamp = s / 30.0
+            code = lib.rf_pipeline_process_frame(p.h, C.byref(f), C.byref(stats), pose)
+            if code != 0:
+                L.check(code)
+            if record is not None:
+                record(p)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    stats = L.rf_frame_stats()
+    pose = (C.c_double * 12)()
+
+    # ---- value: frames resident in HBM, device time on the pipeline's stream
+    pv = api.Pipeline(cfg, device=local)
+    dev_frames = make_frames(True)
+    run_steps(pv, dev_frames, 0, args.warmup, stats, pose)
+    sptr = C.c_void_p()
+    L.check(lib.rf_pipeline_stream(pv.h, C.byref(sptr)))
+    stream = torch.cuda.ExternalStream(sptr.value)
+    L.check(lib.rf_pipeline_set_profiling(pv.h, 1))
+    launches0 = C.c_uint64()
+    L.check(lib.rf_pipeline_stage_times(pv.h, None, None, C.byref(launches0)))
+    agg = {"lost": 0, "iters": 0, "regs": 0, "masked": 0}
+
+    def record(p):  # FrameStats of the step (host fields only, no device traffic)
+        agg["lost"] += stats.tracking_lost
+        agg["iters"] += stats.iterations
+        agg["regs"] += stats.registrations
+        agg["masked"] += stats.masked_pixels
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        run_steps(pv, dev_frames, args.warmup, args.steps, stats, pose, record)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    stage = (C.c_double * 4)()
+    nprof = C.c_uint64()
+    launches1 = C.c_uint64()
+    L.check(lib.rf_pipeline_stage_times(pv.h, stage, C.byref(nprof), C.byref(launches1)))
+    gpu_launches = launches1.value - launches0.value
+    sums = L.rf_frame_counters()
+    L.check(lib.rf_pipeline_profile_counters(pv.h, C.byref(sums)))
+    agg.update(pixel_passes=sums.pixel_passes, visible=sums.visible_bricks, dda=sums.dda_visits,
+               new=sums.new_blocks)
+    num_blocks = pv.volume().num_blocks()
+
+    # ---- e2e: host pinned frames through the C ABI, wall clock
+    pe = api.Pipeline(cfg, device=local)
+    host_frames = make_frames(False)
+    run_steps(pe, host_frames, 0, args.warmup, stats, pose)
+    barrier()
+    t0 = time.perf_counter()
+    run_steps(pe, host_frames, args.warmup, args.steps, stats, pose)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+
+    # ---- max over ranks
+    t = torch.tensor([ms / 1000.0, e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec, e2e_sec = float(t[0]), float(t[1])
+    value = world * args.steps / sec
+    e2e = world * args.steps / e2e_sec
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (SURVEY §8d bytes model)
+    n = args.steps
+    P0 = W * H
+    stage_ms = [stage[i] / max(1, nprof.value) for i in range(4)]
+    bytes_per_frame = {
+        # B_track = sum_passes 9*P_l + 4096*U (U ~ the frame's visible bricks)
+        "track": 9.0 * agg["pixel_passes"] / n + 4096.0 * agg["visible"] / n,
+        # B_alloc = 5*P0 + 16*R_visits + 4096*N_new
+        "allocate": 5.0 * P0 + 16.0 * agg["dda"] / n + 4096.0 * agg["new"] / n,
+        # cull reads 16 B of coordinates per allocated brick
+        "cull": 16.0 * num_blocks,
+        # B_carve+int = 2*4096*|visible| + 7*P0 (depth + colour gathers)
+        "fuse": 2.0 * 4096.0 * agg["visible"] / n + 7.0 * P0,
+    }
+    names = ["track", "allocate", "cull", "fuse"]
+    dom = max(range(4), key=lambda i: stage_ms[i])
+    peak, peak_kind = measured_peaks()
+    achieved = bytes_per_frame[names[dom]] / (stage_ms[dom] / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(names[dom])
+    except Exception:
+        pass
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": n,
+        "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / n, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (GPU-rendered acceptance room + 2 moving boxes, depth noise 0.001*z^2)",
+        "config": {"workload": f"{CONFIG}: synthetic room with 2 moving boxes, 640x480 RGB-D, 1 cm voxels, "
+                               f"200-frame ping-pong sequence, refine_depth off",
+                   "resolution": [W, H], "voxel_size": 0.01, "frames_in_sequence": F,
+                   "parallelism": f"replicas x{world} (independent sequences, no collective)",
+                   "l2": "working set (~20k bricks, 80 MB) L2-resident by design; frames > L2 in total"},
+        "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": P0 * 4 + P0 * 3,
+                "d2h_bytes_per_step": 192 + 32},
+        "gpu_launches": int(gpu_launches),
+        "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 2), "peak": peak,
+                     "peak_source": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 5),
+                     "traffic": traffic, "bytes_per_launch": round(bytes_per_frame[names[dom]]),
+                     "launch_ms": round(stage_ms[dom], 5)},
+        "stages_ms_per_frame": {nm: round(stage_ms[i], 5) for i, nm in enumerate(names)},
+        "workload_stats": {"lm_iterations_per_frame": agg["iters"] / n, "registrations_per_frame": agg["regs"] / n,
+                           "masked_pixels_per_frame": agg["masked"] / n, "lost_frames": agg["lost"],
+                           "visible_bricks_per_frame": agg["visible"] / n, "bricks": num_blocks,
+                           "pixel_passes_per_frame": agg["pixel_passes"] / n},
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(depth_h, rgb_h, k, args.cpu_sample_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def oracle_rate(depth_list, rgb_list, k, budget_s, threads, max_frames=None):
+    """Oracle pipeline over a frame sample: bootstrap on frame 0 (untimed, as
+    the reference's fps excludes frame 0), then time frames until budget_s."""
+    from oracle import oracle as O
+
+    ok = O.OIntr(k.fx, k.fy, k.cx, k.cy, k.width, k.height, k.depth_scale)
+    p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads)))
+    p.process_frame(depth_list(0), rgb_list(0), ok, 0.0)
+    spent, n = 0.0, 0
+    while spent < budget_s and (max_frames is None or n < max_frames):
+        i = n + 1
+        t0 = time.perf_counter()
+        p.process_frame(depth_list(i), rgb_list(i), ok, i / 30.0)
+        spent += time.perf_counter() - t0
+        n += 1
+    return n / spent, n, spent
+
+
+def cpu_baseline(depth_h, rgb_h, k, budget_s):
+    threads = os.cpu_count() or 1
+    F = depth_h.shape[0]
+    rate, n, spent = oracle_rate(lambda i: depth_h[seq_index(i, F)].numpy(), lambda i: rgb_h[seq_index(i, F)].numpy(),
+                                 k, budget_s, threads)
+    return {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle ProcessFrame on frames 1..{n} of the same {CONFIG} sequence ({spent:.1f} s, "
+                      f"{threads} threads for integrate/carve and registration)"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_1905_02082_b200 import scenes
+
+    cfgd = scenes.BENCH_CONFIGS[CONFIG]
+    scene = O.Scene(scenes.bench_script(dynamic=cfgd["dynamic"], frames=cfgd["frames"], seed=cfgd["seed"]))
+    F = len(scene)
+    cache = {}
+
+    def frame(i):
+        j = seq_index(i, F)
+        if j not in cache:
+            cache[j] = scene.render(j)
+        return cache[j]
+
+    threads = os.cpu_count() or 1
+    k = scene.k
+    p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads)))
+    for i in range(args.warmup):
+        f = frame(i)
+        p.process_frame(f["depth"], f["rgb"], k, i / 30.0)
+    for i in range(args.warmup, args.warmup + args.steps):  # render outside the timed loop
+        frame(i)
+    t0 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + args.steps):
+        f = frame(i)
+        p.process_frame(f["depth"], f["rgb"], k, i / 30.0)
+    sec = time.perf_counter() - t0
+    value = args.steps / sec
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": "synthetic (oracle-rendered acceptance room + 2 moving boxes, mt19937 depth noise)",
+        "config": {"workload": f"{CONFIG}: synthetic room with 2 moving boxes, 640x480 RGB-D, 1 cm voxels, "
+                               f"200-frame ping-pong sequence, refine_depth off",
+                   "resolution": [k.width, k.height], "voxel_size": 0.01},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"oracle ProcessFrame, steps {args.warmup}..{args.warmup + args.steps - 1} of the "
+                                   f"{CONFIG} sequence, {threads} threads"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

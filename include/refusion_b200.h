@@ -129,6 +129,8 @@ typedef struct {
 typedef struct {
     uint64_t dda_visits, new_blocks, visible_bricks, num_blocks;
     int32_t floodfill_rounds, overflow;
+    int32_t passes, reserved0;  /* Accumulate passes of the frame's registrations */
+    double pixel_passes;        /* sum of the pixel counts of those passes */
 } rf_frame_counters;
 
 typedef struct rf_volume rf_volume;
@@ -200,6 +202,23 @@ rf_status rf_pipeline_trajectory(const rf_pipeline* p, double* timestamps, doubl
 rf_status rf_pipeline_last_mask(const rf_pipeline* p, uint8_t* out, int32_t* has_mask);    /* FrameDebug::mask */
 rf_status rf_pipeline_last_residuals(const rf_pipeline* p, float* res_sq, uint8_t* res_valid); /* FrameDebug::residuals */
 rf_status rf_pipeline_last_counters(const rf_pipeline* p, rf_frame_counters* out);
+/* Per-stage device time with CUDA events on the pipeline's stream (off by
+ * default). stage_ms[0..3] = track (k_track: pyramid + LM + mask), allocate,
+ * cull, fuse (carve+integrate), accumulated over `frames` frames since the
+ * last enable; `launches` counts every kernel this pipeline launched. */
+rf_status rf_pipeline_set_profiling(rf_pipeline* p, int32_t enable);
+rf_status rf_pipeline_stage_times(const rf_pipeline* p, double stage_ms[4], uint64_t* frames, uint64_t* launches);
+/* Sums of the per-frame counters over the frames profiled since the last enable. */
+rf_status rf_pipeline_profile_counters(const rf_pipeline* p, rf_frame_counters* sums);
+rf_status rf_pipeline_stream(const rf_pipeline* p, void** cuda_stream);                   /* cudaStream_t */
+
+/* ---- synthetic input (synth.cpp:136-203 on the GPU; workload generator) ----
+ * prims: array of rf_synth_primitive records (176 bytes each, see
+ * paper_1905_02082_b200/synth.py) with world-to-object poses for this frame;
+ * outputs are device buffers on `device`. */
+rf_status rf_synth_render(const void* prims, int32_t nprims, const double cam_pose[12], const rf_intrinsics* k,
+                          double noise_sigma_scale, double dropout, uint64_t seed, uint64_t frame_index,
+                          float* depth, uint8_t* rgb, uint8_t* labels, int device);
 
 /* ---- memory helpers ------------------------------------------------------ */
 void* rf_host_alloc(size_t bytes);  /* pinned host memory (fast frame uploads) */

@@ -68,7 +68,8 @@ class rf_linearize_result(C.Structure):
 
 class rf_frame_counters(C.Structure):
     _fields_ = [("dda_visits", C.c_uint64), ("new_blocks", C.c_uint64), ("visible_bricks", C.c_uint64),
-                ("num_blocks", C.c_uint64), ("floodfill_rounds", C.c_int32), ("overflow", C.c_int32)]
+                ("num_blocks", C.c_uint64), ("floodfill_rounds", C.c_int32), ("overflow", C.c_int32),
+                ("passes", C.c_int32), ("reserved0", C.c_int32), ("pixel_passes", C.c_double)]
 
 
 RF_OK, RF_INVALID_ARGUMENT, RF_TRACKING_LOST, RF_RESOURCE_LIMIT, RF_CUDA_ERROR, RF_IO_ERROR, RF_UNSUPPORTED = range(7)
@@ -84,7 +85,8 @@ EXPORTS = [
     "rf_pipeline_create", "rf_pipeline_destroy", "rf_pipeline_process_frame", "rf_pipeline_finalize",
     "rf_pipeline_volume", "rf_pipeline_tracking_losses", "rf_pipeline_trajectory", "rf_pipeline_last_mask",
     "rf_pipeline_last_residuals", "rf_pipeline_last_counters", "rf_host_alloc", "rf_host_free", "rf_device_alloc",
-    "rf_device_free", "rf_copy_to_device",
+    "rf_device_free", "rf_copy_to_device", "rf_pipeline_set_profiling", "rf_pipeline_stage_times",
+    "rf_pipeline_stream", "rf_synth_render", "rf_pipeline_profile_counters",
 ]
 
 _lib = None

@@ -200,6 +200,7 @@ struct rf_volume {
     DevBuf slots, coords, voxels, counters;
     VolumeView view{};
     Workspace ws;
+    cudaEvent_t* prof = nullptr;  // stage markers when a pipeline profiles (see rf_pipeline_set_profiling)
 
     uint64_t num_blocks() {
         uint32_t c = 0;
@@ -262,6 +263,7 @@ struct rf_volume {
         ca.carve_only_before = carve_only_before;
         k_cull<<<4 * 148, 256, 0, ws.stream>>>(ca);
         CK(cudaGetLastError());
+        if (prof) CK(cudaEventRecord(prof[3], ws.stream));
         FuseArgs fa{};
         fa.V = view;
         fa.depth = d;
@@ -450,6 +452,7 @@ rf_status rf_volume_allocate_blocks(rf_volume* v, const int32_t* coords, uint64_
         dc.ensure(n * 12);
         dr.ensure(n * 4);
         CK(cudaMemcpyAsync(dc.p, coords, n * 12, cudaMemcpyHostToDevice, v->ws.stream));
+        v->reset_counter(kOverflow);
         k_alloc_coords<<<unsigned((n + 255) / 256), 256, 0, v->ws.stream>>>(v->view, dc.as<int>(), int(n),
                                                                              dr.as<int>());
         CK(cudaGetLastError());
@@ -471,6 +474,7 @@ rf_status rf_volume_allocate_for_frame(rf_volume* v, const rf_frame* f, const do
         const uint8_t* m = v->mask_of(f, mask);
         v->upload_pose(pose);
         v->reset_counter(kDdaVisits);
+        v->reset_counter(kOverflow);
         v->allocate(d, m, f->intrinsics, v->ws.pose.as<double>(), nullptr);
         v->ws.sync();
         require(v->overflow() == 0, RF_RESOURCE_LIMIT,
@@ -916,6 +920,11 @@ struct rf_pipeline {
     TrackOut last{};
     uint32_t last_counters[kNumCounters] = {};
     bool has_mask = false;
+    bool profiling = false;
+    cudaEvent_t ev[5] = {};
+    double stage_ms[4] = {};
+    rf_frame_counters prof_sums{};
+    uint64_t prof_frames = 0, launches = 0;
 };
 
 namespace {
@@ -965,6 +974,8 @@ rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipel
 
 void rf_pipeline_destroy(rf_pipeline* p) {
     if (!p) return;
+    for (cudaEvent_t& e : p->ev)
+        if (e) cudaEventDestroy(e);
     rf_volume_destroy(p->vol);
     delete p;
 }
@@ -988,17 +999,25 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
         st.frame_index = p->frame_count;
         st.timestamp = f->timestamp;
         double* pose_state = ws.pose.as<double>();
+        v->prof = p->profiling ? p->ev : nullptr;
+        if (v->prof) CK(cudaEventRecord(p->ev[0], ws.stream));
         if (p->first) {  // bootstrap at the identity (pipeline.cpp:66-76)
             static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
             CK(cudaMemcpyAsync(pose_state, kIdentity, 96, cudaMemcpyHostToDevice, ws.stream));
-            CK(cudaMemsetAsync(v->view.counters + kBlocksBefore, 0, 4 * 4, ws.stream));
+            CK(cudaMemsetAsync(v->view.counters + kOverflow, 0, 5 * 4, ws.stream));
+            if (v->prof) CK(cudaEventRecord(p->ev[1], ws.stream));
             v->allocate(d, nullptr, f->intrinsics, pose_state, nullptr);
+            if (v->prof) CK(cudaEventRecord(p->ev[2], ws.stream));
             v->fuse(d, rgb, nullptr, f->intrinsics, pose_state, nullptr, false, true, false);
+            if (v->prof) CK(cudaEventRecord(p->ev[4], ws.stream));
+            p->launches += 3;
             CK(cudaMemcpyAsync(ws.h_counters, v->view.counters, kNumCounters * 4, cudaMemcpyDeviceToHost, ws.stream));
             ws.sync();
             st.converged = 1;
             std::memcpy(p->last.pose, kIdentity, 96);
             p->last.rounds = 0;
+            p->last.passes = 0;
+            p->last.pixel_passes = 0.0;
             p->has_mask = false;
         } else {
             TrackArgs a = v->track_args(f, d, rgb, L);
@@ -1008,10 +1027,14 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             a.mp = to_mask(p->cfg.mask);
             a.vol_counters = v->view.counters;
             v->launch_track(a);
+            if (v->prof) CK(cudaEventRecord(p->ev[1], ws.stream));
             const uint8_t* mask = p->cfg.dynamics_enabled ? a.F.mask[0] : nullptr;
             const int* lost = &ws.out.as<TrackOut>()->lost;
             v->allocate(d, mask, f->intrinsics, pose_state, lost);
+            if (v->prof) CK(cudaEventRecord(p->ev[2], ws.stream));
             v->fuse(d, rgb, mask, f->intrinsics, pose_state, lost, true, true, true);
+            if (v->prof) CK(cudaEventRecord(p->ev[4], ws.stream));
+            p->launches += 4;
             CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
             CK(cudaMemcpyAsync(ws.h_counters, v->view.counters, kNumCounters * 4, cudaMemcpyDeviceToHost, ws.stream));
             ws.sync();
@@ -1032,6 +1055,25 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
         p->traj_p.insert(p->traj_p.end(), p->last.pose, p->last.pose + 12);
         if (pose_out) std::memcpy(pose_out, p->last.pose, 96);
         p->first = false;
+        if (v->prof) {  // all events completed: the stream was synchronised above
+            for (int i = 0; i < 4; ++i) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]));
+                p->stage_ms[i] += ms;
+            }
+            ++p->prof_frames;
+            rf_frame_counters c{};
+            rf_pipeline_last_counters(p, &c);
+            rf_frame_counters& s = p->prof_sums;
+            s.dda_visits += c.dda_visits;
+            s.new_blocks += c.new_blocks;
+            s.visible_bricks += c.visible_bricks;
+            s.num_blocks = c.num_blocks;
+            s.floodfill_rounds += c.floodfill_rounds;
+            s.passes += c.passes;
+            s.pixel_passes += c.pixel_passes;
+            v->prof = nullptr;
+        }
         require(ws.h_counters[kOverflow] == 0, RF_RESOURCE_LIMIT,
                 "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)");
         st.runtime_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1101,6 +1143,50 @@ rf_status rf_pipeline_last_counters(const rf_pipeline* p, rf_frame_counters* out
         out->new_blocks = out->num_blocks - std::min<uint64_t>(c[kBlocksBefore], out->num_blocks);
         out->floodfill_rounds = p->last.rounds;
         out->overflow = int32_t(c[kOverflow]);
+        out->passes = p->last.passes;
+        out->reserved0 = 0;
+        out->pixel_passes = p->last.pixel_passes;
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+rf_status rf_pipeline_set_profiling(rf_pipeline* p, int32_t enable) {
+    return guard([&] {
+        require(p, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(p->vol->device));
+        if (enable && !p->ev[0])
+            for (cudaEvent_t& e : p->ev) CK(cudaEventCreate(&e));
+        p->profiling = enable != 0;
+        for (double& m : p->stage_ms) m = 0.0;
+        p->prof_sums = rf_frame_counters{};
+        p->prof_frames = 0;
+    });
+}
+
+rf_status rf_pipeline_stage_times(const rf_pipeline* p, double stage_ms[4], uint64_t* frames, uint64_t* launches) {
+    return guard([&] {
+        require(p, RF_INVALID_ARGUMENT, "null argument");
+        if (stage_ms)
+            for (int i = 0; i < 4; ++i) stage_ms[i] = p->stage_ms[i];
+        if (frames) *frames = p->prof_frames;
+        if (launches) *launches = p->launches;
+    });
+}
+
+rf_status rf_pipeline_profile_counters(const rf_pipeline* p, rf_frame_counters* sums) {
+    return guard([&] {
+        require(p && sums, RF_INVALID_ARGUMENT, "null argument");
+        *sums = p->prof_sums;
+    });
+}
+
+rf_status rf_pipeline_stream(const rf_pipeline* p, void** cuda_stream) {
+    return guard([&] {
+        require(p && cuda_stream, RF_INVALID_ARGUMENT, "null argument");
+        *cuda_stream = p->vol->ws.stream;
     });
 }
 

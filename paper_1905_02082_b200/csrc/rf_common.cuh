@@ -15,7 +15,8 @@ namespace rfb {
 constexpr int kSide = 8;                      // voxels per brick edge (VolumeConfig::block_side)
 constexpr int kBrickVoxels = kSide * kSide * kSide;
 constexpr uint64_t kEmptyKey = ~0ull;
-constexpr uint32_t kInvalid = 0xFFFFFFFFu;
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;     // slot value before the winner publishes it / not found
+constexpr uint32_t kOverflowed = 0xFFFFFFFEu;  // key claimed but no brick left (max_blocks reached)
 constexpr int kCoordBias = 1 << 20;           // 21-bit signed range per axis, as mesh.cpp:31-37
 constexpr int kAccN = 30;                     // 21 H + 6 b + E_d + E_c + count
 
@@ -126,7 +127,7 @@ __device__ __forceinline__ uint32_t hash_find(const VolumeView& V, int x, int y,
     for (uint32_t probe = 0; probe <= V.hash_mask; ++probe) {
         const uint4 s = __ldg(reinterpret_cast<const uint4*>(V.slots + idx));
         const unsigned long long k = (unsigned long long)s.x | ((unsigned long long)s.y << 32);
-        if (k == key) return s.z;
+        if (k == key) return s.z >= kOverflowed ? kInvalid : s.z;
         if (k == kEmptyKey) return kInvalid;
         idx = (idx + 1) & V.hash_mask;
     }
@@ -144,21 +145,33 @@ __device__ __forceinline__ int hash_insert(const VolumeView& V, int x, int y, in
     uint32_t idx = hash_coord(x, y, z) & V.hash_mask;
     for (uint32_t probe = 0; probe <= V.hash_mask; ++probe) {
         unsigned long long k = *reinterpret_cast<volatile unsigned long long*>(&V.slots[idx].key);
-        if (k == key) return 0;
+        if (k == key) {
+            if (*reinterpret_cast<volatile uint32_t*>(&V.slots[idx].value) == kOverflowed) {
+                atomicOr(&V.counters[kOverflow], 1u);  // AllocateBlock throws again (tsdf_volume.cpp:66-69)
+                return -1;
+            }
+            return 0;
+        }
         if (k == kEmptyKey) {
             const unsigned long long old = atomicCAS(&V.slots[idx].key, kEmptyKey, key);
             if (old == kEmptyKey) {
                 const uint32_t b = atomicAdd(&V.counters[kNumBlocks], 1u);
                 if (b >= V.max_blocks) {
                     atomicOr(&V.counters[kOverflow], 1u);
-                    V.slots[idx].value = kInvalid;
+                    V.slots[idx].value = kOverflowed;
                     return -1;
                 }
                 V.coords[b] = make_int4(x, y, z, 0);
                 V.slots[idx].value = b;
                 return 1;
             }
-            if (old == key) return 0;
+            if (old == key) {
+                if (*reinterpret_cast<volatile uint32_t*>(&V.slots[idx].value) == kOverflowed) {
+                    atomicOr(&V.counters[kOverflow], 1u);
+                    return -1;
+                }
+                return 0;
+            }
         }
         idx = (idx + 1) & V.hash_mask;
     }

@@ -288,6 +288,10 @@ template <bool kJac>
 __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res,
                                      double cw, double* scratch, double* blk, double* out) {
     const bool color = cw > 0.0 && a.F.rgb0 != nullptr;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.out->passes += 1;
+        a.out->pixel_passes += double(a.F.K[level].w) * double(a.F.K[level].h);
+    }
     if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
     else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
 }
@@ -523,6 +527,10 @@ __global__ void __launch_bounds__(kTrackThreads, 2) k_track(TrackArgs a) {
     __shared__ double blk[kAccN + 2];
     __shared__ double red[kAccN + 2];
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    if (lead && a.out) {
+        a.out->passes = 0;
+        a.out->pixel_passes = 0.0;
+    }
 
     if (a.mode == kModeLinearize || a.mode == kModeEvalDepth || a.mode == kModeEvalColor) {
         Pose P;
@@ -608,6 +616,7 @@ __global__ void __launch_bounds__(kTrackThreads, 2) k_track(TrackArgs a) {
             a.vol_counters[kBlocksBefore] = a.vol_counters[kNumBlocks];
             a.vol_counters[kVisible] = 0;
             a.vol_counters[kDdaVisits] = 0;
+            a.vol_counters[kOverflow] = 0;
         }
     }
 }

@@ -43,7 +43,8 @@ struct TrackOut {
     double final_error;
     double acc[kAccN];  // last accumulation (linearize/evaluate entry points)
     int32_t rounds;     // floodfill rounds (diagnostic)
-    int32_t pad;
+    int32_t passes;     // pixel passes run (Accumulate calls)
+    double pixel_passes;  // sum over passes of the level's pixel count (bytes model)
 };
 
 enum TrackMode : int {
