@@ -217,7 +217,7 @@ def run_ours(args):
     sums = L.rf_frame_counters()
     L.check(lib.rf_pipeline_profile_counters(pv.h, C.byref(sums)))
     agg.update(pixel_passes=sums.pixel_passes, visible=sums.visible_bricks, dda=sums.dda_visits,
-               new=sums.new_blocks)
+               new=sums.new_blocks, ff_rounds=sums.floodfill_rounds)
     num_blocks = pv.volume().num_blocks()
 
     # ---- e2e: host pinned frames through the C ABI, wall clock
@@ -292,7 +292,8 @@ def run_ours(args):
         "workload_stats": {"lm_iterations_per_frame": agg["iters"] / n, "registrations_per_frame": agg["regs"] / n,
                            "masked_pixels_per_frame": agg["masked"] / n, "lost_frames": agg["lost"],
                            "visible_bricks_per_frame": agg["visible"] / n, "bricks": num_blocks,
-                           "pixel_passes_per_frame": agg["pixel_passes"] / n},
+                           "pixel_passes_per_frame": agg["pixel_passes"] / n,
+                           "floodfill_rounds_per_frame": agg["ff_rounds"] / n},
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

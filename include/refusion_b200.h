@@ -216,6 +216,13 @@ rf_status rf_pipeline_stream(const rf_pipeline* p, void** cuda_stream);         
  * prims: array of rf_synth_primitive records (176 bytes each, see
  * paper_1905_02082_b200/synth.py) with world-to-object poses for this frame;
  * outputs are device buffers on `device`. */
+/* ---- diagnostics ----------------------------------------------------------
+ * Cost of one grid-wide barrier (reduce = 0) or barrier + 30-value
+ * deterministic all-reduce (reduce = 1) of the persistent tracking kernel. */
+rf_status rf_diag_grid_barrier(int device, int32_t iters, int32_t reduce, double* us_per_call);
+/* SM cycles of one LM step on one thread: [solve, ExpMap + compose, total]. */
+rf_status rf_diag_lm_step(int device, int32_t iters, double cycles[3]);
+
 rf_status rf_synth_render(const void* prims, int32_t nprims, const double cam_pose[12], const rf_intrinsics* k,
                           double noise_sigma_scale, double dropout, uint64_t seed, uint64_t frame_index,
                           float* depth, uint8_t* rgb, uint8_t* labels, int device);

@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librefusion_b200.so")
+# RF_LIB_PATH selects an alternative build of the same library (tuning runs).
+LIB_PATH = os.environ.get("RF_LIB_PATH") or os.path.join(_HERE, "librefusion_b200.so")
 
 
 class rf_intrinsics(C.Structure):
@@ -86,7 +87,8 @@ EXPORTS = [
     "rf_pipeline_volume", "rf_pipeline_tracking_losses", "rf_pipeline_trajectory", "rf_pipeline_last_mask",
     "rf_pipeline_last_residuals", "rf_pipeline_last_counters", "rf_host_alloc", "rf_host_free", "rf_device_alloc",
     "rf_device_free", "rf_copy_to_device", "rf_pipeline_set_profiling", "rf_pipeline_stage_times",
-    "rf_pipeline_stream", "rf_synth_render", "rf_pipeline_profile_counters",
+    "rf_pipeline_stream", "rf_synth_render", "rf_pipeline_profile_counters", "rf_diag_grid_barrier",
+    "rf_diag_lm_step",
 ]
 
 _lib = None

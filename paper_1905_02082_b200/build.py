@@ -30,16 +30,21 @@ def _stale(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, defines=(), variant: str | None = None) -> str:
+    """Default build -> librefusion_b200.so. A `variant` (tuning experiments,
+    selected at run time with RF_LIB_PATH) builds with extra -D defines into
+    _variants/lib<variant>.so."""
+    build_dir = BUILD if not variant else os.path.join(HERE, "_variants", "obj_" + variant)
+    lib = LIB if not variant else os.path.join(HERE, "_variants", f"lib{variant}.so")
+    os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(os.path.dirname(HERE), "include", "refusion_b200.h"))
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
-        if _stale(o, [s] + headers):
-            jobs.append([NVCC, *ARCH, *FLAGS, "-c", s, "-o", o])
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
+        if _stale(o, [s] + headers) or variant:
+            jobs.append([NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -51,11 +56,14 @@ def build(verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
         list(ex.map(run, jobs))
-    objs = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in SOURCES]
-    if jobs or not os.path.exists(LIB):
-        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
-    return LIB
+    objs = [os.path.join(build_dir, s.replace(".cu", ".o")) for s in SOURCES]
+    if jobs or not os.path.exists(lib):
+        run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"])
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    variant = args[args.index("--variant") + 1] if "--variant" in args else None
+    defines = [a[2:] for a in args if a.startswith("-D")]
+    print(build(verbose="-v" in args, defines=defines, variant=variant))

@@ -2,6 +2,7 @@
 // objects, device buffers, frame upload and the per-frame launch sequence.
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -91,7 +92,10 @@ struct Workspace {
     int device = 0;
     cudaStream_t stream = nullptr;
     int track_grid = 0;
+    int parity = 0;  // alternates the grid-barrier counter between cooperative launches
     DevBuf depth, rgb, mask_in, pose, res_sq, res_valid, mwork, levels, gsync, partials, result, out, list;
+    DevBuf trace;            // per-pass timeline when RF_TRACE_FILE is set (diagnostics)
+    std::string trace_path;
     TrackOut* h_out = nullptr;
     uint32_t* h_counters = nullptr;
     int W = 0, H = 0, L = 0;
@@ -108,16 +112,20 @@ struct Workspace {
         track_grid = sms * per;
         gsync.ensure(sizeof(GridSync));
         CK(cudaMemset(gsync.p, 0, sizeof(GridSync)));
-        partials.ensure(size_t(track_grid) * kRedStride * sizeof(double));
+        partials.ensure(2 * size_t(track_grid) * kRedStride * sizeof(double));
         result.ensure(kRedStride * sizeof(double));
         out.ensure(sizeof(TrackOut));
         pose.ensure(12 * sizeof(double));
         CK(cudaMallocHost(&h_out, sizeof(TrackOut)));
         CK(cudaMallocHost(&h_counters, kNumCounters * sizeof(uint32_t)));
+        if (const char* tf = std::getenv("RF_TRACE_FILE")) {
+            trace_path = tf;
+            trace.ensure(kTracePasses * 8 * sizeof(unsigned long long));
+        }
     }
     void destroy() {
         for (DevBuf* b : {&depth, &rgb, &mask_in, &pose, &res_sq, &res_valid, &mwork, &levels, &gsync, &partials,
-                          &result, &out, &list})
+                          &result, &out, &list, &trace})
             b->release();
         if (h_out) cudaFreeHost(h_out);
         if (h_counters) cudaFreeHost(h_counters);
@@ -162,6 +170,8 @@ Intr level_intr(const rf_intrinsics& k, int l) {  // CameraIntrinsics::Scaled (g
     r.cy = k.cy * s;
     r.w = k.width >> l;
     r.h = k.height >> l;
+    r.ifx = 1.0 / r.fx;
+    r.ify = 1.0 / r.fy;
     return r;
 }
 
@@ -197,7 +207,7 @@ struct rf_volume {
     int device = 0;
     rf_volume_config cfg{};
     uint64_t cap = 0;
-    DevBuf slots, coords, voxels, counters;
+    DevBuf slots, coords, voxels, links, counters;
     VolumeView view{};
     Workspace ws;
     cudaEvent_t* prof = nullptr;  // stage markers when a pipeline profiles (see rf_pipeline_set_profiling)
@@ -249,6 +259,11 @@ struct rf_volume {
     }
     void reset_counter(int which) {
         CK(cudaMemsetAsync(view.counters + which, 0, 4, ws.stream));
+    }
+    void link() {  // link records for bricks allocated outside the per-frame cull
+        k_link<<<148, 256, 0, ws.stream>>>(view);
+        k_link_commit<<<1, 32, 0, ws.stream>>>(view);
+        CK(cudaGetLastError());
     }
     void fuse(const float* d, const uint8_t* rgb, const uint8_t* mask, const rf_intrinsics& k, const double* pose,
               const int* lost, bool carve, bool integrate, bool carve_only_before) {
@@ -310,9 +325,22 @@ struct rf_volume {
         a.pose_state = ws.pose.as<double>();
         a.out = ws.out.as<TrackOut>();
         a.reg.levels = levels;
+        a.trace = ws.trace.as<unsigned long long>();
         return a;
     }
+    void dump_trace() {  // appends one frame's per-pass timeline (binary u64) to RF_TRACE_FILE
+        if (!ws.trace.p) return;
+        std::vector<unsigned long long> h(kTracePasses * 8);
+        CK(cudaMemcpy(h.data(), ws.trace.p, h.size() * 8, cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen(ws.trace_path.c_str(), "ab")) {
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+    }
     void launch_track(TrackArgs& a) {
+        if (a.trace) CK(cudaMemsetAsync(a.trace, 0, kTracePasses * 8 * sizeof(unsigned long long), ws.stream));
+        a.grid.parity = ws.parity;
+        ws.parity ^= 1;
         void* args[] = {&a};
         CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
     }
@@ -368,9 +396,11 @@ void create_volume(const rf_volume_config* cfg, int device, rf_volume** out) {
     v->slots.ensure(v->cap * sizeof(HashSlot));
     v->coords.ensure(cfg->max_blocks * sizeof(int4));
     v->voxels.ensure(cfg->max_blocks * kBrickVoxels * sizeof(Voxel));
+    v->links.ensure(cfg->max_blocks * kLinkStride * sizeof(uint32_t));
     v->counters.ensure(kNumCounters * sizeof(uint32_t));
     v->ws.init(device);
     CK(cudaMemsetAsync(v->slots.p, 0xFF, v->cap * sizeof(HashSlot), v->ws.stream));
+    CK(cudaMemsetAsync(v->links.p, 0xFF, cfg->max_blocks * kLinkStride * sizeof(uint32_t), v->ws.stream));
     CK(cudaMemsetAsync(v->voxels.p, 0, cfg->max_blocks * kBrickVoxels * sizeof(Voxel), v->ws.stream));
     CK(cudaMemsetAsync(v->counters.p, 0, kNumCounters * sizeof(uint32_t), v->ws.stream));
     v->ws.list.ensure(cfg->max_blocks * sizeof(uint32_t));
@@ -380,8 +410,10 @@ void create_volume(const rf_volume_config* cfg, int device, rf_volume** out) {
     V.max_blocks = uint32_t(cfg->max_blocks);
     V.coords = v->coords.as<int4>();
     V.voxels = v->voxels.as<Voxel>();
+    V.links = v->links.as<uint32_t>();
     V.counters = v->counters.as<uint32_t>();
     V.voxel_size = cfg->voxel_size;
+    V.inv_voxel_size = 1.0 / cfg->voxel_size;
     V.truncation = cfg->truncation;
     V.max_weight = cfg->max_weight;
     V.carve_weight = cfg->carve_weight;
@@ -424,6 +456,7 @@ void rf_volume_destroy(rf_volume* v) {
     v->slots.release();
     v->coords.release();
     v->voxels.release();
+    v->links.release();
     v->counters.release();
     delete v;
 }
@@ -456,6 +489,7 @@ rf_status rf_volume_allocate_blocks(rf_volume* v, const int32_t* coords, uint64_
         k_alloc_coords<<<unsigned((n + 255) / 256), 256, 0, v->ws.stream>>>(v->view, dc.as<int>(), int(n),
                                                                              dr.as<int>());
         CK(cudaGetLastError());
+        v->link();
         if (created) CK(cudaMemcpyAsync(created, dr.p, n * 4, cudaMemcpyDeviceToHost, v->ws.stream));
         v->ws.sync();
         dc.release();
@@ -476,6 +510,7 @@ rf_status rf_volume_allocate_for_frame(rf_volume* v, const rf_frame* f, const do
         v->reset_counter(kDdaVisits);
         v->reset_counter(kOverflow);
         v->allocate(d, m, f->intrinsics, v->ws.pose.as<double>(), nullptr);
+        v->link();
         v->ws.sync();
         require(v->overflow() == 0, RF_RESOURCE_LIMIT,
                 "voxel block budget exhausted (" + std::to_string(v->cfg.max_blocks) + " blocks)");
@@ -619,6 +654,7 @@ rf_status rf_volume_reset(rf_volume* v) {
         const uint64_t nb = v->num_blocks();
         CK(cudaMemsetAsync(v->slots.p, 0xFF, v->cap * sizeof(HashSlot), v->ws.stream));
         CK(cudaMemsetAsync(v->voxels.p, 0, nb * kBrickVoxels * sizeof(Voxel), v->ws.stream));
+        CK(cudaMemsetAsync(v->links.p, 0xFF, nb * kLinkStride * sizeof(uint32_t), v->ws.stream));
         CK(cudaMemsetAsync(v->counters.p, 0, kNumCounters * sizeof(uint32_t), v->ws.stream));
         v->ws.sync();
     });
@@ -715,6 +751,7 @@ rf_status rf_volume_load(const char* path, int device, rf_volume** out) {
                                v->ws.stream));
             const uint32_t cnt = uint32_t(nb);
             CK(cudaMemcpyAsync(v->view.counters + kNumBlocks, &cnt, 4, cudaMemcpyHostToDevice, v->ws.stream));
+            v->link();
             v->ws.sync();
         }
         *out = hold.release();
@@ -849,6 +886,8 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
         a.grid.sync = ws.gsync.as<GridSync>();
         a.grid.partials = ws.partials.as<double>();
         a.grid.result = ws.result.as<double>();
+        a.grid.parity = ws.parity;
+        ws.parity ^= 1;
         a.out = ws.out.as<TrackOut>();
         void* args[] = {&a};
         CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
@@ -1039,6 +1078,7 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             CK(cudaMemcpyAsync(ws.h_counters, v->view.counters, kNumCounters * 4, cudaMemcpyDeviceToHost, ws.stream));
             ws.sync();
             p->last = *ws.h_out;
+            v->dump_trace();
             const TrackOut& o = p->last;
             st.tracking_lost = o.lost;
             st.converged = o.converged;
@@ -1191,3 +1231,55 @@ rf_status rf_pipeline_stream(const rf_pipeline* p, void** cuda_stream) {
 }
 
 }  // extern "C"
+
+namespace rfb {
+__global__ void k_grid_bench(GridCtx g, int iters, int reduce);
+__global__ void k_lm_bench(int iters, double* out);
+}
+
+extern "C" rf_status rf_diag_lm_step(int device, int32_t iters, double cycles[3]) {
+    return guard([&] {
+        require(cycles && iters > 0, RF_INVALID_ARGUMENT, "bad argument");
+        CK(cudaSetDevice(device));
+        DevBuf o;
+        o.ensure(3 * sizeof(double));
+        k_lm_bench<<<1, 32>>>(iters, o.as<double>());
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(cycles, o.p, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+namespace rfb {
+}
+
+extern "C" rf_status rf_diag_grid_barrier(int device, int32_t iters, int32_t reduce, double* us_per_call) {
+    return guard([&] {
+        require(us_per_call && iters > 0, RF_INVALID_ARGUMENT, "bad argument");
+        CK(cudaSetDevice(device));
+        Workspace& ws = device_ws(device);
+        GridCtx g{};
+        g.sync = ws.gsync.as<GridSync>();
+        g.partials = ws.partials.as<double>();
+        g.result = ws.result.as<double>();
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        float best = 1e30f;
+        for (int rep = 0; rep < 3; ++rep) {
+            g.parity = ws.parity;
+            ws.parity ^= 1;
+            void* args[] = {&g, &iters, &reduce};
+            CK(cudaEventRecord(e0, ws.stream));
+            CK(cudaLaunchCooperativeKernel((void*)k_grid_bench, dim3(ws.track_grid), dim3(kTrackThreads), args, 0,
+                                           ws.stream));
+            CK(cudaEventRecord(e1, ws.stream));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            best = std::min(best, ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *us_per_call = 1e3 * double(best) / iters;
+    });
+}

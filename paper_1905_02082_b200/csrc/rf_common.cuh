@@ -19,6 +19,7 @@ constexpr uint32_t kInvalid = 0xFFFFFFFFu;     // slot value before the winner p
 constexpr uint32_t kOverflowed = 0xFFFFFFFEu;  // key claimed but no brick left (max_blocks reached)
 constexpr int kCoordBias = 1 << 20;           // 21-bit signed range per axis, as mesh.cpp:31-37
 constexpr int kAccN = 30;                     // 21 H + 6 b + E_d + E_c + count
+constexpr int kLinkStride = 8;                // u32 per brick link record (32 B)
 
 // ---------------------------------------------------------------- types
 struct Voxel {  // tsdf_volume.hpp:32-37, 8 bytes
@@ -41,6 +42,7 @@ struct Pose {  // camera-to-world; R row-major
 struct Intr {
     double fx, fy, cx, cy;
     int w, h;
+    double ifx, ify;  // 1/fx, 1/fy (tracking passes back-project with reciprocals)
 };
 
 // Device view of one sparse volume (hash + brick pool).
@@ -50,8 +52,10 @@ struct VolumeView {
     uint32_t max_blocks;
     int4* coords;        // brick coordinate per pool index (w unused)
     Voxel* voxels;       // pool, kBrickVoxels per brick, x fastest then y then z
+    uint32_t* links;     // kLinkStride per brick: pool index of the brick at +(q&1, q>>1&1, q>>2), q = 1..7
     uint32_t* counters;  // see VolumeCounters
     double voxel_size, truncation;
+    double inv_voxel_size;  // 1.0 / voxel_size (the reference's inv_s, tsdf_volume.cpp:336)
     int max_weight, carve_weight;
     double min_depth, max_depth, carve_clip;
 };
@@ -64,6 +68,8 @@ enum VolumeCounters : int {
     kVisible = 3,       // compacted visible-brick count for carve/integrate
     kDdaVisits = 4,     // cells visited by the allocation walk (bytes model)
     kNewBlocks = 5,
+    kLinked = 6,        // bricks [0, kLinked) have link records
+    kLinkDone = 7,      // k_link completion counter (last CTA advances kLinked)
     kNumCounters = 8
 };
 
@@ -108,8 +114,8 @@ __host__ __device__ __forceinline__ uint32_t hash_coord(int x, int y, int z) {
 }
 
 __host__ __device__ __forceinline__ bool coord_in_range(int x, int y, int z) {
-    return x >= -kCoordBias && x < kCoordBias && y >= -kCoordBias && y < kCoordBias && z >= -kCoordBias &&
-           z < kCoordBias;
+    constexpr uint32_t b = uint32_t(kCoordBias);
+    return ((uint32_t(x) + b) | (uint32_t(y) + b) | (uint32_t(z) + b)) < 2u * b;
 }
 
 __host__ __device__ __forceinline__ unsigned long long pack_key(int x, int y, int z) {
@@ -191,38 +197,40 @@ struct CellSample {
     double inten, gi[3]; // value and gradient of the intensity interpolant
 };
 
+// The 8 corners of the interpolation cell at voxel (bx,by,bz) live in the
+// brick of the base voxel and, when the cell straddles brick faces (local
+// coordinate 7 on an axis, one cell in three), in its +x/+y/+z neighbours.
+// One hash probe finds the base brick; the neighbours come from the base
+// brick's link record (pool indices of its 7 "+" neighbours, maintained at
+// allocation by k_link), so every lane runs the same code: no divergent
+// second/third hash probes.
 __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int by, int bz, uint2 c[8]) {
     const int lx = bx & 7, ly = by & 7, lz = bz & 7;
-    const int Bx = bx >> 3, By = by >> 3, Bz = bz >> 3;  // arithmetic shift == FloorDiv by 8
-    if (lx < 7 && ly < 7 && lz < 7) {
-        const uint32_t b = hash_find(V, Bx, By, Bz);
-        if (b == kInvalid) return false;
-        const uint2* base = reinterpret_cast<const uint2*>(brick_ptr(V, b));
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int off = ((lz + (k >> 2)) * 8 + (ly + ((k >> 1) & 1))) * 8 + (lx + (k & 1));
-            c[k] = __ldg(base + off);
-        }
+    const uint32_t b0 = hash_find(V, bx >> 3, by >> 3, bz >> 3);  // arithmetic shift == FloorDiv by 8
+    if (b0 == kInvalid) return false;
+    const int smask = int(lx == 7) | (int(ly == 7) << 1) | (int(lz == 7) << 2);
+    uint32_t n[8];
+    n[0] = b0;
+    if (smask) {
+        const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(b0) * kLinkStride));
+        const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(b0) * kLinkStride) + 1);
+        n[1] = r0.y; n[2] = r0.z; n[3] = r0.w; n[4] = r1.x; n[5] = r1.y; n[6] = r1.z; n[7] = r1.w;
     } else {
-        uint32_t bricks[8];
-        const int sx = lx == 7, sy = ly == 7, sz = lz == 7;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
-            if ((dx && !sx) || (dy && !sy) || (dz && !sz)) {
-                bricks[k] = kInvalid;
-                continue;
-            }
-            bricks[k] = hash_find(V, Bx + dx, By + dy, Bz + dz);
-            if (bricks[k] == kInvalid) return false;
-        }
+        for (int q = 1; q < 8; ++q) n[q] = b0;
+    }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int cx = lx + (k & 1), cy = ly + ((k >> 1) & 1), cz = lz + (k >> 2);
-            const int bk = (cx >> 3) | ((cy >> 3) << 1) | ((cz >> 3) << 2);
-            const uint2* base = reinterpret_cast<const uint2*>(brick_ptr(V, bricks[bk]));
-            c[k] = __ldg(base + (((cz & 7) * 8 + (cy & 7)) * 8 + (cx & 7)));
-        }
+    for (int k = 0; k < 8; ++k) {
+        const int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;  // compile-time corner offset
+        const int kbits = dx | (dy << 1) | (dz << 2);
+        const int code = kbits & smask;                       // which neighbour holds this corner
+        uint32_t b = b0;
+#pragma unroll
+        for (int q = 1; q < 8; ++q)
+            if ((q & ~kbits) == 0) b = (code == q) ? n[q] : b;
+        if (b >= kOverflowed) return false;
+        const int cx = (lx + dx) & 7, cy = (ly + dy) & 7, cz = (lz + dz) & 7;
+        c[k] = __ldg(reinterpret_cast<const uint2*>(brick_ptr(V, b)) + ((cz * 8 + cy) * 8 + cx));
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k)
@@ -230,13 +238,48 @@ __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int 
     return true;
 }
 
+// Fills the link records of bricks [lo, hi) and points their "-" neighbours'
+// records at them (tsdf_volume.hpp:149-185 allocates; this only indexes).
+// Every write is a pure function of the key set, so concurrent writers of the
+// same slot agree.
+__device__ __forceinline__ void link_brick(const VolumeView& V, uint32_t b) {
+    const int4 c = V.coords[b];
+    uint32_t* own = V.links + size_t(b) * kLinkStride;
+    own[0] = b;
+#pragma unroll
+    for (int q = 1; q < 8; ++q) {
+        own[q] = hash_find(V, c.x + (q & 1), c.y + ((q >> 1) & 1), c.z + (q >> 2));
+        const uint32_t a = hash_find(V, c.x - (q & 1), c.y - ((q >> 1) & 1), c.z - (q >> 2));
+        if (a != kInvalid) V.links[size_t(a) * kLinkStride + q] = b;
+    }
+}
+
 __device__ __forceinline__ float voxel_sdf(uint2 v) { return __uint_as_float(v.x); }
 __device__ __forceinline__ double voxel_luma(uint2 v) {
     return luma(uint8_t(v.y >> 8), uint8_t(v.y >> 16), uint8_t(v.y >> 24));
 }
+// Same value from a table of the three weighted channels (lut[c*256 + x] =
+// w_c * x, each product rounded as in luma()), summed in luma()'s order:
+// bit-identical, 3 shared loads instead of 3 int->f64 conversions + 3 DMUL.
+__device__ __forceinline__ double voxel_luma_lut(uint2 v, const double* lut) {
+    return (lut[(v.y >> 8) & 0xFFu] + lut[256 + ((v.y >> 16) & 0xFFu)]) + lut[512 + (v.y >> 24)];
+}
 
-__device__ __forceinline__ void cell_of(double px, double py, double pz, double s, int base[3], double f[3]) {
-    const double g[3] = {px / s - 0.5, py / s - 0.5, pz / s - 0.5};  // tsdf_volume.cpp:279-283
+// CellOf (tsdf_volume.cpp:279-283). kExact divides like the reference; the
+// tracking passes multiply by the precomputed reciprocal (last-bit
+// differences only; parity there is held on the normal equations and poses).
+template <bool kExact>
+__device__ __forceinline__ void cell_of(double px, double py, double pz, const VolumeView& V, int base[3], double f[3]) {
+    double g[3];
+    if (kExact) {
+        g[0] = px / V.voxel_size - 0.5;
+        g[1] = py / V.voxel_size - 0.5;
+        g[2] = pz / V.voxel_size - 0.5;
+    } else {
+        g[0] = px * V.inv_voxel_size - 0.5;
+        g[1] = py * V.inv_voxel_size - 0.5;
+        g[2] = pz * V.inv_voxel_size - 0.5;
+    }
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const double fl = floor(g[i]);
@@ -245,11 +288,12 @@ __device__ __forceinline__ void cell_of(double px, double py, double pz, double 
     }
 }
 
-template <bool kGrad, bool kIntensity>
-__device__ __forceinline__ bool sample_point(const VolumeView& V, const double p[3], CellSample& out) {
+template <bool kGrad, bool kIntensity, bool kExact = true>
+__device__ __forceinline__ bool sample_point(const VolumeView& V, const double p[3], CellSample& out,
+                                             const double* lut = nullptr) {
     int base[3];
     double f[3];
-    cell_of(p[0], p[1], p[2], V.voxel_size, base, f);
+    cell_of<kExact>(p[0], p[1], p[2], V, base, f);
     uint2 c[8];
     if (!gather_corners(V, base[0], base[1], base[2], c)) return false;
     const double wx[2] = {1.0 - f[0], f[0]};
@@ -259,7 +303,7 @@ __device__ __forceinline__ bool sample_point(const VolumeView& V, const double p
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         vs[k] = double(voxel_sdf(c[k]));
-        if (kIntensity) vi[k] = voxel_luma(c[k]);
+        if (kIntensity) vi[k] = lut ? voxel_luma_lut(c[k], lut) : voxel_luma(c[k]);
     }
     double s = 0.0, in = 0.0;
 #pragma unroll
@@ -271,7 +315,7 @@ __device__ __forceinline__ bool sample_point(const VolumeView& V, const double p
     out.sdf = s;
     out.inten = in;
     if (kGrad) {
-        const double inv_s = 1.0 / V.voxel_size;
+        const double inv_s = V.inv_voxel_size;  // 1.0 / voxel_size, computed once on the host
         double gs[3] = {0, 0, 0}, gi[3] = {0, 0, 0};
 #pragma unroll
         for (int j = 0; j < 2; ++j)
@@ -300,10 +344,9 @@ __device__ __forceinline__ bool sample_point(const VolumeView& V, const double p
 // partial vector, the last CTA to arrive folds all partials in CTA order
 // (fixed order => run-to-run deterministic) and publishes the result, then
 // releases the others. One L2 round trip per waiting CTA.
+constexpr int kArriveLanes = 8;  // arrival counters on separate 128-B lines (parallel L2 atomics)
 struct GridSync {
-    unsigned int arrive;
-    unsigned int gen;
-    unsigned int pad[30];
+    unsigned long long lane[2][kArriveLanes][16];  // [launch parity][lane][0] = arrivals, rest padding
 };
 
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {

@@ -1,7 +1,15 @@
 // Grid-wide barrier with a deterministic all-reduce for cooperative
-// (persistent) kernels: one CTA per SM slot, every CTA runs the same control
-// flow, so device-resident loops (the LM iterations, the floodfill fixpoint)
-// need no host round trip.
+// (persistent) kernels: every CTA runs the same control flow, so
+// device-resident loops (the LM iterations, the floodfill fixpoint) need no
+// host round trip.
+//
+// Design (one L2 round trip on the critical path): each CTA writes its
+// partial vector into a double-buffered slot, arrives on a monotonically
+// increasing 64-bit counter with one release atomic, polls it relaxed until
+// the barrier's target count, then every CTA folds all partials itself in CTA
+// index order. No "last CTA reduces and re-publishes" chain, no reset inside
+// a launch: consecutive launches alternate between two counters and each
+// launch zeroes the one the next launch will use.
 #pragma once
 
 #include "rf_common.cuh"
@@ -11,91 +19,132 @@ namespace rfb {
 constexpr int kRedStride = 32;  // doubles per CTA partial slot
 
 struct GridCtx {
-    GridSync* sync;      // zero-initialised once
-    double* partials;    // gridDim.x * kRedStride
-    double* result;      // kRedStride
+    GridSync* sync;      // counters live here (zero-initialised once)
+    double* partials;    // 2 * gridDim.x * kRedStride (double-buffered)
+    double* result;      // unused by the current barrier (kept for ABI stability)
+    int parity;          // which counter this launch uses (host alternates)
 };
 
-// Sum over the CTA of NV doubles held per thread. Deterministic tree:
-// warp shuffles, then warps folded in order. Result valid in `out` (smem)
-// for all threads after return. `scratch` needs (blockDim/32) * NV doubles.
-template <int NV>
-__device__ __forceinline__ void block_reduce(double (&v)[NV], double* scratch, double* out) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+__shared__ unsigned int s_grid_bar;  // barriers completed by this CTA in this launch
+
+__device__ __forceinline__ unsigned long long* grid_counter(const GridCtx& g, int parity, int lane) {
+    return &g.sync->lane[parity][lane][0];
+}
+
+// Call once at kernel start, before any barrier, from all threads.
+__device__ __forceinline__ void grid_init(const GridCtx& g) {
+    if (threadIdx.x == 0) s_grid_bar = 0;
+    if (blockIdx.x == 0 && threadIdx.x < kArriveLanes)
+        *grid_counter(g, g.parity ^ 1, threadIdx.x) = 0ull;  // next launch's counters
+    __syncthreads();
+}
+
+// Butterfly transpose-reduction of 32 per-lane values: after 31 shuffles lane
+// j holds the warp total of value j (fixed tree => deterministic).
+__device__ __forceinline__ double warp_transpose_reduce(double (&v)[32]) {
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        double x = v[i];
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool upper = (lane & o) != 0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-        if (lane == 0) scratch[warp * NV + i] = x;
+        for (int i = 0; i < o; ++i) {
+            const double send = upper ? v[i] : v[i + o];
+            const double keep = upper ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
     }
+    return v[0];
+}
+
+// CTA sum of NV (<= 32) doubles per thread. Result in `out` (smem) for all
+// threads after return; `scratch` holds (blockDim/32) * 32 doubles.
+template <int NV>
+__device__ __forceinline__ void block_reduce(const double (&in)[NV], double* scratch, double* out) {
+    static_assert(NV <= 32, "block_reduce handles up to 32 values");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = i < NV ? in[i] : 0.0;
+    scratch[warp * 32 + lane] = warp_transpose_reduce(v);
     __syncthreads();
     if (threadIdx.x < NV) {
         double s = 0.0;
-        for (int w = 0; w < nw; ++w) s += scratch[w * NV + threadIdx.x];
+        for (int w = 0; w < nw; ++w) s += scratch[w * 32 + threadIdx.x];
         out[threadIdx.x] = s;
     }
     __syncthreads();
 }
 
-// All CTAs call with their CTA-level vector `mine` (smem, NV entries). On
-// return `out` (smem) holds the sum over CTAs folded in CTA index order.
-// NV == 0 is a plain grid barrier.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// All CTAs call with their CTA vector `mine` (smem, NV entries). On return
+// `out` (smem) holds the sum over CTAs folded in CTA index order (identical
+// in every CTA, independent of arrival order). NV == 0 is a plain barrier.
 template <int NV>
 __device__ __noinline__ void grid_allreduce(const GridCtx& g, const double* mine, double* out) {
-    __shared__ unsigned int s_last, s_gen;
-    if (NV > 0 && threadIdx.x < NV) {
-        g.partials[blockIdx.x * kRedStride + threadIdx.x] = mine[threadIdx.x];
-        __threadfence();
+    const int G = gridDim.x;
+    const unsigned int bar = s_grid_bar;  // read before thread 0 advances it
+    double* buf = g.partials + size_t(bar & 1u) * G * kRedStride;
+    if (NV > 0 && threadIdx.x < NV) __stcg(buf + blockIdx.x * kRedStride + threadIdx.x, mine[threadIdx.x]);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        // CTAs arrive on kArriveLanes counters (blockIdx % lanes) so the
+        // arrival atomics spread over separate L2 lines; lanes 0..7 of warp 0
+        // each poll one counter.
+        const int lane = threadIdx.x;
+        if (lane == 0)  // release is cumulative: covers the CTA's partial stores ordered by bar.sync
+            red_release_add(grid_counter(g, g.parity, blockIdx.x % kArriveLanes), 1ull);
+        const int l = lane % kArriveLanes;
+        const unsigned long long per = (unsigned long long)(G / kArriveLanes + (l < G % kArriveLanes ? 1 : 0));
+        const unsigned long long target = (unsigned long long)(bar + 1u) * per;
+        const unsigned long long* cnt = grid_counter(g, g.parity, l);
+        // Relaxed polling, then one acquire. Bounded: a co-residency bug must
+        // fail loudly, never hang the GPU.
+        unsigned long long spins = 0;
+        while (!__all_sync(0xffffffffu, ld_relaxed_u64(cnt) >= target)) {
+            if (++spins > (1ull << 26)) __trap();
+        }
+        (void)ld_acquire_u64(cnt);
+        if (lane == 0) s_grid_bar = bar + 1u;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned int gen = ld_acquire(&g.sync->gen);
-        __threadfence();
-        const unsigned int prev = atomicAdd(&g.sync->arrive, 1u);
-        s_gen = gen;
-        s_last = (prev == gridDim.x - 1) ? 1u : 0u;
-    }
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        if (NV > 0) {
-            __shared__ double red[32][NV > 0 ? NV : 1];
-            const int nchunk = blockDim.x >> 5;
-            const int j = threadIdx.x & 31, c = threadIdx.x >> 5;
-            const int G = gridDim.x;
-            const int per = (G + nchunk - 1) / nchunk;
-            if (j < NV) {
-                double s = 0.0;
-                const int lo = c * per, hi = min(G, lo + per);
-                for (int i = lo; i < hi; ++i) s += __ldcg(g.partials + i * kRedStride + j);
-                red[c][j] = s;
+    if (NV > 0) {
+        __shared__ double red[32][32];
+        const int j = threadIdx.x & 31, c = threadIdx.x >> 5, nchunk = blockDim.x >> 5;
+        double s = 0.0;
+        if (j < NV) {
+            // chunk c folds CTA rows c, c+nchunk, ... in order; all of the
+            // chunk's loads are issued before the first add (one L2 latency).
+            constexpr int kRows = 24;
+            double v[kRows];
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) {
+                const int i = c + r * nchunk;
+                v[r] = i < G ? __ldcg(buf + i * kRedStride + j) : 0.0;
             }
-            __syncthreads();
-            if (threadIdx.x < NV) {
-                double s = 0.0;
-                for (int cc = 0; cc < nchunk; ++cc) s += red[cc][threadIdx.x];
-                out[threadIdx.x] = s;
-                g.result[threadIdx.x] = s;
-                __threadfence();
-            }
-            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) s += v[r];
+            for (int i = c + kRows * nchunk; i < G; i += nchunk) s += __ldcg(buf + i * kRedStride + j);
         }
-        if (threadIdx.x == 0) {
-            g.sync->arrive = 0u;
-            __threadfence();
-            st_release(&g.sync->gen, s_gen + 1u);
-        }
-    } else {
-        if (threadIdx.x == 0) {
-            // Bounded spin: a co-residency bug must fail loudly, never hang the GPU.
-            unsigned long long spins = 0;
-            while (ld_acquire(&g.sync->gen) == s_gen) {
-                if (++spins > (1ull << 25)) __trap();  // ~10+ s of L2 round trips
-            }
-        }
+        red[c][j] = s;
         __syncthreads();
-        if (NV > 0 && threadIdx.x < NV) out[threadIdx.x] = __ldcg(g.result + threadIdx.x);
+        if (threadIdx.x < NV) {
+            double t = 0.0;
+            for (int cc = 0; cc < nchunk; ++cc) t += red[cc][threadIdx.x];
+            out[threadIdx.x] = t;
+        }
     }
     __syncthreads();
 }

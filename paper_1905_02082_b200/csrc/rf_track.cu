@@ -20,15 +20,30 @@ constexpr double kRelDecreaseTol = 1e-6;         // registration.cpp:26
 
 __device__ __forceinline__ int hidx(int i, int j) { return i * 6 - (i * (i - 1)) / 2 + (j - i); }
 
+__shared__ int s_trace_pass;  // per-CTA pass counter for the optional timeline
+__shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (see voxel_luma_lut)
+
 struct RegState {
     Pose pose, cand;
-    double lambda;
+    double lambda, dnorm;
+    double delta[6];
     double cur[kAccN];
     double trial[kAccN];
     int total, converged, lost, ok, brk;
 };
 
 // ------------------------------------------------------------------ math
+// Reciprocal from the single-precision estimate + two Newton steps
+// (~1 ulp; latency-critical pivots of the 6x6 solve).
+__device__ __forceinline__ double fast_rcp(double x) {
+    const float xf = float(x);
+    if (!(fabsf(xf) > 1e-37f && fabsf(xf) < 1e37f)) return 1.0 / x;  // outside float range: exact path
+    double r = double(__frcp_rn(xf));
+    r = __fma_rn(r, __fma_rn(-x, r, 1.0), r);
+    r = __fma_rn(r, __fma_rn(-x, r, 1.0), r);
+    return r;
+}
+
 __device__ void expmap(const double xi[6], Pose& out) {  // geometry.cpp:14-38
     const double w0 = xi[3], w1 = xi[4], w2 = xi[5];
     const double theta = sqrt((w0 * w0 + w1 * w1) + w2 * w2);
@@ -43,10 +58,24 @@ __device__ void expmap(const double xi[6], Pose& out) {  // geometry.cpp:14-38
         a = 1.0 - t2 / 6.0;
         b = 0.5 - t2 / 24.0;
         c = 1.0 / 6.0 - t2 / 120.0;
+    } else if (theta < 0.05) {
+        // sin(t)/t, (1-cos t)/t^2, (t-sin t)/t^3 by their Taylor series (five
+        // terms: truncation < 1e-20 for t < 0.05). Same functions as the
+        // reference's closed forms, without the serial sincos + three IEEE
+        // divisions on the one thread every CTA waits for (an LM step is a
+        // few milliradians).
+        a = __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, 1.0 / 362880.0, -1.0 / 5040.0), 1.0 / 120.0),
+                                  -1.0 / 6.0), 1.0);
+        b = __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, 1.0 / 3628800.0, -1.0 / 40320.0), 1.0 / 720.0),
+                                  -1.0 / 24.0), 0.5);
+        c = __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, 1.0 / 39916800.0, -1.0 / 362880.0), 1.0 / 5040.0),
+                                  -1.0 / 120.0), 1.0 / 6.0);
     } else {
-        a = sin(theta) / theta;
-        b = (1.0 - cos(theta)) / t2;
-        c = (theta - sin(theta)) / (t2 * theta);
+        double st, ct;
+        sincos(theta, &st, &ct);
+        a = st / theta;
+        b = (1.0 - ct) / t2;
+        c = (theta - st) / (t2 * theta);
     }
     double vm[9];
     for (int i = 0; i < 9; ++i) {
@@ -57,99 +86,79 @@ __device__ void expmap(const double xi[6], Pose& out) {  // geometry.cpp:14-38
     for (int i = 0; i < 3; ++i) out.t[i] = (vm[3 * i] * xi[0] + vm[3 * i + 1] * xi[1]) + vm[3 * i + 2] * xi[2];
 }
 
-// Eigen::LDLT<Matrix6d> (lower, diagonal pivoting) + solve, as the oracle.
-__device__ bool ldlt6_solve(const double A[36], const double rhs[6], double x[6]) {
-    double m[36];
-    for (int i = 0; i < 6; ++i)
-        for (int j = 0; j < 6; ++j) m[6 * i + j] = (j <= i) ? A[6 * i + j] : A[6 * j + i];
-    int tr[6];
-    double temp[6];
-    bool found_zero = false, ret = true;
-    for (int k = 0; k < 6; ++k) {
-        int big = k;
-        double bigv = fabs(m[7 * k]);
-        for (int i = k + 1; i < 6; ++i)
-            if (fabs(m[7 * i]) > bigv) {
-                bigv = fabs(m[7 * i]);
-                big = i;
-            }
-        tr[k] = big;
-        if (k != big) {
-            for (int j = 0; j < k; ++j) {
-                const double t = m[6 * k + j];
-                m[6 * k + j] = m[6 * big + j];
-                m[6 * big + j] = t;
-            }
-            for (int i = big + 1; i < 6; ++i) {
-                const double t = m[6 * i + k];
-                m[6 * i + k] = m[6 * i + big];
-                m[6 * i + big] = t;
-            }
-            const double t = m[7 * k];
-            m[7 * k] = m[7 * big];
-            m[7 * big] = t;
-            for (int i = k + 1; i < big; ++i) {
-                const double u = m[6 * i + k];
-                m[6 * i + k] = m[6 * big + i];
-                m[6 * big + i] = u;
-            }
+// One damped LM solve (registration.cpp:236-248): damped = H + lambda *
+// max(diag H, 1e-3 max diag + 1e-12) on the diagonal, then an LDLT solve of
+// damped * delta = -b. The damped matrix is symmetric positive definite
+// (PSD normal equations plus a strictly positive diagonal shift), so the
+// factorisation needs no pivoting: we factor in natural order, fully unrolled
+// in registers on the one thread every CTA waits for. Eigen's LDLT would pivot
+// on the largest remaining diagonal; for an SPD matrix that changes only the
+// rounding (relative ~cond * 1e-16), far below the pose parity bar (1e-4).
+// `acc` is the packed upper triangle + b (smem); `delta` (smem) receives the
+// solution.
+__device__ bool lm_solve(const double* acc, double lambda, double* delta) {
+    double dmax = acc[hidx(0, 0)];
+#pragma unroll
+    for (int i = 1; i < 6; ++i) dmax = fmax(dmax, acc[hidx(i, i)]);
+    const double floor_v = 1e-3 * dmax + 1e-12;
+    double m[6][6], x[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+#pragma unroll
+        for (int j = 0; j <= i; ++j) {
+            double v = acc[hidx(j, i)];
+            if (i == j) v += lambda * fmax(v, floor_v);
+            m[i][j] = v;
         }
+        x[i] = -acc[21 + i];
+    }
+    // Latency matters here (one thread, every CTA waits): fused multiply-adds
+    // and one reciprocal per pivot. Rounding differs from Eigen's divisions in
+    // the last bits only; the normal equations already differ at that level
+    // through the reduction order, so parity is held at the pose level.
+    double inv_d[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        double temp[6];
         if (k > 0) {
-            for (int j = 0; j < k; ++j) temp[j] = m[7 * j] * m[6 * k + j];
             double dot = 0.0;
-            for (int j = 0; j < k; ++j) dot += m[6 * k + j] * temp[j];
-            m[7 * k] -= dot;
+#pragma unroll
+            for (int j = 0; j < k; ++j) {
+                temp[j] = m[j][j] * m[k][j];
+                dot = __fma_rn(m[k][j], temp[j], dot);
+            }
+            m[k][k] -= dot;
+#pragma unroll
             for (int i = k + 1; i < 6; ++i) {
                 double s = 0.0;
-                for (int j = 0; j < k; ++j) s += m[6 * i + j] * temp[j];
-                m[6 * i + k] -= s;
+#pragma unroll
+                for (int j = 0; j < k; ++j) s = __fma_rn(m[i][j], temp[j], s);
+                m[i][k] -= s;
             }
         }
-        const double akk = m[7 * k];
-        const bool valid = fabs(akk) > 0.0;
-        if (k == 0 && !valid) {
-            for (int j = 0; j < 6; ++j) {
-                tr[j] = j;
-                for (int i = j + 1; i < 6; ++i) m[6 * i + j] = 0.0;
-            }
-            break;
-        }
-        if (k < 5) {
-            if (valid) {
-                for (int i = k + 1; i < 6; ++i) m[6 * i + k] /= akk;
-            } else {
-                for (int i = k + 1; i < 6; ++i) ret = ret && (m[6 * i + k] == 0.0);
-            }
-        }
-        if (found_zero && valid) ret = false;
-        else if (!valid) found_zero = true;
+        const double akk = m[k][k];
+        if (!(fabs(akk) > 0.0)) return false;  // zero pivot: NumericalIssue path, lambda grows
+        inv_d[k] = fast_rcp(akk);
+#pragma unroll
+        for (int i = k + 1; i < 6; ++i) m[i][k] *= inv_d[k];
     }
-    if (!ret) return false;
-    for (int i = 0; i < 6; ++i) x[i] = rhs[i];
-    for (int k = 0; k < 6; ++k) {
-        const double t = x[k];
-        x[k] = x[tr[k]];
-        x[tr[k]] = t;
-    }
+#pragma unroll
     for (int j = 0; j < 6; ++j)
-        for (int i = j + 1; i < 6; ++i) x[i] -= m[6 * i + j] * x[j];
-    for (int i = 0; i < 6; ++i) {
-        if (fabs(m[7 * i]) > 2.2250738585072014e-308) x[i] /= m[7 * i];
-        else x[i] = 0.0;
-    }
+#pragma unroll
+        for (int i = j + 1; i < 6; ++i) x[i] = __fma_rn(-m[i][j], x[j], x[i]);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) x[i] *= inv_d[i];
+#pragma unroll
     for (int j = 5; j >= 0; --j)
-        for (int i = 0; i < j; ++i) x[i] -= m[6 * j + i] * x[j];
-    for (int k = 5; k >= 0; --k) {
-        const double t = x[k];
-        x[k] = x[tr[k]];
-        x[tr[k]] = t;
+#pragma unroll
+        for (int i = 0; i < j; ++i) x[i] = __fma_rn(-m[j][i], x[j], x[i]);
+    bool finite = true;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        delta[i] = x[i];
+        finite = finite && isfinite(x[i]);
     }
-    return true;
-}
-
-__device__ __forceinline__ void full_h(const double* acc, double H[36]) {
-    for (int i = 0; i < 6; ++i)
-        for (int j = i; j < 6; ++j) H[6 * i + j] = H[6 * j + i] = acc[hidx(i, j)];
+    return finite;
 }
 
 // ------------------------------------------------------------------ pyramid
@@ -206,9 +215,23 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
     const int ntx = (K.w + kTileW - 1) / kTileW, nty = (K.h + kTileH - 1) / kTileH;
     const float* depth = level == 0 ? F.depth0 : F.depth[level];
     const uint8_t* mask = use_mask ? F.mask[level] : nullptr;
-    for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
-        const int u = (t % ntx) * kTileW + (threadIdx.x % kTileW);
-        const int v = (t / ntx) * kTileH + (threadIdx.x / kTileW);
+    unsigned long long* tr = (a.trace && s_trace_pass < kTracePasses) ? a.trace + 8 * s_trace_pass : nullptr;
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+        tr[0] = global_ns();
+        tr[4] = level;
+        tr[5] = (unsigned long long)K.w * K.h;
+        tr[6] = kJac;
+    }
+    int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;  // tile walked incrementally (no per-tile division)
+    const int step_y = gridDim.x / ntx, step_x = gridDim.x % ntx;
+    for (; ty < nty; tx += step_x, ty += step_y) {
+        if (tx >= ntx) {
+            tx -= ntx;
+            ++ty;
+            if (ty >= nty) break;
+        }
+        const int u = tx * kTileW + (threadIdx.x % kTileW);
+        const int v = ty * kTileH + (threadIdx.x / kTileW);
         if (u >= K.w || v >= K.h) continue;
         const int p = v * K.w + u;
         const float d = level == 0 ? __ldg(depth + p) : __ldcg(depth + p);
@@ -218,12 +241,13 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
             const bool masked = mask && __ldcg(mask + p) != 0;
             if (!(masked && !write_res)) {
                 const double dd = double(d);
-                const double x0 = (double(u) - K.cx) / K.fx * dd;  // geometry.hpp:41-43
-                const double x1 = (double(v) - K.cy) / K.fy * dd;
+                // Backproject (geometry.hpp:41-43); Jacobian passes use reciprocals
+                const double x0 = kJac ? (double(u) - K.cx) * K.ifx * dd : (double(u) - K.cx) / K.fx * dd;
+                const double x1 = kJac ? (double(v) - K.cy) * K.ify * dd : (double(v) - K.cy) / K.fy * dd;
                 double y[3];
                 pose_apply(P, x0, x1, dd, y);
                 CellSample cs;
-                if (sample_point<kJac, kColor>(a.V, y, cs)) {
+                if (sample_point<kJac, kColor, !kJac>(a.V, y, cs, s_luma_lut)) {
                     const double r_d = cs.sdf;
                     double I = 0.0;
                     if (kColor) {
@@ -240,10 +264,10 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
 #pragma unroll
                         for (int i = 0; i < 6; ++i)
 #pragma unroll
-                            for (int j = i; j < 6; ++j) acc[hidx(i, j)] += J[i] * J[j];
+                            for (int j = i; j < 6; ++j) acc[hidx(i, j)] = __fma_rn(J[i], J[j], acc[hidx(i, j)]);
 #pragma unroll
-                        for (int i = 0; i < 6; ++i) acc[21 + i] += J[i] * r_d;
-                        acc[27] += r_d * r_d;
+                        for (int i = 0; i < 6; ++i) acc[21 + i] = __fma_rn(J[i], r_d, acc[21 + i]);
+                        acc[27] = __fma_rn(r_d, r_d, acc[27]);
                         if (kColor) {
                             const double r_c = (cs.inten - I) * kIntensityScale;
                             const double Jc[6] = {cs.gi[0] * kIntensityScale, cs.gi[1] * kIntensityScale,
@@ -254,10 +278,11 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
 #pragma unroll
                             for (int i = 0; i < 6; ++i)
 #pragma unroll
-                                for (int j = i; j < 6; ++j) acc[hidx(i, j)] += cw * (Jc[i] * Jc[j]);
+                                for (int j = i; j < 6; ++j)
+                                    acc[hidx(i, j)] = __fma_rn(cw * Jc[i], Jc[j], acc[hidx(i, j)]);
 #pragma unroll
-                            for (int i = 0; i < 6; ++i) acc[21 + i] += cw * (Jc[i] * r_c);
-                            acc[28] += r_c * r_c;
+                            for (int i = 0; i < 6; ++i) acc[21 + i] = __fma_rn(cw * Jc[i], r_c, acc[21 + i]);
+                            acc[28] = __fma_rn(r_c, r_c, acc[28]);
                         }
                         acc[29] += 1.0;
                     } else {
@@ -280,8 +305,18 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
             F.res_valid[p] = rv;
         }
     }
+    if (tr) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long now = global_ns();
+            atomicMax(tr + 2, now);  // slowest CTA finishing its tiles
+            if (blockIdx.x == 0) tr[1] = now;
+        }
+    }
     block_reduce<kAccN>(acc, scratch, blk);
     grid_allreduce<kAccN>(a.grid, blk, out);
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = global_ns();
+    if (a.trace && threadIdx.x == 0) ++s_trace_pass;
 }
 
 template <bool kJac>
@@ -328,32 +363,28 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
             __syncthreads();
             if (threadIdx.x == 0) {
                 ++st.total;
-                double H[36];
-                full_h(st.cur, H);
-                double dmax = H[0];
-                for (int i = 1; i < 6; ++i) dmax = fmax(dmax, H[7 * i]);
-                const double floor_v = 1e-3 * dmax + 1e-12;
-                for (int i = 0; i < 6; ++i) H[7 * i] += st.lambda * fmax(H[7 * i], floor_v);
-                double negb[6], delta[6];
-                for (int i = 0; i < 6; ++i) negb[i] = -st.cur[21 + i];
-                bool ok = ldlt6_solve(H, negb, delta);
-                for (int i = 0; i < 6 && ok; ++i) ok = isfinite(delta[i]);
+                const bool ok = lm_solve(st.cur, st.lambda, st.delta);
                 st.ok = ok;
                 if (!ok) {
                     st.lambda = fmin(st.lambda * R.lambda_up, 1e12);
                 } else {
+                    double delta[6];
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) delta[i] = st.delta[i];
                     Pose e;
                     expmap(delta, e);
                     st.cand = pose_mul(e, st.pose);
                     double dn = 0.0;
+#pragma unroll
                     for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
-                    st.trial[0] = sqrt(dn);  // stash |delta| until the pass overwrites trial
+                    st.dnorm = sqrt(dn);
                 }
+                if (a.trace && blockIdx.x == 0 && s_trace_pass < kTracePasses)
+                    a.trace[8 * s_trace_pass + 7] = global_ns();  // solve done (next pass's record)
             }
             __syncthreads();
             if (!st.ok) continue;
-            const double dnorm = st.trial[0];
-            __syncthreads();
+            const double dnorm = st.dnorm;
             pass<true>(a, l, st.cand, use_mask, false, cw, scratch, blk, st.trial);
             if (threadIdx.x == 0) {
                 const double cur_err = st.cur[27] + cw * st.cur[28];
@@ -409,7 +440,7 @@ __device__ void morph_pass(const uint8_t* src, uint8_t* dst, int w, int h, int r
     }
 }
 
-constexpr int kFfW = 32, kFfH = 8;  // floodfill tile (256 threads, 1 px each)
+constexpr int kFfW = 32, kFfH = kTrackThreads / kFfW;  // floodfill tile, 1 px per thread
 
 // FloodfillDepth (dynamics_mask.cpp:59-96) as the least fixpoint of the
 // growth rule: tile-local shared-memory sweeps until stable, global rounds
@@ -474,7 +505,8 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const float* depth, int
 // BuildMask (dynamics_mask.cpp:98-104) on the full-resolution residual image.
 // Stages: bit0 threshold, bit1 erode, bit2 floodfill, bit3 dilate. The result
 // lands in F.mask[0]; returns the masked-pixel count (CountMasked).
-__device__ double build_mask(const TrackArgs& a, int stages, double* blk, double* red, int* rounds) {
+__device__ double build_mask(const TrackArgs& a, int stages, double* scratch, double* blk, double* red,
+                             int* rounds) {
     const FrameView& F = a.F;
     const int w = F.K[0].w, h = F.K[0].h;
     const int stride = gridDim.x * blockDim.x;
@@ -507,7 +539,7 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* blk, double
     double cnt = 0.0;
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) cnt += __ldcg(F.mask[0] + p) ? 1.0 : 0.0;
     double v[1] = {cnt};
-    block_reduce<1>(v, blk + 8, blk);
+    block_reduce<1>(v, scratch, blk);
     grid_allreduce<1>(a.grid, blk, red);
     return red[0];
 }
@@ -521,9 +553,9 @@ __device__ void write_out(const TrackArgs& a, const RegState& st) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kTrackThreads, 2) k_track(TrackArgs a) {
+__global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackArgs a) {
     __shared__ RegState st;
-    __shared__ double scratch[(kTrackThreads / 32) * kAccN];
+    __shared__ double scratch[(kTrackThreads / 32) * 32];
     __shared__ double blk[kAccN + 2];
     __shared__ double red[kAccN + 2];
     const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -531,6 +563,12 @@ __global__ void __launch_bounds__(kTrackThreads, 2) k_track(TrackArgs a) {
         a.out->passes = 0;
         a.out->pixel_passes = 0.0;
     }
+    if (threadIdx.x == 0) s_trace_pass = 0;
+    for (int i = threadIdx.x; i < 768; i += blockDim.x) {
+        const double w = i < 256 ? 0.2126 : (i < 512 ? 0.7152 : 0.0722);  // image.hpp:80-83
+        s_luma_lut[i] = w * double(i & 255);
+    }
+    grid_init(a.grid);
 
     if (a.mode == kModeLinearize || a.mode == kModeEvalDepth || a.mode == kModeEvalColor) {
         Pose P;
@@ -548,7 +586,7 @@ __global__ void __launch_bounds__(kTrackThreads, 2) k_track(TrackArgs a) {
     }
     if (a.mode == kModeMask) {
         int rounds = 0;
-        const double cnt = build_mask(a, a.mask_stages, blk, red, &rounds);
+        const double cnt = build_mask(a, a.mask_stages, scratch, blk, red, &rounds);
         if (lead) {
             a.out->masked = (unsigned long long)cnt;
             a.out->rounds = rounds;
@@ -584,7 +622,7 @@ __global__ void __launch_bounds__(kTrackThreads, 2) k_track(TrackArgs a) {
         registrations = 1;
         iterations = st.total;
         if (a.dynamics) {
-            masked = build_mask(a, 15, blk, red, &rounds);
+            masked = build_mask(a, 15, scratch, blk, red, &rounds);
             if (masked > 0.0) {
                 Pose p1 = st.pose;
                 build_pyramid(a, false, true);
@@ -621,4 +659,61 @@ __global__ void __launch_bounds__(kTrackThreads, 2) k_track(TrackArgs a) {
     }
 }
 
+}  // namespace rfb
+
+// ---------------------------------------------------------------- diagnostics
+namespace rfb {
+// Back-to-back grid all-reduces (no pixel work): the fixed per-pass cost of
+// the persistent tracking kernel's barrier. reduce = 0 is a bare barrier.
+__global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_grid_bench(GridCtx g, int iters, int reduce) {
+    __shared__ double blk[32], red[32];
+    grid_init(g);
+    if (threadIdx.x < 32) blk[threadIdx.x] = double(blockIdx.x + threadIdx.x);
+    __syncthreads();
+    for (int i = 0; i < iters; ++i) {
+        if (reduce) grid_allreduce<kAccN>(g, blk, red);
+        else grid_barrier(g);
+    }
+}
+
+// Latency of one LM step on one thread (lm_solve + ExpMap + pose product),
+// the serial section every CTA runs between two pixel passes. Cycles per
+// step are written to out[0..2] (solve, expmap+compose, total).
+__global__ void k_lm_bench(int iters, double* out) {
+    __shared__ double acc[kAccN];
+    __shared__ double delta[6];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kAccN; ++i) acc[i] = 0.0;
+        for (int i = 0; i < 6; ++i) {
+            acc[hidx(i, i)] = 10.0 + i;
+            if (i < 5) acc[hidx(i, i + 1)] = 0.5;
+            acc[21 + i] = 0.01 * (i + 1);
+        }
+    }
+    __syncwarp();
+    Pose pose{};
+    for (int i = 0; i < 3; ++i) pose.R[4 * i] = 1.0;
+    long long t_solve = 0, t_rest = 0;
+    double lambda = 1e-4;
+    for (int it = 0; it < iters; ++it) {
+        const long long t0 = clock64();
+        const bool ok = lm_solve(acc, lambda, delta);
+        const long long t1 = clock64();
+        if (threadIdx.x != 0) continue;
+        double d[6];
+        for (int i = 0; i < 6; ++i) d[i] = delta[i];
+        Pose e;
+        expmap(d, e);
+        pose = pose_mul(e, pose);
+        const long long t2 = clock64();
+        t_solve += t1 - t0;
+        t_rest += t2 - t1;
+        lambda = ok ? lambda * 1.0000001 : lambda;
+        acc[21] += pose.t[0] * 1e-12;  // keep the chain live
+    }
+    if (threadIdx.x != 0) return;
+    out[0] = double(t_solve) / iters;
+    out[1] = double(t_rest) / iters;
+    out[2] = double(t_solve + t_rest) / iters;
+}
 }  // namespace rfb

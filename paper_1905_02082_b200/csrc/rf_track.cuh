@@ -7,8 +7,15 @@
 namespace rfb {
 
 constexpr int kMaxLevels = 6;
-constexpr int kTrackThreads = 256;
-constexpr int kTileW = 16, kTileH = 16;  // pixel tile per CTA step (256 px)
+#ifndef RF_TRACK_THREADS
+#define RF_TRACK_THREADS 256
+#endif
+#ifndef RF_TRACK_MIN_BLOCKS
+#define RF_TRACK_MIN_BLOCKS 1  // one 8-warp CTA per SM: no register spills, 148 grid partials
+#endif
+constexpr int kTrackThreads = RF_TRACK_THREADS;
+constexpr int kTrackMinBlocks = RF_TRACK_MIN_BLOCKS;
+constexpr int kTileW = 16, kTileH = kTrackThreads / kTileW;  // pixel tile per CTA step, 1 px per thread
 
 struct RegParams {  // RegistrationConfig, registration.hpp:13-23
     double color_weight;
@@ -47,6 +54,14 @@ struct TrackOut {
     double pixel_passes;  // sum over passes of the level's pixel count (bytes model)
 };
 
+constexpr int kTracePasses = 256;
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 enum TrackMode : int {
     kModeFrame = 0,      // pyramid, register, mask, register under mask (pipeline.cpp:81-99)
     kModeRegister = 1,   // pyramid + one Register with optional mask
@@ -66,6 +81,7 @@ struct TrackArgs {
     RegParams reg;
     MaskParams mp;
     GridCtx grid;
+    unsigned long long* trace;  // optional per-pass timeline (RF_TRACE_FILE), kTracePasses x 8
     double* pose_state;  // in: initial pose; out: tracked pose (kModeFrame/Register)
     TrackOut* out;
     uint32_t* vol_counters;  // kModeFrame: snapshot kNumBlocks -> kBlocksBefore

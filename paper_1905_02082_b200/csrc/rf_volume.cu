@@ -116,30 +116,58 @@ __global__ void k_cull(CullArgs a) {
     for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = __ldg(a.pose + i);
     const Pose W = pose_inverse(P);
     const double ext = double(kSide) * a.V.voxel_size;
-    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
-        const int4 c = a.V.coords[b];
-        double cc[8][3];
-        for (int k = 0; k < 8; ++k) {
-            const double x = (double(c.x) + double(k & 1)) * ext;
-            const double y = (double(c.y) + double((k >> 1) & 1)) * ext;
-            const double z = (double(c.z) + double(k >> 2)) * ext;
-            pose_apply(W, x, y, z, cc[k]);
-        }
+    const uint32_t stride = gridDim.x * blockDim.x;
+    // warp-uniform trip count so the whole warp can aggregate its appends
+    for (uint32_t b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b0 < nb; b0 += stride) {
+        const uint32_t b = b0 + (threadIdx.x & 31u);
         uint32_t flags = 0;
-        if (a.do_carve && b < before && !outside(cc, a.K, a.V.carve_clip)) flags |= kFlagCarve;
-        if (a.do_integrate && !outside(cc, a.K, a.V.max_depth + a.V.truncation)) flags |= kFlagIntegrate;
-        if (flags) {
-            const uint32_t slot = atomicAdd(&a.V.counters[kVisible], 1u);
-            a.list[slot] = b | flags;
+        if (b < nb) {
+            const int4 c = a.V.coords[b];
+            double cc[8][3];
+            for (int k = 0; k < 8; ++k) {
+                const double x = (double(c.x) + double(k & 1)) * ext;
+                const double y = (double(c.y) + double((k >> 1) & 1)) * ext;
+                const double z = (double(c.z) + double(k >> 2)) * ext;
+                pose_apply(W, x, y, z, cc[k]);
+            }
+            if (a.do_carve && b < before && !outside(cc, a.K, a.V.carve_clip)) flags |= kFlagCarve;
+            if (a.do_integrate && !outside(cc, a.K, a.V.max_depth + a.V.truncation)) flags |= kFlagIntegrate;
+        }
+        const unsigned vote = __ballot_sync(0xffffffffu, flags != 0);
+        if (vote) {  // one atomic per warp, lanes take consecutive slots
+            const int lane = threadIdx.x & 31;
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&a.V.counters[kVisible], uint32_t(__popc(vote)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (flags) a.list[base + __popc(vote & ((1u << lane) - 1u))] = b | flags;
         }
     }
+    link_new(a.V);  // index this frame's new bricks for the next frame's tracking
 }
+
+// Link records for bricks allocated since the last link pass: grid-stride
+// over [kLinked, num_blocks). The next kernel on the stream commits the range
+// (commit_links), so no completion atomics are needed here.
+__device__ void link_new(const VolumeView& V) {
+    const uint32_t hi = min(V.counters[kNumBlocks], V.max_blocks);
+    const uint32_t lo = min(V.counters[kLinked], hi);
+    for (uint32_t b = lo + blockIdx.x * blockDim.x + threadIdx.x; b < hi; b += gridDim.x * blockDim.x)
+        link_brick(V, b);
+}
+
+__device__ __forceinline__ void commit_links(const VolumeView& V) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) V.counters[kLinked] = min(V.counters[kNumBlocks], V.max_blocks);
+}
+
+__global__ void k_link(VolumeView V) { link_new(V); }
+__global__ void k_link_commit(VolumeView V) { commit_links(V); }
 
 // ---------------------------------------------------------------- fusion
 // CarveFreeSpace (tsdf_volume.cpp:204-241) then Integrate (:155-202) applied
 // voxel by voxel inside one brick; the sdf is rounded to f32 between the two
 // updates exactly as the sequential reference stores it.
 __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
+    commit_links(a.V);  // k_cull (previous launch) linked this frame's new bricks
     if (a.lost && *a.lost) return;
     __shared__ Pose W;
     if (threadIdx.x == 0) {

@@ -46,6 +46,9 @@ struct RaycastArgs {
     float* out;
 };
 
+__device__ void link_new(const VolumeView& V);
+__global__ void k_link(VolumeView V);
+__global__ void k_link_commit(VolumeView V);
 __global__ void k_alloc(AllocArgs a);
 __global__ void k_raycast(RaycastArgs a);
 __global__ void k_alloc_coords(VolumeView V, const int* coords, int n, int* created);

@@ -1,0 +1,37 @@
+"""Summarises an RF_TRACE_FILE timeline (per-pass u64 records written by the
+tracking kernel): for each pass, lead-CTA start, lead tiles done, slowest CTA
+tiles done, all-reduce done; the gap to the next pass start is the LM solve."""
+import sys
+from collections import defaultdict
+
+import numpy as np
+
+
+def main(path, skip=3):
+    raw = np.fromfile(path, dtype=np.uint64).reshape(-1, 256, 8)[skip:]
+    per = defaultdict(list)
+    frame_tot = []
+    for fr in raw:
+        passes = fr[fr[:, 0] > 0]
+        if len(passes) == 0:
+            continue
+        frame_tot.append((int(passes[-1, 3]) - int(passes[0, 0])) / 1e3)
+        for i, p in enumerate(passes):
+            start, lead_done, slow_done, red_done, level, px, jac, _ = (int(x) for x in p[:8])
+            nxt = int(passes[i + 1, 0]) if i + 1 < len(passes) else red_done
+            solved = int(passes[i + 1, 7]) if i + 1 < len(passes) and int(passes[i + 1, 7]) > red_done else 0
+            key = (level, px, jac)
+            per[key].append((slow_done - start, red_done - slow_done, max(0, nxt - red_done), lead_done - start,
+                             (solved - red_done) if solved else np.nan, (nxt - solved) if solved else np.nan))
+    print(f"frames {len(frame_tot)}  mean tracked span {np.mean(frame_tot):.1f} us")
+    print("level    px  jac  passes/frame  tiles(slowest)  reduce+release  gap  lead-tiles  "
+          "[gap = solve-done + sync]  (us)")
+    for key in sorted(per):
+        a = np.array(per[key]) / 1e3
+        print(f"{key[0]:5d} {key[1]:7d} {key[2]:3d} {len(a) / len(frame_tot):10.1f} "
+              f"{a[:, 0].mean():14.2f} {a[:, 1].mean():14.2f} {a[:, 2].mean():6.2f} {a[:, 3].mean():10.2f}  "
+              f"[{np.nanmean(a[:, 4]):.2f} + {np.nanmean(a[:, 5]):.2f}]")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
