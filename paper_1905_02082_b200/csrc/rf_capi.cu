@@ -142,7 +142,7 @@ struct Workspace {
         mask_in.ensure(n);
         res_sq.ensure(n * 4);
         res_valid.ensure(n);
-        mwork.ensure(3 * n);
+        mwork.ensure(ff_offset(w, h) + 4 * size_t((w / 32 + 1) * (h / 32 + 1)));  // 3 masks + floodfill stamps
         size_t off = 0;
         for (int l = 0; l < levels_needed; ++l) {
             const size_t nl = size_t(w >> l) * (h >> l);
@@ -159,6 +159,8 @@ struct Workspace {
         L = levels_needed;
     }
     void sync() { CK(cudaStreamSynchronize(stream)); }
+    static size_t ff_offset(int w, int h) { return (4 * size_t(w) * h + 15) & ~size_t(15); }  // 3 masks + grow bits
+    int* ffstamp() const { return reinterpret_cast<int*>(mwork.as<uint8_t>() + ff_offset(W, H)); }
 };
 
 Intr level_intr(const rf_intrinsics& k, int l) {  // CameraIntrinsics::Scaled (geometry.hpp:27-37)
@@ -319,6 +321,8 @@ struct rf_volume {
         a.F.res_valid = ws.res_valid.as<uint8_t>();
         const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
         for (int i = 0; i < 3; ++i) a.F.mwork[i] = ws.mwork.as<uint8_t>() + i * n;
+        a.F.grow = ws.mwork.as<uint8_t>() + 3 * n;
+        a.F.ffstamp = ws.ffstamp();
         a.grid.sync = ws.gsync.as<GridSync>();
         a.grid.partials = ws.partials.as<double>();
         a.grid.result = ws.result.as<double>();
@@ -882,6 +886,8 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
         a.F.res_sq = ws.res_sq.as<float>();
         a.F.res_valid = ws.res_valid.as<uint8_t>();
         for (int i = 0; i < 3; ++i) a.F.mwork[i] = ws.mwork.as<uint8_t>() + i * n;
+        a.F.grow = ws.mwork.as<uint8_t>() + 3 * n;
+        a.F.ffstamp = ws.ffstamp();
         a.F.mask[0] = ws.mask_in.as<uint8_t>();
         a.grid.sync = ws.gsync.as<GridSync>();
         a.grid.partials = ws.partials.as<double>();

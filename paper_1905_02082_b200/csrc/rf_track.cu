@@ -440,57 +440,225 @@ __device__ void morph_pass(const uint8_t* src, uint8_t* dst, int w, int h, int r
     }
 }
 
-constexpr int kFfW = 32, kFfH = kTrackThreads / kFfW;  // floodfill tile, 1 px per thread
+// Tile-based square morphology: one 32x32 output tile per CTA step, the
+// (32+2r)^2 input window staged in shared memory, the separable row and
+// column passes done there (no global intermediate, no grid barrier between
+// them). `src(gx, gy)` yields the input bit of an in-image pixel.
+constexpr int kMorphTile = 32, kMorphMaxR = 8, kMorphS = kMorphTile + 2 * kMorphMaxR;
+template <bool kErode, class Src>
+__device__ void morph_tile(int tx, int ty, int w, int h, int r, Src src, uint8_t* dst, int& count) {
+    __shared__ uint8_t win[kMorphS * kMorphS];
+    __shared__ uint8_t rowv[kMorphS * kMorphTile];
+    const int S = kMorphTile + 2 * r;
+    const int gx0 = tx * kMorphTile - r, gy0 = ty * kMorphTile - r;
+    for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
+        const int gx = gx0 + i % S, gy = gy0 + i / S;
+        win[i] = (gx >= 0 && gx < w && gy >= 0 && gy < h && src(gx, gy)) ? 1 : 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < S * kMorphTile; i += blockDim.x) {
+        const int y = i / kMorphTile, x = i % kMorphTile;
+        uint8_t v = kErode ? 1 : 0;
+        for (int k = 0; k <= 2 * r; ++k) v = kErode ? (v & win[y * S + x + k]) : (v | win[y * S + x + k]);
+        rowv[i] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kMorphTile * kMorphTile; i += blockDim.x) {
+        const int y = i / kMorphTile, x = i % kMorphTile;
+        const int gx = tx * kMorphTile + x, gy = ty * kMorphTile + y;
+        if (gx >= w || gy >= h) continue;
+        uint8_t v = kErode ? 1 : 0;
+        for (int k = 0; k <= 2 * r; ++k)
+            v = kErode ? (v & rowv[(y + k) * kMorphTile + x]) : (v | rowv[(y + k) * kMorphTile + x]);
+        dst[gy * w + gx] = v;
+        count += v;
+    }
+    __syncthreads();
+}
+
+// Growth-edge bits of FloodfillDepth's rule (dynamics_mask.cpp:84-92) for
+// pixel n: bit k set when neighbour p = n - (kDx[k], kDy[k]) may grow into n,
+// i.e. both depths valid and |D(p) - D(n)| < theta * D(p). Static per frame,
+// so the floodfill sweeps are pure bit operations.
+__device__ __forceinline__ uint8_t grow_bits(const float* depth, int w, int h, int x, int y, double theta,
+                                             int conn) {
+    static constexpr int kDx[8] = {1, -1, 0, 0, 1, 1, -1, -1};  // dynamics_mask.cpp:67-68
+    static constexpr int kDy[8] = {0, 0, 1, -1, 1, -1, 1, -1};
+    const float dn = __ldg(depth + y * w + x);
+    if (!depth_valid(dn)) return 0;
+    uint8_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int px = x - kDx[k], py = y - kDy[k];  // p such that p + (kDx, kDy) = n
+        if (k >= conn || px < 0 || px >= w || py < 0 || py >= h) continue;
+        const float dp = __ldg(depth + py * w + px);
+        if (depth_valid(dp) && fabs(double(dp) - double(dn)) < theta * double(dp)) bits |= uint8_t(1u << k);
+    }
+    return bits;
+}
+
+constexpr int kFfW = 32, kFfH = 32;                 // floodfill tile (square: fewer tile crossings per region)
+constexpr int kFfPx = kFfW * kFfH / kTrackThreads;  // pixels per thread in a tile
 
 // FloodfillDepth (dynamics_mask.cpp:59-96) as the least fixpoint of the
-// growth rule: tile-local shared-memory sweeps until stable, global rounds
-// until no tile changes. Returns the number of global rounds.
-__device__ int floodfill(const TrackArgs& a, uint8_t* m, const float* depth, int w, int h, double theta, int conn,
-                         double* blk, double* red) {
-    __shared__ uint8_t sm[(kFfH + 2) * (kFfW + 2)];
-    __shared__ float sd[(kFfH + 2) * (kFfW + 2)];
-    const int ntx = (w + kFfW - 1) / kFfW, nty = (h + kFfH - 1) / kFfH;
-    const int lx = threadIdx.x % kFfW, ly = threadIdx.x / kFfW;
+// growth rule (its BFS result is seed-order independent, so any monotone
+// schedule reaches it). Per 32x32 tile in shared memory: 32 threads sweep the
+// rows (left to right, then back) and 32 the columns (down, then up) with the
+// per-pixel growth bits (grow_bits), carrying the predecessor in a register,
+// so one sweep grows along any row/column-monotone path; for 8-connectivity a
+// parallel pass adds the diagonal edges; sweeps repeat until one changes
+// nothing. Global rounds repeat until no tile changes; rounds after the first
+// only revisit tiles next to a tile that changed in the previous round
+// (per-tile round stamps), and tiles with no set pixel in tile + halo are
+// skipped. Returns the number of global rounds.
+__device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint8_t* grow, int w, int h, int conn, double* blk,
+                         double* red) {
     constexpr int SW = kFfW + 2;
-    const int me = (ly + 1) * SW + (lx + 1);
-    const int offs[8] = {1, -1, SW, -SW, SW + 1, -SW + 1, SW - 1, -SW - 1};  // kDx/kDy order
+    __shared__ uint8_t sm[(kFfH + 2) * SW];
+    __shared__ uint8_t sg[kFfH * kFfW];
+    __shared__ int s_active;
+    int* stamp = a.F.ffstamp;  // round in which each tile last changed (-1: never)
+    const int ntx = (w + kFfW - 1) / kFfW, nty = (h + kFfH - 1) / kFfH;
+    const int lx = threadIdx.x % kFfW, ly0 = threadIdx.x / kFfW;
+    constexpr int kRowStep = kTrackThreads / kFfW;
     int rounds = 0;
     while (true) {
         int changed_cta = 0;
         for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
-            const int x0 = (t % ntx) * kFfW - 1, y0 = (t / ntx) * kFfH - 1;
-            for (int i = threadIdx.x; i < (kFfH + 2) * SW; i += blockDim.x) {
-                const int gx = x0 + i % SW, gy = y0 + i / SW;
-                const bool in = gx >= 0 && gx < w && gy >= 0 && gy < h;
-                sm[i] = in ? __ldcg(m + gy * w + gx) : 0;
-                sd[i] = in ? __ldg(depth + gy * w + gx) : 0.f;
+            const int tx = t % ntx, ty = t / ntx;
+            if (rounds > 0) {  // active iff a tile in the 3x3 neighbourhood changed last round
+                int act = 0;
+                if (threadIdx.x < 9) {
+                    const int nx = tx + threadIdx.x % 3 - 1, ny = ty + threadIdx.x / 3 - 1;
+                    act = nx >= 0 && nx < ntx && ny >= 0 && ny < nty && __ldcg(stamp + ny * ntx + nx) == rounds - 1;
+                }
+                if (!__syncthreads_or(act)) continue;  // uniform across the CTA
             }
-            __syncthreads();
-            const int gx = x0 + 1 + lx, gy = y0 + 1 + ly;
-            const bool inb = gx < w && gy < h;
-            const uint8_t initial = sm[me];
-            const float dn = sd[me];
-            const bool cand = inb && depth_valid(dn);
+            const int x0 = tx * kFfW - 1, y0 = ty * kFfH - 1;
+            int any = 0;
+            const bool full = (w % 4 == 0) && x0 + 1 + kFfW <= w && y0 + 1 + kFfH <= h;
+            if (full) {  // interior as 32-bit words (one per thread), halo as bytes
+                for (int i = threadIdx.x; i < kFfH * kFfW / 4; i += blockDim.x) {
+                    const int r = i / (kFfW / 4), c = 4 * (i % (kFfW / 4));
+                    const size_t gidx = size_t(y0 + 1 + r) * w + (x0 + 1 + c);
+                    const uint32_t mw = __ldcg(reinterpret_cast<const unsigned int*>(m + gidx));
+                    const uint32_t gw = __ldcg(reinterpret_cast<const unsigned int*>(grow + gidx));
+                    uint8_t* d = sm + (r + 1) * SW + 1 + c;
+                    d[0] = uint8_t(mw);
+                    d[1] = uint8_t(mw >> 8);
+                    d[2] = uint8_t(mw >> 16);
+                    d[3] = uint8_t(mw >> 24);
+                    *reinterpret_cast<uint32_t*>(sg + r * kFfW + c) = gw;
+                    any |= mw != 0;
+                }
+                for (int i = threadIdx.x; i < 4 * (kFfW + 1); i += blockDim.x) {  // halo ring
+                    const int side = i / (kFfW + 1), k = i % (kFfW + 1);
+                    int sx, sy;
+                    if (side == 0) { sx = k; sy = 0; }                  // top row (x 0..32)
+                    else if (side == 1) { sx = k + 1; sy = kFfH + 1; }  // bottom row (x 1..33)
+                    else if (side == 2) { sx = 0; sy = k + 1; }         // left column (y 1..33)
+                    else { sx = kFfW + 1; sy = k; }                     // right column (y 0..32)
+                    const int gx = x0 + sx, gy = y0 + sy;
+                    const uint8_t v = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldcg(m + gy * w + gx) : 0;
+                    sm[sy * SW + sx] = v;
+                    any |= v;
+                }
+            } else {
+                for (int i = threadIdx.x; i < (kFfH + 2) * SW; i += blockDim.x) {
+                    const int gx = x0 + i % SW, gy = y0 + i / SW;
+                    sm[i] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldcg(m + gy * w + gx) : 0;
+                    any |= sm[i];
+                }
+                for (int i = threadIdx.x; i < kFfH * kFfW; i += blockDim.x) {
+                    const int gx = x0 + 1 + i % kFfW, gy = y0 + 1 + i / kFfW;
+                    sg[i] = (gx < w && gy < h) ? __ldcg(grow + gy * w + gx) : 0;
+                }
+            }
+            if (!__syncthreads_or(any)) continue;  // nothing to grow from
+            if (a.trace && threadIdx.x == 0) atomicAdd(a.trace + 8 * (kTracePasses - 2), 1ull);  // seeded tiles
+            uint8_t initial[kFfPx];
+#pragma unroll
+            for (int q = 0; q < kFfPx; ++q) initial[q] = sm[(ly0 + q * kRowStep + 1) * SW + lx + 1];
             while (true) {
                 int ch = 0;
-                if (cand && !sm[me]) {
-                    for (int k = 0; k < conn; ++k) {
-                        const int nb = me + offs[k];
-                        const float dp = sd[nb];
-                        if (sm[nb] && depth_valid(dp) && fabs(double(dp) - double(dn)) < theta * double(dp)) {
-                            sm[me] = 1;
-                            ch = 1;
-                            break;
+                if (threadIdx.x < 64) {
+                    // Thread = one row (0..31) or one column (32..63) of the tile.
+                    // The line's mask bits, growth bits and both halo ends are
+                    // gathered into registers (32-bit masks), swept forward
+                    // (bit 0 from the left / bit 2 from above) and back (bit 1 /
+                    // bit 3) with no memory traffic, and changed pixels stored.
+                    const int line = threadIdx.x & 31;
+                    const bool rows = threadIdx.x < 32;
+                    const int s0 = rows ? (line + 1) * SW + 1 : SW + line + 1;
+                    const int ss = rows ? 1 : SW;
+                    const int g0 = rows ? line * kFfW : line, gs = rows ? 1 : kFfW;
+                    uint32_t set = 0, fwd = 0, bwd = 0;
+                    const uint8_t fb = rows ? 1u : 4u, bb = rows ? 2u : 8u;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        set |= uint32_t(sm[s0 + i * ss] != 0) << i;
+                        const uint8_t g = sg[g0 + i * gs];
+                        fwd |= uint32_t((g & fb) != 0) << i;
+                        bwd |= uint32_t((g & bb) != 0) << i;
+                    }
+                    const uint32_t before = set;
+                    uint32_t carry = sm[s0 - ss] != 0;  // halo predecessor
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const uint32_t bit = (set >> i) & 1u;
+                        const uint32_t nb = bit | (carry & (fwd >> i) & 1u);
+                        set |= nb << i;
+                        carry = nb;
+                    }
+                    carry = sm[s0 + 32 * ss] != 0;
+#pragma unroll
+                    for (int i = 31; i >= 0; --i) {
+                        const uint32_t bit = (set >> i) & 1u;
+                        const uint32_t nb = bit | (carry & (bwd >> i) & 1u);
+                        set |= nb << i;
+                        carry = nb;
+                    }
+                    uint32_t grew = set & ~before;
+                    if (grew) ch = 1;
+                    while (grew) {
+                        const int i = __ffs(grew) - 1;
+                        sm[s0 + i * ss] = 1;
+                        grew &= grew - 1u;
+                    }
+                }
+                if (conn == 8) {
+                    __syncthreads();
+                    const int doff[4] = {-SW - 1, SW - 1, -SW + 1, SW + 1};  // p = n - (kDx, kDy), k = 4..7
+#pragma unroll
+                    for (int q = 0; q < kFfPx; ++q) {
+                        const int ly = ly0 + q * kRowStep, me = (ly + 1) * SW + (lx + 1);
+                        const uint8_t g = sg[ly * kFfW + lx];
+                        if (!sm[me] && (g & 0xF0u)) {
+                            for (int k = 0; k < 4; ++k)
+                                if (((g >> (4 + k)) & 1u) && sm[me + doff[k]]) {
+                                    sm[me] = 1;
+                                    ch = 1;
+                                    break;
+                                }
                         }
                     }
                 }
+                if (a.trace && threadIdx.x == 0) atomicAdd(a.trace + 8 * (kTracePasses - 2) + 1, 1ull);  // sweeps
                 if (!__syncthreads_or(ch)) break;
             }
-            if (inb && sm[me] != initial) {
-                m[gy * w + gx] = 1;
-                changed_cta = 1;
+            int tile_changed = 0;
+#pragma unroll
+            for (int q = 0; q < kFfPx; ++q) {
+                const int ly = ly0 + q * kRowStep, gx = x0 + 1 + lx, gy = y0 + 1 + ly;
+                if (gx < w && gy < h && sm[(ly + 1) * SW + lx + 1] != initial[q]) {
+                    m[gy * w + gx] = 1;
+                    tile_changed = 1;
+                }
             }
-            __syncthreads();
+            if (__syncthreads_or(tile_changed)) {
+                changed_cta = 1;
+                if (threadIdx.x == 0) stamp[t] = rounds;
+            }
         }
         const int any = __syncthreads_or(changed_cta);
         if (threadIdx.x == 0) blk[0] = any ? 1.0 : 0.0;
@@ -503,44 +671,74 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const float* depth, int
 }
 
 // BuildMask (dynamics_mask.cpp:98-104) on the full-resolution residual image.
-// Stages: bit0 threshold, bit1 erode, bit2 floodfill, bit3 dilate. The result
-// lands in F.mask[0]; returns the masked-pixel count (CountMasked).
+// Stages: bit0 threshold, bit1 erode, bit2 floodfill, bit3 dilate (a stage
+// that is off is the identity; without bit0 the input mask is mwork[0]).
+// Pass A (one barrier): threshold + erode per 32x32 tile, growth bits, stamp
+// reset. Floodfill rounds. Pass C: dilate per tile + CountMasked, closed by
+// the all-reduce. The result lands in F.mask[0]; returns the masked count.
 __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, double* blk, double* red,
                              int* rounds) {
     const FrameView& F = a.F;
     const int w = F.K[0].w, h = F.K[0].h;
     const int stride = gridDim.x * blockDim.x;
     const MaskParams& M = a.mp;
-    uint8_t* cur = F.mwork[0];
-    if (stages & 1) {  // ThresholdResiduals (dynamics_mask.cpp:9-18)
-        const double thr = M.gamma * M.truncation * M.truncation;
+    unsigned long long* mt = (a.trace && blockIdx.x == 0 && threadIdx.x == 0) ? a.trace + 8 * (kTracePasses - 1) : nullptr;
+    if (mt) mt[0] = global_ns();
+    const int re = (stages & 2) ? M.erode_radius : 0, rd = (stages & 8) ? M.dilate_radius : 0;
+    const int ntx = (w + kMorphTile - 1) / kMorphTile, nty = (h + kMorphTile - 1) / kMorphTile;
+    const uint8_t* input = F.mwork[0];
+    uint8_t* seeds = F.mwork[1];
+    const double thr = M.gamma * M.truncation * M.truncation;  // ThresholdResiduals (dynamics_mask.cpp:9-18)
+    const bool do_thr = stages & 1;
+    int dummy = 0;
+    if (re <= kMorphMaxR) {
+        for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x)
+            morph_tile<true>(t % ntx, t / ntx, w, h, re,
+                             [&](int gx, int gy) {
+                                 const int p = gy * w + gx;
+                                 return do_thr ? (__ldcg(F.res_valid + p) && double(__ldcg(F.res_sq + p)) > thr)
+                                               : __ldcg(input + p) != 0;
+                             },
+                             seeds, dummy);
+    } else {  // wide windows: threshold, then separable passes through global memory
+        uint8_t* thr_img = F.mwork[2];
         for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride)
-            cur[p] = (__ldcg(F.res_valid + p) && double(__ldcg(F.res_sq + p)) > thr) ? 1 : 0;
+            thr_img[p] = do_thr ? ((__ldcg(F.res_valid + p) && double(__ldcg(F.res_sq + p)) > thr) ? 1 : 0)
+                                : __ldcg(input + p);
         grid_barrier(a.grid);
+        morph_pass(thr_img, F.grow, w, h, re, true, true);
+        grid_barrier(a.grid);
+        morph_pass(F.grow, seeds, w, h, re, true, false);
+        grid_barrier(a.grid);  // F.grow is reused below
     }
-    if ((stages & 2) && M.erode_radius > 0) {
-        morph_pass(cur, F.mwork[1], w, h, M.erode_radius, true, true);
-        grid_barrier(a.grid);
-        morph_pass(F.mwork[1], F.mwork[2], w, h, M.erode_radius, true, false);
-        grid_barrier(a.grid);
-        cur = F.mwork[2];
-    }
-    *rounds = 0;
-    if (stages & 4) *rounds = floodfill(a, cur, F.depth0, w, h, M.theta, M.connectivity, blk, red);
-    if ((stages & 8) && M.dilate_radius > 0) {
-        uint8_t* tmp = (cur == F.mwork[1]) ? F.mwork[0] : F.mwork[1];
-        morph_pass(cur, tmp, w, h, M.dilate_radius, false, true);
-        grid_barrier(a.grid);
-        morph_pass(tmp, F.mask[0], w, h, M.dilate_radius, false, false);
-    } else {
-        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) F.mask[0][p] = __ldcg(cur + p);
+    if (stages & 4) {
+        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride)
+            F.grow[p] = grow_bits(F.depth0, w, h, p % w, p / w, M.theta, M.connectivity);
+        const int nft = ((w + kFfW - 1) / kFfW) * ((h + kFfH - 1) / kFfH);
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nft; i += stride) F.ffstamp[i] = -1;
     }
     grid_barrier(a.grid);
-    double cnt = 0.0;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) cnt += __ldcg(F.mask[0] + p) ? 1.0 : 0.0;
-    double v[1] = {cnt};
+    if (mt) mt[1] = mt[2] = mt[3] = global_ns();
+    *rounds = 0;
+    if (stages & 4) *rounds = floodfill(a, seeds, F.grow, w, h, M.connectivity, blk, red);
+    if (mt) mt[4] = global_ns();
+    int cnt = 0;
+    if (rd <= kMorphMaxR) {
+        for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x)
+            morph_tile<false>(t % ntx, t / ntx, w, h, rd, [&](int gx, int gy) { return __ldcg(seeds + gy * w + gx) != 0; },
+                              F.mask[0], cnt);
+    } else {
+        morph_pass(seeds, F.mwork[2], w, h, rd, false, true);
+        grid_barrier(a.grid);
+        morph_pass(F.mwork[2], F.mask[0], w, h, rd, false, false);
+        grid_barrier(a.grid);
+        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) cnt += __ldcg(F.mask[0] + p) ? 1 : 0;
+    }
+    if (mt) mt[5] = global_ns();
+    double v[1] = {double(cnt)};
     block_reduce<1>(v, scratch, blk);
     grid_allreduce<1>(a.grid, blk, red);
+    if (mt) mt[6] = global_ns();
     return red[0];
 }
 

@@ -41,6 +41,8 @@ struct FrameView {
     float* res_sq;            // full-resolution residual image
     uint8_t* res_valid;
     uint8_t* mwork[3];        // mask build scratch
+    int* ffstamp;             // floodfill per-tile round stamps (32x32 tiles)
+    uint8_t* grow;            // floodfill growth-edge bits per pixel
 };
 
 struct TrackOut {

@@ -11,7 +11,18 @@ def main(path, skip=3):
     raw = np.fromfile(path, dtype=np.uint64).reshape(-1, 256, 8)[skip:]
     per = defaultdict(list)
     frame_tot = []
+    mask = raw[:, 255, :7].astype(np.float64)
+    mask = mask[mask[:, 0] > 0]
+    if len(mask):
+        d = np.diff(mask, axis=1) / 1e3
+        print("mask stages (us): threshold %.1f  erode %.1f  stamp-init %.1f  floodfill %.1f  dilate %.1f  count %.1f"
+              % tuple(d.mean(0)))
+    ff = raw[:, 254, :2].astype(np.float64)
+    ff = ff[ff[:, 0] > 0]
+    if len(ff):
+        print("floodfill per frame: seeded tiles %.1f, sweeps %.1f" % tuple(ff.mean(0)))
     for fr in raw:
+        fr = fr[:254]
         passes = fr[fr[:, 0] > 0]
         if len(passes) == 0:
             continue
