@@ -135,6 +135,7 @@ typedef struct {
 
 typedef struct rf_volume rf_volume;
 typedef struct rf_pipeline rf_pipeline;
+typedef struct rf_mesh rf_mesh;
 
 const char* rf_last_error(void);
 const char* rf_version(void);
@@ -188,6 +189,16 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
 /* ---- raycast (ray-march of RenderVirtualDepth, depth_refinement.cpp:32-79) */
 rf_status rf_raycast(const rf_volume* v, const double view_pose[12], const rf_intrinsics* k,
                      int32_t bisection_iterations, float* out_depth);
+
+/* ---- mesh: ExtractMesh / WritePly (mesh.hpp:14-29) -----------------------
+ * The mesh stays on the device; vertices f32 xyz, colours RGB8, faces i32
+ * triples, in the reference's exact order (blocks sorted by x, y, z). */
+rf_status rf_volume_extract_mesh(const rf_volume* v, int32_t min_weight, rf_mesh** out);   /* ExtractMesh */
+rf_status rf_mesh_counts(const rf_mesh* m, uint64_t* vertices, uint64_t* faces);
+rf_status rf_mesh_copy(const rf_mesh* m, float* xyz, uint8_t* rgb, int32_t* faces);       /* host; any may be NULL */
+rf_status rf_mesh_device_buffers(const rf_mesh* m, const float** xyz, const uint8_t** rgb, const int32_t** faces);
+rf_status rf_mesh_write_ply(const rf_mesh* m, const char* path);                          /* WritePly */
+void rf_mesh_destroy(rf_mesh* m);
 
 /* ---- pipeline (pipeline.hpp:51-96) ------------------------------------- */
 rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipeline** out);

@@ -88,7 +88,8 @@ EXPORTS = [
     "rf_pipeline_last_residuals", "rf_pipeline_last_counters", "rf_host_alloc", "rf_host_free", "rf_device_alloc",
     "rf_device_free", "rf_copy_to_device", "rf_pipeline_set_profiling", "rf_pipeline_stage_times",
     "rf_pipeline_stream", "rf_synth_render", "rf_pipeline_profile_counters", "rf_diag_grid_barrier",
-    "rf_diag_lm_step",
+    "rf_diag_lm_step", "rf_volume_extract_mesh", "rf_mesh_counts", "rf_mesh_copy", "rf_mesh_device_buffers",
+    "rf_mesh_write_ply", "rf_mesh_destroy",
 ]
 
 _lib = None
@@ -109,7 +110,7 @@ def load(path: str = LIB_PATH):
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("rf_last_error", "rf_version", "rf_host_alloc", "rf_device_alloc", "rf_volume_destroy",
-                        "rf_pipeline_destroy", "rf_host_free", "rf_device_free"):
+                        "rf_pipeline_destroy", "rf_host_free", "rf_device_free", "rf_mesh_destroy"):
             fn.restype = C.c_int
     L.rf_host_alloc.restype = vp
     L.rf_host_alloc.argtypes = [C.c_size_t]
@@ -119,6 +120,7 @@ def load(path: str = LIB_PATH):
     L.rf_device_free.argtypes = [vp]
     L.rf_volume_destroy.argtypes = [vp]
     L.rf_pipeline_destroy.argtypes = [vp]
+    L.rf_mesh_destroy.argtypes = [vp]
     L.rf_copy_to_device.argtypes = [vp, vp, C.c_size_t]
     _lib = L
     return L

@@ -274,6 +274,24 @@ class TsdfVolume:
         L.check(_lib().rf_raycast(self.h, _p(_f64(pose)), C.byref(k), bisections, _p(out)))
         return out
 
+    def extract_mesh(self, min_weight=2, ply_path=None):
+        """ExtractMesh (mesh.hpp:25): (vertices f32 (N,3), colours u8 (N,3),
+        faces i32 (M,3)) in the reference's order; optionally WritePly."""
+        m = C.c_void_p()
+        L.check(_lib().rf_volume_extract_mesh(self.h, int(min_weight), C.byref(m)))
+        try:
+            nv, nf = C.c_uint64(), C.c_uint64()
+            L.check(_lib().rf_mesh_counts(m, C.byref(nv), C.byref(nf)))
+            v = np.zeros((nv.value, 3), np.float32)
+            c = np.zeros((nv.value, 3), np.uint8)
+            f = np.zeros((nf.value, 3), np.int32)
+            L.check(_lib().rf_mesh_copy(m, _p(v), _p(c), _p(f)))
+            if ply_path is not None:
+                L.check(_lib().rf_mesh_write_ply(m, str(ply_path).encode()))
+        finally:
+            _lib().rf_mesh_destroy(m)
+        return v, c, f
+
 
 # ------------------------------------------------------------------ mask
 def mask_stages(res_sq, res_valid, depth, config=None, stages=15, device=0):

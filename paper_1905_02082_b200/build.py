@@ -20,7 +20,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fno-fast-math", "-Xptxas", "-warn-spills"]
-SOURCES = ["rf_capi.cu", "rf_track.cu", "rf_volume.cu", "rf_raycast.cu", "rf_synth.cu"]
+SOURCES = ["rf_capi.cu", "rf_track.cu", "rf_volume.cu", "rf_raycast.cu", "rf_synth.cu", "rf_mesh.cu"]
 
 
 def _stale(obj, deps):
@@ -37,7 +37,7 @@ def build(verbose: bool = False, defines=(), variant: str | None = None) -> str:
     build_dir = BUILD if not variant else os.path.join(HERE, "_variants", "obj_" + variant)
     lib = LIB if not variant else os.path.join(HERE, "_variants", f"lib{variant}.so")
     os.makedirs(build_dir, exist_ok=True)
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".inc"))]
     headers.append(os.path.join(os.path.dirname(HERE), "include", "refusion_b200.h"))
     jobs = []
     for src in SOURCES:

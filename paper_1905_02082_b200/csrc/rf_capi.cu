@@ -355,6 +355,13 @@ struct rf_volume {
     }
 };
 
+// Indexed triangle mesh resident on the device (Mesh, mesh.hpp:14-18).
+struct rf_mesh {
+    int device = 0;
+    uint64_t nv = 0, nf = 0;
+    DevBuf xyz, rgb, faces;
+};
+
 namespace {
 
 RegParams to_reg(const rf_registration_config& c, int levels) {
@@ -925,6 +932,112 @@ rf_status rf_raycast(const rf_volume* cv, const double view_pose[12], const rf_i
         CK(cudaMemcpyAsync(out_depth, o.p, n * 4, cudaMemcpyDeviceToHost, v->ws.stream));
         v->ws.sync();
     });
+}
+
+// ---------------------------------------------------------------- mesh
+rf_status rf_volume_extract_mesh(const rf_volume* cv, int32_t min_weight, rf_mesh** out) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && out, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(v->device));
+        auto m = std::make_unique<rf_mesh>();
+        m->device = v->device;
+        const uint32_t n = uint32_t(v->num_blocks());
+        if (n) {
+            DevBuf scratch;
+            const size_t bytes = mesh_scratch_bytes(n);
+            scratch.ensure(bytes);
+            uint32_t* totals = v->ws.h_counters;  // pinned, idle between calls
+            MeshArgs a{};
+            CK(mesh_prepare(v->view, n, min_weight, v->ws.stream, scratch.p, bytes, totals, &a));
+            v->ws.sync();
+            m->nv = totals[0];
+            m->nf = totals[1];
+            m->xyz.ensure(m->nv * 12 + 16);
+            m->rgb.ensure(m->nv * 3 + 16);
+            m->faces.ensure(m->nf * 12 + 16);
+            a.xyz = m->xyz.as<float>();
+            a.rgb = m->rgb.as<uint8_t>();
+            a.faces = m->faces.as<int32_t>();
+            if (m->nv || m->nf) CK(mesh_emit(a, v->ws.stream));
+            v->ws.sync();
+        }
+        *out = m.release();
+    });
+}
+
+rf_status rf_mesh_counts(const rf_mesh* m, uint64_t* vertices, uint64_t* faces) {
+    return guard([&] {
+        require(m, RF_INVALID_ARGUMENT, "null argument");
+        if (vertices) *vertices = m->nv;
+        if (faces) *faces = m->nf;
+    });
+}
+
+rf_status rf_mesh_copy(const rf_mesh* m, float* xyz, uint8_t* rgb, int32_t* faces) {
+    return guard([&] {
+        require(m, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(m->device));
+        if (xyz && m->nv) CK(cudaMemcpy(xyz, m->xyz.p, m->nv * 12, cudaMemcpyDeviceToHost));
+        if (rgb && m->nv) CK(cudaMemcpy(rgb, m->rgb.p, m->nv * 3, cudaMemcpyDeviceToHost));
+        if (faces && m->nf) CK(cudaMemcpy(faces, m->faces.p, m->nf * 12, cudaMemcpyDeviceToHost));
+    });
+}
+
+rf_status rf_mesh_device_buffers(const rf_mesh* m, const float** xyz, const uint8_t** rgb, const int32_t** faces) {
+    return guard([&] {
+        require(m, RF_INVALID_ARGUMENT, "null argument");
+        if (xyz) *xyz = m->xyz.as<float>();
+        if (rgb) *rgb = m->rgb.as<uint8_t>();
+        if (faces) *faces = m->faces.as<int32_t>();
+    });
+}
+
+// WritePly (mesh.cpp:192-231): binary little-endian, float xyz + uchar rgb,
+// uchar-counted int faces.
+rf_status rf_mesh_write_ply(const rf_mesh* m, const char* path) {
+    return guard([&] {
+        require(m && path, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(m->device));
+        std::vector<float> xyz(m->nv * 3);
+        std::vector<uint8_t> rgb(m->nv * 3);
+        std::vector<int32_t> f(m->nf * 3);
+        if (m->nv) {
+            CK(cudaMemcpy(xyz.data(), m->xyz.p, m->nv * 12, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(rgb.data(), m->rgb.p, m->nv * 3, cudaMemcpyDeviceToHost));
+        }
+        if (m->nf) CK(cudaMemcpy(f.data(), m->faces.p, m->nf * 12, cudaMemcpyDeviceToHost));
+        std::ofstream out(path, std::ios::binary);
+        require(bool(out), RF_IO_ERROR, std::string("cannot open for writing: ") + path);
+        out << "ply\nformat binary_little_endian 1.0\n";
+        out << "element vertex " << m->nv << "\n";
+        out << "property float x\nproperty float y\nproperty float z\n";
+        out << "property uchar red\nproperty uchar green\nproperty uchar blue\n";
+        out << "element face " << m->nf << "\n";
+        out << "property list uchar int vertex_indices\n";
+        out << "end_header\n";
+        std::vector<char> buf;
+        buf.reserve(m->nv * 15 + m->nf * 13);
+        for (uint64_t i = 0; i < m->nv; ++i) {
+            buf.insert(buf.end(), reinterpret_cast<const char*>(&xyz[3 * i]), reinterpret_cast<const char*>(&xyz[3 * i]) + 12);
+            buf.insert(buf.end(), reinterpret_cast<const char*>(&rgb[3 * i]), reinterpret_cast<const char*>(&rgb[3 * i]) + 3);
+        }
+        for (uint64_t i = 0; i < m->nf; ++i) {
+            buf.push_back(char(3));
+            buf.insert(buf.end(), reinterpret_cast<const char*>(&f[3 * i]), reinterpret_cast<const char*>(&f[3 * i]) + 12);
+        }
+        out.write(buf.data(), std::streamsize(buf.size()));
+        require(bool(out), RF_IO_ERROR, std::string("write failed: ") + path);
+    });
+}
+
+void rf_mesh_destroy(rf_mesh* m) {
+    if (!m) return;
+    cudaSetDevice(m->device);
+    m->xyz.release();
+    m->rgb.release();
+    m->faces.release();
+    delete m;
 }
 
 // ---------------------------------------------------------------- memory helpers

@@ -46,6 +46,30 @@ struct RaycastArgs {
     float* out;
 };
 
+// Marching cubes (rf_mesh.cu): per-cell state lives in one scratch buffer.
+struct MeshArgs {
+    VolumeView V;
+    uint32_t n;  // bricks
+    int min_weight;
+    const uint32_t* order;  // rank -> pool index, bricks sorted by (x, y, z)
+    const uint32_t* rank;   // pool index -> rank
+    uint16_t* info;         // per cell: 0x100 complete | cube index
+    uint16_t* owned;        // per cell: mask of the edges whose vertex it emits
+    uint16_t* vloc;         // per cell: in-brick vertex offset
+    uint16_t* floc;         // per cell: in-brick face offset
+    uint32_t* vcount;       // per rank (n + 1)
+    uint32_t* fcount;
+    uint32_t* vbase;        // exclusive scans of vcount / fcount
+    uint32_t* fbase;
+    float* xyz;
+    uint8_t* rgb;
+    int32_t* faces;
+};
+size_t mesh_scratch_bytes(uint32_t n);
+cudaError_t mesh_prepare(const VolumeView& V, uint32_t n, int min_weight, cudaStream_t stream, void* scratch,
+                         size_t scratch_bytes, uint32_t* totals, MeshArgs* out);
+cudaError_t mesh_emit(const MeshArgs& a, cudaStream_t stream);
+
 __device__ void link_new(const VolumeView& V);
 __global__ void k_link(VolumeView V);
 __global__ void k_link_commit(VolumeView V);
