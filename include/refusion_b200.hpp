@@ -1,0 +1,736 @@
+// refusion_b200.hpp — C++ host layer over the C ABI (refusion_b200.h).
+//
+// Mirrors the tracker/map interfaces of the CPU reference `tsdfslam`
+// (/root/reference/proj/include/tsdfslam: geometry.hpp, image.hpp,
+// tsdf_volume.hpp, registration.hpp, dynamics_mask.hpp, mesh.hpp,
+// pipeline.hpp, errors.hpp) with the same class / function names, argument
+// meaning and exceptions, so a caller of the reference switches by changing
+// the include and the namespace (`namespace tsdfslam = tsdfslam_b200;`).
+// Eigen is not a dependency: vectors are std::array<double, 3>, rotations
+// row-major std::array<double, 9>.
+//
+// Everything computes on the GPU: the methods marshal host images into an
+// rf_frame and call one C entry point. Header-only; link with
+// -lrefusion_b200 (paper_1905_02082_b200/librefusion_b200.so).
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstddef>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "refusion_b200.h"
+
+namespace tsdfslam_b200 {
+
+// ---------------------------------------------------------------- errors (errors.hpp:9-21)
+struct InsufficientOverlapError : std::runtime_error {
+    explicit InsufficientOverlapError(const std::string& what) : std::runtime_error(what) {}
+};
+struct TrackingLostError : std::runtime_error {
+    explicit TrackingLostError(const std::string& what) : std::runtime_error(what) {}
+};
+struct ResourceLimitError : std::runtime_error {
+    explicit ResourceLimitError(const std::string& what) : std::runtime_error(what) {}
+};
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& what) : std::runtime_error(what) {}
+};
+
+// Rethrows an rf_status as the reference's exception type.
+inline void Check(rf_status s) {
+    if (s == RF_OK) return;
+    const std::string msg = rf_last_error();
+    switch (s) {
+        case RF_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case RF_TRACKING_LOST: throw TrackingLostError(msg);
+        case RF_RESOURCE_LIMIT: throw ResourceLimitError(msg);
+        case RF_IO_ERROR: throw std::runtime_error(msg);
+        case RF_UNSUPPORTED: throw std::invalid_argument("unsupported on the CUDA path: " + msg);
+        default: throw CudaError(msg);
+    }
+}
+
+using Vec3 = std::array<double, 3>;
+using Vec3i = std::array<int, 3>;
+using Vec3f = std::array<float, 3>;
+
+// ---------------------------------------------------------------- geometry (geometry.hpp:11-108)
+struct CameraIntrinsics {
+    double fx = 525.0, fy = 525.0, cx = 319.5, cy = 239.5;
+    int width = 640, height = 480;
+    double depth_scale = 5000.0;
+
+    bool Valid() const {
+        return fx > 0.0 && fy > 0.0 && width > 0 && height > 0 && cx > 0.0 && cx < double(width) && cy > 0.0 &&
+               cy < double(height) && depth_scale > 0.0;
+    }
+    CameraIntrinsics Scaled(int level) const {
+        const double s = 1.0 / double(1 << level);
+        CameraIntrinsics k = *this;
+        k.fx *= s;
+        k.fy *= s;
+        k.cx *= s;
+        k.cy *= s;
+        k.width = width >> level;
+        k.height = height >> level;
+        return k;
+    }
+    rf_intrinsics c() const { return rf_intrinsics{fx, fy, cx, cy, width, height, depth_scale}; }
+};
+
+// Camera-to-world rigid transform; the C ABI's 12-double layout (R row-major, t).
+class Pose {
+  public:
+    Pose() : m_{1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0} {}
+    Pose(const std::array<double, 9>& rotation, const Vec3& translation) {
+        std::memcpy(m_.data(), rotation.data(), 9 * sizeof(double));
+        std::memcpy(m_.data() + 9, translation.data(), 3 * sizeof(double));
+    }
+    static Pose Identity() { return Pose(); }
+    static Pose FromArray(const double p[12]) {
+        Pose r;
+        std::memcpy(r.m_.data(), p, 12 * sizeof(double));
+        return r;
+    }
+    std::array<double, 9> rotation() const { return {m_[0], m_[1], m_[2], m_[3], m_[4], m_[5], m_[6], m_[7], m_[8]}; }
+    Vec3 translation() const { return {m_[9], m_[10], m_[11]}; }
+    const double* data() const { return m_.data(); }
+    double* data() { return m_.data(); }
+
+    Vec3 operator*(const Vec3& x) const {
+        Vec3 r;
+        for (int i = 0; i < 3; ++i) r[i] = m_[3 * i] * x[0] + m_[3 * i + 1] * x[1] + m_[3 * i + 2] * x[2] + m_[9 + i];
+        return r;
+    }
+    Pose operator*(const Pose& o) const {
+        Pose r;
+        for (int i = 0; i < 3; ++i) {
+            for (int j = 0; j < 3; ++j)
+                r.m_[3 * i + j] = m_[3 * i] * o.m_[j] + m_[3 * i + 1] * o.m_[3 + j] + m_[3 * i + 2] * o.m_[6 + j];
+            r.m_[9 + i] = m_[3 * i] * o.m_[9] + m_[3 * i + 1] * o.m_[10] + m_[3 * i + 2] * o.m_[11] + m_[9 + i];
+        }
+        return r;
+    }
+    Pose Inverse() const {
+        Pose r;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) r.m_[3 * i + j] = m_[3 * j + i];
+        for (int i = 0; i < 3; ++i)
+            r.m_[9 + i] = -(r.m_[3 * i] * m_[9] + r.m_[3 * i + 1] * m_[10] + r.m_[3 * i + 2] * m_[11]);
+        return r;
+    }
+
+  private:
+    std::array<double, 12> m_;
+};
+
+// ---------------------------------------------------------------- images (image.hpp:13-103)
+template <typename T>
+class Image {
+  public:
+    Image() = default;
+    Image(int width, int height, T fill = T{})
+        : width_(width), height_(height), data_(std::size_t(width) * height, fill) {}
+    int width() const { return width_; }
+    int height() const { return height_; }
+    bool Empty() const { return data_.empty(); }
+    std::size_t PixelCount() const { return data_.size(); }
+    bool InBounds(int x, int y) const { return x >= 0 && x < width_ && y >= 0 && y < height_; }
+    T& operator()(int x, int y) { return data_[std::size_t(y) * width_ + x]; }
+    const T& operator()(int x, int y) const { return data_[std::size_t(y) * width_ + x]; }
+    T* data() { return data_.data(); }
+    const T* data() const { return data_.data(); }
+    void Fill(T value) { data_.assign(data_.size(), value); }
+    bool SameSize(int w, int h) const { return width_ == w && height_ == h; }
+    template <typename U>
+    bool SameSize(const Image<U>& o) const {
+        return SameSize(o.width(), o.height());
+    }
+    friend bool operator==(const Image& a, const Image& b) {
+        return a.width_ == b.width_ && a.height_ == b.height_ && a.data_ == b.data_;
+    }
+
+  private:
+    int width_ = 0, height_ = 0;
+    std::vector<T> data_;
+};
+
+struct Rgb8 {
+    std::uint8_t r = 0, g = 0, b = 0;
+    friend bool operator==(const Rgb8&, const Rgb8&) = default;
+};
+static_assert(sizeof(Rgb8) == 3);
+
+using DepthImage = Image<float>;
+using ColorImage = Image<Rgb8>;
+using PixelMask = Image<std::uint8_t>;
+
+inline bool DepthValid(float d) { return d > 0.0f && std::isfinite(d); }
+inline std::size_t CountMasked(const PixelMask& m) {
+    std::size_t n = 0;
+    for (std::size_t i = 0; i < m.PixelCount(); ++i) n += m.data()[i] != 0;
+    return n;
+}
+
+struct Frame {
+    double timestamp = 0.0;
+    CameraIntrinsics intrinsics;
+    DepthImage depth;
+    ColorImage color;
+    bool SizesConsistent() const {
+        return depth.SameSize(intrinsics.width, intrinsics.height) && color.SameSize(depth);
+    }
+};
+
+namespace detail {
+inline rf_frame ToC(const Frame& f) {
+    rf_frame c{};
+    c.depth = f.depth.data();
+    c.rgb = f.color.Empty() ? nullptr : reinterpret_cast<const std::uint8_t*>(f.color.data());
+    c.intrinsics = f.intrinsics.c();
+    c.timestamp = f.timestamp;
+    c.memory = RF_MEMORY_HOST;
+    return c;
+}
+inline rf_frame ToC(const DepthImage& d, const CameraIntrinsics& k) {
+    rf_frame c{};
+    c.depth = d.data();
+    c.intrinsics = k.c();
+    c.memory = RF_MEMORY_HOST;
+    return c;
+}
+inline void RequireSize(const DepthImage& d, const CameraIntrinsics& k) {
+    if (!d.SameSize(k.width, k.height)) throw std::invalid_argument("depth image does not match the intrinsics");
+}
+inline const std::uint8_t* MaskPtr(const PixelMask* m, int w, int h) {
+    if (!m || m->Empty()) return nullptr;
+    if (!m->SameSize(w, h)) throw std::invalid_argument("mask size does not match the frame");
+    return m->data();
+}
+}  // namespace detail
+
+// ---------------------------------------------------------------- volume (tsdf_volume.hpp:14-134)
+struct VolumeConfig {
+    double voxel_size = 0.01, truncation = 0.1;
+    int block_side = 8, max_weight = 64, carve_weight = 1;
+    double min_depth = 0.1, max_depth = 5.0, carve_clip = 4.0;
+    std::size_t max_blocks = 1000000;
+    std::size_t hash_capacity = 0;  // GPU only: 0 = next power of two >= 4/3 max_blocks
+
+    void Validate() const {
+        if (!(voxel_size > 0) || !(truncation >= voxel_size) || block_side < 2 || max_weight < 1 ||
+            max_weight > 255 || carve_weight < 1 || carve_weight > max_weight || !(min_depth > 0) ||
+            !(max_depth > min_depth) || !(carve_clip > 0) || max_blocks == 0)
+            throw std::invalid_argument("invalid VolumeConfig");
+    }
+    rf_volume_config c() const {
+        rf_volume_config r{};
+        r.voxel_size = voxel_size;
+        r.truncation = truncation;
+        r.block_side = block_side;
+        r.max_weight = max_weight;
+        r.carve_weight = carve_weight;
+        r.min_depth = min_depth;
+        r.max_depth = max_depth;
+        r.carve_clip = carve_clip;
+        r.max_blocks = max_blocks;
+        r.hash_capacity = hash_capacity;
+        return r;
+    }
+};
+
+struct Voxel {
+    float sdf = 0.f;
+    std::uint8_t weight = 0;
+    std::uint8_t r = 0, g = 0, b = 0;
+};
+static_assert(sizeof(Voxel) == 8);
+
+struct VoxelBlock {
+    Vec3i coord{};
+    std::vector<Voxel> voxels;  // 512, x fastest
+};
+
+struct SdfSample {
+    double value = 0.0;
+    bool valid = false;
+};
+struct SdfGradientSample {
+    double value = 0.0;
+    Vec3 gradient{};
+    bool valid = false;
+};
+
+struct Mesh {  // mesh.hpp:14-18
+    std::vector<Vec3f> vertices;
+    std::vector<Rgb8> colors;
+    std::vector<Vec3i> faces;
+};
+
+class TsdfVolume {
+  public:
+    explicit TsdfVolume(VolumeConfig config, int device = 0) : config_(config), owned_(true) {
+        config_.Validate();
+        const rf_volume_config c = config_.c();
+        Check(rf_volume_create(&c, device, &h_));
+    }
+    ~TsdfVolume() {
+        if (owned_ && h_) rf_volume_destroy(h_);
+    }
+    TsdfVolume(const TsdfVolume&) = delete;
+    TsdfVolume& operator=(const TsdfVolume&) = delete;
+    TsdfVolume(TsdfVolume&& o) noexcept : config_(o.config_), h_(o.h_), owned_(o.owned_) { o.h_ = nullptr; }
+
+    const VolumeConfig& config() const { return config_; }
+    rf_volume* handle() const { return h_; }
+
+    std::size_t num_blocks() const {
+        std::uint64_t n = 0;
+        Check(rf_volume_num_blocks(h_, &n));
+        return n;
+    }
+
+    void AllocateForFrame(const DepthImage& depth, const CameraIntrinsics& k, const Pose& camera_to_world,
+                          const PixelMask* mask = nullptr) {
+        detail::RequireSize(depth, k);
+        const rf_frame f = detail::ToC(depth, k);
+        Check(rf_volume_allocate_for_frame(h_, &f, camera_to_world.data(), detail::MaskPtr(mask, k.width, k.height)));
+    }
+    void Integrate(const Frame& frame, const Pose& camera_to_world, const PixelMask* mask = nullptr,
+                   int /*threads*/ = 1) {
+        if (!frame.SizesConsistent() && !(frame.color.Empty() && frame.depth.SameSize(frame.intrinsics.width,
+                                                                                      frame.intrinsics.height)))
+            throw std::invalid_argument("frame sizes are inconsistent");
+        const rf_frame f = detail::ToC(frame);
+        Check(rf_volume_integrate(h_, &f, camera_to_world.data(),
+                                  detail::MaskPtr(mask, frame.intrinsics.width, frame.intrinsics.height)));
+    }
+    void CarveFreeSpace(const DepthImage& depth, const CameraIntrinsics& k, const Pose& camera_to_world,
+                        int /*threads*/ = 1) {
+        detail::RequireSize(depth, k);
+        const rf_frame f = detail::ToC(depth, k);
+        Check(rf_volume_carve(h_, &f, camera_to_world.data()));
+    }
+
+    // Batched sampling (one launch for all points); single-point forms below.
+    std::vector<SdfGradientSample> Sample(int mode, const std::vector<Vec3>& points) const {
+        const std::size_t n = points.size();
+        std::vector<double> val(n), grad(3 * n);
+        std::vector<std::uint8_t> ok(n);
+        if (n) Check(rf_volume_sample(h_, mode, points[0].data(), n, val.data(), grad.data(), ok.data()));
+        std::vector<SdfGradientSample> out(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            out[i].value = val[i];
+            out[i].gradient = {grad[3 * i], grad[3 * i + 1], grad[3 * i + 2]};
+            out[i].valid = ok[i] != 0;
+        }
+        return out;
+    }
+    SdfSample SampleSdf(const Vec3& p) const { return Value(0, p); }
+    SdfSample SampleIntensity(const Vec3& p) const { return Value(1, p); }
+    SdfGradientSample SampleSdfWithGradient(const Vec3& p) const { return Sample(2, {p})[0]; }
+    SdfGradientSample SampleIntensityWithGradient(const Vec3& p) const { return Sample(3, {p})[0]; }
+    SdfGradientSample SampleSdfGradient(const Vec3& p) const { return Sample(4, {p})[0]; }
+
+    // VoxelHandle: the GPU owns the voxels, so reads return a copy and writes
+    // go through SetVoxel (the reference's mutable handle).
+    std::optional<Voxel> VoxelHandle(const Vec3i& voxel) const {
+        Voxel v;
+        std::uint8_t found = 0;
+        Check(rf_volume_get_voxels(h_, voxel.data(), 1, reinterpret_cast<std::uint8_t*>(&v), &found));
+        if (!found) return std::nullopt;
+        return v;
+    }
+    bool SetVoxel(const Vec3i& voxel, const Voxel& value) {
+        std::uint64_t missing = 0;
+        Check(rf_volume_set_voxels(h_, voxel.data(), 1, reinterpret_cast<const std::uint8_t*>(&value), &missing));
+        return missing == 0;
+    }
+    Vec3 VoxelCenter(const Vec3i& v) const {
+        return {(v[0] + 0.5) * config_.voxel_size, (v[1] + 0.5) * config_.voxel_size,
+                (v[2] + 0.5) * config_.voxel_size};
+    }
+    double block_extent() const { return config_.block_side * config_.voxel_size; }
+
+    bool AllocateBlock(const Vec3i& block_coord) {
+        std::int32_t created = 0;
+        Check(rf_volume_allocate_blocks(h_, block_coord.data(), 1, &created));
+        return created != 0;
+    }
+    std::optional<VoxelBlock> FindBlock(const Vec3i& block_coord) const {
+        for (VoxelBlock& b : blocks())
+            if (b.coord == block_coord) return std::move(b);
+        return std::nullopt;
+    }
+    // blocks() in allocation order (a device -> host copy).
+    std::vector<VoxelBlock> blocks() const {
+        std::uint64_t n = 0;
+        Check(rf_volume_export_blocks(h_, nullptr, nullptr, 0, &n));
+        std::vector<std::int32_t> c(3 * n);
+        std::vector<Voxel> v(n * 512);
+        if (n)
+            Check(rf_volume_export_blocks(h_, c.data(), reinterpret_cast<std::uint8_t*>(v.data()), n, &n));
+        std::vector<VoxelBlock> out(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            out[i].coord = {c[3 * i], c[3 * i + 1], c[3 * i + 2]};
+            out[i].voxels.assign(v.begin() + i * 512, v.begin() + (i + 1) * 512);
+        }
+        return out;
+    }
+
+    void Save(const std::string& path) const { Check(rf_volume_save(h_, path.c_str())); }
+    static TsdfVolume Load(const std::string& path, int device = 0) {
+        rf_volume* h = nullptr;
+        Check(rf_volume_load(path.c_str(), device, &h));
+        return TsdfVolume(h, true);
+    }
+    static TsdfVolume Borrow(rf_volume* h) { return TsdfVolume(h, false); }
+
+  private:
+    TsdfVolume(rf_volume* h, bool owned) : h_(h), owned_(owned) {
+        // Config travels with the handle only through Save/Load; callers of
+        // Borrow/Load that need it use the pipeline's config.
+    }
+    SdfSample Value(int mode, const Vec3& p) const {
+        const SdfGradientSample s = Sample(mode, {p})[0];
+        return SdfSample{s.value, s.valid};
+    }
+    VolumeConfig config_;
+    rf_volume* h_ = nullptr;
+    bool owned_ = false;
+};
+
+// ---------------------------------------------------------------- registration (registration.hpp:13-85)
+struct RegistrationConfig {
+    double color_weight = 0.025;
+    int pyramid_levels = 3, max_iterations = 20;
+    double lm_lambda_init = 1e-4, lm_lambda_up = 10.0, lm_lambda_down = 2.0, convergence_eps = 1e-5;
+    int min_valid_residuals = 100, threads = 1;
+    rf_registration_config c() const {
+        return rf_registration_config{color_weight,   pyramid_levels, max_iterations, lm_lambda_init,
+                                      lm_lambda_up,   lm_lambda_down, convergence_eps, min_valid_residuals,
+                                      threads};
+    }
+};
+
+struct ResidualImage {
+    Image<float> squared;
+    PixelMask valid;
+};
+
+struct LinearizeResult {
+    std::array<double, 36> H{};  // row-major 6x6
+    std::array<double, 6> b{};
+    double depth_error = 0.0, color_error = 0.0, error = 0.0;
+    std::size_t valid_count = 0;
+    bool degenerate = false;
+};
+
+struct RegistrationResult {
+    Pose pose = Pose::Identity();
+    bool converged = false;
+    int iterations = 0;
+    std::size_t valid_residuals = 0;
+    double final_error = 0.0;
+    ResidualImage residuals;
+};
+
+inline LinearizeResult Linearize(const TsdfVolume& volume, const Frame& frame, const Pose& pose,
+                                 const RegistrationConfig& config, const PixelMask* mask = nullptr) {
+    const rf_frame f = detail::ToC(frame);
+    const rf_registration_config c = config.c();
+    rf_linearize_result r{};
+    Check(rf_linearize(volume.handle(), &f, pose.data(), &c,
+                       detail::MaskPtr(mask, frame.intrinsics.width, frame.intrinsics.height), &r));
+    LinearizeResult out;
+    std::memcpy(out.H.data(), r.H, sizeof(r.H));
+    std::memcpy(out.b.data(), r.b, sizeof(r.b));
+    out.depth_error = r.depth_error;
+    out.color_error = r.color_error;
+    out.error = r.error;
+    out.valid_count = r.valid_count;
+    out.degenerate = r.degenerate != 0;
+    return out;
+}
+
+inline std::pair<double, ResidualImage> EvaluateDepthError(const TsdfVolume& volume, const Frame& frame,
+                                                           const Pose& pose, const PixelMask* mask = nullptr,
+                                                           int /*threads*/ = 1) {
+    const int w = frame.intrinsics.width, h = frame.intrinsics.height;
+    const rf_frame f = detail::ToC(frame);
+    ResidualImage res{Image<float>(w, h), PixelMask(w, h)};
+    double e = 0.0;
+    Check(rf_evaluate_depth_error(volume.handle(), &f, pose.data(), detail::MaskPtr(mask, w, h), &e,
+                                  res.squared.data(), res.valid.data()));
+    return {e, std::move(res)};
+}
+
+inline double EvaluateColorError(const TsdfVolume& volume, const Frame& frame, const Pose& pose,
+                                 const PixelMask* mask = nullptr, int /*threads*/ = 1) {
+    const rf_frame f = detail::ToC(frame);
+    double e = 0.0;
+    Check(rf_evaluate_color_error(volume.handle(), &f, pose.data(),
+                                  detail::MaskPtr(mask, frame.intrinsics.width, frame.intrinsics.height), &e));
+    return e;
+}
+
+inline RegistrationResult Register(const TsdfVolume& volume, const Frame& frame, const Pose& initial_pose,
+                                   const PixelMask* mask, const RegistrationConfig& config) {
+    const int w = frame.intrinsics.width, h = frame.intrinsics.height;
+    const rf_frame f = detail::ToC(frame);
+    const rf_registration_config c = config.c();
+    rf_registration_result r{};
+    RegistrationResult out;
+    out.residuals = ResidualImage{Image<float>(w, h), PixelMask(w, h)};
+    Check(rf_register(volume.handle(), &f, initial_pose.data(), detail::MaskPtr(mask, w, h), &c, &r,
+                      out.residuals.squared.data(), out.residuals.valid.data()));
+    out.pose = Pose::FromArray(r.pose);
+    out.converged = r.converged != 0;
+    out.iterations = r.iterations;
+    out.valid_residuals = r.valid_residuals;
+    out.final_error = r.final_error;
+    return out;
+}
+
+// ---------------------------------------------------------------- dynamics mask (dynamics_mask.hpp:10-41)
+struct MaskConfig {
+    double gamma = 0.5, truncation = 0.1, theta = 0.007;
+    int erode_radius = 2, dilate_radius = 2, connectivity = 4;
+    rf_mask_config c() const {
+        return rf_mask_config{gamma, truncation, theta, erode_radius, dilate_radius, connectivity, 0};
+    }
+};
+
+namespace detail {
+inline PixelMask MaskStages(const float* sq, const std::uint8_t* valid, const float* depth, int w, int h,
+                            const MaskConfig& config, int stages, int device = 0) {
+    PixelMask out(w, h);
+    const rf_mask_config c = config.c();
+    std::uint64_t n = 0;
+    Check(rf_mask_stages(sq, valid, depth, w, h, &c, stages, device, out.data(), &n));
+    return out;
+}
+}  // namespace detail
+
+inline PixelMask ThresholdResiduals(const ResidualImage& r, const MaskConfig& config) {
+    return detail::MaskStages(r.squared.data(), r.valid.data(), nullptr, r.squared.width(), r.squared.height(),
+                              config, 1);
+}
+inline PixelMask Erode(const PixelMask& mask, int radius) {
+    MaskConfig c;
+    c.erode_radius = radius;
+    return detail::MaskStages(nullptr, mask.data(), nullptr, mask.width(), mask.height(), c, 2);
+}
+inline PixelMask Dilate(const PixelMask& mask, int radius) {
+    MaskConfig c;
+    c.dilate_radius = radius;
+    return detail::MaskStages(nullptr, mask.data(), nullptr, mask.width(), mask.height(), c, 8);
+}
+inline PixelMask FloodfillDepth(const PixelMask& seeds, const DepthImage& depth, double theta, int connectivity) {
+    MaskConfig c;
+    c.theta = theta;
+    c.connectivity = connectivity;
+    return detail::MaskStages(nullptr, seeds.data(), depth.data(), seeds.width(), seeds.height(), c, 4);
+}
+inline PixelMask BuildMask(const ResidualImage& r, const DepthImage& depth, const MaskConfig& config) {
+    return detail::MaskStages(r.squared.data(), r.valid.data(), depth.data(), depth.width(), depth.height(), config,
+                              15);
+}
+
+// ---------------------------------------------------------------- raycast / mesh
+// Ray-march of RenderVirtualDepth (depth_refinement.cpp:32-79) over `volume`.
+inline DepthImage Raycast(const TsdfVolume& volume, const Pose& view_pose, const CameraIntrinsics& k,
+                          int bisection_iterations = 8) {
+    DepthImage out(k.width, k.height);
+    const rf_intrinsics ck = k.c();
+    Check(rf_raycast(volume.handle(), view_pose.data(), &ck, bisection_iterations, out.data()));
+    return out;
+}
+
+inline Mesh ExtractMesh(const TsdfVolume& volume, int min_weight = 2, int /*threads*/ = 1) {
+    rf_mesh* m = nullptr;
+    Check(rf_volume_extract_mesh(volume.handle(), min_weight, &m));
+    Mesh out;
+    std::uint64_t nv = 0, nf = 0;
+    rf_status s = rf_mesh_counts(m, &nv, &nf);
+    if (s == RF_OK) {
+        out.vertices.resize(nv);
+        out.colors.resize(nv);
+        out.faces.resize(nf);
+        s = rf_mesh_copy(m, out.vertices.empty() ? nullptr : out.vertices[0].data(),
+                         out.colors.empty() ? nullptr : &out.colors[0].r,
+                         out.faces.empty() ? nullptr : out.faces[0].data());
+    }
+    rf_mesh_destroy(m);
+    Check(s);
+    return out;
+}
+
+// ---------------------------------------------------------------- pipeline (pipeline.hpp:18-96, config.hpp:12-24)
+struct RefinementConfig {  // depth_refinement.hpp:12-17
+    bool enabled = true;
+    int window = 10;
+    double far_value = 8.0;
+    int bisection_iterations = 8;
+};
+
+struct PipelineConfig {
+    VolumeConfig volume;
+    RegistrationConfig registration;
+    MaskConfig mask;
+    RefinementConfig refinement;
+    bool dynamics_enabled = true;
+    int threads = 1;
+    double max_dt = 0.02;
+
+    void Sync() {  // config.cpp: the mask threshold follows the volume truncation
+        mask.truncation = volume.truncation;
+        volume.Validate();
+    }
+    rf_pipeline_config c() const {
+        rf_pipeline_config r{};
+        r.volume = volume.c();
+        r.registration = registration.c();
+        r.mask = mask.c();
+        r.refine_enabled = refinement.enabled ? 1 : 0;
+        r.refine_window = refinement.window;
+        r.far_value = refinement.far_value;
+        r.bisection_iterations = refinement.bisection_iterations;
+        r.dynamics_enabled = dynamics_enabled ? 1 : 0;
+        r.threads = threads;
+        return r;
+    }
+};
+
+struct FrameStats {
+    std::size_t frame_index = 0;
+    double timestamp = 0.0;
+    bool tracking_lost = false, converged = false;
+    int registrations = 0, iterations = 0;
+    std::size_t valid_residuals = 0, masked_pixels = 0;
+    double final_error = 0.0, runtime_ms = 0.0;
+};
+
+struct FrameDebug {
+    std::size_t frame_index = 0;
+    double timestamp = 0.0;
+    const PixelMask* mask = nullptr;
+    const ResidualImage* residuals = nullptr;
+    const DepthImage* virtual_depth = nullptr;
+    const DepthImage* refined_depth = nullptr;
+};
+
+struct TrajectoryEntry {
+    double timestamp = 0.0;
+    Pose pose;
+};
+using Trajectory = std::vector<TrajectoryEntry>;
+
+class Pipeline {
+  public:
+    explicit Pipeline(PipelineConfig config, int device = 0) : config_(std::move(config)) {
+        config_.Sync();
+        const rf_pipeline_config c = config_.c();
+        Check(rf_pipeline_create(&c, device, &h_));
+        rf_volume* v = nullptr;
+        Check(rf_pipeline_volume(h_, &v));
+        volume_.emplace(TsdfVolume::Borrow(v));
+    }
+    ~Pipeline() {
+        volume_.reset();
+        if (h_) rf_pipeline_destroy(h_);
+    }
+    Pipeline(const Pipeline&) = delete;
+    Pipeline& operator=(const Pipeline&) = delete;
+
+    FrameStats ProcessFrame(const Frame& frame) {
+        if (!frame.depth.SameSize(frame.intrinsics.width, frame.intrinsics.height) ||
+            (!frame.color.Empty() && !frame.color.SameSize(frame.depth)))
+            throw std::invalid_argument("frame sizes are inconsistent");
+        const rf_frame f = detail::ToC(frame);
+        rf_frame_stats s{};
+        double pose[12];
+        Check(rf_pipeline_process_frame(h_, &f, &s, pose));
+        FrameStats out;
+        out.frame_index = s.frame_index;
+        out.timestamp = s.timestamp;
+        out.tracking_lost = s.tracking_lost != 0;
+        out.converged = s.converged != 0;
+        out.registrations = s.registrations;
+        out.iterations = s.iterations;
+        out.valid_residuals = s.valid_residuals;
+        out.masked_pixels = s.masked_pixels;
+        out.final_error = s.final_error;
+        out.runtime_ms = s.runtime_ms;
+        trajectory_.push_back(TrajectoryEntry{frame.timestamp, Pose::FromArray(pose)});
+        stats_.push_back(out);
+        if (debug_sink_) EmitDebug(frame, out);
+        return out;
+    }
+    void Finalize() { Check(rf_pipeline_finalize(h_)); }
+
+    const Trajectory& trajectory() const { return trajectory_; }
+    const TsdfVolume& volume() const { return *volume_; }
+    const std::vector<FrameStats>& stats() const { return stats_; }
+    const PipelineConfig& config() const { return config_; }
+    std::size_t tracking_losses() const {
+        std::uint64_t n = 0;
+        Check(rf_pipeline_tracking_losses(h_, &n));
+        return n;
+    }
+    void set_debug_sink(std::function<void(const FrameDebug&)> sink) { debug_sink_ = std::move(sink); }
+    rf_pipeline* handle() const { return h_; }
+
+  private:
+    void EmitDebug(const Frame& frame, const FrameStats& st) {
+        const int w = frame.intrinsics.width, h = frame.intrinsics.height;
+        FrameDebug d;
+        d.frame_index = st.frame_index;
+        d.timestamp = st.timestamp;
+        PixelMask mask(w, h);
+        std::int32_t has_mask = 0;
+        Check(rf_pipeline_last_mask(h_, mask.data(), &has_mask));
+        ResidualImage res{Image<float>(w, h), PixelMask(w, h)};
+        if (st.frame_index > 0 && !st.tracking_lost) {
+            Check(rf_pipeline_last_residuals(h_, res.squared.data(), res.valid.data()));
+            d.residuals = &res;
+        }
+        if (has_mask) d.mask = &mask;
+        debug_sink_(d);
+    }
+
+    PipelineConfig config_;
+    rf_pipeline* h_ = nullptr;
+    std::optional<TsdfVolume> volume_;
+    Trajectory trajectory_;
+    std::vector<FrameStats> stats_;
+    std::function<void(const FrameDebug&)> debug_sink_;
+};
+
+using FrameSource = std::function<std::optional<Frame>()>;
+struct SequenceSummary {
+    std::size_t frames = 0;
+    std::size_t tracking_losses = 0;
+};
+
+// RunSequence (pipeline.cpp:137-145).
+inline SequenceSummary RunSequence(Pipeline& pipeline, const FrameSource& source) {
+    SequenceSummary s;
+    while (std::optional<Frame> f = source()) {
+        pipeline.ProcessFrame(*f);
+        ++s.frames;
+    }
+    pipeline.Finalize();
+    s.tracking_losses = pipeline.tracking_losses();
+    return s;
+}
+
+}  // namespace tsdfslam_b200
