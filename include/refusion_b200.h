@@ -190,6 +190,16 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
 rf_status rf_raycast(const rf_volume* v, const double view_pose[12], const rf_intrinsics* k,
                      int32_t bisection_iterations, float* out_depth);
 
+/* ---- depth refinement (depth_refinement.hpp:46-57) ----------------------
+ * RenderVirtualDepth over a window of n frames (their poses, masks[i] may be
+ * NULL, masks itself may be NULL) seen from view_pose with intrinsics k, in a
+ * fresh volume of config vcfg; RefineDepth of frames[0] into refined_depth
+ * when it is non-NULL. */
+rf_status rf_render_virtual_depth(const rf_frame* frames, const double* poses, const uint8_t* const* masks, int32_t n,
+                                  const double view_pose[12], const rf_intrinsics* k, const rf_volume_config* vcfg,
+                                  int32_t bisection_iterations, double far_value, int device, float* virtual_depth,
+                                  float* refined_depth);
+
 /* ---- mesh: ExtractMesh / WritePly (mesh.hpp:14-29) -----------------------
  * The mesh stays on the device; vertices f32 xyz, colours RGB8, faces i32
  * triples, in the reference's exact order (blocks sorted by x, y, z). */
@@ -213,6 +223,15 @@ rf_status rf_pipeline_trajectory(const rf_pipeline* p, double* timestamps, doubl
 rf_status rf_pipeline_last_mask(const rf_pipeline* p, uint8_t* out, int32_t* has_mask);    /* FrameDebug::mask */
 rf_status rf_pipeline_last_residuals(const rf_pipeline* p, float* res_sq, uint8_t* res_valid); /* FrameDebug::residuals */
 rf_status rf_pipeline_last_counters(const rf_pipeline* p, rf_frame_counters* out);
+/* Refinement window (refine_enabled): frames waiting for integration, and the
+ * FrameDebug::virtual_depth / refined_depth of the last IntegrateFront. The
+ * pipeline ray-marches only raw-depth holes unless debug images are enabled;
+ * virtual_depth requires them. */
+rf_status rf_pipeline_window_size(const rf_pipeline* p, uint64_t* out);
+rf_status rf_pipeline_finalize_one(rf_pipeline* p);  /* one IntegrateFront of Finalize (no-op when empty) */
+rf_status rf_pipeline_set_debug_images(rf_pipeline* p, int32_t enable);
+rf_status rf_pipeline_last_refinement(const rf_pipeline* p, float* virtual_depth, float* refined_depth,
+                                      uint64_t* frame_index, int32_t* has);
 /* Per-stage device time with CUDA events on the pipeline's stream (off by
  * default). stage_ms[0..3] = track (k_track: pyramid + LM + mask), allocate,
  * cull, fuse (carve+integrate), accumulated over `frames` frames since the

@@ -675,7 +675,16 @@ class Pipeline {
         if (debug_sink_) EmitDebug(frame, out);
         return out;
     }
-    void Finalize() { Check(rf_pipeline_finalize(h_)); }
+    void Finalize() {  // pipeline.cpp:133-135 (IntegrateFront until the window is empty)
+        if (!debug_sink_) {
+            Check(rf_pipeline_finalize(h_));
+            return;
+        }
+        while (window_size() > 0) {  // one IntegrateFront per call so each gets its debug record
+            Check(rf_pipeline_finalize_one(h_));
+            EmitRefinement();
+        }
+    }
 
     const Trajectory& trajectory() const { return trajectory_; }
     const TsdfVolume& volume() const { return *volume_; }
@@ -686,11 +695,41 @@ class Pipeline {
         Check(rf_pipeline_tracking_losses(h_, &n));
         return n;
     }
-    void set_debug_sink(std::function<void(const FrameDebug&)> sink) { debug_sink_ = std::move(sink); }
+    // With a sink installed the refinement window also renders the full
+    // virtual depth image (FrameDebug::virtual_depth), not only its holes.
+    void set_debug_sink(std::function<void(const FrameDebug&)> sink) {
+        debug_sink_ = std::move(sink);
+        Check(rf_pipeline_set_debug_images(h_, debug_sink_ ? 1 : 0));
+    }
+    std::size_t window_size() const {
+        std::uint64_t n = 0;
+        Check(rf_pipeline_window_size(h_, &n));
+        return n;
+    }
     rf_pipeline* handle() const { return h_; }
 
   private:
+    void EmitRefinement() {  // IntegrateFront's debug record (pipeline.cpp:45-54)
+        std::int32_t has = 0;
+        std::uint64_t index = 0;
+        Check(rf_pipeline_last_refinement(h_, nullptr, nullptr, &index, &has));
+        if (!has || index == last_refinement_emitted_) return;
+        last_refinement_emitted_ = index;
+        const int w = stats_.empty() ? 0 : last_w_, h = last_h_;
+        DepthImage virt(w, h), refined(w, h);
+        Check(rf_pipeline_last_refinement(h_, virt.data(), refined.data(), &index, &has));
+        FrameDebug d;
+        d.frame_index = index;
+        d.timestamp = index < stats_.size() ? stats_[index].timestamp : 0.0;
+        d.virtual_depth = &virt;
+        d.refined_depth = &refined;
+        debug_sink_(d);
+    }
     void EmitDebug(const Frame& frame, const FrameStats& st) {
+        last_w_ = frame.intrinsics.width;
+        last_h_ = frame.intrinsics.height;
+        if (config_.refinement.enabled) EmitRefinement();  // IntegrateFront runs before registration
+        if (st.frame_index == 0 || st.tracking_lost) return;  // no registration record (pipeline.cpp:66-76, 122-127)
         const int w = frame.intrinsics.width, h = frame.intrinsics.height;
         FrameDebug d;
         d.frame_index = st.frame_index;
@@ -699,10 +738,8 @@ class Pipeline {
         std::int32_t has_mask = 0;
         Check(rf_pipeline_last_mask(h_, mask.data(), &has_mask));
         ResidualImage res{Image<float>(w, h), PixelMask(w, h)};
-        if (st.frame_index > 0 && !st.tracking_lost) {
-            Check(rf_pipeline_last_residuals(h_, res.squared.data(), res.valid.data()));
-            d.residuals = &res;
-        }
+        Check(rf_pipeline_last_residuals(h_, res.squared.data(), res.valid.data()));
+        d.residuals = &res;
         if (has_mask) d.mask = &mask;
         debug_sink_(d);
     }
@@ -713,6 +750,8 @@ class Pipeline {
     Trajectory trajectory_;
     std::vector<FrameStats> stats_;
     std::function<void(const FrameDebug&)> debug_sink_;
+    std::uint64_t last_refinement_emitted_ = ~std::uint64_t(0);
+    int last_w_ = 0, last_h_ = 0;
 };
 
 using FrameSource = std::function<std::optional<Frame>()>;

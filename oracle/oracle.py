@@ -471,6 +471,35 @@ def build_mask(res_sq, res_valid, depth, cfg=None):
     return out
 
 
+def render_virtual_depth(entries, view, k, vcfg, bisections=8, far_value=8.0, threads=1):
+    """RenderVirtualDepth (depth_refinement.cpp:22-80) + RefineDepth (:82-93).
+    entries: list of dicts {depth, rgb (or None), mask (or None), pose}; returns
+    (virtual depth, refined depth of entries[0])."""
+    n = len(entries)
+    keep = []
+    D = (C.c_void_p * n)()
+    R = (C.c_void_p * n)()
+    M = (C.c_void_p * n)()
+    for i, e in enumerate(entries):
+        d = _f32(e["depth"])
+        keep.append(d)
+        D[i] = d.ctypes.data
+        if e.get("rgb") is not None:
+            r = _u8(e["rgb"])
+            keep.append(r)
+            R[i] = r.ctypes.data
+        if e.get("mask") is not None:
+            m = _u8(e["mask"])
+            keep.append(m)
+            M[i] = m.ctypes.data
+    poses = _f64(np.concatenate([np.asarray(e["pose"], np.float64) for e in entries]))
+    out = np.zeros((k.height, k.width), np.float32)
+    ref = np.zeros((k.height, k.width), np.float32)
+    _check(lib().o_render_virtual_depth(n, D, R, M, _p(poses), C.byref(k), C.byref(vcfg), _p(_f64(view)),
+                                        bisections, C.c_double(far_value), threads, _p(out), _p(ref)))
+    return out, ref
+
+
 class Scene:
     """SceneScript + RenderFrame restated (synth.hpp:43-74)."""
 

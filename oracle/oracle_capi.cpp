@@ -437,6 +437,31 @@ int o_raycast(void* vp, const double pose[12], const OIntr* k, int bisections, i
     });
 }
 
+// RenderVirtualDepth (depth_refinement.cpp:22-80) over a window of n entries;
+// masks[i] may be null. RefineDepth (:82-93) into `refined` when non-null.
+int o_render_virtual_depth(int n, const float* const* depths, const uint8_t* const* rgbs,
+                           const uint8_t* const* masks, const double* poses, const OIntr* k, const OVolCfg* vc,
+                           const double view[12], int bisections, double far_value, int threads, float* out,
+                           float* refined) {
+    return Guard([&] {
+        std::vector<WindowEntry> window(n);
+        for (int i = 0; i < n; ++i) {
+            window[i].frame = ToFrame(depths[i], rgbs ? rgbs[i] : nullptr, k);
+            window[i].pose = Pose::FromArray(poses + 12 * i);
+            if (masks && masks[i]) window[i].mask = ToMaskImg(masks[i], k->width, k->height);
+        }
+        RefinementConfig rc;
+        rc.bisection_iterations = bisections;
+        rc.far_value = far_value;
+        const DepthImage v = RenderVirtualDepth(window, Pose::FromArray(view), ToIntr(k), ToVol(vc), rc, threads);
+        std::memcpy(out, v.d.data(), sizeof(float) * v.d.size());
+        if (refined && n > 0) {
+            const DepthImage r = RefineDepth(window[0].frame.depth, v, far_value);
+            std::memcpy(refined, r.d.data(), sizeof(float) * r.d.size());
+        }
+    });
+}
+
 void* o_mesh_extract(void* vp, int min_weight, int threads) {
     return new Mesh(ExtractMesh(*static_cast<Volume*>(vp), min_weight, threads));
 }

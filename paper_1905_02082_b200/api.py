@@ -63,14 +63,17 @@ def mask_config(**kw) -> L.rf_mask_config:
     return c
 
 
-def pipeline_config(refine=False, window=10, dynamics=True, threads=1, volume=None, registration=None, mask=None):
-    """PipelineConfig (config.hpp:12-24). refine defaults to False: the CUDA
-    path does not implement the depth-refinement window yet."""
+def pipeline_config(refine=True, window=10, dynamics=True, threads=1, volume=None, registration=None, mask=None,
+                    far_value=8.0, bisection_iterations=8):
+    """PipelineConfig (config.hpp:12-24) with the reference's defaults,
+    including RefinementConfig::enabled = true (depth_refinement.hpp:13); the
+    acceptance / bench configuration (TrackingConfig, acceptance.cpp:136)
+    passes refine=False."""
     v = volume or volume_config()
     m = mask or mask_config()
     m.truncation = v.truncation
-    return L.rf_pipeline_config(v, registration or registration_config(), m, int(refine), window, 8.0, 8,
-                                int(dynamics), threads, 0)
+    return L.rf_pipeline_config(v, registration or registration_config(), m, int(refine), window, far_value,
+                                bisection_iterations, int(dynamics), threads, 0)
 
 
 # ------------------------------------------------------------------ frames
@@ -293,6 +296,32 @@ class TsdfVolume:
         return v, c, f
 
 
+# ------------------------------------------------------------------ refinement
+def render_virtual_depth(frames, poses, masks, view_pose, k: L.rf_intrinsics, volume=None, bisections=8,
+                         far_value=8.0, device=0):
+    """RenderVirtualDepth + RefineDepth (depth_refinement.cpp:22-93): frames
+    is a list of Frame, masks a list of u8 images or None. Returns (virtual
+    depth, refined depth of frames[0])."""
+    n = len(frames)
+    fr = (L.rf_frame * n)(*[f.c() for f in frames])
+    keep = list(frames)
+    M = None
+    if masks is not None:
+        M = (C.c_void_p * n)()
+        for i, m in enumerate(masks):
+            if m is not None:
+                a = np.ascontiguousarray(m, np.uint8)
+                keep.append(a)
+                M[i] = a.ctypes.data
+    P = _f64(np.concatenate([np.asarray(p, np.float64) for p in poses]))
+    virt = np.zeros((k.height, k.width), np.float32)
+    ref = np.zeros((k.height, k.width), np.float32)
+    vc = volume or volume_config()
+    L.check(_lib().rf_render_virtual_depth(fr, _p(P), M, n, _p(_f64(view_pose)), C.byref(k), C.byref(vc),
+                                           bisections, C.c_double(far_value), device, _p(virt), _p(ref)))
+    return virt, ref
+
+
 # ------------------------------------------------------------------ mask
 def mask_stages(res_sq, res_valid, depth, config=None, stages=15, device=0):
     """BuildMask (stages=15) or any subset of its stages (dynamics_mask.hpp:21-41)."""
@@ -392,6 +421,25 @@ class Pipeline:
         if not has.value:
             return None
         return has
+
+    def window_size(self) -> int:
+        out = C.c_uint64()
+        L.check(_lib().rf_pipeline_window_size(self.h, C.byref(out)))
+        return out.value
+
+    def set_debug_images(self, enable=True):
+        L.check(_lib().rf_pipeline_set_debug_images(self.h, int(enable)))
+
+    def last_refinement(self, k, with_virtual=False):
+        """FrameDebug::virtual_depth / refined_depth of the last IntegrateFront:
+        (frame_index, virtual or None, refined) or None."""
+        has = C.c_int32()
+        idx = C.c_uint64()
+        virt = np.zeros((k.height, k.width), np.float32) if with_virtual else None
+        ref = np.zeros((k.height, k.width), np.float32)
+        L.check(_lib().rf_pipeline_last_refinement(self.h, _p(virt) if with_virtual else None, _p(ref),
+                                                   C.byref(idx), C.byref(has)))
+        return (idx.value, virt, ref) if has.value else None
 
     def last_mask_image(self, k):
         out = np.zeros((k.height, k.width), dtype=np.uint8)

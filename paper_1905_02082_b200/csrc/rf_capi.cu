@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <fstream>
 #include <map>
 #include <memory>
@@ -26,7 +27,7 @@ __global__ void k_import(VolumeView V, const int* coords, uint32_t n, uint32_t b
     uint32_t idx = hash_coord(x, y, z) & V.hash_mask;
     while (atomicCAS(&V.slots[idx].key, kEmptyKey, key) != kEmptyKey) idx = (idx + 1) & V.hash_mask;
     V.slots[idx].value = base + i;
-    V.coords[base + i] = make_int4(x, y, z, 0);
+    V.coords[base + i] = make_int4(x, y, z, int(idx));
 }
 }  // namespace rfb
 
@@ -91,6 +92,7 @@ struct DevBuf {
 struct Workspace {
     int device = 0;
     cudaStream_t stream = nullptr;
+    bool own_stream = true;  // false when borrowed from another object (refinement temp volume)
     int track_grid = 0;
     int parity = 0;  // alternates the grid-barrier counter between cooperative launches
     DevBuf depth, rgb, mask_in, pose, res_sq, res_valid, mwork, levels, gsync, partials, result, out, list;
@@ -129,7 +131,7 @@ struct Workspace {
             b->release();
         if (h_out) cudaFreeHost(h_out);
         if (h_counters) cudaFreeHost(h_counters);
-        if (stream) cudaStreamDestroy(stream);
+        if (stream && own_stream) cudaStreamDestroy(stream);
         h_out = nullptr;
         h_counters = nullptr;
         stream = nullptr;
@@ -262,13 +264,29 @@ struct rf_volume {
     void reset_counter(int which) {
         CK(cudaMemsetAsync(view.counters + which, 0, 4, ws.stream));
     }
+    // Back to the freshly created state; only the bricks in use are touched
+    // unless an overflow left orphaned hash keys behind (full reset).
+    void clear(bool full) {
+        if (full) {
+            CK(cudaMemsetAsync(slots.p, 0xFF, cap * sizeof(HashSlot), ws.stream));
+            CK(cudaMemsetAsync(links.p, 0xFF, cfg.max_blocks * kLinkStride * sizeof(uint32_t), ws.stream));
+            CK(cudaMemsetAsync(voxels.p, 0, cfg.max_blocks * kBrickVoxels * sizeof(Voxel), ws.stream));
+        } else {
+            k_vol_clear<<<4 * 148, 128, 0, ws.stream>>>(view);
+            CK(cudaGetLastError());
+        }
+        CK(cudaMemsetAsync(view.counters, 0, kNumCounters * sizeof(uint32_t), ws.stream));
+    }
     void link() {  // link records for bricks allocated outside the per-frame cull
         k_link<<<148, 256, 0, ws.stream>>>(view);
         k_link_commit<<<1, 32, 0, ws.stream>>>(view);
         CK(cudaGetLastError());
     }
     void fuse(const float* d, const uint8_t* rgb, const uint8_t* mask, const rf_intrinsics& k, const double* pose,
-              const int* lost, bool carve, bool integrate, bool carve_only_before) {
+              const int* lost, bool carve, bool integrate, bool carve_only_before, bool reset_visible = true) {
+        // The visible list is appended to from counters[kVisible]; the frame
+        // path's tracking kernel already zeroed it.
+        if (reset_visible) reset_counter(kVisible);
         CullArgs ca{};
         ca.V = view;
         ca.K = level_intr(k, 0);
@@ -536,7 +554,6 @@ rf_status rf_volume_integrate(rf_volume* v, const rf_frame* f, const double pose
         const uint8_t* rgb = v->rgb_of(f);
         const uint8_t* m = v->mask_of(f, mask);
         v->upload_pose(pose);
-        v->reset_counter(kVisible);
         v->fuse(d, rgb, m, f->intrinsics, v->ws.pose.as<double>(), nullptr, false, true, false);
         v->ws.sync();
     });
@@ -548,7 +565,6 @@ rf_status rf_volume_carve(rf_volume* v, const rf_frame* f, const double pose[12]
         v->prepare(f);
         const float* d = v->depth_of(f);
         v->upload_pose(pose);
-        v->reset_counter(kVisible);
         v->fuse(d, nullptr, nullptr, f->intrinsics, v->ws.pose.as<double>(), nullptr, true, false, false);
         v->ws.sync();
     });
@@ -934,6 +950,58 @@ rf_status rf_raycast(const rf_volume* cv, const double view_pose[12], const rf_i
     });
 }
 
+// RenderVirtualDepth + RefineDepth (depth_refinement.cpp:22-93) as one call.
+rf_status rf_render_virtual_depth(const rf_frame* frames, const double* poses, const uint8_t* const* masks, int32_t n,
+                                  const double view_pose[12], const rf_intrinsics* k, const rf_volume_config* vcfg,
+                                  int32_t bisection_iterations, double far_value, int device, float* virtual_depth,
+                                  float* refined_depth) {
+    return guard([&] {
+        require(frames && poses && view_pose && k && vcfg && virtual_depth && n >= 1, RF_INVALID_ARGUMENT,
+                "bad argument");
+        require(!refined_depth || (frames[0].intrinsics.width == k->width && frames[0].intrinsics.height == k->height),
+                RF_INVALID_ARGUMENT, "depth size mismatch");
+        rf_volume* t = nullptr;
+        create_volume(vcfg, device, &t);
+        std::unique_ptr<rf_volume, void (*)(rf_volume*)> hold(t, rf_volume_destroy);
+        for (int i = 0; i < n; ++i) {
+            const rf_frame* f = &frames[i];
+            t->prepare(f);
+            const float* d = t->depth_of(f);
+            const uint8_t* rgb = t->rgb_of(f);
+            const uint8_t* m = t->mask_of(f, masks ? masks[i] : nullptr);
+            t->upload_pose(poses + 12 * i);
+            t->reset_counter(kOverflow);
+            t->allocate(d, m, f->intrinsics, t->ws.pose.as<double>(), nullptr);
+            t->fuse(d, rgb, m, f->intrinsics, t->ws.pose.as<double>(), nullptr, false, true, false);
+            t->ws.sync();
+            require(t->overflow() == 0, RF_RESOURCE_LIMIT,
+                    "voxel block budget exhausted (" + std::to_string(vcfg->max_blocks) + " blocks)");
+        }
+        const size_t np = size_t(k->width) * k->height;
+        DevBuf vo, ro;
+        vo.ensure(np * 4);
+        ro.ensure(np * 4);
+        RaycastArgs a{};
+        a.V = t->view;
+        for (int i = 0; i < 9; ++i) a.view.R[i] = view_pose[i];
+        for (int i = 0; i < 3; ++i) a.view.t[i] = view_pose[9 + i];
+        a.K = level_intr(*k, 0);
+        a.bisections = bisection_iterations;
+        a.out = vo.as<float>();
+        if (refined_depth) {
+            t->prepare(&frames[0]);
+            a.raw = t->depth_of(&frames[0]);
+            a.refined = ro.as<float>();
+            a.far_value = float(far_value);
+        }
+        k_raycast<<<unsigned((np + 127) / 128), 128, 0, t->ws.stream>>>(a);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(virtual_depth, vo.p, np * 4, cudaMemcpyDeviceToHost, t->ws.stream));
+        if (refined_depth) CK(cudaMemcpyAsync(refined_depth, ro.p, np * 4, cudaMemcpyDeviceToHost, t->ws.stream));
+        t->ws.sync();
+    });
+}
+
 // ---------------------------------------------------------------- mesh
 rf_status rf_volume_extract_mesh(const rf_volume* cv, int32_t min_weight, rf_mesh** out) {
     return guard([&] {
@@ -1069,9 +1137,30 @@ rf_status rf_copy_to_device(void* dst, const void* src, size_t bytes) {
 // Register, pose update or hold), then AllocateForFrame, the frustum cull and
 // the fused CarveFreeSpace+Integrate, all gated by the device `lost` flag. The
 // host reads back one small struct per frame.
+// One registered frame waiting in the refinement window (WindowEntry,
+// depth_refinement.hpp:20-24); its images live in a device slot.
+struct WinEntry {
+    int slot = 0;
+    double pose[12] = {};
+    bool has_mask = false, has_rgb = false;
+    uint64_t index = 0;
+    rf_intrinsics k{};
+};
+
 struct rf_pipeline {
     rf_pipeline_config cfg{};
     rf_volume* vol = nullptr;
+    // Depth-refinement window (pipeline.cpp:31-55, 111-113, 133-135).
+    rf_volume* temp = nullptr;  // the throw-away TsdfVolume of RenderVirtualDepth, reused
+    bool temp_full_reset = false;
+    std::deque<WinEntry> window;
+    DevBuf win, win_pose, virt, refined;
+    size_t slot_bytes = 0, off_rgb = 0, off_mask = 0;
+    int win_w = 0, win_h = 0;
+    uint32_t* h_front = nullptr;  // pinned: overflow flags of the last IntegrateFront (main, temp)
+    bool full_virtual = false;    // debug images: march every pixel, not only the holes
+    bool has_refinement = false;
+    uint64_t refined_index = 0;
     bool first = true;
     uint64_t frame_count = 0, losses = 0;
     std::vector<double> traj_t, traj_p;
@@ -1105,13 +1194,88 @@ void validate_pipeline_config(rf_pipeline_config c) {  // PipelineConfig::Sync (
     require(c.refine_window >= 1, RF_INVALID_ARGUMENT, "refine_window must be >= 1");
     require(c.far_value > c.volume.max_depth, RF_INVALID_ARGUMENT, "far_value must exceed max_depth");
     require(c.threads >= 1, RF_INVALID_ARGUMENT, "threads must be >= 1");
-    require(!c.refine_enabled, RF_UNSUPPORTED,
-            "depth refinement (RefinementConfig::enabled) is not on the CUDA path yet; set refine_enabled = 0");
+    require(c.bisection_iterations >= 0, RF_INVALID_ARGUMENT, "bisection_iterations must be >= 0");
 }
 
 bool intrinsics_valid(const rf_intrinsics& k) {  // CameraIntrinsics::Valid (geometry.hpp:20-24)
     return k.fx > 0.0 && k.fy > 0.0 && k.width > 0 && k.height > 0 && k.cx > 0.0 && k.cx < double(k.width) &&
            k.cy > 0.0 && k.cy < double(k.height) && k.depth_scale > 0.0;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+float* slot_depth(rf_pipeline* p, int slot) {
+    return reinterpret_cast<float*>(p->win.as<uint8_t>() + size_t(slot) * p->slot_bytes);
+}
+uint8_t* slot_rgb(rf_pipeline* p, int slot) { return p->win.as<uint8_t>() + size_t(slot) * p->slot_bytes + p->off_rgb; }
+uint8_t* slot_mask(rf_pipeline* p, int slot) { return p->win.as<uint8_t>() + size_t(slot) * p->slot_bytes + p->off_mask; }
+double* slot_pose(rf_pipeline* p, int slot) { return p->win_pose.as<double>() + 12 * size_t(slot); }
+
+void ensure_window(rf_pipeline* p, int w, int h) {
+    if (p->win_w == w && p->win_h == h) return;
+    require(p->window.empty(), RF_INVALID_ARGUMENT, "frame size changed while the refinement window holds frames");
+    const size_t n = size_t(w) * h;
+    p->off_rgb = align256(4 * n);
+    p->off_mask = p->off_rgb + align256(3 * n);
+    p->slot_bytes = p->off_mask + align256(n);
+    p->win.ensure(size_t(p->cfg.refine_window) * p->slot_bytes);
+    p->win_pose.ensure(size_t(p->cfg.refine_window) * 96);
+    p->virt.ensure(4 * n);
+    p->refined.ensure(4 * n);
+    p->win_w = w;
+    p->win_h = h;
+}
+
+// IntegrateFront (pipeline.cpp:31-55): fuse the whole window into the reused
+// temp volume (RenderVirtualDepth, depth_refinement.cpp:25-30), ray-march it
+// from the front pose with RefineDepth fused in (only raw-depth holes are
+// marched), then CarveAndIntegrate the refined front frame into the model.
+// All on the pipeline's stream; no host sync.
+void integrate_front(rf_pipeline* p) {
+    rf_volume* v = p->vol;
+    rf_volume* t = p->temp;
+    cudaStream_t s = v->ws.stream;
+    t->clear(p->temp_full_reset);
+    p->temp_full_reset = false;
+    for (const WinEntry& e : p->window) {  // front to back, like window.entries()
+        const uint8_t* m = e.has_mask ? slot_mask(p, e.slot) : nullptr;
+        t->allocate(slot_depth(p, e.slot), m, e.k, slot_pose(p, e.slot), nullptr);
+        t->fuse(slot_depth(p, e.slot), e.has_rgb ? slot_rgb(p, e.slot) : nullptr, m, e.k, slot_pose(p, e.slot),
+                nullptr, false, true, false);
+    }
+    CK(cudaMemcpyAsync(p->h_front + 1, t->view.counters + kOverflow, 4, cudaMemcpyDeviceToHost, s));
+    const WinEntry f = p->window.front();
+    RaycastArgs a{};
+    a.V = t->view;
+    for (int i = 0; i < 9; ++i) a.view.R[i] = f.pose[i];
+    for (int i = 0; i < 3; ++i) a.view.t[i] = f.pose[9 + i];
+    a.K = level_intr(f.k, 0);
+    a.bisections = p->cfg.bisection_iterations;
+    a.out = p->full_virtual ? p->virt.as<float>() : nullptr;
+    a.raw = slot_depth(p, f.slot);
+    a.refined = p->refined.as<float>();
+    a.far_value = float(p->cfg.far_value);
+    const size_t n = size_t(f.k.width) * f.k.height;
+    k_raycast<<<unsigned((n + 127) / 128), 128, 0, s>>>(a);
+    CK(cudaGetLastError());
+    // CarveAndIntegrate (pipeline.cpp:25-29) of the refined front frame.
+    const float* rd = p->refined.as<float>();
+    const uint8_t* m = f.has_mask ? slot_mask(p, f.slot) : nullptr;
+    CK(cudaMemcpyAsync(v->view.counters + kBlocksBefore, v->view.counters + kNumBlocks, 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(v->view.counters + kVisible, 0, 3 * 4, s));
+    v->allocate(rd, m, f.k, slot_pose(p, f.slot), nullptr);
+    v->fuse(rd, f.has_rgb ? slot_rgb(p, f.slot) : nullptr, m, f.k, slot_pose(p, f.slot), nullptr, true, true, true);
+    CK(cudaMemcpyAsync(p->h_front, v->view.counters + kOverflow, 4, cudaMemcpyDeviceToHost, s));
+    p->launches += 3 * p->window.size() + 5;
+    p->has_refinement = true;
+    p->refined_index = f.index;
+    p->window.pop_front();
+}
+
+void check_front_overflow(rf_pipeline* p) {  // after a stream sync
+    if (p->h_front[1]) p->temp_full_reset = true;
+    require(p->h_front[1] == 0 && p->h_front[0] == 0, RF_RESOURCE_LIMIT,
+            "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)");
 }
 
 }  // namespace
@@ -1126,6 +1290,14 @@ rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipel
         p->cfg = *cfg;
         p->cfg.mask.truncation = cfg->volume.truncation;
         create_volume(&p->cfg.volume, device, &p->vol);
+        CK(cudaMallocHost(&p->h_front, 16));
+        std::memset(p->h_front, 0, 16);
+        if (p->cfg.refine_enabled) {
+            create_volume(&p->cfg.volume, device, &p->temp);
+            cudaStreamDestroy(p->temp->ws.stream);  // work runs on the pipeline's stream
+            p->temp->ws.stream = p->vol->ws.stream;
+            p->temp->ws.own_stream = false;
+        }
         *out = p.release();
     });
 }
@@ -1134,6 +1306,9 @@ void rf_pipeline_destroy(rf_pipeline* p) {
     if (!p) return;
     for (cudaEvent_t& e : p->ev)
         if (e) cudaEventDestroy(e);
+    if (p->temp) rf_volume_destroy(p->temp);
+    for (DevBuf* b : {&p->win, &p->win_pose, &p->virt, &p->refined}) b->release();
+    if (p->h_front) cudaFreeHost(p->h_front);
     rf_volume_destroy(p->vol);
     delete p;
 }
@@ -1178,6 +1353,15 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             p->last.pixel_passes = 0.0;
             p->has_mask = false;
         } else {
+            const bool refine = p->cfg.refine_enabled != 0;
+            bool fronted = false;
+            if (refine) {
+                ensure_window(p, f->intrinsics.width, f->intrinsics.height);
+                if (int(p->window.size()) >= p->cfg.refine_window) {  // pipeline.cpp:77
+                    integrate_front(p);
+                    fronted = true;
+                }
+            }
             TrackArgs a = v->track_args(f, d, rgb, L);
             a.mode = kModeFrame;
             a.dynamics = p->cfg.dynamics_enabled;
@@ -1188,11 +1372,27 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             if (v->prof) CK(cudaEventRecord(p->ev[1], ws.stream));
             const uint8_t* mask = p->cfg.dynamics_enabled ? a.F.mask[0] : nullptr;
             const int* lost = &ws.out.as<TrackOut>()->lost;
-            v->allocate(d, mask, f->intrinsics, pose_state, lost);
-            if (v->prof) CK(cudaEventRecord(p->ev[2], ws.stream));
-            v->fuse(d, rgb, mask, f->intrinsics, pose_state, lost, true, true, true);
-            if (v->prof) CK(cudaEventRecord(p->ev[4], ws.stream));
-            p->launches += 4;
+            int slot = -1;
+            if (refine) {  // window.Push (pipeline.cpp:111-113), committed below unless tracking was lost
+                slot = p->window.empty() ? 0 : (p->window.back().slot + 1) % p->cfg.refine_window;
+                const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
+                CK(cudaMemcpyAsync(slot_depth(p, slot), d, 4 * n, cudaMemcpyDeviceToDevice, ws.stream));
+                if (rgb) CK(cudaMemcpyAsync(slot_rgb(p, slot), rgb, 3 * n, cudaMemcpyDeviceToDevice, ws.stream));
+                if (mask) CK(cudaMemcpyAsync(slot_mask(p, slot), mask, n, cudaMemcpyDeviceToDevice, ws.stream));
+                CK(cudaMemcpyAsync(slot_pose(p, slot), pose_state, 96, cudaMemcpyDeviceToDevice, ws.stream));
+                if (v->prof) {
+                    CK(cudaEventRecord(p->ev[2], ws.stream));
+                    CK(cudaEventRecord(p->ev[3], ws.stream));
+                    CK(cudaEventRecord(p->ev[4], ws.stream));
+                }
+                p->launches += 1;
+            } else {
+                v->allocate(d, mask, f->intrinsics, pose_state, lost);
+                if (v->prof) CK(cudaEventRecord(p->ev[2], ws.stream));
+                v->fuse(d, rgb, mask, f->intrinsics, pose_state, lost, true, true, true, false);
+                if (v->prof) CK(cudaEventRecord(p->ev[4], ws.stream));
+                p->launches += 4;
+            }
             CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
             CK(cudaMemcpyAsync(ws.h_counters, v->view.counters, kNumCounters * 4, cudaMemcpyDeviceToHost, ws.stream));
             ws.sync();
@@ -1208,6 +1408,17 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             st.final_error = o.final_error;
             p->has_mask = !o.lost && p->cfg.dynamics_enabled;
             if (o.lost) ++p->losses;
+            if (fronted) check_front_overflow(p);
+            if (refine && !o.lost) {
+                WinEntry e;
+                e.slot = slot;
+                std::memcpy(e.pose, o.pose, 96);
+                e.has_mask = mask != nullptr;
+                e.has_rgb = rgb != nullptr;
+                e.index = p->frame_count;
+                e.k = f->intrinsics;
+                p->window.push_back(e);
+            }
         }
         std::memcpy(p->last_counters, ws.h_counters, sizeof(p->last_counters));
         p->traj_t.push_back(f->timestamp);
@@ -1241,8 +1452,59 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
     });
 }
 
-rf_status rf_pipeline_finalize(rf_pipeline* p) {
-    return guard([&] { require(p, RF_INVALID_ARGUMENT, "null argument"); });
+rf_status rf_pipeline_finalize(rf_pipeline* p) {  // Finalize (pipeline.cpp:133-135)
+    return guard([&] {
+        require(p, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(p->vol->device));
+        while (!p->window.empty()) {
+            integrate_front(p);
+            p->vol->ws.sync();
+            check_front_overflow(p);
+        }
+    });
+}
+
+rf_status rf_pipeline_finalize_one(rf_pipeline* p) {
+    return guard([&] {
+        require(p, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(p->vol->device));
+        if (p->window.empty()) return;
+        integrate_front(p);
+        p->vol->ws.sync();
+        check_front_overflow(p);
+    });
+}
+
+rf_status rf_pipeline_set_debug_images(rf_pipeline* p, int32_t enable) {
+    return guard([&] {
+        require(p, RF_INVALID_ARGUMENT, "null argument");
+        p->full_virtual = enable != 0;
+    });
+}
+
+rf_status rf_pipeline_last_refinement(const rf_pipeline* p, float* virtual_depth, float* refined_depth,
+                                      uint64_t* frame_index, int32_t* has) {
+    return guard([&] {
+        require(p && has, RF_INVALID_ARGUMENT, "null argument");
+        *has = p->has_refinement;
+        if (!p->has_refinement) return;
+        CK(cudaSetDevice(p->vol->device));
+        CK(cudaStreamSynchronize(p->vol->ws.stream));
+        const size_t n = size_t(p->win_w) * p->win_h;
+        if (frame_index) *frame_index = p->refined_index;
+        if (virtual_depth) {
+            require(p->full_virtual, RF_INVALID_ARGUMENT, "virtual depth needs rf_pipeline_set_debug_images(p, 1)");
+            CK(cudaMemcpy(virtual_depth, p->virt.p, 4 * n, cudaMemcpyDeviceToHost));
+        }
+        if (refined_depth) CK(cudaMemcpy(refined_depth, p->refined.p, 4 * n, cudaMemcpyDeviceToHost));
+    });
+}
+
+rf_status rf_pipeline_window_size(const rf_pipeline* p, uint64_t* out) {
+    return guard([&] {
+        require(p && out, RF_INVALID_ARGUMENT, "null argument");
+        *out = p->window.size();
+    });
 }
 
 rf_status rf_pipeline_volume(rf_pipeline* p, rf_volume** out) {

@@ -50,7 +50,7 @@ struct VolumeView {
     HashSlot* slots;
     uint32_t hash_mask;
     uint32_t max_blocks;
-    int4* coords;        // brick coordinate per pool index (w unused)
+    int4* coords;        // brick coordinate per pool index; w = its hash slot
     Voxel* voxels;       // pool, kBrickVoxels per brick, x fastest then y then z
     uint32_t* links;     // kLinkStride per brick: pool index of the brick at +(q&1, q>>1&1, q>>2), q = 1..7
     uint32_t* counters;  // see VolumeCounters
@@ -167,7 +167,7 @@ __device__ __forceinline__ int hash_insert(const VolumeView& V, int x, int y, in
                     V.slots[idx].value = kOverflowed;
                     return -1;
                 }
-                V.coords[b] = make_int4(x, y, z, 0);
+                V.coords[b] = make_int4(x, y, z, int(idx));  // w = hash slot (volume reset)
                 V.slots[idx].value = b;
                 return 1;
             }

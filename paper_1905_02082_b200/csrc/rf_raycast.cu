@@ -20,6 +20,13 @@ __global__ void k_raycast(RaycastArgs a) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.K.w * a.K.h) return;
     const int u = i % a.K.w, v = i / a.K.w;
+    if (a.raw) {
+        const float r = a.raw[i];
+        if (depth_valid(r)) {
+            a.refined[i] = r;
+            if (!a.out) return;
+        }
+    }
     const double step = a.V.truncation / 2.0;
     const double d0 = (double(u) - a.K.cx) / a.K.fx, d1 = (double(v) - a.K.cy) / a.K.fy;
     double prev_z = 0.0, prev_sdf = 0.0;
@@ -55,7 +62,8 @@ __global__ void k_raycast(RaycastArgs a) {
         prev_sdf = s;
         prev_valid = true;
     }
-    a.out[i] = out;
+    if (a.out) a.out[i] = out;
+    if (a.raw && !depth_valid(a.raw[i])) a.refined[i] = depth_valid(out) ? out : a.far_value;
 }
 
 }  // namespace rfb

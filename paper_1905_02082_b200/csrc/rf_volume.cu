@@ -296,4 +296,24 @@ __global__ void k_occupancy(VolumeView V, uint8_t* bitmap) {
         bitmap[i] = V.slots[i].key != kEmptyKey;
 }
 
+// Empties a volume in place for reuse (the refinement window's throw-away
+// TsdfVolume, depth_refinement.cpp:25): every occupied hash slot belongs to
+// one of the bricks [0, n) (no deletion, coords.w = slot), so clearing those
+// slots, their voxels and link records restores the freshly created state
+// without touching the rest of the table. Grid-stride over n read on device.
+__global__ void k_vol_clear(VolumeView V) {
+    const uint32_t n = min(V.counters[kNumBlocks], V.max_blocks);
+    for (uint32_t b = blockIdx.x; b < n; b += gridDim.x) {
+        uint4* vox = reinterpret_cast<uint4*>(V.voxels + size_t(b) * kBrickVoxels);
+        for (int i = threadIdx.x; i < kBrickVoxels * int(sizeof(Voxel)) / 16; i += blockDim.x)
+            vox[i] = make_uint4(0, 0, 0, 0);
+        if (threadIdx.x < kLinkStride) V.links[size_t(b) * kLinkStride + threadIdx.x] = kInvalid;
+        if (threadIdx.x == 0) {
+            const uint32_t slot = uint32_t(V.coords[b].w);
+            V.slots[slot].key = kEmptyKey;
+            V.slots[slot].value = kInvalid;
+        }
+    }
+}
+
 }  // namespace rfb

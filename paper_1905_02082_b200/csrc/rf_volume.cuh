@@ -43,7 +43,13 @@ struct RaycastArgs {
     Pose view;
     Intr K;
     int bisections;
-    float* out;
+    float* out;          // virtual depth (may be null when `refined` is set)
+    // RefineDepth (depth_refinement.cpp:82-93) fused: with `raw` set, pixels
+    // whose raw depth is valid keep it and are not marched unless `out` wants
+    // the full virtual image; the rest take the virtual depth or far_value.
+    const float* raw;
+    float* refined;
+    float far_value;
 };
 
 // Marching cubes (rf_mesh.cu): per-cell state lives in one scratch buffer.
@@ -82,5 +88,6 @@ __global__ void k_sample(VolumeView V, const double* pts, int n, int mode, doubl
                          uint8_t* valid);
 __global__ void k_voxel_rw(VolumeView V, const int* vc, int n, Voxel* io, uint8_t* found, int write);
 __global__ void k_occupancy(VolumeView V, uint8_t* bitmap);
+__global__ void k_vol_clear(VolumeView V);
 
 }  // namespace rfb

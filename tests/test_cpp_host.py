@@ -36,7 +36,8 @@ def test_host_layer_compiles(tmp_path):
 
 
 @pytest.mark.gpu
-def test_host_layer_pipeline_matches(tmp_path):
+@pytest.mark.parametrize("refine", [False, True])
+def test_host_layer_pipeline_matches(tmp_path, refine):
     from oracle import oracle as O
     from paper_1905_02082_b200 import api as G
     from paper_1905_02082_b200 import scenes
@@ -53,8 +54,8 @@ def test_host_layer_pipeline_matches(tmp_path):
             f.write(struct.pack("<d", fr["timestamp"]))
             f.write(np.ascontiguousarray(fr["depth"], np.float32).tobytes())
             f.write(np.ascontiguousarray(fr["rgb"], np.uint8).tobytes())
-    r = subprocess.run([exe, str(tmp_path / "in.bin"), str(tmp_path / "out.bin")], capture_output=True, text=True,
-                       timeout=300)
+    args = [exe, str(tmp_path / "in.bin"), str(tmp_path / "out.bin")] + (["refine"] if refine else [])
+    r = subprocess.run(args, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     data = (tmp_path / "out.bin").read_bytes()
     n = struct.unpack_from("<i", data)[0]
@@ -64,10 +65,13 @@ def test_host_layer_pipeline_matches(tmp_path):
     off = 4 + rec.nbytes
     nv, nf, nb = struct.unpack_from("<3Q", data, off)
     flags = struct.unpack_from("<3i", data, off + 24)
+    calls, masks, refined = struct.unpack_from("<3Q", data, off + 36)
     assert flags == (1, 1, 1), "exception mapping"
+    # one record per registered frame, plus one per IntegrateFront (window 3: all but the first frame)
+    assert calls == (n - 1) + ((n - 1) if refine else 0) and refined == ((n - 1) if refine else 0)
 
-    gp = G.Pipeline(G.pipeline_config())
-    op = O.Pipeline(O.pipe_cfg(refine=False, reg=O.reg_cfg(threads=8)))
+    gp = G.Pipeline(G.pipeline_config(refine=refine, window=3))
+    op = O.Pipeline(O.pipe_cfg(refine=refine, window=3, reg=O.reg_cfg(threads=8)))
     for i, fr in enumerate(frames):
         sg, pg = gp.process_frame(frame(k, fr["depth"], fr["rgb"], fr["timestamp"]))
         so, po = op.process_frame(fr["depth"], fr["rgb"], k, fr["timestamp"])
@@ -75,6 +79,7 @@ def test_host_layer_pipeline_matches(tmp_path):
         assert rec["regs"][i] == sg["registrations"] and rec["iters"][i] == sg["iterations"]
         assert rec["masked"][i] == sg["masked_pixels"]
         assert max(pose_error(po, rec["pose"][i])) <= 1e-4
+    gp.finalize()
     v, c, f = gp.volume().extract_mesh(2)
     assert (nv, nf) == (len(v), len(f)) and nb == gp.volume().num_blocks()
     assert nf > 1000

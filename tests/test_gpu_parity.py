@@ -354,7 +354,7 @@ def run_both(script, n=None, dynamics=True, reg_threads=8):
     n = n or len(s)
     frames = [s.render(i) for i in range(n)]
     op = O.Pipeline(O.pipe_cfg(refine=False, dynamics=dynamics, reg=O.reg_cfg(threads=reg_threads)))
-    gp = G.Pipeline(G.pipeline_config(dynamics=dynamics))
+    gp = G.Pipeline(G.pipeline_config(refine=False, dynamics=dynamics))
     out = []
     for f in frames:
         so, po = op.process_frame(f["depth"], f["rgb"], s.k, f["timestamp"])
