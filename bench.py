@@ -51,11 +51,6 @@ def parse_args():
     return ap.parse_args()
 
 
-def dist_env():
-    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
-            int(os.environ.get("LOCAL_RANK", 0)))
-
-
 def seq_index(step, n):
     """Ping-pong through the n rendered frames: 0..n-1, n-2..1, 0.."""
     period = 2 * n - 2
@@ -86,7 +81,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -127,16 +122,15 @@ def run_ours(args):
     import torch
 
     from paper_1905_02082_b200 import _lib as L
-    from paper_1905_02082_b200 import api, scenes, synth
+    from paper_1905_02082_b200 import api, replicas, scenes, synth
 
-    rank, world, local = dist_env()
+    R = replicas.env()
+    rank, world, local = R.rank, R.world, R.local
     torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    R = replicas.init("nccl")
     lib = L.load()
     cfgd = scenes.BENCH_CONFIGS[CONFIG]
-    seed = cfgd["seed"] + rank  # independent sequence per replica
+    seed = replicas.sequence_seed(cfgd["seed"], R)  # independent sequence per replica
     scene = synth.parse(scenes.bench_script(dynamic=cfgd["dynamic"], frames=cfgd["frames"], seed=seed))
     k = scene.intrinsics
     H, W, F = k.height, k.width, len(scene)
@@ -174,9 +168,7 @@ def run_ours(args):
                 record(p)
 
     def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
+        replicas.barrier(R)
         torch.cuda.synchronize()
 
     stats = L.rf_frame_stats()
@@ -231,19 +223,12 @@ def run_ours(args):
     e2e_s = time.perf_counter() - t0
 
     # ---- max over ranks
-    t = torch.tensor([ms / 1000.0, e2e_s], dtype=torch.float64, device="cuda")
-    if world > 1:
-        import torch.distributed as dist
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    sec, e2e_sec = float(t[0]), float(t[1])
-    value = world * args.steps / sec
-    e2e = world * args.steps / e2e_sec
+    sec, e2e_sec = replicas.max_over_ranks(R, [ms / 1000.0, e2e_s])
+    value = replicas.job_rate(R, args.steps, sec)
+    e2e = replicas.job_rate(R, args.steps, e2e_sec)
 
     if rank != 0:
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-            dist.destroy_process_group()
+        replicas.finish(R)
         return
 
     # ---- roofline of the dominant kernel (SURVEY §8d bytes model)
@@ -299,10 +284,7 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(depth_h, rgb_h, k, args.cpu_sample_seconds)
     print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
+    replicas.finish(R)
 
 
 def oracle_rate(depth_list, rgb_list, k, budget_s, threads, max_frames=None):
@@ -335,8 +317,11 @@ def cpu_baseline(depth_h, rgb_h, k, budget_s):
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
-    rank, world, _ = dist_env()
-    if rank != 0:
+    from paper_1905_02082_b200 import replicas
+
+    R = replicas.env()
+    rank, world = R.rank, R.world
+    if rank != 0:  # rank 0 alone times the host CPU path; the others exit 0
         return
     import numpy as np
 
