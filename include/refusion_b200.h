@@ -251,6 +251,8 @@ rf_status rf_pipeline_stream(const rf_pipeline* p, void** cuda_stream);         
  * deterministic all-reduce (reduce = 1) of the persistent tracking kernel. */
 rf_status rf_diag_grid_barrier(int device, int32_t iters, int32_t reduce, double* us_per_call);
 /* SM cycles of one LM step on one thread: [solve, ExpMap + compose, total]. */
+rf_status rf_diag_pass_bench(rf_volume* v, const rf_frame* f, const double pose[12], int32_t level, int32_t iters,
+                             double color_weight, double* us_per_pass, double* acc);  /* acc: 30 doubles or NULL */
 rf_status rf_diag_lm_step(int device, int32_t iters, double cycles[3]);
 
 rf_status rf_synth_render(const void* prims, int32_t nprims, const double cam_pose[12], const rf_intrinsics* k,

@@ -109,7 +109,16 @@ struct Workspace {
         CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
         int sms = 0, per = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_track, kTrackThreads, 0));
+        // The tracking passes gather voxels through L1: leave it as much of the
+        // unified L1/shared array as the kernel's static shared memory allows.
+        static const int carveout = [] {
+            const char* e = std::getenv("RF_TRACK_CARVEOUT");
+            return e ? std::atoi(e) : int(cudaSharedmemCarveoutMaxL1);
+        }();
+        if (carveout >= 0)
+            CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributePreferredSharedMemoryCarveout, carveout));
+        CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrackDynSmem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_track, kTrackThreads, kTrackDynSmem));
         require(per > 0, RF_CUDA_ERROR, "tracking kernel does not fit on an SM");
         track_grid = sms * per;
         gsync.ensure(sizeof(GridSync));
@@ -364,7 +373,8 @@ struct rf_volume {
         a.grid.parity = ws.parity;
         ws.parity ^= 1;
         void* args[] = {&a};
-        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, kTrackDynSmem,
+                                       ws.stream));
     }
     TrackOut fetch_out() {
         CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
@@ -919,7 +929,8 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
         ws.parity ^= 1;
         a.out = ws.out.as<TrackOut>();
         void* args[] = {&a};
-        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, kTrackDynSmem,
+                                       ws.stream));
         CK(cudaMemcpyAsync(out, ws.mask_in.p, n, cudaMemcpyDeviceToHost, ws.stream));
         CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
         ws.sync();
@@ -1616,6 +1627,31 @@ rf_status rf_pipeline_stream(const rf_pipeline* p, void** cuda_stream) {
 namespace rfb {
 __global__ void k_grid_bench(GridCtx g, int iters, int reduce);
 __global__ void k_lm_bench(int iters, double* out);
+}
+
+// Diagnostics: `iters` Jacobian passes at pyramid `level` of frame f at a
+// fixed pose inside one tracking-kernel launch (per-pass time including the
+// grid all-reduce); the normal equations of the last pass in acc[30].
+extern "C" rf_status rf_diag_pass_bench(rf_volume* v, const rf_frame* f, const double pose[12], int32_t level,
+                                        int32_t iters, double color_weight, double* us_per_pass, double* acc) {
+    return guard([&] {
+        require(v && f && pose && us_per_pass && iters > 0 && level >= 0 && level < kMaxLevels, RF_INVALID_ARGUMENT,
+                "bad argument");
+        v->prepare(f, level + 1);
+        const float* d = v->depth_of(f);
+        const uint8_t* rgb = v->rgb_of(f);
+        TrackArgs a = v->track_args(f, d, rgb, level + 1);
+        a.mode = kModePassBench;
+        a.reg.color_weight = color_weight;
+        a.reg.levels = level + 1;
+        a.bench_iters = iters;
+        a.bench_level = level;
+        v->upload_pose(pose);
+        v->launch_track(a);
+        const TrackOut o = v->fetch_out();
+        *us_per_pass = o.final_error;
+        if (acc) std::memcpy(acc, o.acc, sizeof(o.acc));
+    });
 }
 
 extern "C" rf_status rf_diag_lm_step(int device, int32_t iters, double cycles[3]) {

@@ -288,14 +288,11 @@ __device__ __forceinline__ void cell_of(double px, double py, double pz, const V
     }
 }
 
-template <bool kGrad, bool kIntensity, bool kExact = true>
-__device__ __forceinline__ bool sample_point(const VolumeView& V, const double p[3], CellSample& out,
-                                             const double* lut = nullptr) {
-    int base[3];
-    double f[3];
-    cell_of<kExact>(p[0], p[1], p[2], V, base, f);
-    uint2 c[8];
-    if (!gather_corners(V, base[0], base[1], base[2], c)) return false;
+// Trilinear value and analytic gradient (tsdf_volume.cpp:319-346) of the
+// SDF and intensity interpolants from the 8 gathered corners.
+template <bool kGrad, bool kIntensity>
+__device__ __forceinline__ void interp_cell(const VolumeView& V, const uint2 (&c)[8], const double f[3],
+                                            CellSample& out, const double* lut) {
     const double wx[2] = {1.0 - f[0], f[0]};
     const double wy[2] = {1.0 - f[1], f[1]};
     const double wz[2] = {1.0 - f[2], f[2]};
@@ -336,7 +333,110 @@ __device__ __forceinline__ bool sample_point(const VolumeView& V, const double p
             out.gi[i] = gi[i] * inv_s;
         }
     }
+}
+
+template <bool kGrad, bool kIntensity, bool kExact = true>
+__device__ __forceinline__ bool sample_point(const VolumeView& V, const double p[3], CellSample& out,
+                                             const double* lut = nullptr) {
+    int base[3];
+    double f[3];
+    cell_of<kExact>(p[0], p[1], p[2], V, base, f);
+    uint2 c[8];
+    if (!gather_corners(V, base[0], base[1], base[2], c)) return false;
+    interp_cell<kGrad, kIntensity>(V, c, f, out, lut);
     return true;
+}
+
+// Continues a linear probe after the first slot missed (the rare path of the
+// batched gather below).
+__device__ __forceinline__ uint32_t hash_find_from(const VolumeView& V, unsigned long long key, uint32_t idx) {
+    for (uint32_t probe = 0; probe < V.hash_mask; ++probe) {
+        idx = (idx + 1) & V.hash_mask;
+        const uint4 s = __ldg(reinterpret_cast<const uint4*>(V.slots + idx));
+        const unsigned long long k = (unsigned long long)s.x | ((unsigned long long)s.y << 32);
+        if (k == key) return s.z >= kOverflowed ? kInvalid : s.z;
+        if (k == kEmptyKey) return kInvalid;
+    }
+    return kInvalid;
+}
+
+// gather_corners for NP cells at once, phase by phase (first hash slot, link
+// record, the 8 voxels), so each thread keeps NP independent load chains in
+// flight instead of one: the tracking passes are bound by this latency.
+// Same results as gather_corners per cell. ok[i] in: cell wanted; out: all
+// 8 corners allocated and observed.
+template <int NP>
+__device__ __forceinline__ void gather_corners_batch(const VolumeView& V, const int (&base)[NP][3], bool (&ok)[NP],
+                                                     uint2 (&c)[NP][8]) {
+    unsigned long long key[NP];
+    uint32_t idx[NP], b0[NP];
+    uint4 s[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        const int x = base[i][0] >> 3, y = base[i][1] >> 3, z = base[i][2] >> 3;  // FloorDiv by 8
+        ok[i] = ok[i] && coord_in_range(x, y, z);
+        if (ok[i]) {
+            key[i] = pack_key(x, y, z);
+            idx[i] = hash_coord(x, y, z) & V.hash_mask;
+            s[i] = __ldg(reinterpret_cast<const uint4*>(V.slots + idx[i]));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        if (!ok[i]) continue;
+        const unsigned long long k = (unsigned long long)s[i].x | ((unsigned long long)s[i].y << 32);
+        if (k == key[i]) b0[i] = s[i].z >= kOverflowed ? kInvalid : s[i].z;
+        else if (k == kEmptyKey) b0[i] = kInvalid;
+        else b0[i] = hash_find_from(V, key[i], idx[i]);
+        ok[i] = b0[i] != kInvalid;
+    }
+    int smask[NP];
+    uint4 r0[NP], r1[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        smask[i] = int((base[i][0] & 7) == 7) | (int((base[i][1] & 7) == 7) << 1) | (int((base[i][2] & 7) == 7) << 2);
+        if (ok[i] && smask[i]) {
+            r0[i] = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(b0[i]) * kLinkStride));
+            r1[i] = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(b0[i]) * kLinkStride) + 1);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        if (!ok[i]) continue;
+        uint32_t n[8];
+        n[0] = b0[i];
+        if (smask[i]) {
+            n[1] = r0[i].y; n[2] = r0[i].z; n[3] = r0[i].w; n[4] = r1[i].x; n[5] = r1[i].y; n[6] = r1[i].z;
+            n[7] = r1[i].w;
+        } else {
+#pragma unroll
+            for (int q = 1; q < 8; ++q) n[q] = b0[i];
+        }
+        const int lx = base[i][0] & 7, ly = base[i][1] & 7, lz = base[i][2] & 7;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
+            const int kbits = dx | (dy << 1) | (dz << 2);
+            const int code = kbits & smask[i];
+            uint32_t b = b0[i];
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+                if ((q & ~kbits) == 0) b = (code == q) ? n[q] : b;
+            if (b >= kOverflowed) {
+                ok[i] = false;
+                b = b0[i];
+            }
+            const int cx = (lx + dx) & 7, cy = (ly + dy) & 7, cz = (lz + dz) & 7;
+            c[i][k] = __ldg(reinterpret_cast<const uint2*>(brick_ptr(V, b)) + ((cz * 8 + cy) * 8 + cx));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+        if (ok[i]) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if ((c[i][k].y & 0xFFu) == 0u) ok[i] = false;  // weight byte
+        }
 }
 
 // ---------------------------------------------------------------- grid sync

@@ -22,6 +22,7 @@ __device__ __forceinline__ int hidx(int i, int j) { return i * 6 - (i * (i - 1))
 
 __shared__ int s_trace_pass;  // per-CTA pass counter for the optional timeline
 __shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (see voxel_luma_lut)
+extern __shared__ double s_dyn[];   // kTrackDynSmem bytes: the tensor-core row staging
 
 struct RegState {
     Pose pose, cand;
@@ -33,12 +34,13 @@ struct RegState {
 };
 
 // ------------------------------------------------------------------ math
-// Reciprocal from the single-precision estimate + two Newton steps
-// (~1 ulp; latency-critical pivots of the 6x6 solve).
-__device__ __forceinline__ double fast_rcp(double x) {
-    const float xf = float(x);
-    if (!(fabsf(xf) > 1e-37f && fabsf(xf) < 1e37f)) return 1.0 / x;  // outside float range: exact path
-    double r = double(__frcp_rn(xf));
+// 1/x without the IEEE division's special-case branch: the fp64 reciprocal
+// approximation plus two Newton steps (relative error ~1e-16; pivots of the
+// damped SPD matrix are normal numbers). Branch-free, so the solve below is a
+// single basic block the scheduler can interleave.
+__device__ __forceinline__ double rcp_nobranch(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     r = __fma_rn(r, __fma_rn(-x, r, 1.0), r);
     r = __fma_rn(r, __fma_rn(-x, r, 1.0), r);
     return r;
@@ -46,24 +48,19 @@ __device__ __forceinline__ double fast_rcp(double x) {
 
 __device__ void expmap(const double xi[6], Pose& out) {  // geometry.cpp:14-38
     const double w0 = xi[3], w1 = xi[4], w2 = xi[5];
-    const double theta = sqrt((w0 * w0 + w1 * w1) + w2 * w2);
+    const double t2 = (w0 * w0 + w1 * w1) + w2 * w2;
     const double hat[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
     double hat2[9];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
             hat2[3 * i + j] = (hat[3 * i] * hat[j] + hat[3 * i + 1] * hat[3 + j]) + hat[3 * i + 2] * hat[6 + j];
     double a, b, c;
-    const double t2 = theta * theta;
-    if (theta < 1e-6) {
-        a = 1.0 - t2 / 6.0;
-        b = 0.5 - t2 / 24.0;
-        c = 1.0 / 6.0 - t2 / 120.0;
-    } else if (theta < 0.05) {
-        // sin(t)/t, (1-cos t)/t^2, (t-sin t)/t^3 by their Taylor series (five
-        // terms: truncation < 1e-20 for t < 0.05). Same functions as the
-        // reference's closed forms, without the serial sincos + three IEEE
-        // divisions on the one thread every CTA waits for (an LM step is a
-        // few milliradians).
+    if (t2 < 0.0025) {
+        // theta < 0.05 (an LM step is a few milliradians): sin(t)/t,
+        // (1-cos t)/t^2, (t-sin t)/t^3 by their Taylor series in t^2 (five
+        // terms: truncation < 1e-20), which also covers the reference's
+        // theta < 1e-6 branch (its two-term series). No sqrt, sincos or IEEE
+        // division on the one thread every CTA waits for.
         a = __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, 1.0 / 362880.0, -1.0 / 5040.0), 1.0 / 120.0),
                                   -1.0 / 6.0), 1.0);
         b = __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, 1.0 / 3628800.0, -1.0 / 40320.0), 1.0 / 720.0),
@@ -71,6 +68,7 @@ __device__ void expmap(const double xi[6], Pose& out) {  // geometry.cpp:14-38
         c = __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, __fma_rn(t2, 1.0 / 39916800.0, -1.0 / 362880.0), 1.0 / 5040.0),
                                   -1.0 / 120.0), 1.0 / 6.0);
     } else {
+        const double theta = sqrt(t2);
         double st, ct;
         sincos(theta, &st, &ct);
         a = st / theta;
@@ -112,47 +110,41 @@ __device__ bool lm_solve(const double* acc, double lambda, double* delta) {
         }
         x[i] = -acc[21 + i];
     }
-    // Latency matters here (one thread, every CTA waits): fused multiply-adds
-    // and one reciprocal per pivot. Rounding differs from Eigen's divisions in
-    // the last bits only; the normal equations already differ at that level
-    // through the reduction order, so parity is held at the pose level.
-    double inv_d[6];
+    // Latency matters here (one thread, every CTA waits). Left-looking LDLT
+    // on unscaled columns C (L = C * inv_d): column k subtracts the older
+    // terms first and the (k-1) term last, so only one reciprocal (~58
+    // cycles), one multiply and one FMA per pivot sit on the dependency
+    // chain. Rounding differs from Eigen's divisions in the last bits only;
+    // the normal equations already differ at that level through the
+    // reduction order, so parity is held at the pose level.
+    double L[6][6], inv_d[6];
+    bool pivots_ok = true;  // no early exit: one basic block, so later pivots' work can be hoisted
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
-        double temp[6];
-        if (k > 0) {
-            double dot = 0.0;
 #pragma unroll
-            for (int j = 0; j < k; ++j) {
-                temp[j] = m[j][j] * m[k][j];
-                dot = __fma_rn(m[k][j], temp[j], dot);
-            }
-            m[k][k] -= dot;
+        for (int i = k; i < 6; ++i) {
+            double c = m[i][k];
 #pragma unroll
-            for (int i = k + 1; i < 6; ++i) {
-                double s = 0.0;
-#pragma unroll
-                for (int j = 0; j < k; ++j) s = __fma_rn(m[i][j], temp[j], s);
-                m[i][k] -= s;
-            }
+            for (int j = 0; j < k; ++j) c = __fma_rn(-L[i][j], m[k][j], c);  // m[k][j] holds C[k][j]
+            m[i][k] = c;
         }
         const double akk = m[k][k];
-        if (!(fabs(akk) > 0.0)) return false;  // zero pivot: NumericalIssue path, lambda grows
-        inv_d[k] = fast_rcp(akk);
+        pivots_ok = pivots_ok && fabs(akk) > 0.0;  // zero pivot: NumericalIssue path, lambda grows
+        inv_d[k] = rcp_nobranch(akk);
 #pragma unroll
-        for (int i = k + 1; i < 6; ++i) m[i][k] *= inv_d[k];
+        for (int i = k + 1; i < 6; ++i) L[i][k] = m[i][k] * inv_d[k];
     }
 #pragma unroll
     for (int j = 0; j < 6; ++j)
 #pragma unroll
-        for (int i = j + 1; i < 6; ++i) x[i] = __fma_rn(-m[i][j], x[j], x[i]);
+        for (int i = j + 1; i < 6; ++i) x[i] = __fma_rn(-L[i][j], x[j], x[i]);
 #pragma unroll
     for (int i = 0; i < 6; ++i) x[i] *= inv_d[i];
 #pragma unroll
     for (int j = 5; j >= 0; --j)
 #pragma unroll
-        for (int i = 0; i < j; ++i) x[i] = __fma_rn(-m[j][i], x[j], x[i]);
-    bool finite = true;
+        for (int i = 0; i < j; ++i) x[i] = __fma_rn(-L[j][i], x[j], x[i]);
+    bool finite = pivots_ok;
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
         delta[i] = x[i];
@@ -202,6 +194,175 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
 }
 
 // ------------------------------------------------------------------ pixel pass
+// Jacobian passes accumulate the normal equations on the FP64 tensor cores:
+// per warp and 32 pixels, H | b | E is the 8x8 product R^T R of the pixels'
+// rows R = [J | r | 0] (and, for the photometric term, A^T B with
+// A = [cw Jc | 0 | r_c], B = [Jc | r_c | r_c]), i.e. 16 DMMA.8x8x4 into a
+// 2-double-per-lane fragment instead of 30 fp64 accumulators per thread: the
+// register file then holds twice as many warps to hide the gather latency.
+#ifndef RF_TRACK_MMA
+#define RF_TRACK_MMA 0  // measured slower at 8 warps/SM (tools/pass_bench.py); kept as an option
+#endif
+constexpr bool kUseMma = RF_TRACK_MMA != 0;
+
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// Adds the 32 rows in `rows` (this warp's [32][8] smem block) as R^T R to
+// the fragment; a lane scaled by `ascale` supplies the A operand (colour).
+__device__ __forceinline__ void dmma_rows(const double* rows, double& c0, double& c1, double ascale, bool scaled) {
+    const int lane = threadIdx.x & 31;
+    const double* col = rows + (lane & 3) * 8 + (lane >> 2);  // A[m = lane/4][k = lane%4] of k-step 0
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const double x = col[32 * s];  // pixel 4s + lane%4, component lane/4
+        dmma_884(c0, c1, scaled ? x * ascale : x, x);
+    }
+}
+
+// One Accumulate with Jacobian (registration.cpp:49-95) over level `level`
+// on the tensor cores. Same pixel walk and per-pixel arithmetic as the
+// scalar path; only the summation order of the normal equations differs.
+template <bool kColor>
+__device__ void accumulate_mma(const TrackArgs& a, int level, const Pose& P, bool use_mask, double cw,
+                               double* scratch, double* blk, double* out) {
+    double* rows_sm = s_dyn;  // one [32][8] block per warp (dynamic shared memory, kTrackDynSmem)
+    const FrameView& F = a.F;
+    const Intr K = F.K[level];
+    const double min_depth = a.V.min_depth, max_depth = a.V.max_depth;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* rows = rows_sm + warp * 256;
+    double* mine = rows + lane * 8;
+    // colour A-operand scale by fragment row m = lane/4: cw on J rows, 0 on
+    // the depth-residual row, 1 on the colour-error row
+    const double ascale = (lane >> 2) < 6 ? cw : ((lane >> 2) == 6 ? 0.0 : 1.0);
+    double c0 = 0.0, c1 = 0.0;
+    unsigned int count = 0;
+    const int ntx = (K.w + kTileW - 1) / kTileW, nty = (K.h + kTileH - 1) / kTileH;
+    const float* depth = level == 0 ? F.depth0 : F.depth[level];
+    const uint8_t* mask = use_mask ? F.mask[level] : nullptr;
+    unsigned long long* tr = (a.trace && s_trace_pass < kTracePasses) ? a.trace + 8 * s_trace_pass : nullptr;
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+        tr[0] = global_ns();
+        tr[4] = level;
+        tr[5] = (unsigned long long)K.w * K.h;
+        tr[6] = 1;
+    }
+    int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;  // uniform per CTA: every lane runs every step
+    const int step_y = gridDim.x / ntx, step_x = gridDim.x % ntx;
+    for (; ty < nty; tx += step_x, ty += step_y) {
+        if (tx >= ntx) {
+            tx -= ntx;
+            ++ty;
+            if (ty >= nty) break;
+        }
+        const int u = tx * kTileW + (threadIdx.x % kTileW);
+        const int v = ty * kTileH + (threadIdx.x / kTileW);
+        double J[6] = {0, 0, 0, 0, 0, 0}, Jc[6] = {0, 0, 0, 0, 0, 0}, r_d = 0.0, r_c = 0.0;
+        bool valid = false;
+        if (u < K.w && v < K.h) {
+            const int p = v * K.w + u;
+            const float d = level == 0 ? __ldg(depth + p) : __ldcg(depth + p);
+            if (depth_valid(d) && !(d < min_depth) && !(d > max_depth) && !(mask && __ldcg(mask + p) != 0)) {
+                const double dd = double(d);
+                const double x0 = (double(u) - K.cx) * K.ifx * dd;  // Backproject (geometry.hpp:41-43)
+                const double x1 = (double(v) - K.cy) * K.ify * dd;
+                double y[3];
+                pose_apply(P, x0, x1, dd, y);
+                CellSample cs;
+                if (sample_point<true, kColor, false>(a.V, y, cs, s_luma_lut)) {
+                    valid = true;
+                    r_d = cs.sdf;
+                    J[0] = cs.gs[0];
+                    J[1] = cs.gs[1];
+                    J[2] = cs.gs[2];
+                    J[3] = y[1] * cs.gs[2] - y[2] * cs.gs[1];
+                    J[4] = y[2] * cs.gs[0] - y[0] * cs.gs[2];
+                    J[5] = y[0] * cs.gs[1] - y[1] * cs.gs[0];
+                    if (kColor) {
+                        double I;
+                        if (level == 0) {
+                            const uint8_t* c = F.rgb0 + 3 * size_t(p);
+                            I = double(float(luma(__ldg(c), __ldg(c + 1), __ldg(c + 2))));
+                        } else {
+                            I = double(__ldcg(F.inten[level] + p));
+                        }
+                        r_c = (cs.inten - I) * kIntensityScale;
+                        Jc[0] = cs.gi[0] * kIntensityScale;
+                        Jc[1] = cs.gi[1] * kIntensityScale;
+                        Jc[2] = cs.gi[2] * kIntensityScale;
+                        Jc[3] = (y[1] * cs.gi[2] - y[2] * cs.gi[1]) * kIntensityScale;
+                        Jc[4] = (y[2] * cs.gi[0] - y[0] * cs.gi[2]) * kIntensityScale;
+                        Jc[5] = (y[0] * cs.gi[1] - y[1] * cs.gi[0]) * kIntensityScale;
+                    }
+                }
+            }
+        }
+        count += __popc(__ballot_sync(0xffffffffu, valid));
+        // depth rows [J | r_d | 0]
+        reinterpret_cast<double2*>(mine)[0] = make_double2(J[0], J[1]);
+        reinterpret_cast<double2*>(mine)[1] = make_double2(J[2], J[3]);
+        reinterpret_cast<double2*>(mine)[2] = make_double2(J[4], J[5]);
+        reinterpret_cast<double2*>(mine)[3] = make_double2(r_d, 0.0);
+        __syncwarp();
+        dmma_rows(rows, c0, c1, 1.0, false);
+        if (kColor) {  // colour rows B = [Jc | r_c | r_c], A = B scaled per row (cw, 0, 1)
+            __syncwarp();
+            reinterpret_cast<double2*>(mine)[0] = make_double2(Jc[0], Jc[1]);
+            reinterpret_cast<double2*>(mine)[1] = make_double2(Jc[2], Jc[3]);
+            reinterpret_cast<double2*>(mine)[2] = make_double2(Jc[4], Jc[5]);
+            reinterpret_cast<double2*>(mine)[3] = make_double2(r_c, r_c);
+            __syncwarp();
+            dmma_rows(rows, c0, c1, ascale, true);
+        }
+        __syncwarp();
+    }
+    if (tr) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long now = global_ns();
+            atomicMax(tr + 2, now);
+            if (blockIdx.x == 0) tr[1] = now;
+        }
+    }
+    // CTA sum: fragment element (row lane/4, col 2*(lane%4)+j) -> [warp][8][8]
+    __syncthreads();
+    double* frag = rows_sm;  // reuse: nw * 64 doubles
+    frag[warp * 64 + 2 * lane] = c0;
+    frag[warp * 64 + 2 * lane + 1] = c1;
+    if (lane == 0) scratch[warp] = double(count);
+    __syncthreads();
+    constexpr int nw = kTrackThreads / 32;
+    if (threadIdx.x < kAccN) {
+        const int t = threadIdx.x;
+        int e;  // C entry of accumulator t (acc layout: hidx(i,j) i<=j, b, E_d, E_c, count)
+        if (t < 21) {
+            int i = 0, rem = t;
+            while (rem >= 6 - i) {
+                rem -= 6 - i;
+                ++i;
+            }
+            e = i * 8 + (i + rem);
+        } else if (t < 27) {
+            e = (t - 21) * 8 + 6;
+        } else if (t == 27) {
+            e = 6 * 8 + 6;
+        } else {
+            e = 7 * 8 + 7;
+        }
+        double sum = 0.0;
+        for (int w = 0; w < nw; ++w) sum += t == 29 ? scratch[w] : frag[w * 64 + e];
+        blk[t] = sum;
+    }
+    __syncthreads();
+    grid_allreduce<kAccN>(a.grid, blk, out);
+    if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = global_ns();
+    if (a.trace && threadIdx.x == 0) ++s_trace_pass;
+}
+
 // One Accumulate (registration.cpp:49-117) over pyramid level `level`.
 template <bool kJac, bool kColor>
 __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
@@ -327,6 +488,11 @@ __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& 
         a.out->passes += 1;
         a.out->pixel_passes += double(a.F.K[level].w) * double(a.F.K[level].h);
     }
+    if (kJac && kUseMma) {
+        if (color) accumulate_mma<true>(a, level, P, use_mask, cw, scratch, blk, out);
+        else accumulate_mma<false>(a, level, P, use_mask, cw, scratch, blk, out);
+        return;
+    }
     if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
     else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
 }
@@ -377,7 +543,7 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
                     double dn = 0.0;
 #pragma unroll
                     for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
-                    st.dnorm = sqrt(dn);
+                    st.dnorm = dn;  // squared; the sqrt is taken at the accept test, off this critical path
                 }
                 if (a.trace && blockIdx.x == 0 && s_trace_pass < kTracePasses)
                     a.trace[8 * s_trace_pass + 7] = global_ns();  // solve done (next pass's record)
@@ -395,7 +561,7 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
                     st.pose = st.cand;
                     for (int i = 0; i < kAccN; ++i) st.cur[i] = st.trial[i];
                     st.lambda = fmax(st.lambda / R.lambda_down, 1e-12);
-                    if (dnorm < R.eps || decrease < kRelDecreaseTol * cur_err) {
+                    if (sqrt(dnorm) < R.eps || decrease < kRelDecreaseTol * cur_err) {
                         st.converged = 1;
                         st.brk = 1;
                     }
@@ -498,7 +664,7 @@ __device__ __forceinline__ uint8_t grow_bits(const float* depth, int w, int h, i
 }
 
 constexpr int kFfW = 32, kFfH = 32;                 // floodfill tile (square: fewer tile crossings per region)
-constexpr int kFfPx = kFfW * kFfH / kTrackThreads;  // pixels per thread in a tile
+constexpr int kFfPx = (kFfW * kFfH + kTrackThreads - 1) / kTrackThreads;  // pixels per thread in a tile (ceil)
 
 // FloodfillDepth (dynamics_mask.cpp:59-96) as the least fixpoint of the
 // growth rule (its BFS result is seed-order independent, so any monotone
@@ -578,7 +744,8 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint8_t* grow, in
             if (a.trace && threadIdx.x == 0) atomicAdd(a.trace + 8 * (kTracePasses - 2), 1ull);  // seeded tiles
             uint8_t initial[kFfPx];
 #pragma unroll
-            for (int q = 0; q < kFfPx; ++q) initial[q] = sm[(ly0 + q * kRowStep + 1) * SW + lx + 1];
+            for (int q = 0; q < kFfPx; ++q)
+                initial[q] = (ly0 + q * kRowStep < kFfH) ? sm[(ly0 + q * kRowStep + 1) * SW + lx + 1] : 0;
             while (true) {
                 int ch = 0;
                 if (threadIdx.x < 64) {
@@ -632,6 +799,7 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint8_t* grow, in
 #pragma unroll
                     for (int q = 0; q < kFfPx; ++q) {
                         const int ly = ly0 + q * kRowStep, me = (ly + 1) * SW + (lx + 1);
+                        if (ly >= kFfH) break;
                         const uint8_t g = sg[ly * kFfW + lx];
                         if (!sm[me] && (g & 0xF0u)) {
                             for (int k = 0; k < 4; ++k)
@@ -650,7 +818,7 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint8_t* grow, in
 #pragma unroll
             for (int q = 0; q < kFfPx; ++q) {
                 const int ly = ly0 + q * kRowStep, gx = x0 + 1 + lx, gy = y0 + 1 + ly;
-                if (gx < w && gy < h && sm[(ly + 1) * SW + lx + 1] != initial[q]) {
+                if (ly < kFfH && gx < w && gy < h && sm[(ly + 1) * SW + lx + 1] != initial[q]) {
                     m[gy * w + gx] = 1;
                     tile_changed = 1;
                 }
@@ -795,6 +963,17 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
     Pose init;
     for (int i = 0; i < 9; ++i) init.R[i] = a.pose_state[i];
     for (int i = 0; i < 3; ++i) init.t[i] = a.pose_state[9 + i];
+    if (a.mode == kModePassBench) {
+        build_pyramid(a, true, false);
+        const unsigned long long t0 = global_ns();
+        for (int it = 0; it < a.bench_iters; ++it)
+            pass<true>(a, a.bench_level, init, false, false, a.reg.color_weight, scratch, blk, red);
+        if (lead) {
+            a.out->final_error = double(global_ns() - t0) * 1e-3 / a.bench_iters;  // us per pass (barrier incl.)
+            for (int i = 0; i < kAccN; ++i) a.out->acc[i] = red[i];
+        }
+        return;
+    }
     const bool masked_reg = a.mode == kModeRegister && a.use_mask;
     build_pyramid(a, true, masked_reg);
     run_register(a, init, masked_reg, st, scratch, blk);

@@ -16,6 +16,7 @@ constexpr int kMaxLevels = 6;
 constexpr int kTrackThreads = RF_TRACK_THREADS;
 constexpr int kTrackMinBlocks = RF_TRACK_MIN_BLOCKS;
 constexpr int kTileW = 16, kTileH = kTrackThreads / kTileW;  // pixel tile per CTA step, 1 px per thread
+constexpr int kTrackDynSmem = kTrackThreads * 8 * 8;         // [warp][32][8] fp64 rows for the DMMA passes
 
 struct RegParams {  // RegistrationConfig, registration.hpp:13-23
     double color_weight;
@@ -71,6 +72,7 @@ enum TrackMode : int {
     kModeEvalDepth = 3,  // value pass at level 0 writing residuals (EvaluateDepthError)
     kModeEvalColor = 4,  // value pass at level 0, colour error (EvaluateColorError)
     kModeMask = 5,       // BuildMask stages on given residuals
+    kModePassBench = 6,  // diagnostics: bench_iters Jacobian passes at bench_level (timeline in out)
 };
 
 struct TrackArgs {
@@ -87,6 +89,7 @@ struct TrackArgs {
     double* pose_state;  // in: initial pose; out: tracked pose (kModeFrame/Register)
     TrackOut* out;
     uint32_t* vol_counters;  // kModeFrame: snapshot kNumBlocks -> kBlocksBefore
+    int bench_iters, bench_level;  // kModePassBench
 };
 
 }  // namespace rfb
