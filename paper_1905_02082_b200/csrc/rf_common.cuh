@@ -335,6 +335,56 @@ __device__ __forceinline__ void interp_cell(const VolumeView& V, const uint2 (&c
     }
 }
 
+// Exact integer Rec.709 luma times 1e4 (2126 r + 7152 g + 722 b < 2^22) as a
+// double, without a conversion instruction: OR into the mantissa of 2^52.
+__device__ __forceinline__ double voxel_luma_e4(uint2 v) {
+    const unsigned int L = 2126u * ((v.y >> 8) & 0xFFu) + 7152u * ((v.y >> 16) & 0xFFu) + 722u * (v.y >> 24);
+    return __longlong_as_double(0x4330000000000000ll | (long long)L) - 4503599627370496.0;
+}
+
+// The same interpolant and gradients for the tracking Jacobian passes, as
+// nested lerps with fused multiply-adds (shorter dependency chains, about
+// half the fp64 instructions) and the intensity from exact integer lumas
+// scaled once. Differs from interp_cell in the last bits only; the Jacobian
+// passes are held to the normal-equation (1e-9) and pose (1e-4) bars, the
+// value passes that must be bit-exact keep interp_cell.
+template <bool kIntensity>
+__device__ __forceinline__ void interp_cell_fast(const VolumeView& V, const uint2 (&c)[8], const double f[3],
+                                                 CellSample& out) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = double(voxel_sdf(c[k]));
+    // x-differences at the four (y, z) edges, then lerps in y and z
+    const double dx00 = v[1] - v[0], dx10 = v[3] - v[2], dx01 = v[5] - v[4], dx11 = v[7] - v[6];
+    const double x00 = __fma_rn(f[0], dx00, v[0]), x10 = __fma_rn(f[0], dx10, v[2]);
+    const double x01 = __fma_rn(f[0], dx01, v[4]), x11 = __fma_rn(f[0], dx11, v[6]);
+    const double y0 = __fma_rn(f[1], x10 - x00, x00), y1 = __fma_rn(f[1], x11 - x01, x01);
+    out.sdf = __fma_rn(f[2], y1 - y0, y0);
+    const double inv_s = V.inv_voxel_size;
+    {
+        const double gxz0 = __fma_rn(f[1], dx10 - dx00, dx00), gxz1 = __fma_rn(f[1], dx11 - dx01, dx01);
+        out.gs[0] = __fma_rn(f[2], gxz1 - gxz0, gxz0) * inv_s;
+        out.gs[1] = __fma_rn(f[2], (x11 - x01) - (x10 - x00), x10 - x00) * inv_s;
+        out.gs[2] = (y1 - y0) * inv_s;
+    }
+    if (kIntensity) {
+        double q[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q[k] = voxel_luma_e4(c[k]);
+        const double ex00 = q[1] - q[0], ex10 = q[3] - q[2], ex01 = q[5] - q[4], ex11 = q[7] - q[6];
+        const double a00 = __fma_rn(f[0], ex00, q[0]), a10 = __fma_rn(f[0], ex10, q[2]);
+        const double a01 = __fma_rn(f[0], ex01, q[4]), a11 = __fma_rn(f[0], ex11, q[6]);
+        const double b0 = __fma_rn(f[1], a10 - a00, a00), b1 = __fma_rn(f[1], a11 - a01, a01);
+        constexpr double kE4 = 1e-4;
+        out.inten = __fma_rn(f[2], b1 - b0, b0) * kE4;
+        const double gz0 = __fma_rn(f[1], ex10 - ex00, ex00), gz1 = __fma_rn(f[1], ex11 - ex01, ex01);
+        const double s = inv_s * kE4;
+        out.gi[0] = __fma_rn(f[2], gz1 - gz0, gz0) * s;
+        out.gi[1] = __fma_rn(f[2], (a11 - a01) - (a10 - a00), a10 - a00) * s;
+        out.gi[2] = (b1 - b0) * s;
+    }
+}
+
 template <bool kGrad, bool kIntensity, bool kExact = true>
 __device__ __forceinline__ bool sample_point(const VolumeView& V, const double p[3], CellSample& out,
                                              const double* lut = nullptr) {
@@ -343,7 +393,8 @@ __device__ __forceinline__ bool sample_point(const VolumeView& V, const double p
     cell_of<kExact>(p[0], p[1], p[2], V, base, f);
     uint2 c[8];
     if (!gather_corners(V, base[0], base[1], base[2], c)) return false;
-    interp_cell<kGrad, kIntensity>(V, c, f, out, lut);
+    if (!kExact && kGrad) interp_cell_fast<kIntensity>(V, c, f, out);
+    else interp_cell<kGrad, kIntensity>(V, c, f, out, lut);
     return true;
 }
 
