@@ -117,8 +117,7 @@ struct Workspace {
         }();
         if (carveout >= 0)
             CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributePreferredSharedMemoryCarveout, carveout));
-        CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrackDynSmem));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_track, kTrackThreads, kTrackDynSmem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_track, kTrackThreads, 0));
         require(per > 0, RF_CUDA_ERROR, "tracking kernel does not fit on an SM");
         track_grid = sms * per;
         gsync.ensure(sizeof(GridSync));
@@ -373,8 +372,7 @@ struct rf_volume {
         a.grid.parity = ws.parity;
         ws.parity ^= 1;
         void* args[] = {&a};
-        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, kTrackDynSmem,
-                                       ws.stream));
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
     }
     TrackOut fetch_out() {
         CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
@@ -929,8 +927,7 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
         ws.parity ^= 1;
         a.out = ws.out.as<TrackOut>();
         void* args[] = {&a};
-        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, kTrackDynSmem,
-                                       ws.stream));
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
         CK(cudaMemcpyAsync(out, ws.mask_in.p, n, cudaMemcpyDeviceToHost, ws.stream));
         CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
         ws.sync();

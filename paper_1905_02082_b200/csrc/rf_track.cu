@@ -22,7 +22,6 @@ __device__ __forceinline__ int hidx(int i, int j) { return i * 6 - (i * (i - 1))
 
 __shared__ int s_trace_pass;  // per-CTA pass counter for the optional timeline
 __shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (see voxel_luma_lut)
-extern __shared__ double s_dyn[];   // kTrackDynSmem bytes: the tensor-core row staging
 
 struct RegState {
     Pose pose, cand;
@@ -194,175 +193,6 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
 }
 
 // ------------------------------------------------------------------ pixel pass
-// Jacobian passes accumulate the normal equations on the FP64 tensor cores:
-// per warp and 32 pixels, H | b | E is the 8x8 product R^T R of the pixels'
-// rows R = [J | r | 0] (and, for the photometric term, A^T B with
-// A = [cw Jc | 0 | r_c], B = [Jc | r_c | r_c]), i.e. 16 DMMA.8x8x4 into a
-// 2-double-per-lane fragment instead of 30 fp64 accumulators per thread: the
-// register file then holds twice as many warps to hide the gather latency.
-#ifndef RF_TRACK_MMA
-#define RF_TRACK_MMA 0  // measured slower at 8 warps/SM (tools/pass_bench.py); kept as an option
-#endif
-constexpr bool kUseMma = RF_TRACK_MMA != 0;
-
-__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(c0), "+d"(c1)
-                 : "d"(a), "d"(b));
-}
-
-// Adds the 32 rows in `rows` (this warp's [32][8] smem block) as R^T R to
-// the fragment; a lane scaled by `ascale` supplies the A operand (colour).
-__device__ __forceinline__ void dmma_rows(const double* rows, double& c0, double& c1, double ascale, bool scaled) {
-    const int lane = threadIdx.x & 31;
-    const double* col = rows + (lane & 3) * 8 + (lane >> 2);  // A[m = lane/4][k = lane%4] of k-step 0
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-        const double x = col[32 * s];  // pixel 4s + lane%4, component lane/4
-        dmma_884(c0, c1, scaled ? x * ascale : x, x);
-    }
-}
-
-// One Accumulate with Jacobian (registration.cpp:49-95) over level `level`
-// on the tensor cores. Same pixel walk and per-pixel arithmetic as the
-// scalar path; only the summation order of the normal equations differs.
-template <bool kColor>
-__device__ void accumulate_mma(const TrackArgs& a, int level, const Pose& P, bool use_mask, double cw,
-                               double* scratch, double* blk, double* out) {
-    double* rows_sm = s_dyn;  // one [32][8] block per warp (dynamic shared memory, kTrackDynSmem)
-    const FrameView& F = a.F;
-    const Intr K = F.K[level];
-    const double min_depth = a.V.min_depth, max_depth = a.V.max_depth;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* rows = rows_sm + warp * 256;
-    double* mine = rows + lane * 8;
-    // colour A-operand scale by fragment row m = lane/4: cw on J rows, 0 on
-    // the depth-residual row, 1 on the colour-error row
-    const double ascale = (lane >> 2) < 6 ? cw : ((lane >> 2) == 6 ? 0.0 : 1.0);
-    double c0 = 0.0, c1 = 0.0;
-    unsigned int count = 0;
-    const int ntx = (K.w + kTileW - 1) / kTileW, nty = (K.h + kTileH - 1) / kTileH;
-    const float* depth = level == 0 ? F.depth0 : F.depth[level];
-    const uint8_t* mask = use_mask ? F.mask[level] : nullptr;
-    unsigned long long* tr = (a.trace && s_trace_pass < kTracePasses) ? a.trace + 8 * s_trace_pass : nullptr;
-    if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
-        tr[0] = global_ns();
-        tr[4] = level;
-        tr[5] = (unsigned long long)K.w * K.h;
-        tr[6] = 1;
-    }
-    int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;  // uniform per CTA: every lane runs every step
-    const int step_y = gridDim.x / ntx, step_x = gridDim.x % ntx;
-    for (; ty < nty; tx += step_x, ty += step_y) {
-        if (tx >= ntx) {
-            tx -= ntx;
-            ++ty;
-            if (ty >= nty) break;
-        }
-        const int u = tx * kTileW + (threadIdx.x % kTileW);
-        const int v = ty * kTileH + (threadIdx.x / kTileW);
-        double J[6] = {0, 0, 0, 0, 0, 0}, Jc[6] = {0, 0, 0, 0, 0, 0}, r_d = 0.0, r_c = 0.0;
-        bool valid = false;
-        if (u < K.w && v < K.h) {
-            const int p = v * K.w + u;
-            const float d = level == 0 ? __ldg(depth + p) : __ldcg(depth + p);
-            if (depth_valid(d) && !(d < min_depth) && !(d > max_depth) && !(mask && __ldcg(mask + p) != 0)) {
-                const double dd = double(d);
-                const double x0 = (double(u) - K.cx) * K.ifx * dd;  // Backproject (geometry.hpp:41-43)
-                const double x1 = (double(v) - K.cy) * K.ify * dd;
-                double y[3];
-                pose_apply(P, x0, x1, dd, y);
-                CellSample cs;
-                if (sample_point<true, kColor, false>(a.V, y, cs, s_luma_lut)) {
-                    valid = true;
-                    r_d = cs.sdf;
-                    J[0] = cs.gs[0];
-                    J[1] = cs.gs[1];
-                    J[2] = cs.gs[2];
-                    J[3] = y[1] * cs.gs[2] - y[2] * cs.gs[1];
-                    J[4] = y[2] * cs.gs[0] - y[0] * cs.gs[2];
-                    J[5] = y[0] * cs.gs[1] - y[1] * cs.gs[0];
-                    if (kColor) {
-                        double I;
-                        if (level == 0) {
-                            const uint8_t* c = F.rgb0 + 3 * size_t(p);
-                            I = double(float(luma(__ldg(c), __ldg(c + 1), __ldg(c + 2))));
-                        } else {
-                            I = double(__ldcg(F.inten[level] + p));
-                        }
-                        r_c = (cs.inten - I) * kIntensityScale;
-                        Jc[0] = cs.gi[0] * kIntensityScale;
-                        Jc[1] = cs.gi[1] * kIntensityScale;
-                        Jc[2] = cs.gi[2] * kIntensityScale;
-                        Jc[3] = (y[1] * cs.gi[2] - y[2] * cs.gi[1]) * kIntensityScale;
-                        Jc[4] = (y[2] * cs.gi[0] - y[0] * cs.gi[2]) * kIntensityScale;
-                        Jc[5] = (y[0] * cs.gi[1] - y[1] * cs.gi[0]) * kIntensityScale;
-                    }
-                }
-            }
-        }
-        count += __popc(__ballot_sync(0xffffffffu, valid));
-        // depth rows [J | r_d | 0]
-        reinterpret_cast<double2*>(mine)[0] = make_double2(J[0], J[1]);
-        reinterpret_cast<double2*>(mine)[1] = make_double2(J[2], J[3]);
-        reinterpret_cast<double2*>(mine)[2] = make_double2(J[4], J[5]);
-        reinterpret_cast<double2*>(mine)[3] = make_double2(r_d, 0.0);
-        __syncwarp();
-        dmma_rows(rows, c0, c1, 1.0, false);
-        if (kColor) {  // colour rows B = [Jc | r_c | r_c], A = B scaled per row (cw, 0, 1)
-            __syncwarp();
-            reinterpret_cast<double2*>(mine)[0] = make_double2(Jc[0], Jc[1]);
-            reinterpret_cast<double2*>(mine)[1] = make_double2(Jc[2], Jc[3]);
-            reinterpret_cast<double2*>(mine)[2] = make_double2(Jc[4], Jc[5]);
-            reinterpret_cast<double2*>(mine)[3] = make_double2(r_c, r_c);
-            __syncwarp();
-            dmma_rows(rows, c0, c1, ascale, true);
-        }
-        __syncwarp();
-    }
-    if (tr) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const unsigned long long now = global_ns();
-            atomicMax(tr + 2, now);
-            if (blockIdx.x == 0) tr[1] = now;
-        }
-    }
-    // CTA sum: fragment element (row lane/4, col 2*(lane%4)+j) -> [warp][8][8]
-    __syncthreads();
-    double* frag = rows_sm;  // reuse: nw * 64 doubles
-    frag[warp * 64 + 2 * lane] = c0;
-    frag[warp * 64 + 2 * lane + 1] = c1;
-    if (lane == 0) scratch[warp] = double(count);
-    __syncthreads();
-    constexpr int nw = kTrackThreads / 32;
-    if (threadIdx.x < kAccN) {
-        const int t = threadIdx.x;
-        int e;  // C entry of accumulator t (acc layout: hidx(i,j) i<=j, b, E_d, E_c, count)
-        if (t < 21) {
-            int i = 0, rem = t;
-            while (rem >= 6 - i) {
-                rem -= 6 - i;
-                ++i;
-            }
-            e = i * 8 + (i + rem);
-        } else if (t < 27) {
-            e = (t - 21) * 8 + 6;
-        } else if (t == 27) {
-            e = 6 * 8 + 6;
-        } else {
-            e = 7 * 8 + 7;
-        }
-        double sum = 0.0;
-        for (int w = 0; w < nw; ++w) sum += t == 29 ? scratch[w] : frag[w * 64 + e];
-        blk[t] = sum;
-    }
-    __syncthreads();
-    grid_allreduce<kAccN>(a.grid, blk, out);
-    if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = global_ns();
-    if (a.trace && threadIdx.x == 0) ++s_trace_pass;
-}
-
 // One Accumulate (registration.cpp:49-117) over pyramid level `level`.
 template <bool kJac, bool kColor>
 __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
@@ -487,11 +317,6 @@ __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& 
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.out->passes += 1;
         a.out->pixel_passes += double(a.F.K[level].w) * double(a.F.K[level].h);
-    }
-    if (kJac && kUseMma) {
-        if (color) accumulate_mma<true>(a, level, P, use_mask, cw, scratch, blk, out);
-        else accumulate_mma<false>(a, level, P, use_mask, cw, scratch, blk, out);
-        return;
     }
     if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
     else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out);

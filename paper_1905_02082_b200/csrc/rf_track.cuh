@@ -8,15 +8,14 @@ namespace rfb {
 
 constexpr int kMaxLevels = 6;
 #ifndef RF_TRACK_THREADS
-#define RF_TRACK_THREADS 256
+#define RF_TRACK_THREADS 384  // 12 warps at <= 168 registers (tools/pass_bench.py: 16.6 vs 19.9 us per L0 pass at 256)
 #endif
 #ifndef RF_TRACK_MIN_BLOCKS
-#define RF_TRACK_MIN_BLOCKS 1  // one 8-warp CTA per SM: no register spills, 148 grid partials
+#define RF_TRACK_MIN_BLOCKS 1  // one CTA per SM: 148 grid partials
 #endif
 constexpr int kTrackThreads = RF_TRACK_THREADS;
 constexpr int kTrackMinBlocks = RF_TRACK_MIN_BLOCKS;
 constexpr int kTileW = 16, kTileH = kTrackThreads / kTileW;  // pixel tile per CTA step, 1 px per thread
-constexpr int kTrackDynSmem = kTrackThreads * 8 * 8;         // [warp][32][8] fp64 rows for the DMMA passes
 
 struct RegParams {  // RegistrationConfig, registration.hpp:13-23
     double color_weight;
