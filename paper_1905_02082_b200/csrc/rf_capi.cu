@@ -277,7 +277,7 @@ struct rf_volume {
     void clear(bool full) {
         if (full) {
             CK(cudaMemsetAsync(slots.p, 0xFF, cap * sizeof(HashSlot), ws.stream));
-            CK(cudaMemsetAsync(links.p, 0xFF, cfg.max_blocks * kLinkStride * sizeof(uint32_t), ws.stream));
+            CK(cudaMemsetAsync(links.p, 0xFF, cap * kLinkStride * sizeof(uint32_t), ws.stream));
             CK(cudaMemsetAsync(voxels.p, 0, cfg.max_blocks * kBrickVoxels * sizeof(Voxel), ws.stream));
         } else {
             k_vol_clear<<<4 * 148, 128, 0, ws.stream>>>(view);
@@ -433,11 +433,11 @@ void create_volume(const rf_volume_config* cfg, int device, rf_volume** out) {
     v->slots.ensure(v->cap * sizeof(HashSlot));
     v->coords.ensure(cfg->max_blocks * sizeof(int4));
     v->voxels.ensure(cfg->max_blocks * kBrickVoxels * sizeof(Voxel));
-    v->links.ensure(cfg->max_blocks * kLinkStride * sizeof(uint32_t));
+    v->links.ensure(v->cap * kLinkStride * sizeof(uint32_t));  // one record per hash slot
     v->counters.ensure(kNumCounters * sizeof(uint32_t));
     v->ws.init(device);
     CK(cudaMemsetAsync(v->slots.p, 0xFF, v->cap * sizeof(HashSlot), v->ws.stream));
-    CK(cudaMemsetAsync(v->links.p, 0xFF, cfg->max_blocks * kLinkStride * sizeof(uint32_t), v->ws.stream));
+    CK(cudaMemsetAsync(v->links.p, 0xFF, v->cap * kLinkStride * sizeof(uint32_t), v->ws.stream));
     CK(cudaMemsetAsync(v->voxels.p, 0, cfg->max_blocks * kBrickVoxels * sizeof(Voxel), v->ws.stream));
     CK(cudaMemsetAsync(v->counters.p, 0, kNumCounters * sizeof(uint32_t), v->ws.stream));
     v->ws.list.ensure(cfg->max_blocks * sizeof(uint32_t));
@@ -689,7 +689,7 @@ rf_status rf_volume_reset(rf_volume* v) {
         const uint64_t nb = v->num_blocks();
         CK(cudaMemsetAsync(v->slots.p, 0xFF, v->cap * sizeof(HashSlot), v->ws.stream));
         CK(cudaMemsetAsync(v->voxels.p, 0, nb * kBrickVoxels * sizeof(Voxel), v->ws.stream));
-        CK(cudaMemsetAsync(v->links.p, 0xFF, nb * kLinkStride * sizeof(uint32_t), v->ws.stream));
+        CK(cudaMemsetAsync(v->links.p, 0xFF, v->cap * kLinkStride * sizeof(uint32_t), v->ws.stream));
         CK(cudaMemsetAsync(v->counters.p, 0, kNumCounters * sizeof(uint32_t), v->ws.stream));
         v->ws.sync();
     });

@@ -52,7 +52,7 @@ struct VolumeView {
     uint32_t max_blocks;
     int4* coords;        // brick coordinate per pool index; w = its hash slot
     Voxel* voxels;       // pool, kBrickVoxels per brick, x fastest then y then z
-    uint32_t* links;     // kLinkStride per brick: pool index of the brick at +(q&1, q>>1&1, q>>2), q = 1..7
+    uint32_t* links;     // kLinkStride per HASH SLOT: [0] the slot's brick, [q] the brick at +(q&1, q>>1&1, q>>2)
     uint32_t* counters;  // see VolumeCounters
     double voxel_size, truncation;
     double inv_voxel_size;  // 1.0 / voxel_size (the reference's inv_s, tsdf_volume.cpp:336)
@@ -140,6 +140,34 @@ __device__ __forceinline__ uint32_t hash_find(const VolumeView& V, int x, int y,
     return kInvalid;
 }
 
+// Slot of a brick key (kInvalid when absent or overflowed).
+__device__ __forceinline__ uint32_t hash_find_slot(const VolumeView& V, int x, int y, int z) {
+    if (!coord_in_range(x, y, z)) return kInvalid;
+    const unsigned long long key = pack_key(x, y, z);
+    uint32_t idx = hash_coord(x, y, z) & V.hash_mask;
+    for (uint32_t probe = 0; probe <= V.hash_mask; ++probe) {
+        const uint4 s = __ldg(reinterpret_cast<const uint4*>(V.slots + idx));
+        const unsigned long long k = (unsigned long long)s.x | ((unsigned long long)s.y << 32);
+        if (k == key) return s.z >= kOverflowed ? kInvalid : idx;
+        if (k == kEmptyKey) return kInvalid;
+        idx = (idx + 1) & V.hash_mask;
+    }
+    return kInvalid;
+}
+
+// Continues a linear probe after slot `idx` missed; returns the key's slot
+// (kInvalid when absent).
+__device__ __forceinline__ uint32_t hash_find_slot_from(const VolumeView& V, unsigned long long key, uint32_t idx) {
+    for (uint32_t probe = 0; probe < V.hash_mask; ++probe) {
+        idx = (idx + 1) & V.hash_mask;
+        const uint4 s = __ldg(reinterpret_cast<const uint4*>(V.slots + idx));
+        const unsigned long long k = (unsigned long long)s.x | ((unsigned long long)s.y << 32);
+        if (k == key) return idx;
+        if (k == kEmptyKey) return kInvalid;
+    }
+    return kInvalid;
+}
+
 // Lock-free linear-probing insert (no deletion). Returns 1 when this thread
 // created the brick, 0 when it already existed, -1 on overflow.
 __device__ __forceinline__ int hash_insert(const VolumeView& V, int x, int y, int z) {
@@ -200,57 +228,80 @@ struct CellSample {
 // The 8 corners of the interpolation cell at voxel (bx,by,bz) live in the
 // brick of the base voxel and, when the cell straddles brick faces (local
 // coordinate 7 on an axis, one cell in three), in its +x/+y/+z neighbours.
-// One hash probe finds the base brick; the neighbours come from the base
-// brick's link record (pool indices of its 7 "+" neighbours, maintained at
-// allocation by k_link), so every lane runs the same code: no divergent
-// second/third hash probes.
+// The neighbours come from a link record stored next to the hash slot
+// (links[slot * 8 + q] = pool index of the brick at +(q&1, q>>1&1, q>>2)),
+// so its load is issued together with the slot's, before the key compare:
+// one dependent L2 round trip (slot + record) instead of two, and every
+// lane runs the same code.
 __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int by, int bz, uint2 c[8]) {
     const int lx = bx & 7, ly = by & 7, lz = bz & 7;
-    const uint32_t b0 = hash_find(V, bx >> 3, by >> 3, bz >> 3);  // arithmetic shift == FloorDiv by 8
-    if (b0 == kInvalid) return false;
+    const int cx = bx >> 3, cy = by >> 3, cz = bz >> 3;  // arithmetic shift == FloorDiv by 8
+    if (!coord_in_range(cx, cy, cz)) return false;
+    const unsigned long long key = pack_key(cx, cy, cz);
+    uint32_t idx = hash_coord(cx, cy, cz) & V.hash_mask;
     const int smask = int(lx == 7) | (int(ly == 7) << 1) | (int(lz == 7) << 2);
+    const uint4 s = __ldg(reinterpret_cast<const uint4*>(V.slots + idx));
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0;
+    if (smask) {
+        r0 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(idx) * kLinkStride));
+        r1 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(idx) * kLinkStride) + 1);
+    }
+    const unsigned long long k = (unsigned long long)s.x | ((unsigned long long)s.y << 32);
+    uint32_t b0;
+    if (k == key) {
+        b0 = s.z >= kOverflowed ? kInvalid : s.z;
+    } else if (k == kEmptyKey) {
+        return false;
+    } else {  // collision: continue the probe, then the record of the slot found (rare)
+        idx = hash_find_slot_from(V, key, idx);
+        if (idx == kInvalid) return false;
+        b0 = __ldg(&V.slots[idx].value);
+        if (smask) {
+            r0 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(idx) * kLinkStride));
+            r1 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(idx) * kLinkStride) + 1);
+        }
+    }
+    if (b0 >= kOverflowed) return false;
     uint32_t n[8];
     n[0] = b0;
     if (smask) {
-        const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(b0) * kLinkStride));
-        const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(b0) * kLinkStride) + 1);
         n[1] = r0.y; n[2] = r0.z; n[3] = r0.w; n[4] = r1.x; n[5] = r1.y; n[6] = r1.z; n[7] = r1.w;
     } else {
 #pragma unroll
         for (int q = 1; q < 8; ++q) n[q] = b0;
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;  // compile-time corner offset
+    for (int kk = 0; kk < 8; ++kk) {
+        const int dx = kk & 1, dy = (kk >> 1) & 1, dz = kk >> 2;  // compile-time corner offset
         const int kbits = dx | (dy << 1) | (dz << 2);
-        const int code = kbits & smask;                       // which neighbour holds this corner
+        const int code = kbits & smask;                          // which neighbour holds this corner
         uint32_t b = b0;
 #pragma unroll
         for (int q = 1; q < 8; ++q)
             if ((q & ~kbits) == 0) b = (code == q) ? n[q] : b;
         if (b >= kOverflowed) return false;
-        const int cx = (lx + dx) & 7, cy = (ly + dy) & 7, cz = (lz + dz) & 7;
-        c[k] = __ldg(reinterpret_cast<const uint2*>(brick_ptr(V, b)) + ((cz * 8 + cy) * 8 + cx));
+        const int ox = (lx + dx) & 7, oy = (ly + dy) & 7, oz = (lz + dz) & 7;
+        c[kk] = __ldg(reinterpret_cast<const uint2*>(brick_ptr(V, b)) + ((oz * 8 + oy) * 8 + ox));
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-        if ((c[k].y & 0xFFu) == 0u) return false;  // weight byte
+    for (int kk = 0; kk < 8; ++kk)
+        if ((c[kk].y & 0xFFu) == 0u) return false;  // weight byte
     return true;
 }
 
-// Fills the link records of bricks [lo, hi) and points their "-" neighbours'
-// records at them (tsdf_volume.hpp:149-185 allocates; this only indexes).
-// Every write is a pure function of the key set, so concurrent writers of the
-// same slot agree.
+// Fills the link record of brick b (at its hash slot, coords[b].w) and
+// points its "-" neighbours' records at it (tsdf_volume.hpp:149-185
+// allocates; this only indexes). Every write is a pure function of the key
+// set, so concurrent writers of the same word agree.
 __device__ __forceinline__ void link_brick(const VolumeView& V, uint32_t b) {
     const int4 c = V.coords[b];
-    uint32_t* own = V.links + size_t(b) * kLinkStride;
+    uint32_t* own = V.links + size_t(uint32_t(c.w)) * kLinkStride;
     own[0] = b;
 #pragma unroll
     for (int q = 1; q < 8; ++q) {
         own[q] = hash_find(V, c.x + (q & 1), c.y + ((q >> 1) & 1), c.z + (q >> 2));
-        const uint32_t a = hash_find(V, c.x - (q & 1), c.y - ((q >> 1) & 1), c.z - (q >> 2));
-        if (a != kInvalid) V.links[size_t(a) * kLinkStride + q] = b;
+        const uint32_t sa = hash_find_slot(V, c.x - (q & 1), c.y - ((q >> 1) & 1), c.z - (q >> 2));
+        if (sa != kInvalid) V.links[size_t(sa) * kLinkStride + q] = b;
     }
 }
 
@@ -396,98 +447,6 @@ __device__ __forceinline__ bool sample_point(const VolumeView& V, const double p
     if (!kExact && kGrad) interp_cell_fast<kIntensity>(V, c, f, out);
     else interp_cell<kGrad, kIntensity>(V, c, f, out, lut);
     return true;
-}
-
-// Continues a linear probe after the first slot missed (the rare path of the
-// batched gather below).
-__device__ __forceinline__ uint32_t hash_find_from(const VolumeView& V, unsigned long long key, uint32_t idx) {
-    for (uint32_t probe = 0; probe < V.hash_mask; ++probe) {
-        idx = (idx + 1) & V.hash_mask;
-        const uint4 s = __ldg(reinterpret_cast<const uint4*>(V.slots + idx));
-        const unsigned long long k = (unsigned long long)s.x | ((unsigned long long)s.y << 32);
-        if (k == key) return s.z >= kOverflowed ? kInvalid : s.z;
-        if (k == kEmptyKey) return kInvalid;
-    }
-    return kInvalid;
-}
-
-// gather_corners for NP cells at once, phase by phase (first hash slot, link
-// record, the 8 voxels), so each thread keeps NP independent load chains in
-// flight instead of one: the tracking passes are bound by this latency.
-// Same results as gather_corners per cell. ok[i] in: cell wanted; out: all
-// 8 corners allocated and observed.
-template <int NP>
-__device__ __forceinline__ void gather_corners_batch(const VolumeView& V, const int (&base)[NP][3], bool (&ok)[NP],
-                                                     uint2 (&c)[NP][8]) {
-    unsigned long long key[NP];
-    uint32_t idx[NP], b0[NP];
-    uint4 s[NP];
-#pragma unroll
-    for (int i = 0; i < NP; ++i) {
-        const int x = base[i][0] >> 3, y = base[i][1] >> 3, z = base[i][2] >> 3;  // FloorDiv by 8
-        ok[i] = ok[i] && coord_in_range(x, y, z);
-        if (ok[i]) {
-            key[i] = pack_key(x, y, z);
-            idx[i] = hash_coord(x, y, z) & V.hash_mask;
-            s[i] = __ldg(reinterpret_cast<const uint4*>(V.slots + idx[i]));
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < NP; ++i) {
-        if (!ok[i]) continue;
-        const unsigned long long k = (unsigned long long)s[i].x | ((unsigned long long)s[i].y << 32);
-        if (k == key[i]) b0[i] = s[i].z >= kOverflowed ? kInvalid : s[i].z;
-        else if (k == kEmptyKey) b0[i] = kInvalid;
-        else b0[i] = hash_find_from(V, key[i], idx[i]);
-        ok[i] = b0[i] != kInvalid;
-    }
-    int smask[NP];
-    uint4 r0[NP], r1[NP];
-#pragma unroll
-    for (int i = 0; i < NP; ++i) {
-        smask[i] = int((base[i][0] & 7) == 7) | (int((base[i][1] & 7) == 7) << 1) | (int((base[i][2] & 7) == 7) << 2);
-        if (ok[i] && smask[i]) {
-            r0[i] = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(b0[i]) * kLinkStride));
-            r1[i] = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(b0[i]) * kLinkStride) + 1);
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < NP; ++i) {
-        if (!ok[i]) continue;
-        uint32_t n[8];
-        n[0] = b0[i];
-        if (smask[i]) {
-            n[1] = r0[i].y; n[2] = r0[i].z; n[3] = r0[i].w; n[4] = r1[i].x; n[5] = r1[i].y; n[6] = r1[i].z;
-            n[7] = r1[i].w;
-        } else {
-#pragma unroll
-            for (int q = 1; q < 8; ++q) n[q] = b0[i];
-        }
-        const int lx = base[i][0] & 7, ly = base[i][1] & 7, lz = base[i][2] & 7;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int dx = k & 1, dy = (k >> 1) & 1, dz = k >> 2;
-            const int kbits = dx | (dy << 1) | (dz << 2);
-            const int code = kbits & smask[i];
-            uint32_t b = b0[i];
-#pragma unroll
-            for (int q = 1; q < 8; ++q)
-                if ((q & ~kbits) == 0) b = (code == q) ? n[q] : b;
-            if (b >= kOverflowed) {
-                ok[i] = false;
-                b = b0[i];
-            }
-            const int cx = (lx + dx) & 7, cy = (ly + dy) & 7, cz = (lz + dz) & 7;
-            c[i][k] = __ldg(reinterpret_cast<const uint2*>(brick_ptr(V, b)) + ((cz * 8 + cy) * 8 + cx));
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < NP; ++i)
-        if (ok[i]) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if ((c[i][k].y & 0xFFu) == 0u) ok[i] = false;  // weight byte
-        }
 }
 
 // ---------------------------------------------------------------- grid sync

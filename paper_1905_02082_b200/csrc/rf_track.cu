@@ -225,11 +225,23 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
         const int v = ty * kTileH + (threadIdx.x / kTileW);
         if (u >= K.w || v >= K.h) continue;
         const int p = v * K.w + u;
+        // Every per-pixel input is loaded up front (depth, mask, intensity),
+        // so only the hash slot and voxel gathers are dependent round trips.
         const float d = level == 0 ? __ldg(depth + p) : __ldcg(depth + p);
+        const bool masked = mask && __ldcg(mask + p) != 0;
+        uint32_t rgbw = 0;
+        float inten = 0.f;
+        if (kColor) {
+            if (level == 0) {
+                const uint8_t* c = F.rgb0 + 3 * size_t(p);
+                rgbw = uint32_t(__ldg(c)) | (uint32_t(__ldg(c + 1)) << 8) | (uint32_t(__ldg(c + 2)) << 16);
+            } else {
+                inten = __ldcg(F.inten[level] + p);
+            }
+        }
         float rs = 0.f;
         uint8_t rv = 0;
         if (depth_valid(d) && !(d < min_depth) && !(d > max_depth)) {
-            const bool masked = mask && __ldcg(mask + p) != 0;
             if (!(masked && !write_res)) {
                 const double dd = double(d);
                 // Backproject (geometry.hpp:41-43); Jacobian passes use reciprocals
@@ -241,14 +253,9 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
                 if (sample_point<kJac, kColor, !kJac>(a.V, y, cs, s_luma_lut)) {
                     const double r_d = cs.sdf;
                     double I = 0.0;
-                    if (kColor) {
-                        if (level == 0) {
-                            const uint8_t* c = F.rgb0 + 3 * size_t(p);
-                            I = double(float(luma(__ldg(c), __ldg(c + 1), __ldg(c + 2))));
-                        } else {
-                            I = double(__ldcg(F.inten[level] + p));
-                        }
-                    }
+                    if (kColor)  // ToIntensity (image.hpp:85-91) at level 0, the pyramid's f32 above
+                        I = level == 0 ? double(float(luma(uint8_t(rgbw), uint8_t(rgbw >> 8), uint8_t(rgbw >> 16))))
+                                       : double(inten);
                     if (kJac) {
                         const double J[6] = {cs.gs[0], cs.gs[1], cs.gs[2], y[1] * cs.gs[2] - y[2] * cs.gs[1],
                                              y[2] * cs.gs[0] - y[0] * cs.gs[2], y[0] * cs.gs[1] - y[1] * cs.gs[0]};

@@ -307,9 +307,9 @@ __global__ void k_vol_clear(VolumeView V) {
         uint4* vox = reinterpret_cast<uint4*>(V.voxels + size_t(b) * kBrickVoxels);
         for (int i = threadIdx.x; i < kBrickVoxels * int(sizeof(Voxel)) / 16; i += blockDim.x)
             vox[i] = make_uint4(0, 0, 0, 0);
-        if (threadIdx.x < kLinkStride) V.links[size_t(b) * kLinkStride + threadIdx.x] = kInvalid;
+        const uint32_t slot = uint32_t(V.coords[b].w);
+        if (threadIdx.x < kLinkStride) V.links[size_t(slot) * kLinkStride + threadIdx.x] = kInvalid;
         if (threadIdx.x == 0) {
-            const uint32_t slot = uint32_t(V.coords[b].w);
             V.slots[slot].key = kEmptyKey;
             V.slots[slot].value = kInvalid;
         }
