@@ -289,17 +289,19 @@ __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int 
     return true;
 }
 
-// Fills the link record of brick b (at its hash slot, coords[b].w) and
-// points its "-" neighbours' records at it (tsdf_volume.hpp:149-185
-// allocates; this only indexes). Every write is a pure function of the key
-// set, so concurrent writers of the same word agree.
-__device__ __forceinline__ void link_brick(const VolumeView& V, uint32_t b) {
+// Link records (tsdf_volume.hpp:149-185 allocates; this only indexes): the
+// record at brick b's hash slot (coords[b].w) lists the pool indices of its
+// "+" neighbours, and b is entered into its "-" neighbours' records. Every
+// write is a pure function of the key set, so concurrent writers of the same
+// word agree.
+// One word of link_brick: dir 0 fills own[q] (q = 0: the brick itself),
+// dir 1 points the "-q" neighbour's record at b.
+__device__ __forceinline__ void link_brick_item(const VolumeView& V, uint32_t b, int q, int dir) {
     const int4 c = V.coords[b];
-    uint32_t* own = V.links + size_t(uint32_t(c.w)) * kLinkStride;
-    own[0] = b;
-#pragma unroll
-    for (int q = 1; q < 8; ++q) {
-        own[q] = hash_find(V, c.x + (q & 1), c.y + ((q >> 1) & 1), c.z + (q >> 2));
+    if (dir == 0) {
+        V.links[size_t(uint32_t(c.w)) * kLinkStride + q] =
+            q == 0 ? b : hash_find(V, c.x + (q & 1), c.y + ((q >> 1) & 1), c.z + (q >> 2));
+    } else if (q != 0) {
         const uint32_t sa = hash_find_slot(V, c.x - (q & 1), c.y - ((q >> 1) & 1), c.z - (q >> 2));
         if (sa != kInvalid) V.links[size_t(sa) * kLinkStride + q] = b;
     }

@@ -438,6 +438,38 @@ __device__ void morph_pass(const uint8_t* src, uint8_t* dst, int w, int h, int r
     }
 }
 
+// grow_bits for the 32x32 tile (tx, ty) from a shared-memory copy of its
+// depth with a one-pixel halo (coalesced row loads instead of nine scattered
+// loads per pixel).
+__device__ void grow_tile(const float* depth, uint8_t* grow, int w, int h, int tx, int ty, double theta, int conn) {
+    constexpr int S = 32 + 2;
+    __shared__ float dt[S * S];
+    static constexpr int kDx[8] = {1, -1, 0, 0, 1, 1, -1, -1};  // dynamics_mask.cpp:67-68
+    static constexpr int kDy[8] = {0, 0, 1, -1, 1, -1, 1, -1};
+    const int gx0 = tx * 32 - 1, gy0 = ty * 32 - 1;
+    for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
+        const int gx = gx0 + i % S, gy = gy0 + i / S;
+        dt[i] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldg(depth + gy * w + gx) : 0.f;  // 0: invalid
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
+        const int x = i % 32, y = i / 32, gx = tx * 32 + x, gy = ty * 32 + y;
+        if (gx >= w || gy >= h) continue;
+        const float dn = dt[(y + 1) * S + x + 1];
+        uint8_t bits = 0;
+        if (depth_valid(dn)) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (k >= conn) break;
+                const float dp = dt[(y + 1 - kDy[k]) * S + (x + 1 - kDx[k])];  // p = n - (kDx, kDy); off-image: 0
+                if (depth_valid(dp) && fabs(double(dp) - double(dn)) < theta * double(dp)) bits |= uint8_t(1u << k);
+            }
+        }
+        grow[gy * w + gx] = bits;
+    }
+    __syncthreads();
+}
+
 // Tile-based square morphology: one 32x32 output tile per CTA step, the
 // (32+2r)^2 input window staged in shared memory, the separable row and
 // column passes done there (no global intermediate, no grid barrier between
@@ -692,7 +724,7 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
     const bool do_thr = stages & 1;
     int dummy = 0;
     if (re <= kMorphMaxR) {
-        for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x)
+        for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
             morph_tile<true>(t % ntx, t / ntx, w, h, re,
                              [&](int gx, int gy) {
                                  const int p = gy * w + gx;
@@ -700,6 +732,9 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
                                                : __ldcg(input + p) != 0;
                              },
                              seeds, dummy);
+            if (stages & 4)  // the floodfill's growth bits, same 32x32 tiling
+                grow_tile(F.depth0, F.grow, w, h, t % ntx, t / ntx, M.theta, M.connectivity);
+        }
     } else {  // wide windows: threshold, then separable passes through global memory
         uint8_t* thr_img = F.mwork[2];
         for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride)
@@ -712,8 +747,9 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
         grid_barrier(a.grid);  // F.grow is reused below
     }
     if (stages & 4) {
-        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride)
-            F.grow[p] = grow_bits(F.depth0, w, h, p % w, p / w, M.theta, M.connectivity);
+        if (re > kMorphMaxR)  // (the tiled path above computed them with the erosion)
+            for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride)
+                F.grow[p] = grow_bits(F.depth0, w, h, p % w, p / w, M.theta, M.connectivity);
         const int nft = ((w + kFfW - 1) / kFfW) * ((h + kFfH - 1) / kFfH);
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nft; i += stride) F.ffstamp[i] = -1;
     }

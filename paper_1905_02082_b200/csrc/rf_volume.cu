@@ -148,11 +148,14 @@ __global__ void k_cull(CullArgs a) {
 // Link records for bricks allocated since the last link pass: grid-stride
 // over [kLinked, num_blocks). The next kernel on the stream commits the range
 // (commit_links), so no completion atomics are needed here.
+// One thread per (brick, neighbour q, direction): the 14 hash probes of a
+// brick's record run in parallel instead of as one thread's serial chain.
 __device__ void link_new(const VolumeView& V) {
     const uint32_t hi = min(V.counters[kNumBlocks], V.max_blocks);
     const uint32_t lo = min(V.counters[kLinked], hi);
-    for (uint32_t b = lo + blockIdx.x * blockDim.x + threadIdx.x; b < hi; b += gridDim.x * blockDim.x)
-        link_brick(V, b);
+    const uint32_t items = (hi - lo) * 16u;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < items; i += gridDim.x * blockDim.x)
+        link_brick_item(V, lo + i / 16u, int(i & 7u), int((i >> 3) & 1u));
 }
 
 __device__ __forceinline__ void commit_links(const VolumeView& V) {
