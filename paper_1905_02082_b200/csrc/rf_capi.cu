@@ -1,5 +1,6 @@
 // C ABI (include/refusion_b200.h) over the CUDA kernels: volume / pipeline
 // objects, device buffers, frame upload and the per-frame launch sequence.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -152,7 +153,8 @@ struct Workspace {
         mask_in.ensure(n);
         res_sq.ensure(n * 4);
         res_valid.ensure(n);
-        mwork.ensure(ff_offset(w, h) + 4 * size_t((w / 32 + 1) * (h / 32 + 1)));  // 3 masks + floodfill stamps
+        const size_t nft = size_t((w + 31) / 32) * ((h + 31) / 32);
+        mwork.ensure(ff_offset(w, h) + 4 * (3 * nft + 64));  // 3 masks + grow bits + floodfill worklists
         size_t off = 0;
         for (int l = 0; l < levels_needed; ++l) {
             const size_t nl = size_t(w >> l) * (h >> l);
@@ -169,7 +171,11 @@ struct Workspace {
         L = levels_needed;
     }
     void sync() { CK(cudaStreamSynchronize(stream)); }
-    static size_t ff_offset(int w, int h) { return (4 * size_t(w) * h + 15) & ~size_t(15); }  // 3 masks + grow bits
+    // 3 masks, then the floodfill growth planes (8 words per row of every 32x32 tile), then the worklists
+    static size_t ff_offset(int w, int h) {
+        const size_t nft = size_t((w + 31) / 32) * ((h + 31) / 32);
+        return (3 * size_t(w) * h + 255) / 256 * 256 + std::max(size_t(w) * h, nft * 8 * 32 * 4);
+    }
     int* ffstamp() const { return reinterpret_cast<int*>(mwork.as<uint8_t>() + ff_offset(W, H)); }
 };
 
@@ -347,7 +353,7 @@ struct rf_volume {
         a.F.res_valid = ws.res_valid.as<uint8_t>();
         const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
         for (int i = 0; i < 3; ++i) a.F.mwork[i] = ws.mwork.as<uint8_t>() + i * n;
-        a.F.grow = ws.mwork.as<uint8_t>() + 3 * n;
+        a.F.grow = ws.mwork.as<uint8_t>() + (3 * n + 255) / 256 * 256;
         a.F.ffstamp = ws.ffstamp();
         a.grid.sync = ws.gsync.as<GridSync>();
         a.grid.partials = ws.partials.as<double>();
@@ -917,7 +923,7 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
         a.F.res_sq = ws.res_sq.as<float>();
         a.F.res_valid = ws.res_valid.as<uint8_t>();
         for (int i = 0; i < 3; ++i) a.F.mwork[i] = ws.mwork.as<uint8_t>() + i * n;
-        a.F.grow = ws.mwork.as<uint8_t>() + 3 * n;
+        a.F.grow = ws.mwork.as<uint8_t>() + (3 * n + 255) / 256 * 256;
         a.F.ffstamp = ws.ffstamp();
         a.F.mask[0] = ws.mask_in.as<uint8_t>();
         a.grid.sync = ws.gsync.as<GridSync>();

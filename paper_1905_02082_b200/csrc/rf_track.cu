@@ -438,34 +438,44 @@ __device__ void morph_pass(const uint8_t* src, uint8_t* dst, int w, int h, int r
     }
 }
 
-// grow_bits for the 32x32 tile (tx, ty) from a shared-memory copy of its
-// depth with a one-pixel halo (coalesced row loads instead of nine scattered
-// loads per pixel).
-__device__ void grow_tile(const float* depth, uint8_t* grow, int w, int h, int tx, int ty, double theta, int conn) {
+// Growth-edge bits of the floodfill rule (dynamics_mask.cpp:59-96) for the
+// 32x32 tile (tx, ty), from a shared-memory copy of its depth with a
+// one-pixel halo: bit k of pixel n is set when a set pixel p = n - (kDx[k],
+// kDy[k]) may grow into n (n and p valid, |D(p) - D(n)| < theta * D(p)).
+// Stored as bit planes, one 32-bit word per (tile, k, row), x = bit: the
+// floodfill works on whole rows at once.
+__device__ void grow_tile(const float* depth, uint32_t* planes, int w, int h, int tx, int ty, double theta,
+                          int conn) {
     constexpr int S = 32 + 2;
     __shared__ float dt[S * S];
     static constexpr int kDx[8] = {1, -1, 0, 0, 1, 1, -1, -1};  // dynamics_mask.cpp:67-68
     static constexpr int kDy[8] = {0, 0, 1, -1, 1, -1, 1, -1};
+    const int ntx = (w + 31) / 32;
+    uint32_t* tp = planes + size_t(ty * ntx + tx) * 8 * 32;
     const int gx0 = tx * 32 - 1, gy0 = ty * 32 - 1;
     for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
         const int gx = gx0 + i % S, gy = gy0 + i / S;
         dt[i] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldg(depth + gy * w + gx) : 0.f;  // 0: invalid
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
-        const int x = i % 32, y = i / 32, gx = tx * 32 + x, gy = ty * 32 + y;
-        if (gx >= w || gy >= h) continue;
+    const int lane = threadIdx.x & 31;
+    for (int y = threadIdx.x >> 5; y < 32; y += blockDim.x >> 5) {  // warp = one row, lane = x
+        const int x = lane, gx = tx * 32 + x, gy = ty * 32 + y;
         const float dn = dt[(y + 1) * S + x + 1];
-        uint8_t bits = 0;
-        if (depth_valid(dn)) {
+        uint32_t bits = 0;
+        if (gx < w && gy < h && depth_valid(dn)) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 if (k >= conn) break;
-                const float dp = dt[(y + 1 - kDy[k]) * S + (x + 1 - kDx[k])];  // p = n - (kDx, kDy); off-image: 0
-                if (depth_valid(dp) && fabs(double(dp) - double(dn)) < theta * double(dp)) bits |= uint8_t(1u << k);
+                const float dp = dt[(y + 1 - kDy[k]) * S + (x + 1 - kDx[k])];  // off-image: 0 (invalid)
+                if (depth_valid(dp) && fabs(double(dp) - double(dn)) < theta * double(dp)) bits |= 1u << k;
             }
         }
-        grow[gy * w + gx] = bits;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t word = __ballot_sync(0xffffffffu, (bits >> k) & 1u);
+            if (lane == k) tp[k * 32 + y] = word;
+        }
     }
     __syncthreads();
 }
@@ -506,198 +516,169 @@ __device__ void morph_tile(int tx, int ty, int w, int h, int r, Src src, uint8_t
     __syncthreads();
 }
 
-// Growth-edge bits of FloodfillDepth's rule (dynamics_mask.cpp:84-92) for
-// pixel n: bit k set when neighbour p = n - (kDx[k], kDy[k]) may grow into n,
-// i.e. both depths valid and |D(p) - D(n)| < theta * D(p). Static per frame,
-// so the floodfill sweeps are pure bit operations.
-__device__ __forceinline__ uint8_t grow_bits(const float* depth, int w, int h, int x, int y, double theta,
-                                             int conn) {
-    static constexpr int kDx[8] = {1, -1, 0, 0, 1, 1, -1, -1};  // dynamics_mask.cpp:67-68
-    static constexpr int kDy[8] = {0, 0, 1, -1, 1, -1, 1, -1};
-    const float dn = __ldg(depth + y * w + x);
-    if (!depth_valid(dn)) return 0;
-    uint8_t bits = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const int px = x - kDx[k], py = y - kDy[k];  // p such that p + (kDx, kDy) = n
-        if (k >= conn || px < 0 || px >= w || py < 0 || py >= h) continue;
-        const float dp = __ldg(depth + py * w + px);
-        if (depth_valid(dp) && fabs(double(dp) - double(dn)) < theta * double(dp)) bits |= uint8_t(1u << k);
+constexpr int kFfW = 32, kFfH = 32;  // floodfill tile: one warp, lane = row, bit = column
+
+// Floodfill worklists. F.ffstamp holds, for nft = ntx * nty tiles:
+//   [0, nft)          queued[t]: last round tile t was queued for (-1: never)
+//   [nft, 3 nft)      two tile lists (rounds alternate)
+//   [3 nft, +64)      per-round list lengths (round r uses r % 64)
+constexpr int kFfCounts = 64;
+__device__ __forceinline__ int* ff_list(int* base, int nft, int round) { return base + nft * (1 + (round & 1)); }
+__device__ __forceinline__ unsigned int* ff_count(int* base, int nft, int round) {
+    return reinterpret_cast<unsigned int*>(base + 3 * nft) + (round % kFfCounts);
+}
+// Queues tile (tx, ty)'s 3x3 neighbourhood for `round` (once per tile per
+// round); lanes 0..8 of the calling warp (or threads 0..8 with warp == 0).
+__device__ __forceinline__ void ff_enqueue3x3(int* base, int ntx, int nty, int tx, int ty, int round) {
+    const int nft = ntx * nty, lane = threadIdx.x & 31;
+    if (lane < 9) {
+        const int nx = tx + lane % 3 - 1, ny = ty + lane / 3 - 1;
+        if (nx >= 0 && nx < ntx && ny >= 0 && ny < nty) {
+            const int n = ny * ntx + nx;
+            if (atomicMax(base + n, round) < round)
+                ff_list(base, nft, round)[atomicAdd(ff_count(base, nft, round), 1u)] = n;
+        }
     }
-    return bits;
 }
 
-constexpr int kFfW = 32, kFfH = 32;                 // floodfill tile (square: fewer tile crossings per region)
-constexpr int kFfPx = (kFfW * kFfH + kTrackThreads - 1) / kTrackThreads;  // pixels per thread in a tile (ceil)
+// Kogge-Stone fills of a 32-bit row: every pixel reachable from `g` by
+// moves of one pixel in the given direction through pixels whose entry bit
+// (`p`) is set, in five steps.
+__device__ __forceinline__ uint32_t fill_xplus(uint32_t g, uint32_t p) {  // x-1 -> x
+    g |= p & (g << 1);  p &= p << 1;
+    g |= p & (g << 2);  p &= p << 2;
+    g |= p & (g << 4);  p &= p << 4;
+    g |= p & (g << 8);  p &= p << 8;
+    return g | (p & (g << 16));
+}
+__device__ __forceinline__ uint32_t fill_xminus(uint32_t g, uint32_t p) {  // x+1 -> x
+    g |= p & (g >> 1);  p &= p >> 1;
+    g |= p & (g >> 2);  p &= p >> 2;
+    g |= p & (g >> 4);  p &= p >> 4;
+    g |= p & (g >> 8);  p &= p >> 8;
+    return g | (p & (g >> 16));
+}
+// The same across the warp's lanes (lane = row): y-1 -> y, then y+1 -> y.
+__device__ __forceinline__ uint32_t fill_yplus(uint32_t g, uint32_t p, int lane) {
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+        const uint32_t gu = __shfl_up_sync(0xffffffffu, g, k), pu = __shfl_up_sync(0xffffffffu, p, k);
+        g |= lane >= k ? (p & gu) : 0u;
+        p &= lane >= k ? pu : 0u;
+    }
+    return g;
+}
+__device__ __forceinline__ uint32_t fill_yminus(uint32_t g, uint32_t p, int lane) {
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+        const uint32_t gd = __shfl_down_sync(0xffffffffu, g, k), pd = __shfl_down_sync(0xffffffffu, p, k);
+        g |= lane + k < 32 ? (p & gd) : 0u;
+        p &= lane + k < 32 ? pd : 0u;
+    }
+    return g;
+}
 
 // FloodfillDepth (dynamics_mask.cpp:59-96) as the least fixpoint of the
 // growth rule (its BFS result is seed-order independent, so any monotone
-// schedule reaches it). Per 32x32 tile in shared memory: 32 threads sweep the
-// rows (left to right, then back) and 32 the columns (down, then up) with the
-// per-pixel growth bits (grow_bits), carrying the predecessor in a register,
-// so one sweep grows along any row/column-monotone path; for 8-connectivity a
-// parallel pass adds the diagonal edges; sweeps repeat until one changes
-// nothing. Global rounds repeat until no tile changes; rounds after the first
-// only revisit tiles next to a tile that changed in the previous round
-// (per-tile round stamps), and tiles with no set pixel in tile + halo are
-// skipped. Returns the number of global rounds.
-__device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint8_t* grow, int w, int h, int conn, double* blk,
-                         double* red) {
-    constexpr int SW = kFfW + 2;
-    __shared__ uint8_t sm[(kFfH + 2) * SW];
-    __shared__ uint8_t sg[kFfH * kFfW];
-    __shared__ int s_active;
-    int* stamp = a.F.ffstamp;  // round in which each tile last changed (-1: never)
-    const int ntx = (w + kFfW - 1) / kFfW, nty = (h + kFfH - 1) / kFfH;
-    const int lx = threadIdx.x % kFfW, ly0 = threadIdx.x / kFfW;
-    constexpr int kRowStep = kTrackThreads / kFfW;
+// schedule reaches it). A 32x32 tile is one warp: lane = row, the row's
+// mask and its eight growth-edge planes are 32-bit words, and one iteration
+// runs complete fills along +x, -x (bit-parallel Kogge-Stone in the word)
+// and +y, -y (across lanes with shuffles) plus the four diagonal steps for
+// 8-connectivity; iterations repeat until the tile stops changing. The set
+// pixels of the surrounding ring (neighbour tiles) seed the tile once. Global
+// rounds visit only queued tiles -- round 0: the 3x3 neighbourhoods of tiles
+// with seeds, then those of tiles that changed -- one tile per warp across
+// the grid, until a round changes nothing. Returns the number of rounds.
+__device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint32_t* planes, int w, int h, int conn) {
+    int* wl = a.F.ffstamp;  // worklists (see ff_list): round 0 was queued by the erosion pass
+    const int ntx = (w + kFfW - 1) / kFfW, nty = (h + kFfH - 1) / kFfH, nft = ntx * nty;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int G = gridDim.x;
+    auto at = [&](int gx, int gy) -> uint32_t {  // mask bit of an image pixel (0 outside)
+        return (gx >= 0 && gx < w && gy >= 0 && gy < h) ? uint32_t(__ldcg(m + size_t(gy) * w + gx) != 0) : 0u;
+    };
     int rounds = 0;
     while (true) {
-        int changed_cta = 0;
-        for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
-            const int tx = t % ntx, ty = t / ntx;
-            if (rounds > 0) {  // active iff a tile in the 3x3 neighbourhood changed last round
-                int act = 0;
-                if (threadIdx.x < 9) {
-                    const int nx = tx + threadIdx.x % 3 - 1, ny = ty + threadIdx.x / 3 - 1;
-                    act = nx >= 0 && nx < ntx && ny >= 0 && ny < nty && __ldcg(stamp + ny * ntx + nx) == rounds - 1;
-                }
-                if (!__syncthreads_or(act)) continue;  // uniform across the CTA
-            }
-            const int x0 = tx * kFfW - 1, y0 = ty * kFfH - 1;
-            int any = 0;
-            const bool full = (w % 4 == 0) && x0 + 1 + kFfW <= w && y0 + 1 + kFfH <= h;
-            if (full) {  // interior as 32-bit words (one per thread), halo as bytes
-                for (int i = threadIdx.x; i < kFfH * kFfW / 4; i += blockDim.x) {
-                    const int r = i / (kFfW / 4), c = 4 * (i % (kFfW / 4));
-                    const size_t gidx = size_t(y0 + 1 + r) * w + (x0 + 1 + c);
-                    const uint32_t mw = __ldcg(reinterpret_cast<const unsigned int*>(m + gidx));
-                    const uint32_t gw = __ldcg(reinterpret_cast<const unsigned int*>(grow + gidx));
-                    uint8_t* d = sm + (r + 1) * SW + 1 + c;
-                    d[0] = uint8_t(mw);
-                    d[1] = uint8_t(mw >> 8);
-                    d[2] = uint8_t(mw >> 16);
-                    d[3] = uint8_t(mw >> 24);
-                    *reinterpret_cast<uint32_t*>(sg + r * kFfW + c) = gw;
-                    any |= mw != 0;
-                }
-                for (int i = threadIdx.x; i < 4 * (kFfW + 1); i += blockDim.x) {  // halo ring
-                    const int side = i / (kFfW + 1), k = i % (kFfW + 1);
-                    int sx, sy;
-                    if (side == 0) { sx = k; sy = 0; }                  // top row (x 0..32)
-                    else if (side == 1) { sx = k + 1; sy = kFfH + 1; }  // bottom row (x 1..33)
-                    else if (side == 2) { sx = 0; sy = k + 1; }         // left column (y 1..33)
-                    else { sx = kFfW + 1; sy = k; }                     // right column (y 0..32)
-                    const int gx = x0 + sx, gy = y0 + sy;
-                    const uint8_t v = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldcg(m + gy * w + gx) : 0;
-                    sm[sy * SW + sx] = v;
-                    any |= v;
-                }
-            } else {
-                for (int i = threadIdx.x; i < (kFfH + 2) * SW; i += blockDim.x) {
-                    const int gx = x0 + i % SW, gy = y0 + i / SW;
-                    sm[i] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldcg(m + gy * w + gx) : 0;
-                    any |= sm[i];
-                }
-                for (int i = threadIdx.x; i < kFfH * kFfW; i += blockDim.x) {
-                    const int gx = x0 + 1 + i % kFfW, gy = y0 + 1 + i / kFfW;
-                    sg[i] = (gx < w && gy < h) ? __ldcg(grow + gy * w + gx) : 0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) *ff_count(wl, nft, rounds + 2) = 0u;  // not touched this round
+        if (a.trace && rounds < 8 && blockIdx.x == 0 && threadIdx.x == 0)
+            a.trace[8 * (kTracePasses - 3) + rounds] = global_ns();
+        const int nq = int(__ldcg(ff_count(wl, nft, rounds)));
+        const int* list = ff_list(wl, nft, rounds);
+        for (int qi = warp * G + blockIdx.x; qi < nq; qi += G * nwarps) {  // one tile per warp
+            const int t = __ldcg(list + qi);
+            const int tx = t % ntx, ty = t / ntx, x0 = tx * kFfW, y0 = ty * kFfH;
+            const int gy = y0 + lane;
+            // row words: mask, validity, growth planes (x = bit)
+            const uint32_t valid = (gy < h) ? (w - x0 >= 32 ? 0xffffffffu : ((1u << (w - x0)) - 1u)) : 0u;
+            uint32_t set = 0;
+            if (gy < h) {
+                const uint8_t* row = m + size_t(gy) * w + x0;
+                if ((w & 3) == 0 && w - x0 >= 32) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint32_t v = __ldcg(reinterpret_cast<const unsigned int*>(row) + c) & 0x01010101u;
+                        set |= ((v | (v >> 7) | (v >> 14) | (v >> 21)) & 0xFu) << (4 * c);
+                    }
+                } else {
+                    for (int x = 0; x < 32 && x0 + x < w; ++x) set |= uint32_t(__ldcg(row + x) != 0) << x;
                 }
             }
-            if (!__syncthreads_or(any)) continue;  // nothing to grow from
-            if (a.trace && threadIdx.x == 0) atomicAdd(a.trace + 8 * (kTracePasses - 2), 1ull);  // seeded tiles
-            uint8_t initial[kFfPx];
+            const uint32_t* tp = planes + size_t(t) * 8 * 32 + lane;
+            uint32_t P[8];
 #pragma unroll
-            for (int q = 0; q < kFfPx; ++q)
-                initial[q] = (ly0 + q * kRowStep < kFfH) ? sm[(ly0 + q * kRowStep + 1) * SW + lx + 1] : 0;
-            while (true) {
-                int ch = 0;
-                if (threadIdx.x < 64) {
-                    // Thread = one row (0..31) or one column (32..63) of the tile.
-                    // The line's mask bits, growth bits and both halo ends are
-                    // gathered into registers (32-bit masks), swept forward
-                    // (bit 0 from the left / bit 2 from above) and back (bit 1 /
-                    // bit 3) with no memory traffic, and changed pixels stored.
-                    const int line = threadIdx.x & 31;
-                    const bool rows = threadIdx.x < 32;
-                    const int s0 = rows ? (line + 1) * SW + 1 : SW + line + 1;
-                    const int ss = rows ? 1 : SW;
-                    const int g0 = rows ? line * kFfW : line, gs = rows ? 1 : kFfW;
-                    uint32_t set = 0, fwd = 0, bwd = 0;
-                    const uint8_t fb = rows ? 1u : 4u, bb = rows ? 2u : 8u;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        set |= uint32_t(sm[s0 + i * ss] != 0) << i;
-                        const uint8_t g = sg[g0 + i * gs];
-                        fwd |= uint32_t((g & fb) != 0) << i;
-                        bwd |= uint32_t((g & bb) != 0) << i;
-                    }
-                    const uint32_t before = set;
-                    uint32_t carry = sm[s0 - ss] != 0;  // halo predecessor
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const uint32_t bit = (set >> i) & 1u;
-                        const uint32_t nb = bit | (carry & (fwd >> i) & 1u);
-                        set |= nb << i;
-                        carry = nb;
-                    }
-                    carry = sm[s0 + 32 * ss] != 0;
-#pragma unroll
-                    for (int i = 31; i >= 0; --i) {
-                        const uint32_t bit = (set >> i) & 1u;
-                        const uint32_t nb = bit | (carry & (bwd >> i) & 1u);
-                        set |= nb << i;
-                        carry = nb;
-                    }
-                    uint32_t grew = set & ~before;
-                    if (grew) ch = 1;
-                    while (grew) {
-                        const int i = __ffs(grew) - 1;
-                        sm[s0 + i * ss] = 1;
-                        grew &= grew - 1u;
-                    }
-                }
+            for (int k = 0; k < 8; ++k) P[k] = k < conn ? (__ldcg(tp + k * 32) & valid) : 0u;
+            // the ring around the tile
+            const uint32_t hl = at(x0 - 1, gy), hr = at(x0 + 32, gy);
+            const uint32_t top = __ballot_sync(0xffffffffu, at(x0 + lane, y0 - 1) != 0);
+            const uint32_t bot = __ballot_sync(0xffffffffu, at(x0 + lane, y0 + 32) != 0);
+            const uint32_t tl = at(x0 - 1, y0 - 1), tr = at(x0 + 32, y0 - 1);
+            const uint32_t bl = at(x0 - 1, y0 + 32), br = at(x0 + 32, y0 + 32);
+            const uint32_t hl_up = __shfl_up_sync(0xffffffffu, hl, 1), hr_up = __shfl_up_sync(0xffffffffu, hr, 1);
+            const uint32_t hl_dn = __shfl_down_sync(0xffffffffu, hl, 1), hr_dn = __shfl_down_sync(0xffffffffu, hr, 1);
+            set &= valid;
+            const uint32_t initial = set;
+            uint32_t g = set;
+            // seeds from the ring (bit k: from n - (kDx[k], kDy[k]))
+            g |= P[0] & hl;                                  // from (x-1, y): x = 0
+            g |= P[1] & (hr << 31);                          // from (x+1, y): x = 31
+            if (lane == 0) g |= P[2] & top;                  // from (x, y-1)
+            if (lane == 31) g |= P[3] & bot;                 // from (x, y+1)
+            if (conn == 8) {
+                g |= P[4] & (lane == 0 ? ((top << 1) | tl) : hl_up);          // from (x-1, y-1)
+                g |= P[5] & (lane == 31 ? ((bot << 1) | bl) : hl_dn);         // from (x-1, y+1)
+                g |= P[6] & (lane == 0 ? ((top >> 1) | (tr << 31)) : (hr_up << 31));   // from (x+1, y-1)
+                g |= P[7] & (lane == 31 ? ((bot >> 1) | (br << 31)) : (hr_dn << 31));  // from (x+1, y+1)
+            }
+            g &= valid;
+            for (int it = 0;; ++it) {
+                const uint32_t old = g;
+                g = fill_xplus(g, P[0]);
+                g = fill_xminus(g, P[1]);
+                g = fill_yplus(g, P[2], lane);
+                g = fill_yminus(g, P[3], lane);
                 if (conn == 8) {
-                    __syncthreads();
-                    const int doff[4] = {-SW - 1, SW - 1, -SW + 1, SW + 1};  // p = n - (kDx, kDy), k = 4..7
-#pragma unroll
-                    for (int q = 0; q < kFfPx; ++q) {
-                        const int ly = ly0 + q * kRowStep, me = (ly + 1) * SW + (lx + 1);
-                        if (ly >= kFfH) break;
-                        const uint8_t g = sg[ly * kFfW + lx];
-                        if (!sm[me] && (g & 0xF0u)) {
-                            for (int k = 0; k < 4; ++k)
-                                if (((g >> (4 + k)) & 1u) && sm[me + doff[k]]) {
-                                    sm[me] = 1;
-                                    ch = 1;
-                                    break;
-                                }
-                        }
-                    }
+                    const uint32_t gu0 = __shfl_up_sync(0xffffffffu, g, 1);
+                    const uint32_t gd0 = __shfl_down_sync(0xffffffffu, g, 1);
+                    const uint32_t gu = lane > 0 ? gu0 : 0u, gdn = lane < 31 ? gd0 : 0u;
+                    g |= (P[4] & (gu << 1)) | (P[5] & (gdn << 1)) | (P[6] & (gu >> 1)) | (P[7] & (gdn >> 1));
                 }
-                if (a.trace && threadIdx.x == 0) atomicAdd(a.trace + 8 * (kTracePasses - 2) + 1, 1ull);  // sweeps
-                if (!__syncthreads_or(ch)) break;
+                if (!__any_sync(0xffffffffu, g != old)) break;
+                if (it > 4096) __trap();  // cannot happen (monotone, <= 1024 pixels); fail loudly
             }
-            int tile_changed = 0;
-#pragma unroll
-            for (int q = 0; q < kFfPx; ++q) {
-                const int ly = ly0 + q * kRowStep, gx = x0 + 1 + lx, gy = y0 + 1 + ly;
-                if (ly < kFfH && gx < w && gy < h && sm[(ly + 1) * SW + lx + 1] != initial[q]) {
-                    m[gy * w + gx] = 1;
-                    tile_changed = 1;
-                }
+            uint32_t grew = g & ~initial;
+            const bool changed = __any_sync(0xffffffffu, grew != 0);
+            while (grew) {
+                const int x = __ffs(grew) - 1;
+                m[size_t(gy) * w + x0 + x] = 1;
+                grew &= grew - 1u;
             }
-            if (__syncthreads_or(tile_changed)) {
-                changed_cta = 1;
-                if (threadIdx.x == 0) stamp[t] = rounds;
-            }
+            if (a.trace && lane == 0) atomicAdd(a.trace + 8 * (kTracePasses - 2), 1ull);  // tile visits
+            if (changed) ff_enqueue3x3(wl, ntx, nty, tx, ty, rounds + 1);
         }
-        const int any = __syncthreads_or(changed_cta);
-        if (threadIdx.x == 0) blk[0] = any ? 1.0 : 0.0;
-        __syncthreads();
-        grid_allreduce<1>(a.grid, blk, red);
+        if (a.trace && rounds < 8 && threadIdx.x == 0) atomicMax(a.trace + 8 * (kTracePasses - 4) + rounds, global_ns());
+        grid_barrier(a.grid);
         ++rounds;
-        if (red[0] == 0.0) break;
+        if (__ldcg(ff_count(wl, nft, rounds)) == 0u) break;  // nothing queued: fixpoint reached
     }
     return rounds;
 }
@@ -725,15 +706,19 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
     int dummy = 0;
     if (re <= kMorphMaxR) {
         for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
+            int nseed = 0;
             morph_tile<true>(t % ntx, t / ntx, w, h, re,
                              [&](int gx, int gy) {
                                  const int p = gy * w + gx;
                                  return do_thr ? (__ldcg(F.res_valid + p) && double(__ldcg(F.res_sq + p)) > thr)
                                                : __ldcg(input + p) != 0;
                              },
-                             seeds, dummy);
-            if (stages & 4)  // the floodfill's growth bits, same 32x32 tiling
-                grow_tile(F.depth0, F.grow, w, h, t % ntx, t / ntx, M.theta, M.connectivity);
+                             seeds, nseed);
+            if (stages & 4) {  // the floodfill's growth bits (same 32x32 tiling) and round-0 worklist
+                grow_tile(F.depth0, reinterpret_cast<uint32_t*>(F.grow), w, h, t % ntx, t / ntx, M.theta,
+                          M.connectivity);
+                if (__syncthreads_or(nseed)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
+            }
         }
     } else {  // wide windows: threshold, then separable passes through global memory
         uint8_t* thr_img = F.mwork[2];
@@ -746,17 +731,22 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
         morph_pass(F.grow, seeds, w, h, re, true, false);
         grid_barrier(a.grid);  // F.grow is reused below
     }
-    if (stages & 4) {
-        if (re > kMorphMaxR)  // (the tiled path above computed them with the erosion)
-            for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride)
-                F.grow[p] = grow_bits(F.depth0, w, h, p % w, p / w, M.theta, M.connectivity);
-        const int nft = ((w + kFfW - 1) / kFfW) * ((h + kFfH - 1) / kFfH);
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nft; i += stride) F.ffstamp[i] = -1;
+    if ((stages & 4) && re > kMorphMaxR) {  // (the tiled path above did this with the erosion)
+        for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
+            grow_tile(F.depth0, reinterpret_cast<uint32_t*>(F.grow), w, h, t % ntx, t / ntx, M.theta, M.connectivity);
+            int any = 0;
+            const int x0 = (t % ntx) * kMorphTile, y0 = (t / ntx) * kMorphTile;
+            for (int i = threadIdx.x; i < kMorphTile * kMorphTile; i += blockDim.x) {
+                const int gx = x0 + i % kMorphTile, gy = y0 + i / kMorphTile;
+                any |= (gx < w && gy < h && __ldcg(seeds + gy * w + gx)) ? 1 : 0;
+            }
+            if (__syncthreads_or(any)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
+        }
     }
     grid_barrier(a.grid);
     if (mt) mt[1] = mt[2] = mt[3] = global_ns();
     *rounds = 0;
-    if (stages & 4) *rounds = floodfill(a, seeds, F.grow, w, h, M.connectivity, blk, red);
+    if (stages & 4) *rounds = floodfill(a, seeds, reinterpret_cast<const uint32_t*>(F.grow), w, h, M.connectivity);
     if (mt) mt[4] = global_ns();
     int cnt = 0;
     if (rd <= kMorphMaxR) {
@@ -803,6 +793,11 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
         s_luma_lut[i] = w * double(i & 255);
     }
     grid_init(a.grid);
+    if ((a.mode == kModeFrame && a.dynamics) || a.mode == kModeMask) {  // floodfill worklists (ff_list)
+        const int nft = ((a.F.K[0].w + kFfW - 1) / kFfW) * ((a.F.K[0].h + kFfH - 1) / kFfH);
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * nft + kFfCounts; i += gridDim.x * blockDim.x)
+            a.F.ffstamp[i] = i < nft ? -1 : 0;
+    }
 
     if (a.mode == kModeLinearize || a.mode == kModeEvalDepth || a.mode == kModeEvalColor) {
         Pose P;
@@ -819,6 +814,7 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
         return;
     }
     if (a.mode == kModeMask) {
+        grid_barrier(a.grid);  // worklist reset above, before the erosion pass queues round 0
         int rounds = 0;
         const double cnt = build_mask(a, a.mask_stages, scratch, blk, red, &rounds);
         if (lead) {

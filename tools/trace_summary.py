@@ -21,8 +21,19 @@ def main(path, skip=3):
     ff = ff[ff[:, 0] > 0]
     if len(ff):
         print("floodfill per frame: seeded tiles %.1f, sweeps %.1f" % tuple(ff.mean(0)))
+    rs = raw[:, 253, :8].astype(np.float64)  # floodfill round starts (CTA 0)
+    rd = raw[:, 252, :8].astype(np.float64)  # slowest CTA's tiles done per round
+    if (rs[:, 0] > 0).any():
+        tiles, bar = [], []
+        for a, b in zip(rs, rd):
+            n = int((a > 0).sum())
+            for r in range(n):
+                tiles.append((b[r] - a[r]) / 1e3)
+                if r + 1 < n:
+                    bar.append((a[r + 1] - b[r]) / 1e3)
+        print("floodfill rounds: tiles (slowest) %.2f us, barrier+next %.2f us per round" % (np.mean(tiles), np.mean(bar) if bar else 0))
     for fr in raw:
-        fr = fr[:254]
+        fr = fr[:252]
         passes = fr[fr[:, 0] > 0]
         if len(passes) == 0:
             continue
