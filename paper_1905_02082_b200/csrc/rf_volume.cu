@@ -169,60 +169,121 @@ __global__ void k_link_commit(VolumeView V) { commit_links(V); }
 // CarveFreeSpace (tsdf_volume.cpp:204-241) then Integrate (:155-202) applied
 // voxel by voxel inside one brick; the sdf is rounded to f32 between the two
 // updates exactly as the sequential reference stores it.
+// Exact arithmetic shortcuts for the fused update (results bit-identical to
+// the reference's divisions, which stay as the fallback):
+//  * Project: x = fx * X / Z + cx only feeds lround, so a reciprocal-based x
+//    (within a few ulp) is exact unless x lies within 1e-9 of a half-integer;
+//  * sdf = f32((sdf * w + u) / (w + k)): the quotient from a correctly rounded
+//    reciprocal (table) is within 3 ulp of the f64 quotient; when every f64
+//    in q * (1 +- 2^-50) rounds to the same f32, that f32 is the result;
+//  * colour: lround(n / d) of integers n >= 0, d <= 256 is (2n + d) / (2d)
+//    (no f64 quotient of such a fraction is within rounding of a half).
+__device__ __forceinline__ double fuse_rcp(double x) {  // ~1 ulp, branch-free
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = __fma_rn(r, __fma_rn(-x, r, 1.0), r);
+    return __fma_rn(r, __fma_rn(-x, r, 1.0), r);
+}
+__device__ __forceinline__ long project_lround(double num, double z, double rz, double c) {
+    const double xa = num * rz + c;
+    const double fr = xa - floor(xa);
+    if (fabs(xa) < 1e6 && fabs(fr - 0.5) > 1e-9) return lround(xa);
+    return lround(num / z + c);  // Project, geometry.hpp:46-48
+}
+__device__ __forceinline__ float div_f32(double a, double b, double rb) {
+    const double q = a * rb;
+    const float lo = __double2float_rn(q * (1.0 - 0x1p-50)), hi = __double2float_rn(q * (1.0 + 0x1p-50));
+    return lo == hi ? lo : float(a / b);
+}
+__device__ __forceinline__ uint32_t colour_avg(uint32_t c, uint32_t w, uint32_t in) {
+    const uint32_t n = c * w + in, d = w + 1u;  // lround((c * w + in) / (w + 1)), tsdf_volume.cpp:190-196
+    return (2u * n + d) / (2u * d);
+}
+
 __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
     commit_links(a.V);  // k_cull (previous launch) linked this frame's new bricks
     if (a.lost && *a.lost) return;
     __shared__ Pose W;
+    __shared__ double s_rcp[512];  // RN(1 / i): i = w + 1 (integrate) or w + carve_weight (carve), <= 510
     if (threadIdx.x == 0) {
         Pose P;
         for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = a.pose[i];
         W = pose_inverse(P);
     }
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_rcp[i] = i ? 1.0 / double(i) : 0.0;
     __syncthreads();
     const uint32_t nvis = a.V.counters[kVisible];
     const int x = threadIdx.x & 7, y = (threadIdx.x >> 3) & 7, z = threadIdx.x >> 6;
     const double s = a.V.voxel_size, tau = a.V.truncation;
     const int cw = a.V.carve_weight, mw = a.V.max_weight;
-    for (uint32_t i = blockIdx.x; i < nvis; i += gridDim.x) {
-        const uint32_t e = __ldcg(a.list + i);
+    // Software-pipelined over this CTA's bricks: the list entry two bricks
+    // ahead and the coordinates + this thread's voxel one brick ahead are in
+    // flight while the current brick projects and reads the frame, so each
+    // step waits on one dependent round trip (the depth gather), not four.
+    const uint32_t G = gridDim.x;
+    uint32_t i = blockIdx.x;
+    uint32_t e_nx = i < nvis ? __ldcg(a.list + i) : 0u;
+    uint32_t e_nx2 = i + G < nvis ? __ldcg(a.list + i + G) : 0u;
+    int4 c_nx = make_int4(0, 0, 0, 0);
+    uint2 v_nx = make_uint2(0, 0);
+    if (i < nvis) {
+        c_nx = a.V.coords[e_nx & kIndexMask];
+        v_nx = *reinterpret_cast<const uint2*>(a.V.voxels + size_t(e_nx & kIndexMask) * kBrickVoxels + threadIdx.x);
+    }
+    for (; i < nvis; i += G) {
+        const uint32_t e = e_nx;
         const uint32_t b = e & kIndexMask;
-        const int4 c = a.V.coords[b];
+        const int4 c = c_nx;
+        uint2 raw = v_nx;
+        e_nx = e_nx2;
+        if (i + 2 * G < nvis) e_nx2 = __ldcg(a.list + i + 2 * G);
+        if (i + G < nvis) {
+            c_nx = a.V.coords[e_nx & kIndexMask];
+            v_nx = *reinterpret_cast<const uint2*>(a.V.voxels + size_t(e_nx & kIndexMask) * kBrickVoxels +
+                                                   threadIdx.x);
+        }
         const double cx = (double(c.x * kSide + x) + 0.5) * s;  // VoxelCenter, tsdf_volume.hpp:117-119
         const double cy = (double(c.y * kSide + y) + 0.5) * s;
         const double cz = (double(c.z * kSide + z) + 0.5) * s;
         double pc[3];
         pose_apply(W, cx, cy, cz, pc);
         if (!(pc[2] <= 1e-9)) {
-            const double pu_d = a.K.fx * pc[0] / pc[2] + a.K.cx;  // Project, geometry.hpp:46-48
-            const double pv_d = a.K.fy * pc[1] / pc[2] + a.K.cy;
-            const long pu = lround(pu_d), pv = lround(pv_d);
+            const double rz = fuse_rcp(pc[2]);
+            const long pu = project_lround(a.K.fx * pc[0], pc[2], rz, a.K.cx);
+            const long pv = project_lround(a.K.fy * pc[1], pc[2], rz, a.K.cy);
             if (pu >= 0 && pu < a.K.w && pv >= 0 && pv < a.K.h) {
                 const int pix = int(pv) * a.K.w + int(pu);
-                const float d = __ldg(a.depth + pix);
+                const float d = __ldg(a.depth + pix);  // depth, mask and colour in one round trip
+                const bool pix_masked = a.mask && __ldg(a.mask + pix);
+                uint32_t cr = 0, cg = 0, cb = 0;
+                if (a.rgb) {
+                    const uint8_t* col = a.rgb + 3 * size_t(pix);
+                    cr = __ldg(col);
+                    cg = __ldg(col + 1);
+                    cb = __ldg(col + 2);
+                }
                 Voxel* vp = a.V.voxels + size_t(b) * kBrickVoxels + threadIdx.x;
-                uint2 raw = *reinterpret_cast<uint2*>(vp);
                 float sdf = __uint_as_float(raw.x);
                 uint32_t wgt = raw.y & 0xFFu, r = (raw.y >> 8) & 0xFFu, g = (raw.y >> 16) & 0xFFu,
                          bl = raw.y >> 24;
                 bool dirty = false;
                 if ((e & kFlagCarve) && pc[2] < a.V.carve_clip && depth_valid(d) && !(pc[2] >= double(d) - tau)) {
                     const double w = double(wgt);
-                    sdf = float((double(sdf) * w + tau * cw) / (w + cw));
+                    sdf = div_f32(double(sdf) * w + tau * cw, w + cw, s_rcp[wgt + uint32_t(cw)]);
                     wgt = min(wgt + uint32_t(cw), uint32_t(mw));
                     dirty = true;
                 }
-                if ((e & kFlagIntegrate) && !(a.mask && __ldg(a.mask + pix)) && depth_valid(d) &&
+                if ((e & kFlagIntegrate) && !pix_masked && depth_valid(d) &&
                     !(d < a.V.min_depth) && !(d > a.V.max_depth)) {
                     const double dist = double(d) - pc[2];
                     if (!(dist <= -tau)) {
                         const double clamped = fmin(dist, tau);
                         const double w = double(wgt);
-                        sdf = float((double(sdf) * w + clamped) / (w + 1.0));
+                        sdf = div_f32(double(sdf) * w + clamped, w + 1.0, s_rcp[wgt + 1u]);
                         if (fabs(dist) <= tau && a.rgb) {
-                            const uint8_t* col = a.rgb + 3 * size_t(pix);
-                            r = uint32_t(lround((double(r) * w + double(__ldg(col))) / (w + 1.0)));
-                            g = uint32_t(lround((double(g) * w + double(__ldg(col + 1))) / (w + 1.0)));
-                            bl = uint32_t(lround((double(bl) * w + double(__ldg(col + 2))) / (w + 1.0)));
+                            r = colour_avg(r, wgt, cr);
+                            g = colour_avg(g, wgt, cg);
+                            bl = colour_avg(bl, wgt, cb);
                         }
                         wgt = min(wgt + 1u, uint32_t(mw));
                         dirty = true;
