@@ -1,6 +1,7 @@
 // C ABI (include/refusion_b200.h) over the CUDA kernels: volume / pipeline
 // objects, device buffers, frame upload and the per-frame launch sequence.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -19,6 +20,25 @@
 #include "rf_volume.cuh"
 
 namespace rfb {
+// Per-frame results written by the GPU straight into mapped pinned host
+// memory, then a sequence number the host spins on: replaces two D2H copies
+// and a stream synchronisation at the end of every ProcessFrame.
+struct FrameSignal {
+    TrackOut out;
+    uint32_t counters[kNumCounters];
+    unsigned long long seq;
+};
+__global__ void k_signal(const TrackOut* out, const uint32_t* counters, FrameSignal* sig, unsigned long long seq) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(out);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&sig->out);
+    for (int i = threadIdx.x; i < int(sizeof(TrackOut) / 4); i += blockDim.x) dst[i] = __ldcg(src + i);
+    if (threadIdx.x < kNumCounters) sig->counters[threadIdx.x] = __ldcg(counters + threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned long long*>(&sig->seq) = seq;
+    }
+}
 __global__ void k_track(TrackArgs a);
 __global__ void k_import(VolumeView V, const int* coords, uint32_t n, uint32_t base) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -101,6 +121,9 @@ struct Workspace {
     std::string trace_path;
     TrackOut* h_out = nullptr;
     uint32_t* h_counters = nullptr;
+    FrameSignal* h_sig = nullptr;  // mapped pinned (k_signal)
+    FrameSignal* d_sig = nullptr;
+    unsigned long long sig_seq = 0;
     int W = 0, H = 0, L = 0;
     size_t lvl_off_depth[kMaxLevels] = {}, lvl_off_inten[kMaxLevels] = {}, lvl_off_mask[kMaxLevels] = {};
 
@@ -129,6 +152,9 @@ struct Workspace {
         pose.ensure(12 * sizeof(double));
         CK(cudaMallocHost(&h_out, sizeof(TrackOut)));
         CK(cudaMallocHost(&h_counters, kNumCounters * sizeof(uint32_t)));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&h_sig), sizeof(FrameSignal), cudaHostAllocMapped));
+        std::memset(h_sig, 0, sizeof(FrameSignal));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_sig), h_sig, 0));
         if (const char* tf = std::getenv("RF_TRACE_FILE")) {
             trace_path = tf;
             trace.ensure(kTracePasses * 8 * sizeof(unsigned long long));
@@ -140,6 +166,8 @@ struct Workspace {
             b->release();
         if (h_out) cudaFreeHost(h_out);
         if (h_counters) cudaFreeHost(h_counters);
+        if (h_sig) cudaFreeHost(h_sig);
+        h_sig = nullptr;
         if (stream && own_stream) cudaStreamDestroy(stream);
         h_out = nullptr;
         h_counters = nullptr;
@@ -171,6 +199,24 @@ struct Workspace {
         L = levels_needed;
     }
     void sync() { CK(cudaStreamSynchronize(stream)); }
+    // Enqueues k_signal after the frame's work and spins on its sequence
+    // number; copies the results into h_out / h_counters.
+    void signal_wait(const TrackOut* d_out, const uint32_t* d_counters) {
+        const unsigned long long seq = ++sig_seq;
+        k_signal<<<1, 128, 0, stream>>>(d_out, d_counters, d_sig, seq);
+        CK(cudaGetLastError());
+        const volatile unsigned long long* flag = &h_sig->seq;
+        for (unsigned long long spins = 1; *flag != seq; ++spins) {
+            if ((spins & 0x3FFFu) == 0) {  // now and then: surface stream errors, never spin on a dead stream
+                const cudaError_t e = cudaStreamQuery(stream);
+                if (e != cudaSuccess && e != cudaErrorNotReady) CK(e);
+                if (e == cudaSuccess && *flag != seq) CK(cudaErrorUnknown);
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        std::memcpy(h_out, const_cast<const TrackOut*>(&h_sig->out), sizeof(TrackOut));
+        std::memcpy(h_counters, const_cast<const uint32_t*>(h_sig->counters), sizeof(h_sig->counters));
+    }
     // 3 masks, then the floodfill growth planes (8 words per row of every 32x32 tile), then the worklists
     static size_t ff_offset(int w, int h) {
         const size_t nft = size_t((w + 31) / 32) * ((h + 31) / 32);
@@ -1357,9 +1403,8 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             if (v->prof) CK(cudaEventRecord(p->ev[2], ws.stream));
             v->fuse(d, rgb, nullptr, f->intrinsics, pose_state, nullptr, false, true, false);
             if (v->prof) CK(cudaEventRecord(p->ev[4], ws.stream));
-            p->launches += 3;
-            CK(cudaMemcpyAsync(ws.h_counters, v->view.counters, kNumCounters * 4, cudaMemcpyDeviceToHost, ws.stream));
-            ws.sync();
+            p->launches += 4;
+            ws.signal_wait(ws.out.as<TrackOut>(), v->view.counters);
             st.converged = 1;
             std::memcpy(p->last.pose, kIdentity, 96);
             p->last.rounds = 0;
@@ -1407,9 +1452,8 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
                 if (v->prof) CK(cudaEventRecord(p->ev[4], ws.stream));
                 p->launches += 4;
             }
-            CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
-            CK(cudaMemcpyAsync(ws.h_counters, v->view.counters, kNumCounters * 4, cudaMemcpyDeviceToHost, ws.stream));
-            ws.sync();
+            p->launches += 1;
+            ws.signal_wait(ws.out.as<TrackOut>(), v->view.counters);
             p->last = *ws.h_out;
             v->dump_trace();
             const TrackOut& o = p->last;
