@@ -21,6 +21,13 @@ constexpr double kRelDecreaseTol = 1e-6;         // registration.cpp:26
 __device__ __forceinline__ int hidx(int i, int j) { return i * 6 - (i * (i - 1)) / 2 + (j - i); }
 
 __shared__ int s_trace_pass;  // per-CTA pass counter for the optional timeline
+// Per-thread copy of the first kPxCache pixels' inputs {depth (0: skip), intensity}
+// for the Jacobian passes: a thread sees the same pixels in every pass at a
+// level, so after the first pass they come from shared memory instead of an
+// L2 round trip (the coarse levels are one or two pixels per thread).
+constexpr int kPxCache = 2;
+__shared__ float2 s_pxc[kPxCache * kTrackThreads];
+__shared__ int s_pxc_tag;  // (level + 1) | 16 * use_mask of the cached inputs, 0: none
 __shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (see voxel_luma_lut)
 
 struct RegState {
@@ -213,9 +220,11 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
         tr[5] = (unsigned long long)K.w * K.h;
         tr[6] = kJac;
     }
+    const int pxc_tag = (level + 1) | (use_mask ? 16 : 0);
+    const bool pxc_hit = kJac && s_pxc_tag == pxc_tag;
     int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;  // tile walked incrementally (no per-tile division)
     const int step_y = gridDim.x / ntx, step_x = gridDim.x % ntx;
-    for (; ty < nty; tx += step_x, ty += step_y) {
+    for (int it = 0; ty < nty; tx += step_x, ty += step_y, ++it) {
         if (tx >= ntx) {
             tx -= ntx;
             ++ty;
@@ -227,17 +236,26 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
         const int p = v * K.w + u;
         // Every per-pixel input is loaded up front (depth, mask, intensity),
         // so only the hash slot and voxel gathers are dependent round trips.
-        const float d = level == 0 ? __ldg(depth + p) : __ldcg(depth + p);
-        const bool masked = mask && __ldcg(mask + p) != 0;
-        uint32_t rgbw = 0;
-        float inten = 0.f;
-        if (kColor) {
-            if (level == 0) {
-                const uint8_t* c = F.rgb0 + 3 * size_t(p);
-                rgbw = uint32_t(__ldg(c)) | (uint32_t(__ldg(c + 1)) << 8) | (uint32_t(__ldg(c + 2)) << 16);
-            } else {
-                inten = __ldcg(F.inten[level] + p);
+        float d;
+        bool masked;
+        float inten = 0.f;  // ToIntensity (image.hpp:85-91) at level 0, the pyramid's f32 above
+        if (pxc_hit && it < kPxCache) {
+            const float2 c = s_pxc[it * kTrackThreads + threadIdx.x];
+            d = c.x;
+            inten = c.y;
+            masked = false;  // a masked pixel was cached with depth 0
+        } else {
+            d = level == 0 ? __ldg(depth + p) : __ldcg(depth + p);
+            masked = mask && __ldcg(mask + p) != 0;
+            if (kColor) {
+                if (level == 0) {
+                    const uint8_t* c = F.rgb0 + 3 * size_t(p);
+                    inten = float(luma(__ldg(c), __ldg(c + 1), __ldg(c + 2)));
+                } else {
+                    inten = __ldcg(F.inten[level] + p);
+                }
             }
+            if (kJac && it < kPxCache) s_pxc[it * kTrackThreads + threadIdx.x] = make_float2(masked ? 0.f : d, inten);
         }
         float rs = 0.f;
         uint8_t rv = 0;
@@ -252,10 +270,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
                 CellSample cs;
                 if (sample_point<kJac, kColor, !kJac>(a.V, y, cs, s_luma_lut)) {
                     const double r_d = cs.sdf;
-                    double I = 0.0;
-                    if (kColor)  // ToIntensity (image.hpp:85-91) at level 0, the pyramid's f32 above
-                        I = level == 0 ? double(float(luma(uint8_t(rgbw), uint8_t(rgbw >> 8), uint8_t(rgbw >> 16))))
-                                       : double(inten);
+                    const double I = kColor ? double(inten) : 0.0;
                     if (kJac) {
                         const double J[6] = {cs.gs[0], cs.gs[1], cs.gs[2], y[1] * cs.gs[2] - y[2] * cs.gs[1],
                                              y[2] * cs.gs[0] - y[0] * cs.gs[2], y[0] * cs.gs[1] - y[1] * cs.gs[0]};
@@ -311,7 +326,8 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
             if (blockIdx.x == 0) tr[1] = now;
         }
     }
-    block_reduce<kAccN>(acc, scratch, blk);
+    block_reduce<kAccN>(acc, scratch, blk);  // (its barriers: every thread has read s_pxc_tag)
+    if (kJac && threadIdx.x == 0) s_pxc_tag = pxc_tag;
     grid_allreduce<kAccN>(a.grid, blk, out);
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = global_ns();
     if (a.trace && threadIdx.x == 0) ++s_trace_pass;
@@ -787,7 +803,10 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
         a.out->passes = 0;
         a.out->pixel_passes = 0.0;
     }
-    if (threadIdx.x == 0) s_trace_pass = 0;
+    if (threadIdx.x == 0) {
+        s_trace_pass = 0;
+        s_pxc_tag = 0;
+    }
     for (int i = threadIdx.x; i < 768; i += blockDim.x) {
         const double w = i < 256 ? 0.2126 : (i < 512 ? 0.7152 : 0.0722);  // image.hpp:80-83
         s_luma_lut[i] = w * double(i & 255);
