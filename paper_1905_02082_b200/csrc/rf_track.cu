@@ -28,15 +28,18 @@ __shared__ int s_trace_pass;  // per-CTA pass counter for the optional timeline
 constexpr int kPxCache = 2;
 __shared__ float2 s_pxc[kPxCache * kTrackThreads];
 __shared__ int s_pxc_tag;  // (level + 1) | 16 * use_mask of the cached inputs, 0: none
+__shared__ int s_passes;   // Accumulate passes run (CTA 0; TrackOut.passes / pixel_passes)
+__shared__ double s_pixel_passes;
 __shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (see voxel_luma_lut)
 
 struct RegState {
     Pose pose, cand;
     double lambda, dnorm;
     double delta[6];
-    double cur[kAccN];
-    double trial[kAccN];
-    int total, converged, lost, ok, brk;
+    double buf[2][kAccN];  // normal equations at the current pose / at the candidate
+    double* cur;           // -> buf[.], swapped on an accepted step (no copy)
+    double* trial;
+    int total, converged, lost, go, brk, level_it;
 };
 
 // ------------------------------------------------------------------ math
@@ -338,8 +341,8 @@ __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& 
                                      double cw, double* scratch, double* blk, double* out) {
     const bool color = cw > 0.0 && a.F.rgb0 != nullptr;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.out->passes += 1;
-        a.out->pixel_passes += double(a.F.K[level].w) * double(a.F.K[level].h);
+        s_passes += 1;  // CTA 0's tally, published once at kernel exit (no global RMW on the pass path)
+        s_pixel_passes += double(a.F.K[level].w) * double(a.F.K[level].h);
     }
     if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
     else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
@@ -357,6 +360,8 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
         st.total = 0;
         st.converged = 0;
         st.lost = 0;
+        st.cur = st.buf[0];
+        st.trial = st.buf[1];
     }
     __syncthreads();
     for (int l = R.levels - 1; l >= 0; --l) {
@@ -372,16 +377,21 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
         if (threadIdx.x == 0) {
             st.lambda = R.lambda_init;
             st.converged = 0;
+            st.brk = 0;
+            st.level_it = 0;
         }
-        for (int it = 0; it < R.max_iterations; ++it) {
-            __syncthreads();
+        // One barrier per LM iteration: thread 0 judges the last trial and
+        // solves for the next candidate in one go (registration.cpp:233-272).
+        for (;;) {
             if (threadIdx.x == 0) {
-                ++st.total;
-                const bool ok = lm_solve(st.cur, st.lambda, st.delta);
-                st.ok = ok;
-                if (!ok) {
-                    st.lambda = fmin(st.lambda * R.lambda_up, 1e12);
-                } else {
+                st.go = 0;
+                while (!st.brk && st.level_it < R.max_iterations) {
+                    ++st.level_it;
+                    ++st.total;
+                    if (!lm_solve(st.cur, st.lambda, st.delta)) {
+                        st.lambda = fmin(st.lambda * R.lambda_up, 1e12);  // NumericalIssue: damp more, retry
+                        continue;
+                    }
                     double delta[6];
 #pragma unroll
                     for (int i = 0; i < 6; ++i) delta[i] = st.delta[i];
@@ -392,24 +402,26 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
 #pragma unroll
                     for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
                     st.dnorm = dn;  // squared; the sqrt is taken at the accept test, off this critical path
+                    st.go = 1;
+                    break;
                 }
                 if (a.trace && blockIdx.x == 0 && s_trace_pass < kTracePasses)
                     a.trace[8 * s_trace_pass + 7] = global_ns();  // solve done (next pass's record)
             }
             __syncthreads();
-            if (!st.ok) continue;
-            const double dnorm = st.dnorm;
+            if (!st.go) break;
             pass<true>(a, l, st.cand, use_mask, false, cw, scratch, blk, st.trial);
             if (threadIdx.x == 0) {
                 const double cur_err = st.cur[27] + cw * st.cur[28];
                 const double trial_err = st.trial[27] + cw * st.trial[28];
-                st.brk = 0;
                 if (st.trial[29] >= min_valid && trial_err < cur_err) {
                     const double decrease = cur_err - trial_err;
                     st.pose = st.cand;
-                    for (int i = 0; i < kAccN; ++i) st.cur[i] = st.trial[i];
+                    double* t = st.cur;
+                    st.cur = st.trial;
+                    st.trial = t;
                     st.lambda = fmax(st.lambda / R.lambda_down, 1e-12);
-                    if (sqrt(dnorm) < R.eps || decrease < kRelDecreaseTol * cur_err) {
+                    if (sqrt(st.dnorm) < R.eps || decrease < kRelDecreaseTol * cur_err) {
                         st.converged = 1;
                         st.brk = 1;
                     }
@@ -421,8 +433,6 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
                     }
                 }
             }
-            __syncthreads();
-            if (st.brk) break;
         }
         __syncthreads();
     }
@@ -793,25 +803,9 @@ __device__ void write_out(const TrackArgs& a, const RegState& st) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackArgs a) {
-    __shared__ RegState st;
-    __shared__ double scratch[(kTrackThreads / 32) * 32];
-    __shared__ double blk[kAccN + 2];
-    __shared__ double red[kAccN + 2];
-    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-    if (lead && a.out) {
-        a.out->passes = 0;
-        a.out->pixel_passes = 0.0;
-    }
-    if (threadIdx.x == 0) {
-        s_trace_pass = 0;
-        s_pxc_tag = 0;
-    }
-    for (int i = threadIdx.x; i < 768; i += blockDim.x) {
-        const double w = i < 256 ? 0.2126 : (i < 512 ? 0.7152 : 0.0722);  // image.hpp:80-83
-        s_luma_lut[i] = w * double(i & 255);
-    }
-    grid_init(a.grid);
+// The body of k_track (every mode); the kernel publishes CTA 0's pass tally after it.
+__device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, double* scratch, double* blk,
+                                           double* red, bool lead) {
     if ((a.mode == kModeFrame && a.dynamics) || a.mode == kModeMask) {  // floodfill worklists (ff_list)
         const int nft = ((a.F.K[0].w + kFfW - 1) / kFfW) * ((a.F.K[0].h + kFfH - 1) / kFfH);
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * nft + kFfCounts; i += gridDim.x * blockDim.x)
@@ -916,6 +910,32 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
             a.vol_counters[kDdaVisits] = 0;
             a.vol_counters[kOverflow] = 0;
         }
+    }
+}
+
+__global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackArgs a) {
+    __shared__ RegState st;
+    __shared__ double scratch[(kTrackThreads / 32) * 32];
+    __shared__ double blk[kAccN + 2];
+    __shared__ double red[kAccN + 2];
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    if (lead && a.out) {
+        s_passes = 0;
+        s_pixel_passes = 0.0;
+    }
+    if (threadIdx.x == 0) {
+        s_trace_pass = 0;
+        s_pxc_tag = 0;
+    }
+    for (int i = threadIdx.x; i < 768; i += blockDim.x) {
+        const double w = i < 256 ? 0.2126 : (i < 512 ? 0.7152 : 0.0722);  // image.hpp:80-83
+        s_luma_lut[i] = w * double(i & 255);
+    }
+    grid_init(a.grid);
+    track_main(a, st, scratch, blk, red, lead);
+    if (lead && a.out) {
+        a.out->passes = s_passes;
+        a.out->pixel_passes = s_pixel_passes;
     }
 }
 
