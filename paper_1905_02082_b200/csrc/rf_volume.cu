@@ -52,7 +52,22 @@ __global__ void k_alloc(AllocArgs a) {
                 }
             }
             const int max_steps = abs(end[0] - cell[0]) + abs(end[1] - cell[1]) + abs(end[2] - cell[2]) + 3;
-            hash_insert(a.V, cell[0], cell[1], cell[2]);
+            // The walk is run one cell ahead of the inserts: the first hash slot
+            // of the next cell is loaded while the current one is checked, and a
+            // cell whose key already sits in its first slot (almost all of them
+            // once the scene is mapped) needs no atomic. Same key set as
+            // inserting every visited cell (hash_insert of a present key is a no-op).
+            auto first_slot = [&](const int (&c)[3]) -> uint4 {
+                if (!coord_in_range(c[0], c[1], c[2])) return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
+                return __ldg(reinterpret_cast<const uint4*>(a.V.slots + (hash_coord(c[0], c[1], c[2]) & a.V.hash_mask)));
+            };
+            auto settle = [&](const int (&c)[3], uint4 sl) {
+                const unsigned long long k = (unsigned long long)sl.x | ((unsigned long long)sl.y << 32);
+                if (!(coord_in_range(c[0], c[1], c[2]) && k == pack_key(c[0], c[1], c[2]) && sl.z < kOverflowed))
+                    hash_insert(a.V, c[0], c[1], c[2]);
+            };
+            int cur[3] = {cell[0], cell[1], cell[2]};
+            uint4 cur_sl = first_slot(cur);
             ++visits;
             for (int n = 0; n < max_steps && (cell[0] != end[0] || cell[1] != end[1] || cell[2] != end[2]); ++n) {
                 int axis = 0;
@@ -61,9 +76,15 @@ __global__ void k_alloc(AllocArgs a) {
                 if (tmax[axis] > 1.0) break;
                 tmax[axis] += tdel[axis];
                 cell[axis] += step[axis];
-                hash_insert(a.V, cell[0], cell[1], cell[2]);
+                const uint4 next_sl = first_slot(cell);
+                settle(cur, cur_sl);
+                cur[0] = cell[0];
+                cur[1] = cell[1];
+                cur[2] = cell[2];
+                cur_sl = next_sl;
                 ++visits;
             }
+            settle(cur, cur_sl);
         }
     }
     // warp-aggregated visit counter (for the algorithmic-bytes model)
