@@ -215,6 +215,12 @@ rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipel
 void rf_pipeline_destroy(rf_pipeline* p);
 rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_stats* stats,
                                     double pose_out[12]);                                  /* ProcessFrame */
+/* ProcessFrame over n frames with the GPU work of up to 64 frames enqueued back to back
+ * (RunSequence, pipeline.cpp:137-145, without a host round trip per frame). stats
+ * (n records) and poses (12 n doubles) may be NULL. Host frames must stay valid for the
+ * call. With refinement, profiling or tracing on, the frames are processed one by one. */
+rf_status rf_pipeline_process_frames(rf_pipeline* p, const rf_frame* frames, uint64_t n, rf_frame_stats* stats,
+                                     double* poses);
 rf_status rf_pipeline_finalize(rf_pipeline* p);                                            /* Finalize */
 rf_status rf_pipeline_volume(rf_pipeline* p, rf_volume** out);                             /* volume() (borrowed) */
 rf_status rf_pipeline_tracking_losses(const rf_pipeline* p, uint64_t* out);               /* tracking_losses() */

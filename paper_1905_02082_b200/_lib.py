@@ -90,7 +90,7 @@ EXPORTS = [
     "rf_pipeline_stream", "rf_synth_render", "rf_pipeline_profile_counters", "rf_diag_grid_barrier",
     "rf_diag_lm_step", "rf_volume_extract_mesh", "rf_mesh_counts", "rf_mesh_copy", "rf_mesh_device_buffers",
     "rf_mesh_write_ply", "rf_mesh_destroy", "rf_render_virtual_depth", "rf_pipeline_window_size",
-    "rf_pipeline_set_debug_images", "rf_pipeline_last_refinement", "rf_pipeline_finalize_one", "rf_diag_pass_bench",
+    "rf_pipeline_set_debug_images", "rf_pipeline_last_refinement", "rf_pipeline_finalize_one", "rf_diag_pass_bench", "rf_pipeline_process_frames",
 ]
 
 _lib = None

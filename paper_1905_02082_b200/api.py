@@ -388,6 +388,19 @@ class Pipeline:
         self.stats.append(s)
         return s, np.array(pose)
 
+    def process_frames(self, frames):
+        """ProcessFrame over a list of Frame with the GPU work enqueued back to
+        back (RunSequence without a host round trip per frame): (stats list,
+        poses (n, 12))."""
+        n = len(frames)
+        fr = (L.rf_frame * n)(*[f.c() for f in frames])
+        st = (L.rf_frame_stats * n)()
+        poses = np.zeros((n, 12))
+        L.check(_lib().rf_pipeline_process_frames(self.h, fr, C.c_uint64(n), st, _p(poses)))
+        out = [{k: getattr(st[i], k) for k, _ in L.rf_frame_stats._fields_} for i in range(n)]
+        self.stats.extend(out)
+        return out, poses
+
     def process_frame_raw(self, f: L.rf_frame, st: L.rf_frame_stats, pose):
         """Minimal-overhead call for timing loops (no Python-side conversion)."""
         return _lib().rf_pipeline_process_frame(self.h, C.byref(f), C.byref(st), pose)

@@ -121,7 +121,8 @@ struct Workspace {
     std::string trace_path;
     TrackOut* h_out = nullptr;
     uint32_t* h_counters = nullptr;
-    FrameSignal* h_sig = nullptr;  // mapped pinned (k_signal)
+    static constexpr int kSigSlots = 64;  // frames in flight per batch (rf_pipeline_process_frames)
+    FrameSignal* h_sig = nullptr;          // kSigSlots records, mapped pinned (k_signal)
     FrameSignal* d_sig = nullptr;
     unsigned long long sig_seq = 0;
     int W = 0, H = 0, L = 0;
@@ -152,8 +153,8 @@ struct Workspace {
         pose.ensure(12 * sizeof(double));
         CK(cudaMallocHost(&h_out, sizeof(TrackOut)));
         CK(cudaMallocHost(&h_counters, kNumCounters * sizeof(uint32_t)));
-        CK(cudaHostAlloc(reinterpret_cast<void**>(&h_sig), sizeof(FrameSignal), cudaHostAllocMapped));
-        std::memset(h_sig, 0, sizeof(FrameSignal));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&h_sig), kSigSlots * sizeof(FrameSignal), cudaHostAllocMapped));
+        std::memset(h_sig, 0, kSigSlots * sizeof(FrameSignal));
         CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_sig), h_sig, 0));
         if (const char* tf = std::getenv("RF_TRACE_FILE")) {
             trace_path = tf;
@@ -199,13 +200,18 @@ struct Workspace {
         L = levels_needed;
     }
     void sync() { CK(cudaStreamSynchronize(stream)); }
-    // Enqueues k_signal after the frame's work and spins on its sequence
-    // number; copies the results into h_out / h_counters.
-    void signal_wait(const TrackOut* d_out, const uint32_t* d_counters) {
+    // Enqueues k_signal after the frame's work: the frame's results land in
+    // record `slot`, tagged with a new sequence number (returned).
+    unsigned long long signal(const TrackOut* d_out, const uint32_t* d_counters, int slot) {
         const unsigned long long seq = ++sig_seq;
-        k_signal<<<1, 128, 0, stream>>>(d_out, d_counters, d_sig, seq);
+        k_signal<<<1, 128, 0, stream>>>(d_out, d_counters, d_sig + slot, seq);
         CK(cudaGetLastError());
-        const volatile unsigned long long* flag = &h_sig->seq;
+        return seq;
+    }
+    // Spins until record `slot` carries `seq` (stream errors surface, never a
+    // spin on a dead stream), then copies it into h_out / h_counters.
+    void wait_signal(int slot, unsigned long long seq) {
+        const volatile unsigned long long* flag = &h_sig[slot].seq;
         for (unsigned long long spins = 1; *flag != seq; ++spins) {
             if ((spins & 0x3FFFu) == 0) {  // now and then: surface stream errors, never spin on a dead stream
                 const cudaError_t e = cudaStreamQuery(stream);
@@ -214,9 +220,13 @@ struct Workspace {
             }
         }
         std::atomic_thread_fence(std::memory_order_acquire);
-        std::memcpy(h_out, const_cast<const TrackOut*>(&h_sig->out), sizeof(TrackOut));
-        std::memcpy(h_counters, const_cast<const uint32_t*>(h_sig->counters), sizeof(h_sig->counters));
+        read_signal(slot);
     }
+    void read_signal(int slot) {
+        std::memcpy(h_out, const_cast<const TrackOut*>(&h_sig[slot].out), sizeof(TrackOut));
+        std::memcpy(h_counters, const_cast<const uint32_t*>(h_sig[slot].counters), sizeof(h_sig[slot].counters));
+    }
+    void signal_wait(const TrackOut* d_out, const uint32_t* d_counters) { wait_signal(0, signal(d_out, d_counters, 0)); }
     // 3 masks, then the floodfill growth planes (8 words per row of every 32x32 tile), then the worklists
     static size_t ff_offset(int w, int h) {
         const size_t nft = size_t((w + 31) / 32) * ((h + 31) / 32);
@@ -1507,6 +1517,127 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
         st.runtime_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         ++p->frame_count;
         if (stats) *stats = st;
+    });
+}
+
+// rf_pipeline_process_frames: the same per-frame work as ProcessFrame, with
+// up to Workspace::kSigSlots frames enqueued back to back before the host
+// waits -- the GPU never idles on the host between frames (RunSequence,
+// pipeline.cpp:137-145). Each frame's results land in its own mapped record.
+namespace {
+void validate_frame(const rf_pipeline* p, const rf_frame* f) {
+    require(f, RF_INVALID_ARGUMENT, "null argument");
+    require(intrinsics_valid(f->intrinsics) && f->depth && f->rgb, RF_INVALID_ARGUMENT,
+            "frame images do not match the intrinsics");
+    for (int l = 1; l < p->cfg.registration.pyramid_levels; ++l)
+        require((f->intrinsics.width >> l) >= 1 && (f->intrinsics.height >> l) >= 1, RF_INVALID_ARGUMENT,
+                "image too small for pyramid level");
+}
+
+unsigned long long enqueue_frame(rf_pipeline* p, const rf_frame* f, int slot, bool first) {
+    rf_volume* v = p->vol;
+    Workspace& ws = v->ws;
+    const int L = p->cfg.registration.pyramid_levels;
+    v->prepare(f, L);
+    const float* d = v->depth_of(f);
+    const uint8_t* rgb = v->rgb_of(f);
+    double* pose_state = ws.pose.as<double>();
+    if (first) {  // bootstrap at the identity (pipeline.cpp:66-76)
+        static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+        CK(cudaMemcpyAsync(pose_state, kIdentity, 96, cudaMemcpyHostToDevice, ws.stream));
+        CK(cudaMemsetAsync(v->view.counters + kOverflow, 0, 5 * 4, ws.stream));
+        v->allocate(d, nullptr, f->intrinsics, pose_state, nullptr);
+        v->fuse(d, rgb, nullptr, f->intrinsics, pose_state, nullptr, false, true, false);
+        p->launches += 4;
+    } else {
+        TrackArgs a = v->track_args(f, d, rgb, L);
+        a.mode = kModeFrame;
+        a.dynamics = p->cfg.dynamics_enabled;
+        a.reg = to_reg(p->cfg.registration, L);
+        a.mp = to_mask(p->cfg.mask);
+        a.vol_counters = v->view.counters;
+        a.trace = nullptr;
+        v->launch_track(a);
+        const uint8_t* mask = p->cfg.dynamics_enabled ? a.F.mask[0] : nullptr;
+        const int* lost = &ws.out.as<TrackOut>()->lost;
+        v->allocate(d, mask, f->intrinsics, pose_state, lost);
+        v->fuse(d, rgb, mask, f->intrinsics, pose_state, lost, true, true, true, false);
+        p->launches += 5;
+    }
+    return ws.signal(ws.out.as<TrackOut>(), v->view.counters, slot);
+}
+
+// Host half: FrameStats, trajectory and counters from the frame's record
+// (already read into h_out / h_counters).
+void finish_frame(rf_pipeline* p, const rf_frame* f, bool first, rf_frame_stats* stats, double pose_out[12]) {
+    Workspace& ws = p->vol->ws;
+    rf_frame_stats st{};
+    st.frame_index = p->frame_count;
+    st.timestamp = f->timestamp;
+    if (first) {
+        static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+        st.converged = 1;
+        std::memcpy(p->last.pose, kIdentity, 96);
+        p->last.rounds = 0;
+        p->last.passes = 0;
+        p->last.pixel_passes = 0.0;
+        p->has_mask = false;
+    } else {
+        p->last = *ws.h_out;
+        const TrackOut& o = p->last;
+        st.tracking_lost = o.lost;
+        st.converged = o.converged;
+        st.registrations = o.registrations;
+        st.iterations = o.iterations;
+        st.valid_residuals = o.valid;
+        st.masked_pixels = o.masked;
+        st.final_error = o.final_error;
+        p->has_mask = !o.lost && p->cfg.dynamics_enabled;
+        if (o.lost) ++p->losses;
+    }
+    std::memcpy(p->last_counters, ws.h_counters, sizeof(p->last_counters));
+    p->traj_t.push_back(f->timestamp);
+    p->traj_p.insert(p->traj_p.end(), p->last.pose, p->last.pose + 12);
+    if (pose_out) std::memcpy(pose_out, p->last.pose, 96);
+    p->first = false;
+    ++p->frame_count;
+    if (stats) *stats = st;
+    require(ws.h_counters[kOverflow] == 0, RF_RESOURCE_LIMIT,
+            "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)");
+}
+}  // namespace
+
+rf_status rf_pipeline_process_frames(rf_pipeline* p, const rf_frame* frames, uint64_t n, rf_frame_stats* stats,
+                                     double* poses) {
+    return guard([&] {
+        require(p && (frames || n == 0), RF_INVALID_ARGUMENT, "null argument");
+        if (p->cfg.refine_enabled || p->profiling || !p->vol->ws.trace_path.empty()) {
+            // the refinement window's host bookkeeping is per frame: one call at a time
+            for (uint64_t i = 0; i < n; ++i) {
+                const rf_status r = rf_pipeline_process_frame(p, &frames[i], stats ? &stats[i] : nullptr,
+                                                              poses ? poses + 12 * i : nullptr);
+                if (r != RF_OK) throw Error{r, g_err};
+            }
+            return;
+        }
+        Workspace& ws = p->vol->ws;
+        CK(cudaSetDevice(p->vol->device));
+        for (uint64_t i = 0; i < n; ++i) validate_frame(p, &frames[i]);
+        for (uint64_t c0 = 0; c0 < n; c0 += Workspace::kSigSlots) {
+            const uint64_t m = std::min<uint64_t>(Workspace::kSigSlots, n - c0);
+            const bool first0 = p->first;
+            unsigned long long last_seq = 0;
+            for (uint64_t j = 0; j < m; ++j) last_seq = enqueue_frame(p, &frames[c0 + j], int(j), first0 && j == 0);
+            ws.wait_signal(int(m - 1), last_seq);  // stream order: every earlier record is complete too
+            for (uint64_t j = 0; j < m; ++j) {
+                const auto t0 = std::chrono::steady_clock::now();
+                ws.read_signal(int(j));
+                finish_frame(p, &frames[c0 + j], first0 && j == 0, stats ? &stats[c0 + j] : nullptr,
+                             poses ? poses + 12 * (c0 + j) : nullptr);
+                if (stats) stats[c0 + j].runtime_ms = std::chrono::duration<double, std::milli>(
+                                                          std::chrono::steady_clock::now() - t0).count();
+            }
+        }
     });
 }
 

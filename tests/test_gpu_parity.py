@@ -414,3 +414,24 @@ def test_pipeline_bench_scene_640x480_prefix():
         assert dt <= POSE_TOL_T and dr <= POSE_TOL_R
         assert so["registrations"] == sg["registrations"]
         assert abs(so["masked_pixels"] - sg["masked_pixels"]) <= 0.001 * 640 * 480
+
+
+def test_process_frames_batch_matches_single():
+    """rf_pipeline_process_frames (frames enqueued back to back) gives the same
+    poses, stats and volume as frame-by-frame ProcessFrame, over more frames
+    than one batch holds."""
+    s = O.Scene(scenes.room_script(with_mover=True, width=160, height=120, frames=70))
+    frames = [s.render(i) for i in range(len(s))]
+    cfg = G.pipeline_config(refine=False, volume=G.volume_config(voxel_size=0.02, max_blocks=200000))
+    a, b = G.Pipeline(cfg), G.Pipeline(cfg)
+    single = [a.process_frame(frame(s.k, f["depth"], f["rgb"], f["timestamp"])) for f in frames]
+    stats, poses = b.process_frames([frame(s.k, f["depth"], f["rgb"], f["timestamp"]) for f in frames])
+    for (sa, pa), sb, pb in zip(single, stats, poses):
+        assert np.array_equal(pa, pb)
+        for key in ("frame_index", "tracking_lost", "registrations", "iterations", "masked_pixels", "valid_residuals",
+                    "final_error"):
+            assert sa[key] == sb[key], key
+    assert np.array_equal(a.trajectory()[1], b.trajectory()[1])
+    ca, va = canonical(*a.volume().export())
+    cb, vb = canonical(*b.volume().export())
+    assert (ca == cb).all() and va.tobytes() == vb.tobytes()
