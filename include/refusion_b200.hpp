@@ -659,20 +659,31 @@ class Pipeline {
         rf_frame_stats s{};
         double pose[12];
         Check(rf_pipeline_process_frame(h_, &f, &s, pose));
-        FrameStats out;
-        out.frame_index = s.frame_index;
-        out.timestamp = s.timestamp;
-        out.tracking_lost = s.tracking_lost != 0;
-        out.converged = s.converged != 0;
-        out.registrations = s.registrations;
-        out.iterations = s.iterations;
-        out.valid_residuals = s.valid_residuals;
-        out.masked_pixels = s.masked_pixels;
-        out.final_error = s.final_error;
-        out.runtime_ms = s.runtime_ms;
-        trajectory_.push_back(TrajectoryEntry{frame.timestamp, Pose::FromArray(pose)});
-        stats_.push_back(out);
+        const FrameStats out = Record(frame.timestamp, s, pose);
         if (debug_sink_) EmitDebug(frame, out);
+        return out;
+    }
+    // ProcessFrame over several frames with their GPU work enqueued back to
+    // back (rf_pipeline_process_frames); per-frame debug records need
+    // ProcessFrame, so with a debug sink this is a plain loop.
+    std::vector<FrameStats> ProcessFrames(const std::vector<Frame>& frames) {
+        std::vector<FrameStats> out;
+        if (debug_sink_) {
+            for (const Frame& f : frames) out.push_back(ProcessFrame(f));
+            return out;
+        }
+        std::vector<rf_frame> cf;
+        for (const Frame& f : frames) {
+            if (!f.depth.SameSize(f.intrinsics.width, f.intrinsics.height) ||
+                (!f.color.Empty() && !f.color.SameSize(f.depth)))
+                throw std::invalid_argument("frame sizes are inconsistent");
+            cf.push_back(detail::ToC(f));
+        }
+        std::vector<rf_frame_stats> st(frames.size());
+        std::vector<double> poses(12 * frames.size());
+        Check(rf_pipeline_process_frames(h_, cf.data(), cf.size(), st.data(), poses.data()));
+        for (std::size_t i = 0; i < frames.size(); ++i)
+            out.push_back(Record(frames[i].timestamp, st[i], poses.data() + 12 * i));
         return out;
     }
     void Finalize() {  // pipeline.cpp:133-135 (IntegrateFront until the window is empty)
@@ -709,6 +720,22 @@ class Pipeline {
     rf_pipeline* handle() const { return h_; }
 
   private:
+    FrameStats Record(double timestamp, const rf_frame_stats& s, const double pose[12]) {
+        FrameStats out;
+        out.frame_index = s.frame_index;
+        out.timestamp = s.timestamp;
+        out.tracking_lost = s.tracking_lost != 0;
+        out.converged = s.converged != 0;
+        out.registrations = s.registrations;
+        out.iterations = s.iterations;
+        out.valid_residuals = s.valid_residuals;
+        out.masked_pixels = s.masked_pixels;
+        out.final_error = s.final_error;
+        out.runtime_ms = s.runtime_ms;
+        trajectory_.push_back(TrajectoryEntry{timestamp, Pose::FromArray(pose)});
+        stats_.push_back(out);
+        return out;
+    }
     void EmitRefinement() {  // IntegrateFront's debug record (pipeline.cpp:45-54)
         std::int32_t has = 0;
         std::uint64_t index = 0;
@@ -761,11 +788,24 @@ struct SequenceSummary {
 };
 
 // RunSequence (pipeline.cpp:137-145).
+// Frames are pulled in batches of up to 64 and processed with their GPU work
+// enqueued back to back (results identical to one ProcessFrame at a time).
 inline SequenceSummary RunSequence(Pipeline& pipeline, const FrameSource& source) {
     SequenceSummary s;
-    while (std::optional<Frame> f = source()) {
-        pipeline.ProcessFrame(*f);
-        ++s.frames;
+    std::vector<Frame> batch;
+    bool more = true;
+    while (more) {
+        batch.clear();
+        while (batch.size() < 64) {
+            std::optional<Frame> f = source();
+            if (!f) {
+                more = false;
+                break;
+            }
+            batch.push_back(std::move(*f));
+        }
+        if (!batch.empty()) pipeline.ProcessFrames(batch);
+        s.frames += batch.size();
     }
     pipeline.Finalize();
     s.tracking_losses = pipeline.tracking_losses();

@@ -2,13 +2,14 @@
 // the reference's tsdfslam::Pipeline would (proj/tools/main.cpp:90-141):
 // frames in, trajectory + mesh out. Used by tests/test_cpp_host.py.
 //
-//   host_layer_demo <in.bin> <out.bin> [refine]
+//   host_layer_demo <in.bin> <out.bin> [refine|nodebug]
 // in.bin : i32 W, H, N; f64 fx, fy, cx, cy; then N x (f64 t, f32 depth[W*H], u8 rgb[W*H*3])
 // out.bin: i32 N; N x (f64 t, f64 pose[12], i32 lost, i32 regs, i32 iters, u64 masked);
 //          u64 nv, nf, nblocks; then error-behaviour flags (i32 x 3)
 #include <cstdio>
 #include <fstream>
 #include <iostream>
+#include <string>
 
 #include "refusion_b200.hpp"
 
@@ -16,7 +17,7 @@ namespace ts = tsdfslam_b200;
 
 int main(int argc, char** argv) {
     if (argc != 3 && argc != 4) {
-        std::cerr << "usage: host_layer_demo in.bin out.bin [refine]\n";
+        std::cerr << "usage: host_layer_demo in.bin out.bin [refine|nodebug]\n";
         return 2;
     }
     std::ifstream in(argv[1], std::ios::binary);
@@ -33,15 +34,17 @@ int main(int argc, char** argv) {
     k.height = h;
 
     ts::PipelineConfig cfg;
-    cfg.refinement.enabled = argc == 4;  // default-on in the reference; TrackingConfig turns it off (acceptance.cpp:136)
+    const std::string opt = argc == 4 ? argv[3] : "";
+    cfg.refinement.enabled = opt == "refine";  // default-on in the reference; TrackingConfig turns it off (acceptance.cpp:136)
     cfg.refinement.window = 3;
     ts::Pipeline pipe(cfg);
     std::size_t debug_calls = 0, debug_masks = 0, debug_refined = 0;
-    pipe.set_debug_sink([&](const ts::FrameDebug& d) {
-        ++debug_calls;
-        if (d.mask) debug_masks += ts::CountMasked(*d.mask) > 0;
-        if (d.refined_depth && d.virtual_depth) ++debug_refined;
-    });
+    if (opt != "nodebug")  // without a sink RunSequence submits frames in batches (ProcessFrames)
+        pipe.set_debug_sink([&](const ts::FrameDebug& d) {
+            ++debug_calls;
+            if (d.mask) debug_masks += ts::CountMasked(*d.mask) > 0;
+            if (d.refined_depth && d.virtual_depth) ++debug_refined;
+        });
     int frames_read = 0;
     ts::FrameSource src = [&]() -> std::optional<ts::Frame> {
         if (frames_read == n) return std::nullopt;
