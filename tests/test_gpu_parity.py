@@ -435,3 +435,27 @@ def test_process_frames_batch_matches_single():
     ca, va = canonical(*a.volume().export())
     cb, vb = canonical(*b.volume().export())
     assert (ca == cb).all() and va.tobytes() == vb.tobytes()
+
+
+def test_pipeline_tracking_loss_single_and_batch():
+    """A frame with no usable depth loses tracking (registration.cpp:228-231):
+    the pose is held, nothing is integrated, later frames recover
+    (pipeline.cpp:117-122) -- frame by frame against the oracle, and the batched
+    call (loss handled on the device) identical to the single calls."""
+    s = O.Scene(scenes.room_script(with_mover=False, width=160, height=120, frames=8))
+    frames = [s.render(i) for i in range(len(s))]
+    frames[4] = dict(frames[4], depth=np.zeros_like(frames[4]["depth"]))
+    vc = O.vol_cfg(voxel_size=0.02, max_blocks=200000)
+    op = O.Pipeline(O.pipe_cfg(refine=False, volume=vc, reg=O.reg_cfg(threads=8)))
+    cfg = G.pipeline_config(refine=False, volume=gcfg(vc))
+    ga, gb = G.Pipeline(cfg), G.Pipeline(cfg)
+    gframes = [frame(s.k, f["depth"], f["rgb"], f["timestamp"]) for f in frames]
+    bstats, bposes = gb.process_frames(gframes)
+    for i, f in enumerate(frames):
+        so, po = op.process_frame(f["depth"], f["rgb"], s.k, f["timestamp"])
+        sg, pg = ga.process_frame(gframes[i])
+        assert so["tracking_lost"] == sg["tracking_lost"] == bstats[i]["tracking_lost"], i
+        assert max(pose_error(po, pg)) <= 1e-4
+        assert np.array_equal(pg, bposes[i])
+    assert bstats[4]["tracking_lost"] == 1 and np.array_equal(bposes[4], bposes[3])
+    assert ga.tracking_losses() == gb.tracking_losses() == 1
