@@ -479,6 +479,7 @@ __device__ void grow_tile(const float* depth, uint32_t* planes, int w, int h, in
     const int ntx = (w + 31) / 32;
     uint32_t* tp = planes + size_t(ty * ntx + tx) * 8 * 32;
     const int gx0 = tx * 32 - 1, gy0 = ty * 32 - 1;
+#pragma unroll 4
     for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
         const int gx = gx0 + i % S, gy = gy0 + i / S;
         dt[i] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldg(depth + gy * w + gx) : 0.f;  // 0: invalid
@@ -517,7 +518,8 @@ __device__ void morph_tile(int tx, int ty, int w, int h, int r, Src src, uint8_t
     __shared__ uint8_t rowv[kMorphS * kMorphTile];
     const int S = kMorphTile + 2 * r;
     const int gx0 = tx * kMorphTile - r, gy0 = ty * kMorphTile - r;
-    for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < S * S; i += blockDim.x) {  // (unrolled: several pixels' loads in flight)
         const int gx = gx0 + i % S, gy = gy0 + i / S;
         win[i] = (gx >= 0 && gx < w && gy >= 0 && gy < h && src(gx, gy)) ? 1 : 0;
     }
@@ -734,10 +736,12 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
         for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
             int nseed = 0;
             morph_tile<true>(t % ntx, t / ntx, w, h, re,
-                             [&](int gx, int gy) {
+                             [&](int gx, int gy) -> bool {  // both loads issued together (no short-circuit)
                                  const int p = gy * w + gx;
-                                 return do_thr ? (__ldcg(F.res_valid + p) && double(__ldcg(F.res_sq + p)) > thr)
-                                               : __ldcg(input + p) != 0;
+                                 if (!do_thr) return __ldcg(input + p) != 0;
+                                 const uint8_t valid = __ldcg(F.res_valid + p);
+                                 const float sq = __ldcg(F.res_sq + p);
+                                 return (valid != 0) & (double(sq) > thr);
                              },
                              seeds, nseed);
             if (stages & 4) {  // the floodfill's growth bits (same 32x32 tiling) and round-0 worklist
