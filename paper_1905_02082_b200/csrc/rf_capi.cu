@@ -87,9 +87,13 @@ void require(bool ok, rf_status code, const std::string& msg) {
     if (!ok) throw Error{code, msg};
 }
 
-struct DevBuf {
+struct DevBuf {  // owning device allocation (freed on scope exit, also on error paths)
     void* p = nullptr;
     size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
     void ensure(size_t bytes) {
         if (bytes <= n) return;
         if (p) cudaFree(p);
