@@ -286,6 +286,7 @@ struct rf_volume {
     rf_volume_config cfg{};
     uint64_t cap = 0;
     DevBuf slots, coords, voxels, links, counters;
+    DevBuf win_first;  // refinement temp volume: first window entry per hash slot
     VolumeView view{};
     Workspace ws;
     cudaEvent_t* prof = nullptr;  // stage markers when a pipeline profiles (see rf_pipeline_set_profiling)
@@ -340,16 +341,65 @@ struct rf_volume {
     }
     // Back to the freshly created state; only the bricks in use are touched
     // unless an overflow left orphaned hash keys behind (full reset).
-    void clear(bool full) {
+    void clear(bool full, bool voxels_too = true) {
         if (full) {
             CK(cudaMemsetAsync(slots.p, 0xFF, cap * sizeof(HashSlot), ws.stream));
             CK(cudaMemsetAsync(links.p, 0xFF, cap * kLinkStride * sizeof(uint32_t), ws.stream));
             CK(cudaMemsetAsync(voxels.p, 0, cfg.max_blocks * kBrickVoxels * sizeof(Voxel), ws.stream));
+            if (win_first.p) CK(cudaMemsetAsync(win_first.p, 0xFF, cap * sizeof(uint32_t), ws.stream));
         } else {
-            k_vol_clear<<<4 * 148, 128, 0, ws.stream>>>(view);
+            k_vol_clear<<<4 * 148, 128, 0, ws.stream>>>(view, voxels_too);
             CK(cudaGetLastError());
         }
         CK(cudaMemsetAsync(view.counters, 0, kNumCounters * sizeof(uint32_t), ws.stream));
+    }
+    // RenderVirtualDepth's temp-volume fusion (depth_refinement.cpp:25-30) of
+    // n same-size entries, front to back, kMaxWin entries per alloc / cull /
+    // fuse triple (rf_volume.cuh WindowArgs).
+    struct WinIn {
+        const float* depth;
+        const uint8_t* rgb;
+        const uint8_t* mask;
+        const double* pose;  // device
+        rf_intrinsics k;
+        const int4* blist = nullptr;      // optional recorded brick list (device) ...
+        const uint32_t* bcount = nullptr;  // ... and its length (device)
+    };
+    void fuse_window(const WinIn* in, int n) {
+        if (!win_first.p) {
+            win_first.ensure(cap * sizeof(uint32_t));
+            CK(cudaMemsetAsync(win_first.p, 0xFF, cap * sizeof(uint32_t), ws.stream));
+            view.win_first = win_first.as<uint32_t>();
+        }
+        ws.list.ensure(2 * cfg.max_blocks * sizeof(uint32_t));
+        for (int c0 = 0; c0 < n; c0 += kMaxWin) {
+            const int m = std::min(kMaxWin, n - c0);
+            WindowArgs wa{};
+            wa.V = view;
+            wa.n = m;
+            wa.list = ws.list.as<uint32_t>();
+            for (int j = 0; j < m; ++j) {
+                wa.depth[j] = in[c0 + j].depth;
+                wa.rgb[j] = in[c0 + j].rgb;
+                wa.mask[j] = in[c0 + j].mask;
+                wa.pose[j] = in[c0 + j].pose;
+                wa.K[j] = level_intr(in[c0 + j].k, 0);
+                wa.blist[j] = in[c0 + j].blist;
+                wa.bcount[j] = in[c0 + j].bcount;
+            }
+            if (c0 > 0) k_win_first_reset<<<148, 256, 0, ws.stream>>>(view);
+            bool lists = false, walks = false;
+            for (int j = 0; j < m; ++j) (in[c0 + j].bcount ? lists : walks) = true;
+            if (lists) k_insert_window<<<2 * 148, 256, 0, ws.stream>>>(wa);
+            // entries without a list (or whose list overflowed: decided on the device) walk their pixels
+            const long long total = (long long)in[c0].k.width * in[c0].k.height * m;
+            (void)walks;
+            k_alloc_window<<<unsigned((total + 255) / 256), 256, 0, ws.stream>>>(wa);
+            reset_counter(kVisible);
+            k_cull_window<<<4 * 148, 256, 0, ws.stream>>>(wa);
+            k_fuse_window<<<4 * 148, kBrickVoxels, 0, ws.stream>>>(wa);
+            CK(cudaGetLastError());
+        }
     }
     void link() {  // link records for bricks allocated outside the per-frame cull
         k_link<<<148, 256, 0, ws.stream>>>(view);
@@ -1034,23 +1084,41 @@ rf_status rf_render_virtual_depth(const rf_frame* frames, const double* poses, c
                 "bad argument");
         require(!refined_depth || (frames[0].intrinsics.width == k->width && frames[0].intrinsics.height == k->height),
                 RF_INVALID_ARGUMENT, "depth size mismatch");
+        for (int i = 1; i < n; ++i)
+            require(frames[i].intrinsics.width == frames[0].intrinsics.width &&
+                        frames[i].intrinsics.height == frames[0].intrinsics.height,
+                    RF_INVALID_ARGUMENT, "window frames must share one size");
         rf_volume* t = nullptr;
         create_volume(vcfg, device, &t);
         std::unique_ptr<rf_volume, void (*)(rf_volume*)> hold(t, rf_volume_destroy);
+        // every entry resident at once (the window kernels read them together)
+        const size_t nf = size_t(frames[0].intrinsics.width) * frames[0].intrinsics.height;
+        std::vector<DevBuf> ed(n), er(n), em(n);
+        DevBuf ep;
+        ep.ensure(size_t(n) * 96);
+        CK(cudaMemcpyAsync(ep.p, poses, size_t(n) * 96, cudaMemcpyHostToDevice, t->ws.stream));
+        std::vector<rf_volume::WinIn> in(n);
         for (int i = 0; i < n; ++i) {
             const rf_frame* f = &frames[i];
-            t->prepare(f);
-            const float* d = t->depth_of(f);
-            const uint8_t* rgb = t->rgb_of(f);
-            const uint8_t* m = t->mask_of(f, masks ? masks[i] : nullptr);
-            t->upload_pose(poses + 12 * i);
-            t->reset_counter(kOverflow);
-            t->allocate(d, m, f->intrinsics, t->ws.pose.as<double>(), nullptr);
-            t->fuse(d, rgb, m, f->intrinsics, t->ws.pose.as<double>(), nullptr, false, true, false);
-            t->ws.sync();
-            require(t->overflow() == 0, RF_RESOURCE_LIMIT,
-                    "voxel block budget exhausted (" + std::to_string(vcfg->max_blocks) + " blocks)");
+            const cudaMemcpyKind kind = f->memory == RF_MEMORY_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+            ed[i].ensure(4 * nf);
+            CK(cudaMemcpyAsync(ed[i].p, f->depth, 4 * nf, kind, t->ws.stream));
+            if (f->rgb) {
+                er[i].ensure(3 * nf);
+                CK(cudaMemcpyAsync(er[i].p, f->rgb, 3 * nf, kind, t->ws.stream));
+            }
+            if (masks && masks[i]) {
+                em[i].ensure(nf);
+                CK(cudaMemcpyAsync(em[i].p, masks[i], nf, kind, t->ws.stream));
+            }
+            in[i] = {ed[i].as<float>(), f->rgb ? er[i].as<uint8_t>() : nullptr,
+                     (masks && masks[i]) ? em[i].as<uint8_t>() : nullptr, ep.as<double>() + 12 * i, f->intrinsics};
         }
+        t->reset_counter(kOverflow);
+        t->fuse_window(in.data(), n);
+        t->ws.sync();
+        require(t->overflow() == 0, RF_RESOURCE_LIMIT,
+                "voxel block budget exhausted (" + std::to_string(vcfg->max_blocks) + " blocks)");
         const size_t np = size_t(k->width) * k->height;
         DevBuf vo, ro;
         vo.ensure(np * 4);
@@ -1226,6 +1294,9 @@ struct rf_pipeline {
     rf_volume* vol = nullptr;
     // Depth-refinement window (pipeline.cpp:31-55, 111-113, 133-135).
     rf_volume* temp = nullptr;  // the throw-away TsdfVolume of RenderVirtualDepth, reused
+    rf_volume* scratch = nullptr;  // records each window entry's AllocateForFrame brick list
+    DevBuf win_lists, win_counts;
+    static constexpr uint32_t kSlotBricks = 1u << 18;
     bool temp_full_reset = false;
     std::deque<WinEntry> window;
     DevBuf win, win_pose, virt, refined;
@@ -1293,6 +1364,8 @@ void ensure_window(rf_pipeline* p, int w, int h) {
     p->off_mask = p->off_rgb + align256(3 * n);
     p->slot_bytes = p->off_mask + align256(n);
     p->win.ensure(size_t(p->cfg.refine_window) * p->slot_bytes);
+    p->win_lists.ensure(size_t(p->cfg.refine_window) * rf_pipeline::kSlotBricks * sizeof(int4));
+    p->win_counts.ensure(size_t(p->cfg.refine_window) * sizeof(uint32_t));
     p->win_pose.ensure(size_t(p->cfg.refine_window) * 96);
     p->virt.ensure(4 * n);
     p->refined.ensure(4 * n);
@@ -1311,12 +1384,14 @@ void integrate_front(rf_pipeline* p) {
     cudaStream_t s = v->ws.stream;
     t->clear(p->temp_full_reset);
     p->temp_full_reset = false;
-    for (const WinEntry& e : p->window) {  // front to back, like window.entries()
-        const uint8_t* m = e.has_mask ? slot_mask(p, e.slot) : nullptr;
-        t->allocate(slot_depth(p, e.slot), m, e.k, slot_pose(p, e.slot), nullptr);
-        t->fuse(slot_depth(p, e.slot), e.has_rgb ? slot_rgb(p, e.slot) : nullptr, m, e.k, slot_pose(p, e.slot),
-                nullptr, false, true, false);
-    }
+    std::vector<rf_volume::WinIn> in;
+    for (const WinEntry& e : p->window)  // front to back, like window.entries()
+        in.push_back({slot_depth(p, e.slot), e.has_rgb ? slot_rgb(p, e.slot) : nullptr,
+                      e.has_mask ? slot_mask(p, e.slot) : nullptr, slot_pose(p, e.slot), e.k,
+                      p->win_lists.as<int4>() + size_t(e.slot) * rf_pipeline::kSlotBricks,
+                      p->win_counts.as<uint32_t>() + e.slot});
+    t->fuse_window(in.data(), int(in.size()));
+    p->launches += 4 * ((in.size() + kMaxWin - 1) / kMaxWin);
     CK(cudaMemcpyAsync(p->h_front + 1, t->view.counters + kOverflow, 4, cudaMemcpyDeviceToHost, s));
     const WinEntry f = p->window.front();
     RaycastArgs a{};
@@ -1340,7 +1415,7 @@ void integrate_front(rf_pipeline* p) {
     v->allocate(rd, m, f.k, slot_pose(p, f.slot), nullptr);
     v->fuse(rd, f.has_rgb ? slot_rgb(p, f.slot) : nullptr, m, f.k, slot_pose(p, f.slot), nullptr, true, true, true);
     CK(cudaMemcpyAsync(p->h_front, v->view.counters + kOverflow, 4, cudaMemcpyDeviceToHost, s));
-    p->launches += 3 * p->window.size() + 5;
+    p->launches += 5;
     p->has_refinement = true;
     p->refined_index = f.index;
     p->window.pop_front();
@@ -1367,10 +1442,16 @@ rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipel
         CK(cudaMallocHost(&p->h_front, 16));
         std::memset(p->h_front, 0, 16);
         if (p->cfg.refine_enabled) {
+            rf_volume_config sc = p->cfg.volume;  // per-entry brick lists: bounded scratch volume
+            sc.max_blocks = std::min<uint64_t>(sc.max_blocks, rf_pipeline::kSlotBricks);
+            sc.hash_capacity = 0;
             create_volume(&p->cfg.volume, device, &p->temp);
-            cudaStreamDestroy(p->temp->ws.stream);  // work runs on the pipeline's stream
-            p->temp->ws.stream = p->vol->ws.stream;
-            p->temp->ws.own_stream = false;
+            create_volume(&sc, device, &p->scratch);
+            for (rf_volume* t : {p->temp, p->scratch}) {
+                cudaStreamDestroy(t->ws.stream);  // work runs on the pipeline's stream
+                t->ws.stream = p->vol->ws.stream;
+                t->ws.own_stream = false;
+            }
         }
         *out = p.release();
     });
@@ -1381,6 +1462,7 @@ void rf_pipeline_destroy(rf_pipeline* p) {
     for (cudaEvent_t& e : p->ev)
         if (e) cudaEventDestroy(e);
     if (p->temp) rf_volume_destroy(p->temp);
+    if (p->scratch) rf_volume_destroy(p->scratch);
     for (DevBuf* b : {&p->win, &p->win_pose, &p->virt, &p->refined}) b->release();
     if (p->h_front) cudaFreeHost(p->h_front);
     rf_volume_destroy(p->vol);
@@ -1453,6 +1535,15 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
                 if (rgb) CK(cudaMemcpyAsync(slot_rgb(p, slot), rgb, 3 * n, cudaMemcpyDeviceToDevice, ws.stream));
                 if (mask) CK(cudaMemcpyAsync(slot_mask(p, slot), mask, n, cudaMemcpyDeviceToDevice, ws.stream));
                 CK(cudaMemcpyAsync(slot_pose(p, slot), pose_state, 96, cudaMemcpyDeviceToDevice, ws.stream));
+                // the entry's AllocateForFrame brick list, for every later IntegrateFront
+                rf_volume* sv = p->scratch;
+                sv->clear(false, false);  // hash only: its voxels are never written
+                sv->allocate(slot_depth(p, slot), mask ? slot_mask(p, slot) : nullptr, f->intrinsics,
+                             slot_pose(p, slot), lost);
+                k_brick_list<<<148, 256, 0, ws.stream>>>(sv->view, p->win_lists.as<int4>() + size_t(slot) * rf_pipeline::kSlotBricks,
+                                                         rf_pipeline::kSlotBricks, p->win_counts.as<uint32_t>() + slot);
+                CK(cudaGetLastError());
+                p->launches += 3;
                 if (v->prof) {
                     CK(cudaEventRecord(p->ev[2], ws.stream));
                     CK(cudaEventRecord(p->ev[3], ws.stream));

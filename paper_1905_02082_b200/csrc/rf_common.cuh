@@ -54,6 +54,7 @@ struct VolumeView {
     Voxel* voxels;       // pool, kBrickVoxels per brick, x fastest then y then z
     uint32_t* links;     // kLinkStride per HASH SLOT: [0] the slot's brick, [q] the brick at +(q&1, q>>1&1, q>>2)
     uint32_t* counters;  // see VolumeCounters
+    uint32_t* win_first; // refinement temp volume only: per hash slot, first window entry that allocated it
     double voxel_size, truncation;
     double inv_voxel_size;  // 1.0 / voxel_size (the reference's inv_s, tsdf_volume.cpp:336)
     int max_weight, carve_weight;
@@ -170,7 +171,7 @@ __device__ __forceinline__ uint32_t hash_find_slot_from(const VolumeView& V, uns
 
 // Lock-free linear-probing insert (no deletion). Returns 1 when this thread
 // created the brick, 0 when it already existed, -1 on overflow.
-__device__ __forceinline__ int hash_insert(const VolumeView& V, int x, int y, int z) {
+__device__ __forceinline__ int hash_insert(const VolumeView& V, int x, int y, int z, uint32_t* slot_out = nullptr) {
     if (!coord_in_range(x, y, z)) {
         atomicOr(&V.counters[kOverflow], 2u);
         return -1;
@@ -184,6 +185,7 @@ __device__ __forceinline__ int hash_insert(const VolumeView& V, int x, int y, in
                 atomicOr(&V.counters[kOverflow], 1u);  // AllocateBlock throws again (tsdf_volume.cpp:66-69)
                 return -1;
             }
+            if (slot_out) *slot_out = idx;
             return 0;
         }
         if (k == kEmptyKey) {
@@ -197,6 +199,7 @@ __device__ __forceinline__ int hash_insert(const VolumeView& V, int x, int y, in
                 }
                 V.coords[b] = make_int4(x, y, z, int(idx));  // w = hash slot (volume reset)
                 V.slots[idx].value = b;
+                if (slot_out) *slot_out = idx;
                 return 1;
             }
             if (old == key) {
@@ -204,6 +207,7 @@ __device__ __forceinline__ int hash_insert(const VolumeView& V, int x, int y, in
                     atomicOr(&V.counters[kOverflow], 1u);
                     return -1;
                 }
+                if (slot_out) *slot_out = idx;
                 return 0;
             }
         }

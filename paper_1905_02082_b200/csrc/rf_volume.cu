@@ -11,81 +11,95 @@ namespace rfb {
 // tsdf_volume.hpp:149-185), one thread per pixel, all cells inserted with
 // atomicCAS. The set of inserted keys, and so the occupied-slot set of the
 // linear-probing table, is independent of thread order.
+// The ray segment of pixel p (AllocateForFrame, tsdf_volume.cpp:93-113):
+// [max(d - tau, 1e-4), d + tau] along the pixel's ray, walked through the
+// block grid (WalkGridSegment, tsdf_volume.hpp:149-185); `visit(cell)` for
+// every block cell in order. Returns the cells visited (0: pixel unusable).
+template <class Visit>
+__device__ __forceinline__ unsigned walk_pixel(const VolumeView& V, const float* depth, const uint8_t* mask,
+                                               const Intr& K, const double* pose, int p, Visit visit) {
+    const int u = p % K.w, v = p / K.w;
+    const float d = __ldg(depth + p);
+    const bool masked = mask && __ldg(mask + p);
+    if (!(depth_valid(d) && !(d < V.min_depth) && !(d > V.max_depth) && !masked)) return 0;
+    Pose P;
+    for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = __ldg(pose + i);
+    const double tau = V.truncation;
+    const double ext = double(kSide) * V.voxel_size;  // block_extent(), tsdf_volume.hpp:123
+    const double dir0 = (double(u) - K.cx) / K.fx, dir1 = (double(v) - K.cy) / K.fy;
+    const double z0 = fmax(double(d) - tau, 1e-4);
+    const double z1 = double(d) + tau;
+    double w0[3], w1[3];
+    pose_apply(P, z0 * dir0, z0 * dir1, z0 * 1.0, w0);
+    pose_apply(P, z1 * dir0, z1 * dir1, z1 * 1.0, w1);
+    const double p0[3] = {w0[0] / ext, w0[1] / ext, w0[2] / ext};
+    const double p1[3] = {w1[0] / ext, w1[1] / ext, w1[2] / ext};
+    int cell[3], end[3], step[3];
+    double tmax[3], tdel[3];
+    for (int i = 0; i < 3; ++i) {
+        const double dd = p1[i] - p0[i];
+        cell[i] = int(floor(p0[i]));
+        end[i] = int(floor(p1[i]));
+        step[i] = 0;
+        tmax[i] = tdel[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+        if (dd > 0) {
+            step[i] = 1;
+            tmax[i] = (floor(p0[i]) + 1.0 - p0[i]) / dd;
+            tdel[i] = 1.0 / dd;
+        } else if (dd < 0) {
+            step[i] = -1;
+            tmax[i] = (p0[i] - floor(p0[i])) / -dd;
+            tdel[i] = 1.0 / -dd;
+        }
+    }
+    const int max_steps = abs(end[0] - cell[0]) + abs(end[1] - cell[1]) + abs(end[2] - cell[2]) + 3;
+    unsigned visits = 1;
+    visit(cell);
+    for (int n = 0; n < max_steps && (cell[0] != end[0] || cell[1] != end[1] || cell[2] != end[2]); ++n) {
+        int axis = 0;
+        if (tmax[1] < tmax[axis]) axis = 1;
+        if (tmax[2] < tmax[axis]) axis = 2;
+        if (tmax[axis] > 1.0) break;
+        tmax[axis] += tdel[axis];
+        cell[axis] += step[axis];
+        visit(cell);
+        ++visits;
+    }
+    return visits;
+}
+
 __global__ void k_alloc(AllocArgs a) {
     if (a.lost && *a.lost) return;
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    const int w = a.K.w, h = a.K.h;
     unsigned visits = 0;
-    if (p < w * h) {
-        const int u = p % w, v = p / w;
-        const float d = __ldg(a.depth + p);
-        const bool masked = a.mask && __ldg(a.mask + p);
-        if (depth_valid(d) && !(d < a.V.min_depth) && !(d > a.V.max_depth) && !masked) {
-            Pose P;
-            for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = __ldg(a.pose + i);
-            const double tau = a.V.truncation;
-            const double ext = double(kSide) * a.V.voxel_size;  // block_extent(), tsdf_volume.hpp:123
-            const double dir0 = (double(u) - a.K.cx) / a.K.fx, dir1 = (double(v) - a.K.cy) / a.K.fy;
-            const double z0 = fmax(double(d) - tau, 1e-4);
-            const double z1 = double(d) + tau;
-            double w0[3], w1[3];
-            pose_apply(P, z0 * dir0, z0 * dir1, z0 * 1.0, w0);
-            pose_apply(P, z1 * dir0, z1 * dir1, z1 * 1.0, w1);
-            const double p0[3] = {w0[0] / ext, w0[1] / ext, w0[2] / ext};
-            const double p1[3] = {w1[0] / ext, w1[1] / ext, w1[2] / ext};
-            int cell[3], end[3], step[3];
-            double tmax[3], tdel[3];
-            for (int i = 0; i < 3; ++i) {
-                const double dd = p1[i] - p0[i];
-                cell[i] = int(floor(p0[i]));
-                end[i] = int(floor(p1[i]));
-                step[i] = 0;
-                tmax[i] = tdel[i] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-                if (dd > 0) {
-                    step[i] = 1;
-                    tmax[i] = (floor(p0[i]) + 1.0 - p0[i]) / dd;
-                    tdel[i] = 1.0 / dd;
-                } else if (dd < 0) {
-                    step[i] = -1;
-                    tmax[i] = (p0[i] - floor(p0[i])) / -dd;
-                    tdel[i] = 1.0 / -dd;
-                }
-            }
-            const int max_steps = abs(end[0] - cell[0]) + abs(end[1] - cell[1]) + abs(end[2] - cell[2]) + 3;
-            // The walk is run one cell ahead of the inserts: the first hash slot
-            // of the next cell is loaded while the current one is checked, and a
-            // cell whose key already sits in its first slot (almost all of them
-            // once the scene is mapped) needs no atomic. Same key set as
-            // inserting every visited cell (hash_insert of a present key is a no-op).
-            auto first_slot = [&](const int (&c)[3]) -> uint4 {
-                if (!coord_in_range(c[0], c[1], c[2])) return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
-                return __ldg(reinterpret_cast<const uint4*>(a.V.slots + (hash_coord(c[0], c[1], c[2]) & a.V.hash_mask)));
-            };
-            auto settle = [&](const int (&c)[3], uint4 sl) {
-                const unsigned long long k = (unsigned long long)sl.x | ((unsigned long long)sl.y << 32);
-                if (!(coord_in_range(c[0], c[1], c[2]) && k == pack_key(c[0], c[1], c[2]) && sl.z < kOverflowed))
-                    hash_insert(a.V, c[0], c[1], c[2]);
-            };
-            int cur[3] = {cell[0], cell[1], cell[2]};
-            uint4 cur_sl = first_slot(cur);
-            ++visits;
-            for (int n = 0; n < max_steps && (cell[0] != end[0] || cell[1] != end[1] || cell[2] != end[2]); ++n) {
-                int axis = 0;
-                if (tmax[1] < tmax[axis]) axis = 1;
-                if (tmax[2] < tmax[axis]) axis = 2;
-                if (tmax[axis] > 1.0) break;
-                tmax[axis] += tdel[axis];
-                cell[axis] += step[axis];
-                const uint4 next_sl = first_slot(cell);
-                settle(cur, cur_sl);
-                cur[0] = cell[0];
-                cur[1] = cell[1];
-                cur[2] = cell[2];
-                cur_sl = next_sl;
-                ++visits;
-            }
-            settle(cur, cur_sl);
-        }
+    if (p < a.K.w * a.K.h) {
+        // The walk runs one cell ahead of the inserts: the first hash slot of
+        // the next cell is loaded while the current one is checked, and a cell
+        // whose key already sits in its first slot (almost all of them once the
+        // scene is mapped) needs no atomic. Same key set as inserting every
+        // visited cell (hash_insert of a present key is a no-op).
+        auto first_slot = [&](const int (&c)[3]) -> uint4 {
+            if (!coord_in_range(c[0], c[1], c[2])) return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
+            return __ldg(reinterpret_cast<const uint4*>(a.V.slots + (hash_coord(c[0], c[1], c[2]) & a.V.hash_mask)));
+        };
+        auto settle = [&](const int (&c)[3], uint4 sl) {
+            const unsigned long long k = (unsigned long long)sl.x | ((unsigned long long)sl.y << 32);
+            if (!(coord_in_range(c[0], c[1], c[2]) && k == pack_key(c[0], c[1], c[2]) && sl.z < kOverflowed))
+                hash_insert(a.V, c[0], c[1], c[2]);
+        };
+        int cur[3] = {0, 0, 0};
+        uint4 cur_sl = make_uint4(0, 0, 0, 0);
+        bool have = false;
+        visits = walk_pixel(a.V, a.depth, a.mask, a.K, a.pose, p, [&](const int (&c)[3]) {
+            const uint4 next_sl = first_slot(c);
+            if (have) settle(cur, cur_sl);
+            cur[0] = c[0];
+            cur[1] = c[1];
+            cur[2] = c[2];
+            cur_sl = next_sl;
+            have = true;
+        });
+        if (have) settle(cur, cur_sl);
     }
     // warp-aggregated visit counter (for the algorithmic-bytes model)
     for (int o = 16; o > 0; o >>= 1) visits += __shfl_down_sync(0xffffffffu, visits, o);
@@ -386,17 +400,174 @@ __global__ void k_occupancy(VolumeView V, uint8_t* bitmap) {
 // one of the bricks [0, n) (no deletion, coords.w = slot), so clearing those
 // slots, their voxels and link records restores the freshly created state
 // without touching the rest of the table. Grid-stride over n read on device.
-__global__ void k_vol_clear(VolumeView V) {
+__global__ void k_vol_clear(VolumeView V, bool voxels) {
     const uint32_t n = min(V.counters[kNumBlocks], V.max_blocks);
     for (uint32_t b = blockIdx.x; b < n; b += gridDim.x) {
         uint4* vox = reinterpret_cast<uint4*>(V.voxels + size_t(b) * kBrickVoxels);
-        for (int i = threadIdx.x; i < kBrickVoxels * int(sizeof(Voxel)) / 16; i += blockDim.x)
-            vox[i] = make_uint4(0, 0, 0, 0);
+        if (voxels)
+            for (int i = threadIdx.x; i < kBrickVoxels * int(sizeof(Voxel)) / 16; i += blockDim.x)
+                vox[i] = make_uint4(0, 0, 0, 0);
         const uint32_t slot = uint32_t(V.coords[b].w);
         if (threadIdx.x < kLinkStride) V.links[size_t(slot) * kLinkStride + threadIdx.x] = kInvalid;
         if (threadIdx.x == 0) {
+            if (V.win_first) V.win_first[slot] = 0xFFFFFFFFu;
             V.slots[slot].key = kEmptyKey;
             V.slots[slot].value = kInvalid;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- refinement window
+// Bricks already present before a chunk take updates from all of its entries.
+__global__ void k_win_first_reset(VolumeView V) {
+    const uint32_t n = min(V.counters[kNumBlocks], V.max_blocks);
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x)
+        V.win_first[uint32_t(V.coords[b].w)] = 0u;
+}
+
+// AllocateForFrame of every entry of the chunk (one thread per entry pixel);
+// each visited brick records the smallest entry that reached it.
+__global__ void k_alloc_window(WindowArgs a) {
+    const int P = a.K[0].w * a.K[0].h;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)P * a.n) return;
+    const int j = int(i / P), p = int(i % P);
+    if (a.bcount[j] && *a.bcount[j] != kListOverflow) return;  // inserted from its brick list
+    walk_pixel(a.V, a.depth[j], a.mask[j], a.K[j], a.pose[j], p, [&](const int (&c)[3]) {
+        uint32_t slot = kInvalid;
+        if (hash_insert(a.V, c[0], c[1], c[2], &slot) >= 0 && slot != kInvalid) atomicMin(a.V.win_first + slot, uint32_t(j));
+    });
+}
+
+// Inserts the entries' recorded brick lists (entry j's list = the bricks its
+// AllocateForFrame allocates), each brick recording its smallest entry.
+__global__ void k_insert_window(WindowArgs a) {
+    for (int j = 0; j < a.n; ++j) {
+        if (!a.bcount[j]) continue;
+        const uint32_t cnt = *a.bcount[j];
+        if (cnt == kListOverflow) continue;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+            const int4 c = a.blist[j][i];
+            uint32_t slot = kInvalid;
+            if (hash_insert(a.V, c.x, c.y, c.z, &slot) >= 0 && slot != kInvalid) atomicMin(a.V.win_first + slot, uint32_t(j));
+        }
+    }
+}
+
+// The bricks of a (scratch) volume as a list: AllocateForFrame's result for
+// one window entry. count = kListOverflow when they do not fit (or the
+// scratch volume overflowed): that entry is walked again at fusion time.
+__global__ void k_brick_list(VolumeView S, int4* dst, uint32_t cap, uint32_t* count) {
+    const uint32_t nb = S.counters[kNumBlocks];
+    const bool ok = nb <= cap && nb <= S.max_blocks && S.counters[kOverflow] == 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *count = ok ? nb : kListOverflow;
+    if (!ok) return;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) dst[i] = S.coords[i];
+}
+
+// Per brick: the entries (from its first one on) whose frustum it meets;
+// links the new bricks for the ray-march.
+__global__ void k_cull_window(WindowArgs a) {
+    const uint32_t nb = min(a.V.counters[kNumBlocks], a.V.max_blocks);
+    const double ext = double(kSide) * a.V.voxel_size;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b0 < nb; b0 += stride) {
+        const uint32_t b = b0 + (threadIdx.x & 31u);
+        uint32_t bits = 0;
+        if (b < nb) {
+            const int4 c = a.V.coords[b];
+            const uint32_t first = a.V.win_first[uint32_t(c.w)];
+            for (int j = int(first); j < a.n; ++j) {
+                Pose P;
+                for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = __ldg(a.pose[j] + i);
+                const Pose W = pose_inverse(P);
+                double cc[8][3];
+                for (int k = 0; k < 8; ++k) {
+                    const double x = (double(c.x) + double(k & 1)) * ext;
+                    const double y = (double(c.y) + double((k >> 1) & 1)) * ext;
+                    const double z = (double(c.z) + double(k >> 2)) * ext;
+                    pose_apply(W, x, y, z, cc[k]);
+                }
+                if (!outside(cc, a.K[j], a.V.max_depth + a.V.truncation)) bits |= 1u << j;
+            }
+        }
+        const unsigned vote = __ballot_sync(0xffffffffu, bits != 0);
+        if (vote) {  // one atomic per warp, lanes take consecutive slots
+            const int lane = threadIdx.x & 31;
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&a.V.counters[kVisible], uint32_t(__popc(vote)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (bits) {
+                const uint32_t at = base + __popc(vote & ((1u << lane) - 1u));
+                a.list[2 * at] = b;
+                a.list[2 * at + 1] = bits;
+            }
+        }
+    }
+    link_new(a.V);
+}
+
+// Integrate (tsdf_volume.cpp:155-202) of the chunk's entries, in order, into
+// each listed brick: the voxel is read once, updated by every entry whose bit
+// is set, and written once.
+__global__ void __launch_bounds__(kBrickVoxels) k_fuse_window(WindowArgs a) {
+    commit_links(a.V);
+    __shared__ Pose Ws[kMaxWin];
+    __shared__ double s_rcp[512];  // RN(1 / i) for the running averages (see div_f32)
+    if (threadIdx.x < a.n) {
+        Pose P;
+        for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = a.pose[threadIdx.x][i];
+        Ws[threadIdx.x] = pose_inverse(P);
+    }
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_rcp[i] = i ? 1.0 / double(i) : 0.0;
+    __syncthreads();
+    const uint32_t nvis = a.V.counters[kVisible];
+    const int x = threadIdx.x & 7, y = (threadIdx.x >> 3) & 7, z = threadIdx.x >> 6;
+    const double s = a.V.voxel_size, tau = a.V.truncation;
+    const int mw = a.V.max_weight;
+    for (uint32_t i = blockIdx.x; i < nvis; i += gridDim.x) {
+        const uint32_t b = __ldcg(a.list + 2 * i), bits = __ldcg(a.list + 2 * i + 1);
+        const int4 c = a.V.coords[b];
+        Voxel* vp = a.V.voxels + size_t(b) * kBrickVoxels + threadIdx.x;
+        uint2 raw = *reinterpret_cast<uint2*>(vp);
+        float sdf = __uint_as_float(raw.x);
+        uint32_t wgt = raw.y & 0xFFu, r = (raw.y >> 8) & 0xFFu, g = (raw.y >> 16) & 0xFFu, bl = raw.y >> 24;
+        bool dirty = false;
+        const double cx = (double(c.x * kSide + x) + 0.5) * s;  // VoxelCenter, tsdf_volume.hpp:117-119
+        const double cy = (double(c.y * kSide + y) + 0.5) * s;
+        const double cz = (double(c.z * kSide + z) + 0.5) * s;
+        for (uint32_t m = bits; m; m &= m - 1u) {
+            const int j = __ffs(m) - 1;
+            const Intr& K = a.K[j];
+            double pc[3];
+            pose_apply(Ws[j], cx, cy, cz, pc);
+            if (pc[2] <= 1e-9) continue;
+            const double rz = fuse_rcp(pc[2]);
+            const long pu = project_lround(K.fx * pc[0], pc[2], rz, K.cx);
+            const long pv = project_lround(K.fy * pc[1], pc[2], rz, K.cy);
+            if (!(pu >= 0 && pu < K.w && pv >= 0 && pv < K.h)) continue;
+            const int pix = int(pv) * K.w + int(pu);
+            const float d = __ldg(a.depth[j] + pix);
+            if (a.mask[j] && __ldg(a.mask[j] + pix)) continue;
+            if (!(depth_valid(d) && !(d < a.V.min_depth) && !(d > a.V.max_depth))) continue;
+            const double dist = double(d) - pc[2];
+            if (dist <= -tau) continue;
+            const double clamped = fmin(dist, tau);
+            const double w = double(wgt);
+            sdf = div_f32(double(sdf) * w + clamped, w + 1.0, s_rcp[wgt + 1u]);
+            if (fabs(dist) <= tau && a.rgb[j]) {
+                const uint8_t* col = a.rgb[j] + 3 * size_t(pix);
+                r = colour_avg(r, wgt, __ldg(col));
+                g = colour_avg(g, wgt, __ldg(col + 1));
+                bl = colour_avg(bl, wgt, __ldg(col + 2));
+            }
+            wgt = min(wgt + 1u, uint32_t(mw));
+            dirty = true;
+        }
+        if (dirty) {
+            raw.x = __float_as_uint(sdf);
+            raw.y = (wgt & 0xFFu) | ((r & 0xFFu) << 8) | ((g & 0xFFu) << 16) | ((bl & 0xFFu) << 24);
+            *reinterpret_cast<uint2*>(vp) = raw;
         }
     }
 }

@@ -38,6 +38,29 @@ struct FuseArgs {
     const uint32_t* list;
 };
 
+// The refinement window fused in one pass per chunk of <= kMaxWin entries
+// (RenderVirtualDepth, depth_refinement.cpp:25-30: AllocateForFrame then
+// Integrate, entry after entry). A brick receives an entry's update only from
+// the first entry that allocated it onwards (win_first), so allocating the
+// whole chunk first changes nothing; every voxel applies its entries in order.
+constexpr int kMaxWin = 16;
+struct WindowArgs {
+    VolumeView V;
+    int n;                          // entries in the chunk
+    const float* depth[kMaxWin];
+    const uint8_t* rgb[kMaxWin];    // may be null
+    const uint8_t* mask[kMaxWin];   // may be null
+    const double* pose[kMaxWin];    // device, camera-to-world
+    Intr K[kMaxWin];
+    uint32_t* list;                 // visible bricks as {brick, entry bitmask} pairs
+    // Optional per-entry brick lists (what AllocateForFrame of the entry
+    // allocates, recorded when the frame entered the window): entries with a
+    // list are inserted from it instead of re-walking their pixels.
+    const int4* blist[kMaxWin];
+    const uint32_t* bcount[kMaxWin];  // list length; kListOverflow: no list (walk)
+};
+constexpr uint32_t kListOverflow = 0xFFFFFFFFu;
+
 struct RaycastArgs {
     VolumeView V;
     Pose view;
@@ -88,6 +111,12 @@ __global__ void k_sample(VolumeView V, const double* pts, int n, int mode, doubl
                          uint8_t* valid);
 __global__ void k_voxel_rw(VolumeView V, const int* vc, int n, Voxel* io, uint8_t* found, int write);
 __global__ void k_occupancy(VolumeView V, uint8_t* bitmap);
-__global__ void k_vol_clear(VolumeView V);
+__global__ void k_vol_clear(VolumeView V, bool voxels);  // voxels=false: hash only
+__global__ void k_win_first_reset(VolumeView V);
+__global__ void k_alloc_window(WindowArgs a);
+__global__ void k_insert_window(WindowArgs a);
+__global__ void k_brick_list(VolumeView S, int4* dst, uint32_t cap, uint32_t* count);
+__global__ void k_cull_window(WindowArgs a);
+__global__ void k_fuse_window(WindowArgs a);
 
 }  // namespace rfb
