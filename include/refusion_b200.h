@@ -41,7 +41,8 @@ typedef enum {
     RF_RESOURCE_LIMIT = 3,  /* ResourceLimitError (errors.hpp:19) */
     RF_CUDA_ERROR = 4,
     RF_IO_ERROR = 5,
-    RF_UNSUPPORTED = 6
+    RF_UNSUPPORTED = 6,
+    RF_FAILED = 7           /* any other std::runtime_error of the reference */
 } rf_status;
 
 enum { RF_MEMORY_HOST = 0, RF_MEMORY_DEVICE = 1 };
@@ -209,6 +210,22 @@ rf_status rf_mesh_copy(const rf_mesh* m, float* xyz, uint8_t* rgb, int32_t* face
 rf_status rf_mesh_device_buffers(const rf_mesh* m, const float** xyz, const uint8_t** rgb, const int32_t** faces);
 rf_status rf_mesh_write_ply(const rf_mesh* m, const char* path);                          /* WritePly */
 void rf_mesh_destroy(rf_mesh* m);
+
+/* ---- evaluation (evaluation.hpp:12-50) ----------------------------------
+ * Trajectories are n timestamps plus 12 n pose doubles (camera-to-world).
+ * Point clouds are f32 xyz triples; `memory` says whether queries, reference
+ * and out (NearestDistances) or distances (DistanceCdf) are host or device
+ * pointers. Bin edges and the CDF are host arrays. */
+rf_status rf_ate_rmse(const double* est_t, const double* est_poses, uint64_t n_est, const double* gt_t,
+                      const double* gt_poses, uint64_t n_gt, double max_dt, double* rmse, double alignment[12],
+                      uint64_t* pairs);                                                    /* AteRmse; < 3 pairs: RF_FAILED */
+rf_status rf_rpe_over_time(const double* est_t, const double* est_poses, uint64_t n_est, const double* gt_t,
+                           const double* gt_poses, uint64_t n_gt, double delta, double max_dt, double* timestamps,
+                           double* errors, uint64_t capacity, uint64_t* count);            /* RpeOverTime */
+rf_status rf_nearest_distances(const float* queries, uint64_t nq, const float* reference, uint64_t nr, int32_t memory,
+                               int device, double* out);                                  /* NearestDistances */
+rf_status rf_distance_cdf(const double* distances, uint64_t n, int32_t memory, int device, const double* edges,
+                          uint64_t ne, double* cdf);                                       /* DistanceCdf */
 
 /* ---- pipeline (pipeline.hpp:51-96) ------------------------------------- */
 rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipeline** out);

@@ -53,6 +53,7 @@ inline void Check(rf_status s) {
         case RF_TRACKING_LOST: throw TrackingLostError(msg);
         case RF_RESOURCE_LIMIT: throw ResourceLimitError(msg);
         case RF_IO_ERROR: throw std::runtime_error(msg);
+        case RF_FAILED: throw std::runtime_error(msg);
         case RF_UNSUPPORTED: throw std::invalid_argument("unsupported on the CUDA path: " + msg);
         default: throw CudaError(msg);
     }
@@ -810,6 +811,77 @@ inline SequenceSummary RunSequence(Pipeline& pipeline, const FrameSource& source
     pipeline.Finalize();
     s.tracking_losses = pipeline.tracking_losses();
     return s;
+}
+
+// ---------------------------------------------------------------- evaluation (evaluation.hpp:12-50)
+struct AteResult {
+    double rmse = 0.0;
+    Pose alignment;  // rigid transform mapping estimated into ground truth
+    std::size_t pairs = 0;
+};
+
+namespace detail {
+inline void Flatten(const Trajectory& tr, std::vector<double>& ts, std::vector<double>& poses) {
+    ts.resize(tr.size());
+    poses.resize(12 * tr.size());
+    for (std::size_t i = 0; i < tr.size(); ++i) {
+        ts[i] = tr[i].timestamp;
+        std::memcpy(poses.data() + 12 * i, tr[i].pose.data(), 12 * sizeof(double));
+    }
+}
+}  // namespace detail
+
+// AteRmse (evaluation.cpp:26-62); throws std::runtime_error below 3 pairs.
+inline AteResult AteRmse(const Trajectory& estimated, const Trajectory& ground_truth, double max_dt = 0.02) {
+    std::vector<double> et, ep, gt, gp;
+    detail::Flatten(estimated, et, ep);
+    detail::Flatten(ground_truth, gt, gp);
+    AteResult r;
+    std::uint64_t pairs = 0;
+    Check(rf_ate_rmse(et.data(), ep.data(), et.size(), gt.data(), gp.data(), gt.size(), max_dt, &r.rmse,
+                      r.alignment.data(), &pairs));
+    r.pairs = static_cast<std::size_t>(pairs);
+    return r;
+}
+
+struct RpeSample {
+    double timestamp = 0.0;
+    double translation_error = 0.0;  // meters over the delta interval
+};
+
+// RpeOverTime (evaluation.cpp:64-92)
+inline std::vector<RpeSample> RpeOverTime(const Trajectory& estimated, const Trajectory& ground_truth,
+                                          double delta = 1.0, double max_dt = 0.02) {
+    std::vector<double> et, ep, gt, gp;
+    detail::Flatten(estimated, et, ep);
+    detail::Flatten(ground_truth, gt, gp);
+    std::vector<double> ts(et.size() + 1), err(et.size() + 1);
+    std::uint64_t n = 0;
+    Check(rf_rpe_over_time(et.data(), ep.data(), et.size(), gt.data(), gp.data(), gt.size(), delta, max_dt,
+                           ts.data(), err.data(), ts.size(), &n));
+    std::vector<RpeSample> out(static_cast<std::size_t>(n));
+    for (std::size_t i = 0; i < out.size(); ++i) out[i] = {ts[i], err[i]};
+    return out;
+}
+
+// NearestDistances (evaluation.cpp:203-217) on the GPU; `threads` is accepted and ignored.
+inline std::vector<double> NearestDistances(const std::vector<Vec3f>& queries, const std::vector<Vec3f>& reference,
+                                            int threads = 1, int device = 0) {
+    (void)threads;
+    std::vector<double> out(queries.size());
+    Check(rf_nearest_distances(queries.empty() ? nullptr : queries[0].data(), queries.size(),
+                               reference.empty() ? nullptr : reference[0].data(), reference.size(), RF_MEMORY_HOST,
+                               device, out.data()));
+    return out;
+}
+
+// DistanceCdf (evaluation.cpp:219-236)
+inline std::vector<double> DistanceCdf(const std::vector<double>& distances, const std::vector<double>& bin_edges,
+                                       int device = 0) {
+    std::vector<double> cdf(bin_edges.size());
+    Check(rf_distance_cdf(distances.data(), distances.size(), RF_MEMORY_HOST, device, bin_edges.data(),
+                          bin_edges.size(), cdf.data()));
+    return cdf;
 }
 
 }  // namespace tsdfslam_b200

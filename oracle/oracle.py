@@ -581,3 +581,68 @@ class Pipeline:
         v = np.zeros((k.height, k.width), dtype=np.uint8)
         lib().op_last_residuals(self.p, _p(sq), _p(v))
         return sq, v
+
+
+# ------------------------------------------------------------------ evaluation (evaluation.hpp:12-50)
+def _traj(tr):
+    """(timestamps[n], poses[n,12]) or a list of (timestamp, pose12)."""
+    if isinstance(tr, tuple) and len(tr) == 2 and np.ndim(tr[1]) == 2:
+        ts, poses = tr
+    else:
+        ts = [t for t, _ in tr]
+        poses = [np.asarray(p, np.float64).reshape(12) for _, p in tr]
+    ts = _f64(np.asarray(ts, np.float64).reshape(-1))
+    poses = _f64(np.asarray(poses, np.float64).reshape(-1, 12))
+    return ts, poses
+
+
+def ate_rmse(estimated, ground_truth, max_dt=0.02):
+    """AteRmse (evaluation.cpp:26-62) -> (rmse, alignment pose12, pairs)."""
+    et, ep = _traj(estimated)
+    gt, gp = _traj(ground_truth)
+    rmse = C.c_double()
+    al = np.zeros(12)
+    n = C.c_uint64()
+    code = lib().o_ate_rmse(_p(et), _p(ep), C.c_uint64(len(et)), _p(gt), _p(gp), C.c_uint64(len(gt)),
+                            C.c_double(max_dt), C.byref(rmse), _p(al), C.byref(n))
+    if code:
+        raise OracleError(code, lib().o_last_error().decode())
+    return rmse.value, al, n.value
+
+
+def rpe_over_time(estimated, ground_truth, delta=1.0, max_dt=0.02):
+    """RpeOverTime (evaluation.cpp:64-92) -> (timestamps, translation errors)."""
+    et, ep = _traj(estimated)
+    gt, gp = _traj(ground_truth)
+    cap = max(len(et), 1)
+    ts = np.zeros(cap)
+    err = np.zeros(cap)
+    f = lib().o_rpe_over_time
+    f.restype = C.c_int64
+    n = f(_p(et), _p(ep), C.c_uint64(len(et)), _p(gt), _p(gp), C.c_uint64(len(gt)), C.c_double(delta),
+          C.c_double(max_dt), _p(ts), _p(err), C.c_uint64(cap))
+    if n < 0:
+        raise ValueError("delta must be positive")
+    return ts[:n].copy(), err[:n].copy()
+
+
+def nearest_distances(queries, reference):
+    """NearestDistances (evaluation.cpp:203-217): f32 xyz clouds -> f64 distances."""
+    q = _f32(np.asarray(queries, np.float32).reshape(-1, 3))
+    r = _f32(np.asarray(reference, np.float32).reshape(-1, 3))
+    out = np.zeros(len(q))
+    code = lib().o_nearest_distances(_p(q), C.c_uint64(len(q)), _p(r), C.c_uint64(len(r)), _p(out))
+    if code:
+        raise ValueError(lib().o_last_error().decode())
+    return out
+
+
+def distance_cdf(distances, bin_edges):
+    """DistanceCdf (evaluation.cpp:219-236)."""
+    d = _f64(np.asarray(distances, np.float64).reshape(-1))
+    e = _f64(np.asarray(bin_edges, np.float64).reshape(-1))
+    out = np.zeros(len(e))
+    code = lib().o_distance_cdf(_p(d), C.c_uint64(len(d)), _p(e), C.c_uint64(len(e)), _p(out))
+    if code:
+        raise ValueError(lib().o_last_error().decode())
+    return out

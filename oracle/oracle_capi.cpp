@@ -73,6 +73,15 @@ int Guard(F&& f) {
     }
 }
 
+}  // namespace
+
+extern "C" int o_eval_guard_set(const char* m) {  // error text for oracle_eval.cpp
+    g_err = m;
+    return 0;
+}
+
+namespace {
+
 Intrinsics ToIntr(const OIntr* k) {
     Intrinsics r;
     r.fx = k->fx; r.fy = k->fy; r.cx = k->cx; r.cy = k->cy;

@@ -73,7 +73,7 @@ class rf_frame_counters(C.Structure):
                 ("passes", C.c_int32), ("reserved0", C.c_int32), ("pixel_passes", C.c_double)]
 
 
-RF_OK, RF_INVALID_ARGUMENT, RF_TRACKING_LOST, RF_RESOURCE_LIMIT, RF_CUDA_ERROR, RF_IO_ERROR, RF_UNSUPPORTED = range(7)
+RF_OK, RF_INVALID_ARGUMENT, RF_TRACKING_LOST, RF_RESOURCE_LIMIT, RF_CUDA_ERROR, RF_IO_ERROR, RF_UNSUPPORTED, RF_FAILED = range(8)
 RF_MEMORY_HOST, RF_MEMORY_DEVICE = 0, 1
 
 # Every exported symbol of include/refusion_b200.h (checked by the CPU tests).
@@ -91,6 +91,7 @@ EXPORTS = [
     "rf_diag_lm_step", "rf_volume_extract_mesh", "rf_mesh_counts", "rf_mesh_copy", "rf_mesh_device_buffers",
     "rf_mesh_write_ply", "rf_mesh_destroy", "rf_render_virtual_depth", "rf_pipeline_window_size",
     "rf_pipeline_set_debug_images", "rf_pipeline_last_refinement", "rf_pipeline_finalize_one", "rf_diag_pass_bench", "rf_pipeline_process_frames",
+    "rf_ate_rmse", "rf_rpe_over_time", "rf_nearest_distances", "rf_distance_cdf",
 ]
 
 _lib = None

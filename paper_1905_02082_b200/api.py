@@ -470,3 +470,74 @@ class Pipeline:
         c = L.rf_frame_counters()
         L.check(_lib().rf_pipeline_last_counters(self.h, C.byref(c)))
         return {k: getattr(c, k) for k, _ in L.rf_frame_counters._fields_}
+
+
+# ------------------------------------------------------------------ evaluation (evaluation.hpp:12-50)
+def _traj(tr):
+    """(timestamps[n], poses[n,12]) (Pipeline.trajectory()) or a list of (timestamp, pose12)."""
+    if isinstance(tr, tuple) and len(tr) == 2 and np.ndim(tr[1]) == 2:
+        ts, poses = tr
+    else:
+        ts = [t for t, _ in tr]
+        poses = [np.asarray(p, np.float64).reshape(12) for _, p in tr]
+    return _f64(np.asarray(ts, np.float64).reshape(-1)), _f64(np.asarray(poses, np.float64).reshape(-1, 12))
+
+
+def ate_rmse(estimated, ground_truth, max_dt=0.02):
+    """AteRmse (evaluation.cpp:26-62) -> (rmse, alignment pose12, pairs).
+    Fewer than 3 associated pairs raise RfError (a RuntimeError)."""
+    et, ep = _traj(estimated)
+    gt, gp = _traj(ground_truth)
+    rmse, n = C.c_double(), C.c_uint64()
+    al = np.zeros(12)
+    L.check(_lib().rf_ate_rmse(_p(et), _p(ep), C.c_uint64(len(et)), _p(gt), _p(gp), C.c_uint64(len(gt)),
+                               C.c_double(max_dt), C.byref(rmse), _p(al), C.byref(n)))
+    return rmse.value, al, n.value
+
+
+def rpe_over_time(estimated, ground_truth, delta=1.0, max_dt=0.02):
+    """RpeOverTime (evaluation.cpp:64-92) -> (timestamps, translation errors)."""
+    et, ep = _traj(estimated)
+    gt, gp = _traj(ground_truth)
+    cap = max(len(et), 1)
+    ts, err, n = np.zeros(cap), np.zeros(cap), C.c_uint64()
+    L.check(_lib().rf_rpe_over_time(_p(et), _p(ep), C.c_uint64(len(et)), _p(gt), _p(gp), C.c_uint64(len(gt)),
+                                    C.c_double(delta), C.c_double(max_dt), _p(ts), _p(err), C.c_uint64(cap),
+                                    C.byref(n)))
+    return ts[:n.value].copy(), err[:n.value].copy()
+
+
+def nearest_distances(queries, reference, device=0):
+    """NearestDistances (evaluation.cpp:203-217) on the GPU. f32 xyz clouds as
+    numpy arrays (-> numpy f64) or CUDA torch tensors (-> CUDA f64 tensor)."""
+    if _is_cuda(queries) or _is_cuda(reference):
+        import torch
+        q = queries.reshape(-1, 3).to(torch.float32).contiguous()
+        r = reference.reshape(-1, 3).to(torch.float32).contiguous()
+        out = torch.empty(q.shape[0], dtype=torch.float64, device=q.device)
+        L.check(_lib().rf_nearest_distances(C.c_void_p(q.data_ptr()), C.c_uint64(q.shape[0]),
+                                            C.c_void_p(r.data_ptr()), C.c_uint64(r.shape[0]),
+                                            L.RF_MEMORY_DEVICE, q.device.index or 0, C.c_void_p(out.data_ptr())))
+        return out
+    q = np.ascontiguousarray(np.asarray(queries, np.float32).reshape(-1, 3))
+    r = np.ascontiguousarray(np.asarray(reference, np.float32).reshape(-1, 3))
+    out = np.zeros(len(q))
+    L.check(_lib().rf_nearest_distances(_p(q), C.c_uint64(len(q)), _p(r), C.c_uint64(len(r)), L.RF_MEMORY_HOST,
+                                        device, _p(out)))
+    return out
+
+
+def distance_cdf(distances, bin_edges, device=0):
+    """DistanceCdf (evaluation.cpp:219-236): cumulative percentage at or below
+    each (ascending) edge; distances numpy or a CUDA tensor."""
+    e = _f64(np.asarray(bin_edges, np.float64).reshape(-1))
+    out = np.zeros(len(e))
+    if _is_cuda(distances):
+        d = distances.reshape(-1).double().contiguous()
+        L.check(_lib().rf_distance_cdf(C.c_void_p(d.data_ptr()), C.c_uint64(d.numel()), L.RF_MEMORY_DEVICE,
+                                       d.device.index or 0, _p(e), C.c_uint64(len(e)), _p(out)))
+        return out
+    d = _f64(np.asarray(distances, np.float64).reshape(-1))
+    L.check(_lib().rf_distance_cdf(_p(d) if len(d) else None, C.c_uint64(len(d)), L.RF_MEMORY_HOST, device,
+                                   _p(e) if len(e) else None, C.c_uint64(len(e)), _p(out) if len(out) else None))
+    return out

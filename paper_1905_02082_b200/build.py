@@ -20,7 +20,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fno-fast-math", "-Xptxas", "-warn-spills"]
-SOURCES = ["rf_capi.cu", "rf_track.cu", "rf_volume.cu", "rf_raycast.cu", "rf_synth.cu", "rf_mesh.cu"]
+SOURCES = ["rf_capi.cu", "rf_track.cu", "rf_volume.cu", "rf_raycast.cu", "rf_synth.cu", "rf_mesh.cu", "rf_eval.cu"]
 
 
 def _stale(obj, deps):

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/refusion_b200.h"
+#include "rf_host.cuh"
 #include "rf_track.cuh"
 #include "rf_volume.cuh"
 
@@ -54,64 +55,11 @@ __global__ void k_import(VolumeView V, const int* coords, uint32_t n, uint32_t b
 
 using namespace rfb;
 
-namespace {
-
+namespace rfb {
 thread_local std::string g_err;
+}  // namespace rfb
 
-struct Error {
-    rf_status code;
-    std::string msg;
-};
-
-#define CK(x)                                                                                    \
-    do {                                                                                         \
-        cudaError_t e_ = (x);                                                                    \
-        if (e_ != cudaSuccess) throw Error{RF_CUDA_ERROR, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
-    } while (0)
-
-template <class F>
-rf_status guard(F&& f) {
-    try {
-        f();
-        return RF_OK;
-    } catch (const Error& e) {
-        g_err = e.msg;
-        return e.code;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return RF_CUDA_ERROR;
-    }
-}
-
-void require(bool ok, rf_status code, const std::string& msg) {
-    if (!ok) throw Error{code, msg};
-}
-
-struct DevBuf {  // owning device allocation (freed on scope exit, also on error paths)
-    void* p = nullptr;
-    size_t n = 0;
-    DevBuf() = default;
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() { release(); }
-    void ensure(size_t bytes) {
-        if (bytes <= n) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-        CK(cudaMalloc(&p, bytes));
-        n = bytes;
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    template <class T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-};
+namespace {
 
 // Per-object scratch: stream, frame images, pyramid, grid-sync state.
 struct Workspace {
