@@ -131,7 +131,7 @@ def run_ours(args):
     lib = L.load()
     cfgd = scenes.BENCH_CONFIGS[CONFIG]
     seed = replicas.sequence_seed(cfgd["seed"], R)  # independent sequence per replica
-    scene = synth.parse(scenes.bench_script(dynamic=cfgd["dynamic"], frames=cfgd["frames"], seed=seed))
+    scene = synth.parse(scenes.config_script(CONFIG, seed=seed))
     k = scene.intrinsics
     H, W, F = k.height, k.width, len(scene)
     depth = torch.empty((F, H, W), dtype=torch.float32, device="cuda")
@@ -343,8 +343,7 @@ def run_reference(args):
     from oracle import oracle as O
     from paper_1905_02082_b200 import scenes
 
-    cfgd = scenes.BENCH_CONFIGS[CONFIG]
-    scene = O.Scene(scenes.bench_script(dynamic=cfgd["dynamic"], frames=cfgd["frames"], seed=cfgd["seed"]))
+    scene = O.Scene(scenes.config_script(CONFIG))
     F = len(scene)
     cache = {}
 

@@ -30,6 +30,7 @@ struct FrameSignal {
     unsigned long long seq;
 };
 __global__ void k_signal(const TrackOut* out, const uint32_t* counters, FrameSignal* sig, unsigned long long seq) {
+    pdl_enter();
     const uint32_t* src = reinterpret_cast<const uint32_t*>(out);
     uint32_t* dst = reinterpret_cast<uint32_t*>(&sig->out);
     for (int i = threadIdx.x; i < int(sizeof(TrackOut) / 4); i += blockDim.x) dst[i] = __ldcg(src + i);
@@ -60,6 +61,36 @@ thread_local std::string g_err;
 }  // namespace rfb
 
 namespace {
+
+// Per-frame kernels launch with programmatic stream serialization (the
+// kernels call pdl_enter()); RF_PDL=0 turns it off (A/B runs).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("RF_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+template <class... P, class... A>
+void launch(void (*k)(P...), dim3 grid, dim3 block, cudaStream_t s, bool cooperative, A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    int n = 0;
+    if (pdl_enabled()) {
+        at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[n++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (cooperative) {
+        at[n].id = cudaLaunchAttributeCooperative;
+        at[n++].val.cooperative = 1;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    CK(cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...));
+}
 
 // Per-object scratch: stream, frame images, pyramid, grid-sync state.
 struct Workspace {
@@ -156,8 +187,7 @@ struct Workspace {
     // record `slot`, tagged with a new sequence number (returned).
     unsigned long long signal(const TrackOut* d_out, const uint32_t* d_counters, int slot) {
         const unsigned long long seq = ++sig_seq;
-        k_signal<<<1, 128, 0, stream>>>(d_out, d_counters, d_sig + slot, seq);
-        CK(cudaGetLastError());
+        launch(k_signal, 1, 128, stream, false, d_out, d_counters, d_sig + slot, seq);
         return seq;
     }
     // Spins until record `slot` carries `seq` (stream errors surface, never a
@@ -368,8 +398,7 @@ struct rf_volume {
         ca.do_carve = carve;
         ca.do_integrate = integrate;
         ca.carve_only_before = carve_only_before;
-        k_cull<<<4 * 148, 256, 0, ws.stream>>>(ca);
-        CK(cudaGetLastError());
+        launch(k_cull, 4 * 148, 256, ws.stream, false, ca);
         if (prof) CK(cudaEventRecord(prof[3], ws.stream));
         FuseArgs fa{};
         fa.V = view;
@@ -380,8 +409,7 @@ struct rf_volume {
         fa.pose = pose;
         fa.lost = lost;
         fa.list = ca.list;
-        k_fuse<<<4 * 148, kBrickVoxels, 0, ws.stream>>>(fa);
-        CK(cudaGetLastError());
+        launch(k_fuse, 4 * 148, kBrickVoxels, ws.stream, false, fa);
     }
     void allocate(const float* d, const uint8_t* mask, const rf_intrinsics& k, const double* pose, const int* lost) {
         AllocArgs aa{};
@@ -392,8 +420,7 @@ struct rf_volume {
         aa.pose = pose;
         aa.lost = lost;
         const int n = k.width * k.height;
-        k_alloc<<<(n + 255) / 256, 256, 0, ws.stream>>>(aa);
-        CK(cudaGetLastError());
+        launch(k_alloc, (n + 255) / 256, 256, ws.stream, false, aa);
     }
     TrackArgs track_args(const rf_frame* f, const float* d, const uint8_t* rgb, int levels) {
         TrackArgs a{};
@@ -435,8 +462,7 @@ struct rf_volume {
         if (a.trace) CK(cudaMemsetAsync(a.trace, 0, kTracePasses * 8 * sizeof(unsigned long long), ws.stream));
         a.grid.parity = ws.parity;
         ws.parity ^= 1;
-        void* args[] = {&a};
-        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
+        launch(k_track, ws.track_grid, kTrackThreads, ws.stream, true, a);
     }
     TrackOut fetch_out() {
         CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));

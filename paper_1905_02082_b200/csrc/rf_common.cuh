@@ -11,6 +11,15 @@
 
 namespace rfb {
 
+// Programmatic dependent launch (per-frame kernels): each kernel lets its
+// stream successor launch as soon as all of its own CTAs are resident, and
+// waits for its predecessor's completion (and memory flush) before touching
+// any data. Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- constants
 constexpr int kSide = 8;                      // voxels per brick edge (VolumeConfig::block_side)
 constexpr int kBrickVoxels = kSide * kSide * kSide;

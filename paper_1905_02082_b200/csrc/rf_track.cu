@@ -918,6 +918,7 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
 }
 
 __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackArgs a) {
+    pdl_enter();
     __shared__ RegState st;
     __shared__ double scratch[(kTrackThreads / 32) * 32];
     __shared__ double blk[kAccN + 2];

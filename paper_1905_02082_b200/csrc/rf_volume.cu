@@ -69,6 +69,7 @@ __device__ __forceinline__ unsigned walk_pixel(const VolumeView& V, const float*
 }
 
 __global__ void k_alloc(AllocArgs a) {
+    pdl_enter();
     if (a.lost && *a.lost) return;
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned visits = 0;
@@ -144,6 +145,7 @@ __device__ __forceinline__ bool outside(const double cc[8][3], const Intr& K, do
 }
 
 __global__ void k_cull(CullArgs a) {
+    pdl_enter();
     if (a.lost && *a.lost) return;
     const uint32_t nb = min(a.V.counters[kNumBlocks], a.V.max_blocks);
     const uint32_t before = a.carve_only_before ? min(a.V.counters[kBlocksBefore], nb) : nb;
@@ -236,6 +238,7 @@ __device__ __forceinline__ uint32_t colour_avg(uint32_t c, uint32_t w, uint32_t 
 }
 
 __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
+    pdl_enter();
     commit_links(a.V);  // k_cull (previous launch) linked this frame's new bricks
     if (a.lost && *a.lost) return;
     __shared__ Pose W;

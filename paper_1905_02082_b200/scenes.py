@@ -106,6 +106,18 @@ def pipeline_static_scene(frames=7):
 
 
 BENCH_CONFIGS = {
+    # RoomScript(false) at 640x480 with the default K, its path extended to 50 frames
     "C1": dict(dynamic=False, frames=50, seed=42),
+    # the acceptance room + 2 crossing boxes on a closed 200-frame orbit
     "C2": dict(dynamic=True, frames=200, seed=43),
 }
+
+
+def config_script(name: str, seed: int | None = None) -> str:
+    """Scene script of BASELINE.json workload `name` (C1 or C2); `seed`
+    overrides the noise seed (independent replicas)."""
+    c = BENCH_CONFIGS[name]
+    s = c["seed"] if seed is None else seed
+    if name == "C1":
+        return room_script(False, 640, 480, frames=c["frames"], seed=s)
+    return bench_script(dynamic=c["dynamic"], frames=c["frames"], seed=s)
