@@ -1291,6 +1291,14 @@ struct rf_pipeline {
     double stage_ms[4] = {};
     rf_frame_counters prof_sums{};
     uint64_t prof_frames = 0, launches = 0;
+    // Batched host frames (rf_pipeline_process_frames): uploads run on their
+    // own stream into a ring of staging buffers, kUpSlots - 1 frames ahead of
+    // the compute stream, so the H2D copies overlap the previous frames' kernels.
+    static constexpr int kUpSlots = 3;
+    cudaStream_t up_stream = nullptr;
+    cudaEvent_t up_done[kUpSlots] = {}, use_done[kUpSlots] = {};
+    bool up_used[kUpSlots] = {};
+    DevBuf up_depth[kUpSlots], up_rgb[kUpSlots];
 };
 
 namespace {
@@ -1433,8 +1441,14 @@ rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipel
 
 void rf_pipeline_destroy(rf_pipeline* p) {
     if (!p) return;
+    cudaSetDevice(p->vol->device);
     for (cudaEvent_t& e : p->ev)
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < rf_pipeline::kUpSlots; ++i) {
+        if (p->up_done[i]) cudaEventDestroy(p->up_done[i]);
+        if (p->use_done[i]) cudaEventDestroy(p->use_done[i]);
+    }
+    if (p->up_stream) cudaStreamDestroy(p->up_stream);
     if (p->temp) rf_volume_destroy(p->temp);
     if (p->scratch) rf_volume_destroy(p->scratch);
     for (DevBuf* b : {&p->win, &p->win_pose, &p->virt, &p->refined}) b->release();
@@ -1636,6 +1650,33 @@ unsigned long long enqueue_frame(rf_pipeline* p, const rf_frame* f, int slot, bo
     return ws.signal(ws.out.as<TrackOut>(), v->view.counters, slot);
 }
 
+// Copies a host frame into upload slot u on the upload stream (after the
+// frame that last used the slot is done with it) and makes the compute stream
+// wait for the copy; returns the frame pointing at the device copy.
+rf_frame stage_upload(rf_pipeline* p, const rf_frame* f, int u) {
+    Workspace& ws = p->vol->ws;
+    if (!p->up_stream) {
+        CK(cudaStreamCreateWithFlags(&p->up_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < rf_pipeline::kUpSlots; ++i) {
+            CK(cudaEventCreateWithFlags(&p->up_done[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&p->use_done[i], cudaEventDisableTiming));
+        }
+    }
+    const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
+    p->up_depth[u].ensure(n * 4);
+    p->up_rgb[u].ensure(n * 3);
+    if (p->up_used[u]) CK(cudaStreamWaitEvent(p->up_stream, p->use_done[u], 0));
+    CK(cudaMemcpyAsync(p->up_depth[u].p, f->depth, n * 4, cudaMemcpyHostToDevice, p->up_stream));
+    CK(cudaMemcpyAsync(p->up_rgb[u].p, f->rgb, n * 3, cudaMemcpyHostToDevice, p->up_stream));
+    CK(cudaEventRecord(p->up_done[u], p->up_stream));
+    CK(cudaStreamWaitEvent(ws.stream, p->up_done[u], 0));
+    rf_frame d = *f;
+    d.depth = p->up_depth[u].as<float>();
+    d.rgb = p->up_rgb[u].as<uint8_t>();
+    d.memory = RF_MEMORY_DEVICE;
+    return d;
+}
+
 // Host half: FrameStats, trajectory and counters from the frame's record
 // (already read into h_out / h_counters).
 void finish_frame(rf_pipeline* p, const rf_frame* f, bool first, rf_frame_stats* stats, double pose_out[12]) {
@@ -1696,7 +1737,18 @@ rf_status rf_pipeline_process_frames(rf_pipeline* p, const rf_frame* frames, uin
             const uint64_t m = std::min<uint64_t>(Workspace::kSigSlots, n - c0);
             const bool first0 = p->first;
             unsigned long long last_seq = 0;
-            for (uint64_t j = 0; j < m; ++j) last_seq = enqueue_frame(p, &frames[c0 + j], int(j), first0 && j == 0);
+            for (uint64_t j = 0; j < m; ++j) {
+                const rf_frame* f = &frames[c0 + j];
+                if (f->memory != RF_MEMORY_DEVICE) {
+                    const int u = int((c0 + j) % rf_pipeline::kUpSlots);
+                    const rf_frame staged = stage_upload(p, f, u);
+                    last_seq = enqueue_frame(p, &staged, int(j), first0 && j == 0);
+                    CK(cudaEventRecord(p->use_done[u], ws.stream));  // the frame's kernels are done with slot u
+                    p->up_used[u] = true;
+                } else {
+                    last_seq = enqueue_frame(p, f, int(j), first0 && j == 0);
+                }
+            }
             ws.wait_signal(int(m - 1), last_seq);  // stream order: every earlier record is complete too
             for (uint64_t j = 0; j < m; ++j) {
                 const auto t0 = std::chrono::steady_clock::now();
