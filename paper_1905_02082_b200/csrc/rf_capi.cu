@@ -72,10 +72,11 @@ bool pdl_enabled() {
     return on;
 }
 template <class... P, class... A>
-void launch(void (*k)(P...), dim3 grid, dim3 block, cudaStream_t s, bool cooperative, A&&... args) {
+void launch(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool cooperative, A&&... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     int n = 0;
@@ -123,9 +124,10 @@ struct Workspace {
             const char* e = std::getenv("RF_TRACK_CARVEOUT");
             return e ? std::atoi(e) : int(cudaSharedmemCarveoutMaxL1);
         }();
+        CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTrackDynSmem)));
         if (carveout >= 0)
             CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributePreferredSharedMemoryCarveout, carveout));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_track, kTrackThreads, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_track, kTrackThreads, kTrackDynSmem));
         require(per > 0, RF_CUDA_ERROR, "tracking kernel does not fit on an SM");
         track_grid = sms * per;
         gsync.ensure(sizeof(GridSync));
@@ -187,7 +189,7 @@ struct Workspace {
     // record `slot`, tagged with a new sequence number (returned).
     unsigned long long signal(const TrackOut* d_out, const uint32_t* d_counters, int slot) {
         const unsigned long long seq = ++sig_seq;
-        launch(k_signal, 1, 128, stream, false, d_out, d_counters, d_sig + slot, seq);
+        launch(k_signal, 1, 128, 0, stream, false, d_out, d_counters, d_sig + slot, seq);
         return seq;
     }
     // Spins until record `slot` carries `seq` (stream errors surface, never a
@@ -398,7 +400,7 @@ struct rf_volume {
         ca.do_carve = carve;
         ca.do_integrate = integrate;
         ca.carve_only_before = carve_only_before;
-        launch(k_cull, 4 * 148, 256, ws.stream, false, ca);
+        launch(k_cull, 4 * 148, 256, 0, ws.stream, false, ca);
         if (prof) CK(cudaEventRecord(prof[3], ws.stream));
         FuseArgs fa{};
         fa.V = view;
@@ -409,7 +411,7 @@ struct rf_volume {
         fa.pose = pose;
         fa.lost = lost;
         fa.list = ca.list;
-        launch(k_fuse, 4 * 148, kBrickVoxels, ws.stream, false, fa);
+        launch(k_fuse, 4 * 148, kBrickVoxels, 0, ws.stream, false, fa);
     }
     void allocate(const float* d, const uint8_t* mask, const rf_intrinsics& k, const double* pose, const int* lost) {
         AllocArgs aa{};
@@ -420,7 +422,7 @@ struct rf_volume {
         aa.pose = pose;
         aa.lost = lost;
         const int n = k.width * k.height;
-        launch(k_alloc, (n + 255) / 256, 256, ws.stream, false, aa);
+        launch(k_alloc, (n + 255) / 256, 256, 0, ws.stream, false, aa);
     }
     TrackArgs track_args(const rf_frame* f, const float* d, const uint8_t* rgb, int levels) {
         TrackArgs a{};
@@ -462,7 +464,7 @@ struct rf_volume {
         if (a.trace) CK(cudaMemsetAsync(a.trace, 0, kTracePasses * 8 * sizeof(unsigned long long), ws.stream));
         a.grid.parity = ws.parity;
         ws.parity ^= 1;
-        launch(k_track, ws.track_grid, kTrackThreads, ws.stream, true, a);
+        launch(k_track, ws.track_grid, kTrackThreads, kTrackDynSmem, ws.stream, true, a);
     }
     TrackOut fetch_out() {
         CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
@@ -1017,7 +1019,8 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
         ws.parity ^= 1;
         a.out = ws.out.as<TrackOut>();
         void* args[] = {&a};
-        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, 0, ws.stream));
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, kTrackDynSmem,
+                                       ws.stream));
         CK(cudaMemcpyAsync(out, ws.mask_in.p, n, cudaMemcpyDeviceToHost, ws.stream));
         CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
         ws.sync();

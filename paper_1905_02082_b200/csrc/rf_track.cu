@@ -21,12 +21,12 @@ constexpr double kRelDecreaseTol = 1e-6;         // registration.cpp:26
 __device__ __forceinline__ int hidx(int i, int j) { return i * 6 - (i * (i - 1)) / 2 + (j - i); }
 
 __shared__ int s_trace_pass;  // per-CTA pass counter for the optional timeline
-// Per-thread copy of the first kPxCache pixels' inputs {depth (0: skip), intensity}
-// for the Jacobian passes: a thread sees the same pixels in every pass at a
-// level, so after the first pass they come from shared memory instead of an
-// L2 round trip (the coarse levels are one or two pixels per thread).
-constexpr int kPxCache = 2;
-__shared__ float2 s_pxc[kPxCache * kTrackThreads];
+// Per-thread copy of the first kTrackPxCache pixels' inputs {depth (0: skip),
+// intensity} for the Jacobian passes: a thread sees the same pixels in every
+// pass at a level, so after the first pass they come from shared memory
+// instead of an L2 round trip (dynamic shared memory, kTrackDynSmem).
+extern __shared__ __align__(16) unsigned char s_dyn[];
+__device__ __forceinline__ float2* pxc_base() { return reinterpret_cast<float2*>(s_dyn); }
 __shared__ int s_pxc_tag;  // (level + 1) | 16 * use_mask of the cached inputs, 0: none
 __shared__ int s_passes;   // Accumulate passes run (CTA 0; TrackOut.passes / pixel_passes)
 __shared__ double s_pixel_passes;
@@ -242,8 +242,8 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
         float d;
         bool masked;
         float inten = 0.f;  // ToIntensity (image.hpp:85-91) at level 0, the pyramid's f32 above
-        if (pxc_hit && it < kPxCache) {
-            const float2 c = s_pxc[it * kTrackThreads + threadIdx.x];
+        if (pxc_hit && it < kTrackPxCache) {
+            const float2 c = pxc_base()[it * kTrackThreads + threadIdx.x];
             d = c.x;
             inten = c.y;
             masked = false;  // a masked pixel was cached with depth 0
@@ -258,7 +258,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
                     inten = __ldcg(F.inten[level] + p);
                 }
             }
-            if (kJac && it < kPxCache) s_pxc[it * kTrackThreads + threadIdx.x] = make_float2(masked ? 0.f : d, inten);
+            if (kJac && it < kTrackPxCache) pxc_base()[it * kTrackThreads + threadIdx.x] = make_float2(masked ? 0.f : d, inten);
         }
         float rs = 0.f;
         uint8_t rv = 0;

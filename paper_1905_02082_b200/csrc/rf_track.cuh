@@ -16,6 +16,14 @@ constexpr int kMaxLevels = 6;
 constexpr int kTrackThreads = RF_TRACK_THREADS;
 constexpr int kTrackMinBlocks = RF_TRACK_MIN_BLOCKS;
 constexpr int kTileW = 16, kTileH = kTrackThreads / kTileW;  // pixel tile per CTA step, 1 px per thread
+// Per-thread cache of the Jacobian passes' pixel inputs {depth, intensity},
+// one entry per tile step (a thread meets the same pixels in every pass of a
+// level), in dynamic shared memory: 8 steps cover 640x480 (<= 6 steps per CTA).
+#ifndef RF_TRACK_PXC
+#define RF_TRACK_PXC 8
+#endif
+constexpr int kTrackPxCache = RF_TRACK_PXC;
+constexpr size_t kTrackDynSmem = size_t(kTrackPxCache) * kTrackThreads * 8;
 
 struct RegParams {  // RegistrationConfig, registration.hpp:13-23
     double color_weight;
