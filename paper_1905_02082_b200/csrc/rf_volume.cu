@@ -513,7 +513,10 @@ __global__ void k_cull_window(WindowArgs a) {
 // Integrate (tsdf_volume.cpp:155-202) of the chunk's entries, in order, into
 // each listed brick: the voxel is read once, updated by every entry whose bit
 // is set, and written once.
-__global__ void __launch_bounds__(kBrickVoxels) k_fuse_window(WindowArgs a) {
+#ifndef RF_WIN_MINB
+#define RF_WIN_MINB 2
+#endif
+__global__ void __launch_bounds__(kBrickVoxels, RF_WIN_MINB) k_fuse_window(WindowArgs a) {
     commit_links(a.V);
     __shared__ Pose Ws[kMaxWin];
     __shared__ double s_rcp[512];  // RN(1 / i) for the running averages (see div_f32)
@@ -539,33 +542,64 @@ __global__ void __launch_bounds__(kBrickVoxels) k_fuse_window(WindowArgs a) {
         const double cx = (double(c.x * kSide + x) + 0.5) * s;  // VoxelCenter, tsdf_volume.hpp:117-119
         const double cy = (double(c.y * kSide + y) + 0.5) * s;
         const double cz = (double(c.z * kSide + z) + 0.5) * s;
-        for (uint32_t m = bits; m; m &= m - 1u) {
-            const int j = __ffs(m) - 1;
-            const Intr& K = a.K[j];
-            double pc[3];
-            pose_apply(Ws[j], cx, cy, cz, pc);
-            if (pc[2] <= 1e-9) continue;
-            const double rz = fuse_rcp(pc[2]);
-            const long pu = project_lround(K.fx * pc[0], pc[2], rz, K.cx);
-            const long pv = project_lround(K.fy * pc[1], pc[2], rz, K.cy);
-            if (!(pu >= 0 && pu < K.w && pv >= 0 && pv < K.h)) continue;
-            const int pix = int(pv) * K.w + int(pu);
-            const float d = __ldg(a.depth[j] + pix);
-            if (a.mask[j] && __ldg(a.mask[j] + pix)) continue;
-            if (!(depth_valid(d) && !(d < a.V.min_depth) && !(d > a.V.max_depth))) continue;
-            const double dist = double(d) - pc[2];
-            if (dist <= -tau) continue;
-            const double clamped = fmin(dist, tau);
-            const double w = double(wgt);
-            sdf = div_f32(double(sdf) * w + clamped, w + 1.0, s_rcp[wgt + 1u]);
-            if (fabs(dist) <= tau && a.rgb[j]) {
-                const uint8_t* col = a.rgb[j] + 3 * size_t(pix);
-                r = colour_avg(r, wgt, __ldg(col));
-                g = colour_avg(g, wgt, __ldg(col + 1));
-                bl = colour_avg(bl, wgt, __ldg(col + 2));
+        // Entries in groups of kGroup: the frame reads of a group (projection
+        // only depends on the entry's pose) are all issued before the first
+        // update, then the updates run in window order.
+#ifndef RF_WIN_GROUP
+#define RF_WIN_GROUP 4
+#endif
+        constexpr int kGroup = RF_WIN_GROUP;
+        for (uint32_t m = bits; m;) {
+            int jj[kGroup];
+            float dd[kGroup];
+            double zz[kGroup];
+            uint32_t col[kGroup];
+#pragma unroll
+            for (int k = 0; k < kGroup; ++k) {
+                jj[k] = -1;
+                dd[k] = 0.f;
+                zz[k] = 0.0;
+                col[k] = 0u;
+                if (!m) continue;
+                const int j = __ffs(m) - 1;
+                m &= m - 1u;
+                const Intr& K = a.K[j];
+                double pc[3];
+                pose_apply(Ws[j], cx, cy, cz, pc);
+                if (pc[2] <= 1e-9) continue;
+                const double rz = fuse_rcp(pc[2]);
+                const long pu = project_lround(K.fx * pc[0], pc[2], rz, K.cx);
+                const long pv = project_lround(K.fy * pc[1], pc[2], rz, K.cy);
+                if (!(pu >= 0 && pu < K.w && pv >= 0 && pv < K.h)) continue;
+                const int pix = int(pv) * K.w + int(pu);
+                if (a.mask[j] && __ldg(a.mask[j] + pix)) continue;
+                jj[k] = j;
+                zz[k] = pc[2];
+                dd[k] = __ldg(a.depth[j] + pix);
+                if (a.rgb[j]) {
+                    const uint8_t* cp = a.rgb[j] + 3 * size_t(pix);
+                    col[k] = uint32_t(__ldg(cp)) | (uint32_t(__ldg(cp + 1)) << 8) | (uint32_t(__ldg(cp + 2)) << 16) |
+                             0x1000000u;  // bit 24: the entry has colour
+                }
             }
-            wgt = min(wgt + 1u, uint32_t(mw));
-            dirty = true;
+#pragma unroll
+            for (int k = 0; k < kGroup; ++k) {
+                if (jj[k] < 0) continue;
+                const float d = dd[k];
+                if (!(depth_valid(d) && !(d < a.V.min_depth) && !(d > a.V.max_depth))) continue;
+                const double dist = double(d) - zz[k];
+                if (dist <= -tau) continue;
+                const double clamped = fmin(dist, tau);
+                const double w = double(wgt);
+                sdf = div_f32(double(sdf) * w + clamped, w + 1.0, s_rcp[wgt + 1u]);
+                if (fabs(dist) <= tau && (col[k] >> 24)) {
+                    r = colour_avg(r, wgt, col[k] & 0xFFu);
+                    g = colour_avg(g, wgt, (col[k] >> 8) & 0xFFu);
+                    bl = colour_avg(bl, wgt, (col[k] >> 16) & 0xFFu);
+                }
+                wgt = min(wgt + 1u, uint32_t(mw));
+                dirty = true;
+            }
         }
         if (dirty) {
             raw.x = __float_as_uint(sdf);
