@@ -380,8 +380,13 @@ def test_pipeline_acceptance_room(mover):
     worst = max(max(pose_error(po, pg)) for _, po, _, pg in out)
     assert worst <= 1e-4
     gt = [s.camera(i)[1] for i in range(len(s))]
-    assert H.ate_rmse([pg for *_, pg in out], gt) < 0.01 * (2 if mover else 1)
+    bound = 0.01 * (2 if mover else 1)
+    assert H.ate_rmse([pg for *_, pg in out], gt) < bound
     assert gp.tracking_losses() == 0
+    # the same criterion through the product's AteRmse (timestamp association, evaluation.cpp:26-62)
+    rmse, _, pairs = G.ate_rmse(gp.trajectory(), [s.camera(i) for i in range(len(s))])
+    assert pairs == len(s) == 30 and rmse < bound
+    assert abs(rmse - H.ate_rmse([pg for *_, pg in out], gt)) < 1e-9
 
 
 def test_pipeline_lockstep_volume_bitexact():
