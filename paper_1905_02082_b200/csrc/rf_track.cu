@@ -28,6 +28,9 @@ __shared__ int s_trace_pass;  // per-CTA pass counter for the optional timeline
 extern __shared__ __align__(16) unsigned char s_dyn[];
 __device__ __forceinline__ float2* pxc_base() { return reinterpret_cast<float2*>(s_dyn); }
 __shared__ int s_pxc_tag;  // (level + 1) | 16 * use_mask of the cached inputs, 0: none
+#ifdef RF_LM_PROFILE
+__shared__ long long s_lmp[5];  // [1..4]: steps, judge->solve-done, solve, expmap+compose (cycle sums)
+#endif
 __shared__ int s_passes;   // Accumulate passes run (CTA 0; TrackOut.passes / pixel_passes)
 __shared__ double s_pixel_passes;
 __shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (see voxel_luma_lut)
@@ -35,10 +38,13 @@ __shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (se
 struct RegState {
     Pose pose, cand;
     double lambda, dnorm;
-    double delta[6];
     double buf[2][kAccN];  // normal equations at the current pose / at the candidate
-    double* cur;           // -> buf[.], swapped on an accepted step (no copy)
-    double* trial;
+    int ci;                // buf[ci]: current, buf[ci ^ 1]: trial; swapped on an accepted step (no copy)
+    __device__ double* cur() { return buf[ci]; }
+    __device__ double* trial() { return buf[ci ^ 1]; }
+    // judge inputs that do not depend on the trial, computed while the pass runs
+    double cur_err, tol, lam_acc, lam_rej;
+    int small_step;
     int total, converged, lost, go, brk, level_it;
 };
 
@@ -360,15 +366,14 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
         st.total = 0;
         st.converged = 0;
         st.lost = 0;
-        st.cur = st.buf[0];
-        st.trial = st.buf[1];
+        st.ci = 0;
     }
     __syncthreads();
     for (int l = R.levels - 1; l >= 0; --l) {
         const long long mv = (long long)(max(R.min_valid, 1)) >> (2 * l);
         const double min_valid = double(mv > 16 ? mv : 16);
-        pass<true>(a, l, st.pose, use_mask, false, cw, scratch, blk, st.cur);
-        if (st.cur[29] < min_valid) {
+        pass<true>(a, l, st.pose, use_mask, false, cw, scratch, blk, st.cur());
+        if (st.cur()[29] < min_valid) {
             if (threadIdx.x == 0) st.lost = 1;
             __syncthreads();
             return;
@@ -381,63 +386,101 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
             st.level_it = 0;
         }
         // One barrier per LM iteration: thread 0 judges the last trial and
-        // solves for the next candidate in one go (registration.cpp:233-272).
+        // solves for the next candidate in one straight-line section on
+        // local copies of its state (registration.cpp:233-272).
+        bool judge = false;  // a trial was evaluated since the last solve
         for (;;) {
             if (threadIdx.x == 0) {
-                st.go = 0;
-                while (!st.brk && st.level_it < R.max_iterations) {
-                    ++st.level_it;
-                    ++st.total;
-                    if (!lm_solve(st.cur, st.lambda, st.delta)) {
-                        st.lambda = fmin(st.lambda * R.lambda_up, 1e12);  // NumericalIssue: damp more, retry
+#ifdef RF_LM_PROFILE
+                const long long cj = clock64();
+#endif
+                double lambda = st.lambda;
+                int brk = st.brk, level_it = st.level_it, total = st.total, converged = st.converged, ci = st.ci;
+                const double* tr = st.buf[ci ^ 1];
+                if (judge) {
+                    const double cur_err = st.cur_err;
+                    const double trial_err = tr[27] + cw * tr[28];
+                    if (tr[29] >= min_valid && trial_err < cur_err) {
+                        const double decrease = cur_err - trial_err;
+                        st.pose = st.cand;
+                        ci ^= 1;
+                        lambda = st.lam_acc;
+                        if (st.small_step || decrease < st.tol) {
+                            converged = 1;
+                            brk = 1;
+                        }
+                    } else {
+                        lambda = st.lam_rej;
+                        if (lambda >= 1e12) {
+                            converged = 1;
+                            brk = 1;
+                        }
+                    }
+                }
+#ifdef RF_LM_PROFILE
+                long long c0 = clock64(), c1 = c0;
+#endif
+                int go = 0;
+                while (!brk && level_it < R.max_iterations) {
+                    ++level_it;
+                    ++total;
+                    const Pose P0 = st.pose;
+                    double delta[6];  // in registers: ExpMap and the norm read it straight from the solve
+                    const bool solved = lm_solve(st.buf[ci], lambda, delta);
+#ifdef RF_LM_PROFILE
+                    c1 = clock64();
+#endif
+                    if (!solved) {
+                        lambda = fmin(lambda * R.lambda_up, 1e12);  // NumericalIssue: damp more, retry
                         continue;
                     }
-                    double delta[6];
-#pragma unroll
-                    for (int i = 0; i < 6; ++i) delta[i] = st.delta[i];
                     Pose e;
                     expmap(delta, e);
-                    st.cand = pose_mul(e, st.pose);
+                    st.cand = pose_mul(e, P0);
                     double dn = 0.0;
 #pragma unroll
                     for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
-                    st.dnorm = dn;  // squared; the sqrt is taken at the accept test, off this critical path
-                    st.go = 1;
+                    st.dnorm = dn;  // squared; the sqrt is taken off the critical path below
+                    go = 1;
                     break;
                 }
+                st.lambda = lambda;
+                st.brk = brk;
+                st.level_it = level_it;
+                st.total = total;
+                st.converged = converged;
+                st.ci = ci;
+                st.go = go;
+#ifdef RF_LM_PROFILE
+                {
+                    const long long c2 = clock64();
+                    if (judge) {
+                        s_lmp[1] += 1;
+                        s_lmp[2] += c2 - cj;
+                        s_lmp[3] += c1 - c0;
+                        s_lmp[4] += c2 - c1;
+                    }
+                }
+#endif
                 if (a.trace && blockIdx.x == 0 && s_trace_pass < kTracePasses)
                     a.trace[8 * s_trace_pass + 7] = global_ns();  // solve done (next pass's record)
             }
             __syncthreads();
             if (!st.go) break;
-            pass<true>(a, l, st.cand, use_mask, false, cw, scratch, blk, st.trial);
-            if (threadIdx.x == 0) {
-                const double cur_err = st.cur[27] + cw * st.cur[28];
-                const double trial_err = st.trial[27] + cw * st.trial[28];
-                if (st.trial[29] >= min_valid && trial_err < cur_err) {
-                    const double decrease = cur_err - trial_err;
-                    st.pose = st.cand;
-                    double* t = st.cur;
-                    st.cur = st.trial;
-                    st.trial = t;
-                    st.lambda = fmax(st.lambda / R.lambda_down, 1e-12);
-                    if (sqrt(st.dnorm) < R.eps || decrease < kRelDecreaseTol * cur_err) {
-                        st.converged = 1;
-                        st.brk = 1;
-                    }
-                } else {
-                    st.lambda = fmin(st.lambda * R.lambda_up, 1e12);
-                    if (st.lambda >= 1e12) {
-                        st.converged = 1;
-                        st.brk = 1;
-                    }
-                }
+            if (threadIdx.x == 0) {  // everything of the judge but the trial's error, off the critical path
+                st.cur_err = st.cur()[27] + cw * st.cur()[28];
+                st.tol = kRelDecreaseTol * st.cur_err;
+                st.lam_acc = fmax(st.lambda / R.lambda_down, 1e-12);
+                st.lam_rej = fmin(st.lambda * R.lambda_up, 1e12);
+                st.small_step = sqrt(st.dnorm) < R.eps;
             }
+            pass<true>(a, l, st.cand, use_mask, false, cw, scratch, blk, st.trial());
+            judge = true;
         }
         __syncthreads();
     }
     // Full-resolution residual image at the final pose, mask ignored (:282-284).
-    pass<false>(a, 0, st.pose, false, true, 0.0, scratch, blk, st.trial);
+    pass<false>(a, 0, st.pose, false, true, 0.0, scratch, blk, st.trial());
 }
 
 // ------------------------------------------------------------------ mask
@@ -865,9 +908,9 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
             a.out->converged = st.converged;
             a.out->iterations = st.total;
             a.out->registrations = 1;
-            a.out->valid = (unsigned long long)st.cur[29];
-            a.out->final_error = st.cur[27] + a.reg.color_weight * st.cur[28];
-            for (int i = 0; i < kAccN; ++i) a.out->acc[i] = st.cur[i];
+            a.out->valid = (unsigned long long)st.cur()[29];
+            a.out->final_error = st.cur()[27] + a.reg.color_weight * st.cur()[28];
+            for (int i = 0; i < kAccN; ++i) a.out->acc[i] = st.cur()[i];
         }
         write_out(a, st);
         return;
@@ -901,8 +944,8 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
         o->masked = (unsigned long long)masked;
         o->rounds = rounds;
         o->converged = st.lost ? 0 : st.converged;
-        o->valid = st.lost ? 0ull : (unsigned long long)st.cur[29];
-        o->final_error = st.lost ? 0.0 : st.cur[27] + a.reg.color_weight * st.cur[28];
+        o->valid = st.lost ? 0ull : (unsigned long long)st.cur()[29];
+        o->final_error = st.lost ? 0.0 : st.cur()[27] + a.reg.color_weight * st.cur()[28];
         if (!st.lost) {  // hold the previous pose on loss (pipeline.cpp:117-122)
             for (int i = 0; i < 9; ++i) a.pose_state[i] = st.pose.R[i];
             for (int i = 0; i < 3; ++i) a.pose_state[9 + i] = st.pose.t[i];
@@ -931,6 +974,9 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
     if (threadIdx.x == 0) {
         s_trace_pass = 0;
         s_pxc_tag = 0;
+#ifdef RF_LM_PROFILE
+        for (int i = 0; i < 5; ++i) s_lmp[i] = 0;
+#endif
     }
     for (int i = threadIdx.x; i < 768; i += blockDim.x) {
         const double w = i < 256 ? 0.2126 : (i < 512 ? 0.7152 : 0.0722);  // image.hpp:80-83
@@ -942,6 +988,10 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
         a.out->passes = s_passes;
         a.out->pixel_passes = s_pixel_passes;
     }
+#ifdef RF_LM_PROFILE
+    if (lead && a.trace)  // diagnostic variant: record 251 = {steps, judge..solved, solve, expmap+compose} cycles
+        for (int i = 0; i < 4; ++i) a.trace[8 * 251 + i] = (unsigned long long)s_lmp[i + 1];
+#endif
 }
 
 }  // namespace rfb
