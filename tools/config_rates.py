@@ -47,6 +47,8 @@ def rate(name, script, vcfg=None, frames=200, warm=10, mesh=False):
     line = f"{name}: {1000.0 / ms:.1f} frames/s ({ms:.3f} ms/frame, {k.width}x{k.height}, " \
            f"{p.volume().num_blocks()} bricks, {p.tracking_losses()} losses)"
     if mesh:
+        p.volume().extract_mesh(2)  # first call loads the mesh kernels' modules (lazy loading)
+        torch.cuda.synchronize()
         e0.record(stream)
         v, _, fc = p.volume().extract_mesh(2)
         e1.record(stream)
