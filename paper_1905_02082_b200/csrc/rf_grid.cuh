@@ -89,6 +89,62 @@ __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned 
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Warp 0: arrive on the barrier's counter (after the CTA's partial stores,
+// which warp 0 has observed through a CTA or warp barrier) and poll until
+// every CTA has arrived. Returns the barrier index this call completed.
+__device__ __forceinline__ void grid_arrive_wait(const GridCtx& g, unsigned int bar) {
+    const int G = gridDim.x;
+    // CTAs arrive on kArriveLanes counters (blockIdx % lanes) so the
+    // arrival atomics spread over separate L2 lines; lanes 0..7 of warp 0
+    // each poll one counter.
+    const int lane = threadIdx.x;
+    if (lane == 0)  // release is cumulative: covers the CTA's partial stores ordered by the barrier
+        red_release_add(grid_counter(g, g.parity, blockIdx.x % kArriveLanes), 1ull);
+    const int l = lane % kArriveLanes;
+    const unsigned long long per = (unsigned long long)(G / kArriveLanes + (l < G % kArriveLanes ? 1 : 0));
+    const unsigned long long target = (unsigned long long)(bar + 1u) * per;
+    const unsigned long long* cnt = grid_counter(g, g.parity, l);
+    // Relaxed polling, then one acquire. Bounded: a co-residency bug must
+    // fail loudly, never hang the GPU.
+    unsigned long long spins = 0;
+    while (!__all_sync(0xffffffffu, ld_relaxed_u64(cnt) >= target)) {
+        if (++spins > (1ull << 26)) __trap();
+    }
+    (void)ld_acquire_u64(cnt);
+    if (lane == 0) s_grid_bar = bar + 1u;
+}
+
+// All threads, after grid_arrive_wait: `out` (smem) = the sum of every CTA's
+// partial, folded in CTA index order.
+template <int NV>
+__device__ __forceinline__ void grid_fold(const double* buf, double* out) {
+    const int G = gridDim.x;
+    __shared__ double red[32][32];
+    const int j = threadIdx.x & 31, c = threadIdx.x >> 5, nchunk = blockDim.x >> 5;
+    double s = 0.0;
+    if (j < NV) {
+        // chunk c folds CTA rows c, c+nchunk, ... in order; all of the
+        // chunk's loads are issued before the first add (one L2 latency).
+        constexpr int kRows = 24;
+        double v[kRows];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+            const int i = c + r * nchunk;
+            v[r] = i < G ? __ldcg(buf + i * kRedStride + j) : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) s += v[r];
+        for (int i = c + kRows * nchunk; i < G; i += nchunk) s += __ldcg(buf + i * kRedStride + j);
+    }
+    red[c][j] = s;
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double t = 0.0;
+        for (int cc = 0; cc < nchunk; ++cc) t += red[cc][threadIdx.x];
+        out[threadIdx.x] = t;
+    }
+}
+
 // All CTAs call with their CTA vector `mine` (smem, NV entries). On return
 // `out` (smem) holds the sum over CTAs folded in CTA index order (identical
 // in every CTA, independent of arrival order). NV == 0 is a plain barrier.
@@ -99,53 +155,40 @@ __device__ __noinline__ void grid_allreduce(const GridCtx& g, const double* mine
     double* buf = g.partials + size_t(bar & 1u) * G * kRedStride;
     if (NV > 0 && threadIdx.x < NV) __stcg(buf + blockIdx.x * kRedStride + threadIdx.x, mine[threadIdx.x]);
     __syncthreads();
-    if (threadIdx.x < 32) {
-        // CTAs arrive on kArriveLanes counters (blockIdx % lanes) so the
-        // arrival atomics spread over separate L2 lines; lanes 0..7 of warp 0
-        // each poll one counter.
-        const int lane = threadIdx.x;
-        if (lane == 0)  // release is cumulative: covers the CTA's partial stores ordered by bar.sync
-            red_release_add(grid_counter(g, g.parity, blockIdx.x % kArriveLanes), 1ull);
-        const int l = lane % kArriveLanes;
-        const unsigned long long per = (unsigned long long)(G / kArriveLanes + (l < G % kArriveLanes ? 1 : 0));
-        const unsigned long long target = (unsigned long long)(bar + 1u) * per;
-        const unsigned long long* cnt = grid_counter(g, g.parity, l);
-        // Relaxed polling, then one acquire. Bounded: a co-residency bug must
-        // fail loudly, never hang the GPU.
-        unsigned long long spins = 0;
-        while (!__all_sync(0xffffffffu, ld_relaxed_u64(cnt) >= target)) {
-            if (++spins > (1ull << 26)) __trap();
+    if (threadIdx.x < 32) grid_arrive_wait(g, bar);
+    __syncthreads();
+    if (NV > 0) grid_fold<NV>(buf, out);
+    __syncthreads();
+}
+
+// Block sum + grid all-reduce of NV (<= 30) per-thread doubles in one: warp
+// partials by the transpose reduce, then warp 0 sums them (fixed warp order)
+// and stores the CTA vector straight into its grid slot before arriving, with
+// no CTA-wide barrier between the block sum and the arrival. Same sums, same
+// order as block_reduce + grid_allreduce.
+template <int NV>
+__device__ __forceinline__ void block_grid_allreduce(const GridCtx& g, const double (&in)[NV], double* scratch,
+                                                     double* out) {
+    static_assert(NV <= 32, "one warp holds the CTA vector");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = i < NV ? in[i] : 0.0;
+    scratch[warp * 32 + lane] = warp_transpose_reduce(v);
+    const unsigned int bar = s_grid_bar;  // read before warp 0 advances it (it does so after the barrier)
+    double* buf = g.partials + size_t(bar & 1u) * gridDim.x * kRedStride;
+    __syncthreads();
+    if (warp == 0) {
+        if (lane < NV) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += scratch[w * 32 + lane];
+            __stcg(buf + blockIdx.x * kRedStride + lane, s);
         }
-        (void)ld_acquire_u64(cnt);
-        if (lane == 0) s_grid_bar = bar + 1u;
+        __syncwarp();  // orders the lanes' partial stores before lane 0's release
+        grid_arrive_wait(g, bar);
     }
     __syncthreads();
-    if (NV > 0) {
-        __shared__ double red[32][32];
-        const int j = threadIdx.x & 31, c = threadIdx.x >> 5, nchunk = blockDim.x >> 5;
-        double s = 0.0;
-        if (j < NV) {
-            // chunk c folds CTA rows c, c+nchunk, ... in order; all of the
-            // chunk's loads are issued before the first add (one L2 latency).
-            constexpr int kRows = 24;
-            double v[kRows];
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) {
-                const int i = c + r * nchunk;
-                v[r] = i < G ? __ldcg(buf + i * kRedStride + j) : 0.0;
-            }
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) s += v[r];
-            for (int i = c + kRows * nchunk; i < G; i += nchunk) s += __ldcg(buf + i * kRedStride + j);
-        }
-        red[c][j] = s;
-        __syncthreads();
-        if (threadIdx.x < NV) {
-            double t = 0.0;
-            for (int cc = 0; cc < nchunk; ++cc) t += red[cc][threadIdx.x];
-            out[threadIdx.x] = t;
-        }
-    }
+    grid_fold<NV>(buf, out);
     __syncthreads();
 }
 

@@ -335,9 +335,17 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
             if (blockIdx.x == 0) tr[1] = now;
         }
     }
+#ifndef RF_FUSED_REDUCE
+#define RF_FUSED_REDUCE 1
+#endif
+#if RF_FUSED_REDUCE
+    block_grid_allreduce<kAccN>(a.grid, acc, scratch, out);
+    if (kJac && threadIdx.x == 0) s_pxc_tag = pxc_tag;  // (every thread read it before the barriers above)
+#else
     block_reduce<kAccN>(acc, scratch, blk);  // (its barriers: every thread has read s_pxc_tag)
     if (kJac && threadIdx.x == 0) s_pxc_tag = pxc_tag;
     grid_allreduce<kAccN>(a.grid, blk, out);
+#endif
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = global_ns();
     if (a.trace && threadIdx.x == 0) ++s_trace_pass;
 }
