@@ -55,13 +55,25 @@ __device__ __forceinline__ unsigned walk_pixel(const VolumeView& V, const float*
     const int max_steps = abs(end[0] - cell[0]) + abs(end[1] - cell[1]) + abs(end[2] - cell[2]) + 3;
     unsigned visits = 1;
     visit(cell);
+    // The step loop on scalars (a runtime axis index would put tmax / cell in
+    // local memory): the same comparisons and updates as WalkGridSegment.
+    double t0 = tmax[0], t1 = tmax[1], t2 = tmax[2];
     for (int n = 0; n < max_steps && (cell[0] != end[0] || cell[1] != end[1] || cell[2] != end[2]); ++n) {
-        int axis = 0;
-        if (tmax[1] < tmax[axis]) axis = 1;
-        if (tmax[2] < tmax[axis]) axis = 2;
-        if (tmax[axis] > 1.0) break;
-        tmax[axis] += tdel[axis];
-        cell[axis] += step[axis];
+        const bool a1 = t1 < t0;
+        const double tm01 = a1 ? t1 : t0;
+        const bool a2 = t2 < tm01;
+        const double tmin = a2 ? t2 : tm01;
+        if (tmin > 1.0) break;
+        if (a2) {
+            t2 += tdel[2];
+            cell[2] += step[2];
+        } else if (a1) {
+            t1 += tdel[1];
+            cell[1] += step[1];
+        } else {
+            t0 += tdel[0];
+            cell[0] += step[0];
+        }
         visit(cell);
         ++visits;
     }
