@@ -131,19 +131,25 @@ __global__ void k_alloc_coords(VolumeView V, const int* coords, int n, int* crea
 // BlockOutsideFrustum (tsdf_volume.cpp:119-151) for every allocated brick,
 // evaluated once for the carve bound (carve_clip) and the integrate bound
 // (max_depth + truncation). Visible bricks are appended with their flags.
-__device__ __forceinline__ bool outside(const double cc[8][3], const Intr& K, double max_z) {
-    bool any_behind = false;
+// The part of BlockOutsideFrustum that does not depend on the depth bound:
+// min corner depth, and whether the brick is outside for any bound (corners
+// behind the camera, or the projected corner box off the image). Then
+// outside(max_z) = min_z > max_z || rest: the 16 divisions run once for both
+// of k_cull's bounds.
+struct FrustumTest {
+    double min_z;
+    bool rest;
+    __device__ bool outside(double max_z) const { return min_z > max_z || rest; }
+};
+__device__ __forceinline__ FrustumTest frustum_test(const double cc[8][3], const Intr& K) {
+    bool any_behind = false, any_front = false;
     double min_z = __longlong_as_double(0x7ff0000000000000ll);
     for (int c = 0; c < 8; ++c) {
         if (cc[c][2] <= 1e-9) any_behind = true;
+        if (cc[c][2] > 1e-9) any_front = true;
         min_z = fmin(min_z, cc[c][2]);
     }
-    if (min_z > max_z) return true;
-    if (any_behind) {
-        for (int c = 0; c < 8; ++c)
-            if (cc[c][2] > 1e-9) return false;
-        return true;
-    }
+    if (any_behind) return {min_z, !any_front};
     double min_u = __longlong_as_double(0x7ff0000000000000ll), max_u = -min_u, min_v = min_u, max_v = -min_u;
     for (int c = 0; c < 8; ++c) {
         const double pu = K.fx * cc[c][0] / cc[c][2] + K.cx;
@@ -153,7 +159,7 @@ __device__ __forceinline__ bool outside(const double cc[8][3], const Intr& K, do
         min_v = fmin(min_v, pv);
         max_v = fmax(max_v, pv);
     }
-    return max_u < -0.5 || min_u > K.w - 0.5 || max_v < -0.5 || min_v > K.h - 0.5;
+    return {min_z, max_u < -0.5 || min_u > K.w - 0.5 || max_v < -0.5 || min_v > K.h - 0.5};
 }
 
 __global__ void k_cull(CullArgs a) {
@@ -179,8 +185,9 @@ __global__ void k_cull(CullArgs a) {
                 const double z = (double(c.z) + double(k >> 2)) * ext;
                 pose_apply(W, x, y, z, cc[k]);
             }
-            if (a.do_carve && b < before && !outside(cc, a.K, a.V.carve_clip)) flags |= kFlagCarve;
-            if (a.do_integrate && !outside(cc, a.K, a.V.max_depth + a.V.truncation)) flags |= kFlagIntegrate;
+            const FrustumTest ft = frustum_test(cc, a.K);
+            if (a.do_carve && b < before && !ft.outside(a.V.carve_clip)) flags |= kFlagCarve;
+            if (a.do_integrate && !ft.outside(a.V.max_depth + a.V.truncation)) flags |= kFlagIntegrate;
         }
         const unsigned vote = __ballot_sync(0xffffffffu, flags != 0);
         if (vote) {  // one atomic per warp, lanes take consecutive slots
@@ -503,7 +510,7 @@ __global__ void k_cull_window(WindowArgs a) {
                     const double z = (double(c.z) + double(k >> 2)) * ext;
                     pose_apply(W, x, y, z, cc[k]);
                 }
-                if (!outside(cc, a.K[j], a.V.max_depth + a.V.truncation)) bits |= 1u << j;
+                if (!frustum_test(cc, a.K[j]).outside(a.V.max_depth + a.V.truncation)) bits |= 1u << j;
             }
         }
         const unsigned vote = __ballot_sync(0xffffffffu, bits != 0);
