@@ -842,9 +842,8 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
         for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) cnt += __ldcg(F.mask[0] + p) ? 1 : 0;
     }
     if (mt) mt[5] = global_ns();
-    double v[1] = {double(cnt)};
-    block_reduce<1>(v, scratch, blk);
-    grid_allreduce<1>(a.grid, blk, red);
+    const double v[1] = {double(cnt)};
+    block_grid_allreduce<1>(a.grid, v, scratch, red);
     if (mt) mt[6] = global_ns();
     return red[0];
 }
