@@ -89,17 +89,24 @@ __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned 
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+struct NoHook {
+    __device__ void operator()() const {}
+};
+
 // Warp 0: arrive on the barrier's counter (after the CTA's partial stores,
-// which warp 0 has observed through a CTA or warp barrier) and poll until
-// every CTA has arrived. Returns the barrier index this call completed.
-__device__ __forceinline__ void grid_arrive_wait(const GridCtx& g, unsigned int bar) {
+// which warp 0 has observed through a CTA or warp barrier), run `hook` on
+// lane 0 while the arrivals propagate, and poll until every CTA has arrived.
+template <class Hook = NoHook>
+__device__ __forceinline__ void grid_arrive_wait(const GridCtx& g, unsigned int bar, const Hook& hook = Hook()) {
     const int G = gridDim.x;
     // CTAs arrive on kArriveLanes counters (blockIdx % lanes) so the
     // arrival atomics spread over separate L2 lines; lanes 0..7 of warp 0
     // each poll one counter.
     const int lane = threadIdx.x;
-    if (lane == 0)  // release is cumulative: covers the CTA's partial stores ordered by the barrier
+    if (lane == 0) {  // release is cumulative: covers the CTA's partial stores ordered by the barrier
         red_release_add(grid_counter(g, g.parity, blockIdx.x % kArriveLanes), 1ull);
+        hook();
+    }
     const int l = lane % kArriveLanes;
     const unsigned long long per = (unsigned long long)(G / kArriveLanes + (l < G % kArriveLanes ? 1 : 0));
     const unsigned long long target = (unsigned long long)(bar + 1u) * per;
@@ -176,9 +183,9 @@ __device__ RF_GRID_INLINE void grid_allreduce(const GridCtx& g, const double* mi
 // and stores the CTA vector straight into its grid slot before arriving, with
 // no CTA-wide barrier between the block sum and the arrival. Same sums, same
 // order as block_reduce + grid_allreduce.
-template <int NV>
+template <int NV, class Hook = NoHook>
 __device__ __forceinline__ void block_grid_allreduce(const GridCtx& g, const double (&in)[NV], double* scratch,
-                                                     double* out) {
+                                                     double* out, const Hook& hook = Hook()) {
     static_assert(NV <= 32, "one warp holds the CTA vector");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double v[32];
@@ -195,7 +202,7 @@ __device__ __forceinline__ void block_grid_allreduce(const GridCtx& g, const dou
             __stcg(buf + blockIdx.x * kRedStride + lane, s);
         }
         __syncwarp();  // orders the lanes' partial stores before lane 0's release
-        grid_arrive_wait(g, bar);
+        grid_arrive_wait(g, bar, hook);
     }
     __syncthreads();
     grid_fold<NV>(buf, out);

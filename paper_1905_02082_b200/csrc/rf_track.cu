@@ -210,9 +210,9 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
 
 // ------------------------------------------------------------------ pixel pass
 // One Accumulate (registration.cpp:49-117) over pyramid level `level`.
-template <bool kJac, bool kColor>
+template <bool kJac, bool kColor, class Hook>
 __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
-                           double* scratch, double* blk, double* out) {
+                           double* scratch, double* blk, double* out, const Hook& hook) {
     const FrameView& F = a.F;
     const Intr K = F.K[level];
     const double min_depth = a.V.min_depth, max_depth = a.V.max_depth;
@@ -339,7 +339,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
 #define RF_FUSED_REDUCE 1
 #endif
 #if RF_FUSED_REDUCE
-    block_grid_allreduce<kAccN>(a.grid, acc, scratch, out);
+    block_grid_allreduce<kAccN>(a.grid, acc, scratch, out, hook);
     if (kJac && threadIdx.x == 0) s_pxc_tag = pxc_tag;  // (every thread read it before the barriers above)
 #else
     block_reduce<kAccN>(acc, scratch, blk);  // (its barriers: every thread has read s_pxc_tag)
@@ -350,16 +350,18 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
     if (a.trace && threadIdx.x == 0) ++s_trace_pass;
 }
 
-template <bool kJac>
+// `hook` runs on thread 0 once the CTA has arrived at the pass's all-reduce
+// (work that must not delay the CTA's own pixels or arrival).
+template <bool kJac, class Hook = NoHook>
 __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res,
-                                     double cw, double* scratch, double* blk, double* out) {
+                                     double cw, double* scratch, double* blk, double* out, const Hook& hook = Hook()) {
     const bool color = cw > 0.0 && a.F.rgb0 != nullptr;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         s_passes += 1;  // CTA 0's tally, published once at kernel exit (no global RMW on the pass path)
         s_pixel_passes += double(a.F.K[level].w) * double(a.F.K[level].h);
     }
-    if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
-    else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out);
+    if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook);
+    else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook);
 }
 
 // ------------------------------------------------------------------ Register
@@ -475,14 +477,15 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
             }
             __syncthreads();
             if (!st.go) break;
-            if (threadIdx.x == 0) {  // everything of the judge but the trial's error, off the critical path
+            // everything of the judge but the trial's error, on thread 0 while the
+            // all-reduce's arrivals propagate (off every critical path)
+            pass<true>(a, l, st.cand, use_mask, false, cw, scratch, blk, st.trial(), [&] {
                 st.cur_err = st.cur()[27] + cw * st.cur()[28];
                 st.tol = kRelDecreaseTol * st.cur_err;
                 st.lam_acc = fmax(st.lambda / R.lambda_down, 1e-12);
                 st.lam_rej = fmin(st.lambda * R.lambda_up, 1e12);
                 st.small_step = sqrt(st.dnorm) < R.eps;
-            }
-            pass<true>(a, l, st.cand, use_mask, false, cw, scratch, blk, st.trial());
+            });
             judge = true;
         }
         __syncthreads();
