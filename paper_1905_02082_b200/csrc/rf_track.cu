@@ -29,7 +29,8 @@ extern __shared__ __align__(16) unsigned char s_dyn[];
 __device__ __forceinline__ float2* pxc_base() { return reinterpret_cast<float2*>(s_dyn); }
 __shared__ int s_pxc_tag;  // (level + 1) | 16 * use_mask of the cached inputs, 0: none
 #ifdef RF_LM_PROFILE
-__shared__ long long s_lmp[5];  // [1..4]: steps, judge->solve-done, solve, expmap+compose (cycle sums)
+__shared__ long long s_lmp[5];  // [1..4]: steps, judge->solve-done, solve, expmap+compose; [0]: warm repeat
+__shared__ volatile double s_lmp_sink;
 #endif
 __shared__ int s_passes;   // Accumulate passes run (CTA 0; TrackOut.passes / pixel_passes)
 __shared__ double s_pixel_passes;
@@ -469,6 +470,16 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
                         s_lmp[2] += c2 - cj;
                         s_lmp[3] += c1 - c0;
                         s_lmp[4] += c2 - c1;
+                        // the same solve + ExpMap + compose again, now with warm caches
+                        const long long h0 = clock64();
+                        double d2[6];
+                        const bool ok2 = lm_solve(st.buf[st.ci], st.lambda, d2);
+                        Pose e2;
+                        expmap(d2, e2);
+                        const Pose c2p = pose_mul(e2, st.pose);
+                        const long long h1 = clock64();
+                        s_lmp_sink = c2p.t[0] + (ok2 ? 1.0 : 0.0);
+                        s_lmp[0] += h1 - h0;
                     }
                 }
 #endif
@@ -999,8 +1010,10 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
         a.out->pixel_passes = s_pixel_passes;
     }
 #ifdef RF_LM_PROFILE
-    if (lead && a.trace)  // diagnostic variant: record 251 = {steps, judge..solved, solve, expmap+compose} cycles
+    if (lead && a.trace) {  // diagnostic variant: record 251 = {steps, judge..solved, solve, expmap+compose, warm repeat}
         for (int i = 0; i < 4; ++i) a.trace[8 * 251 + i] = (unsigned long long)s_lmp[i + 1];
+        a.trace[8 * 251 + 4] = (unsigned long long)s_lmp[0];
+    }
 #endif
 }
 
