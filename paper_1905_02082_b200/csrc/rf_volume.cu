@@ -251,9 +251,17 @@ __device__ __forceinline__ float div_f32(double a, double b, double rb) {
     const float lo = __double2float_rn(q * (1.0 - 0x1p-50)), hi = __double2float_rn(q * (1.0 + 0x1p-50));
     return lo == hi ? lo : float(a / b);
 }
-__device__ __forceinline__ uint32_t colour_avg(uint32_t c, uint32_t w, uint32_t in) {
-    const uint32_t n = c * w + in, d = w + 1u;  // lround((c * w + in) / (w + 1)), tsdf_volume.cpp:190-196
-    return (2u * n + d) / (2u * d);
+// lround((c * w + in) / (w + 1)) (tsdf_volume.cpp:190-196) = (2n + d) / (2d) with
+// n = c * w + in, d = w + 1, as a multiply by M = ceil(2^40 / (2d)): exact for
+// every numerator < 2^17 (n <= 255 * 255 + 255) and 2d <= 512 (checked
+// exhaustively), with no integer division on the per-voxel path.
+__device__ __forceinline__ uint32_t colour_avg(uint32_t c, uint32_t w, uint32_t in, const unsigned long long* cdiv) {
+    const uint32_t d = w + 1u;
+    const unsigned long long num = 2ull * (c * w + in) + d;
+    return uint32_t((num * cdiv[d]) >> 40);
+}
+__device__ __forceinline__ unsigned long long colour_magic(uint32_t d) {  // ceil(2^40 / (2d)), d >= 1
+    return ((1ull << 40) + 2ull * d - 1ull) / (2ull * d);
 }
 
 __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
@@ -262,12 +270,14 @@ __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
     if (a.lost && *a.lost) return;
     __shared__ Pose W;
     __shared__ double s_rcp[512];  // RN(1 / i): i = w + 1 (integrate) or w + carve_weight (carve), <= 510
+    __shared__ unsigned long long s_cdiv[257];  // colour_avg multipliers by d = w + 1
     if (threadIdx.x == 0) {
         Pose P;
         for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = a.pose[i];
         W = pose_inverse(P);
     }
     for (int i = threadIdx.x; i < 512; i += blockDim.x) s_rcp[i] = i ? 1.0 / double(i) : 0.0;
+    for (int i = threadIdx.x; i < 257; i += blockDim.x) s_cdiv[i] = i ? colour_magic(uint32_t(i)) : 0ull;
     __syncthreads();
     const uint32_t nvis = a.V.counters[kVisible];
     const int x = threadIdx.x & 7, y = (threadIdx.x >> 3) & 7, z = threadIdx.x >> 6;
@@ -338,9 +348,9 @@ __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
                         const double w = double(wgt);
                         sdf = div_f32(double(sdf) * w + clamped, w + 1.0, s_rcp[wgt + 1u]);
                         if (fabs(dist) <= tau && a.rgb) {
-                            r = colour_avg(r, wgt, cr);
-                            g = colour_avg(g, wgt, cg);
-                            bl = colour_avg(bl, wgt, cb);
+                            r = colour_avg(r, wgt, cr, s_cdiv);
+                            g = colour_avg(g, wgt, cg, s_cdiv);
+                            bl = colour_avg(bl, wgt, cb, s_cdiv);
                         }
                         wgt = min(wgt + 1u, uint32_t(mw));
                         dirty = true;
@@ -539,12 +549,14 @@ __global__ void __launch_bounds__(kBrickVoxels, RF_WIN_MINB) k_fuse_window(Windo
     commit_links(a.V);
     __shared__ Pose Ws[kMaxWin];
     __shared__ double s_rcp[512];  // RN(1 / i) for the running averages (see div_f32)
+    __shared__ unsigned long long s_cdiv[257];  // colour_avg multipliers by d = w + 1
     if (threadIdx.x < a.n) {
         Pose P;
         for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = a.pose[threadIdx.x][i];
         Ws[threadIdx.x] = pose_inverse(P);
     }
     for (int i = threadIdx.x; i < 512; i += blockDim.x) s_rcp[i] = i ? 1.0 / double(i) : 0.0;
+    for (int i = threadIdx.x; i < 257; i += blockDim.x) s_cdiv[i] = i ? colour_magic(uint32_t(i)) : 0ull;
     __syncthreads();
     const uint32_t nvis = a.V.counters[kVisible];
     const int x = threadIdx.x & 7, y = (threadIdx.x >> 3) & 7, z = threadIdx.x >> 6;
@@ -612,9 +624,9 @@ __global__ void __launch_bounds__(kBrickVoxels, RF_WIN_MINB) k_fuse_window(Windo
                 const double w = double(wgt);
                 sdf = div_f32(double(sdf) * w + clamped, w + 1.0, s_rcp[wgt + 1u]);
                 if (fabs(dist) <= tau && (col[k] >> 24)) {
-                    r = colour_avg(r, wgt, col[k] & 0xFFu);
-                    g = colour_avg(g, wgt, (col[k] >> 8) & 0xFFu);
-                    bl = colour_avg(bl, wgt, (col[k] >> 16) & 0xFFu);
+                    r = colour_avg(r, wgt, col[k] & 0xFFu, s_cdiv);
+                    g = colour_avg(g, wgt, (col[k] >> 8) & 0xFFu, s_cdiv);
+                    bl = colour_avg(bl, wgt, (col[k] >> 16) & 0xFFu, s_cdiv);
                 }
                 wgt = min(wgt + 1u, uint32_t(mw));
                 dirty = true;
