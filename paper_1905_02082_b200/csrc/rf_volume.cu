@@ -11,6 +11,20 @@ namespace rfb {
 // tsdf_volume.hpp:149-185), one thread per pixel, all cells inserted with
 // atomicCAS. The set of inserted keys, and so the occupied-slot set of the
 // linear-probing table, is independent of thread order.
+// a / b correctly rounded from rb = RN(1 / b): q = RN(a rb) is within an ulp,
+// the FMA residual is exact, and one correction step rounds correctly
+// (Markstein); no IEEE division sequence on the walk's setup chain. A zero
+// quotient comes out +0 where a / b gives -0; the walk only floors and
+// subtracts these values, where the two zeros agree.
+__device__ __forceinline__ double div_rn(double a, double b, double rb) {
+#ifdef RF_WALK_IEEE_DIV
+    return a / b;
+#else
+    const double q = a * rb;
+    return __fma_rn(__fma_rn(-q, b, a), rb, q);
+#endif
+}
+
 // The ray segment of pixel p (AllocateForFrame, tsdf_volume.cpp:93-113):
 // [max(d - tau, 1e-4), d + tau] along the pixel's ray, walked through the
 // block grid (WalkGridSegment, tsdf_volume.hpp:149-185); `visit(cell)` for
@@ -26,14 +40,15 @@ __device__ __forceinline__ unsigned walk_pixel(const VolumeView& V, const float*
     for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = __ldg(pose + i);
     const double tau = V.truncation;
     const double ext = double(kSide) * V.voxel_size;  // block_extent(), tsdf_volume.hpp:123
-    const double dir0 = (double(u) - K.cx) / K.fx, dir1 = (double(v) - K.cy) / K.fy;
+    const double rext = V.inv_voxel_size * (1.0 / double(kSide));  // RN(1/ext): RN(1/s) scaled by 2^-3
+    const double dir0 = div_rn(double(u) - K.cx, K.fx, K.ifx), dir1 = div_rn(double(v) - K.cy, K.fy, K.ify);
     const double z0 = fmax(double(d) - tau, 1e-4);
     const double z1 = double(d) + tau;
     double w0[3], w1[3];
     pose_apply(P, z0 * dir0, z0 * dir1, z0 * 1.0, w0);
     pose_apply(P, z1 * dir0, z1 * dir1, z1 * 1.0, w1);
-    const double p0[3] = {w0[0] / ext, w0[1] / ext, w0[2] / ext};
-    const double p1[3] = {w1[0] / ext, w1[1] / ext, w1[2] / ext};
+    const double p0[3] = {div_rn(w0[0], ext, rext), div_rn(w0[1], ext, rext), div_rn(w0[2], ext, rext)};
+    const double p1[3] = {div_rn(w1[0], ext, rext), div_rn(w1[1], ext, rext), div_rn(w1[2], ext, rext)};
     int cell[3], end[3], step[3];
     double tmax[3], tdel[3];
     for (int i = 0; i < 3; ++i) {

@@ -23,3 +23,37 @@ def test_colour_average_matches_rounded_quotient():
     d = w + 1
     want = np.floor(n / d + 0.5).astype(np.int64)  # n, d >= 0: lround = floor(q + 1/2)
     np.testing.assert_array_equal((2 * n + d) // (2 * d), want)
+
+
+def _fma(x, y, z):
+    """fma(x, y, z) with one rounding (Fraction arithmetic is exact; float() of a
+    Fraction rounds to nearest even)."""
+    from fractions import Fraction
+    return float(Fraction(x) * Fraction(y) + Fraction(z))
+
+
+def test_walk_division_by_reciprocal_is_correctly_rounded():
+    """div_rn (rf_volume.cu, the ray-segment setup of WalkGridSegment,
+    tsdf_volume.hpp:149-185): q = RN(a rb), r = fma(-q, b, a), q' = fma(r, rb, q) with
+    rb = RN(1/b) equals the IEEE quotient a / b. Checked on the walk's operand ranges:
+    pixel offsets over focal lengths, and world coordinates over brick extents
+    (8 voxel sizes; the reciprocal there is RN(1/s) scaled by 2^-3)."""
+    rng = np.random.default_rng(7)
+    cases = []
+    for f in (525.0, 517.3, 481.2, 600.0, 910.7, 1000.0 / 3.0):
+        for u in rng.uniform(-700.0, 700.0, 300):
+            cases.append((float(u), f, 1.0 / f))
+        for u in range(-64, 65):
+            cases.append((float(u) + 0.5, f, 1.0 / f))
+    for s in (0.005, 0.01, 0.02, 0.0075, 0.004):
+        ext, rext = 8.0 * s, (1.0 / s) * (1.0 / 8.0)
+        assert rext == 1.0 / ext
+        for w in rng.uniform(-20.0, 20.0, 600):
+            cases.append((float(w), ext, rext))
+        for k in range(-50, 51):  # coordinates on and next to brick faces
+            for w in (k * ext, np.nextafter(k * ext, np.inf), np.nextafter(k * ext, -np.inf)):
+                cases.append((float(w), ext, rext))
+    for a, b, rb in cases:
+        q = a * rb
+        r = _fma(-q, b, a)
+        assert _fma(r, rb, q) == a / b or (a == 0.0), (a, b)
