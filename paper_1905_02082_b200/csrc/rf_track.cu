@@ -211,6 +211,9 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
 
 // ------------------------------------------------------------------ pixel pass
 // One Accumulate (registration.cpp:49-117) over pyramid level `level`.
+#ifndef RF_TRACK_SPREAD
+#define RF_TRACK_SPREAD 64
+#endif
 template <bool kJac, bool kColor, class Hook>
 __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
                            double* scratch, double* blk, double* out, const Hook& hook) {
@@ -232,17 +235,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
     }
     const int pxc_tag = (level + 1) | (use_mask ? 16 : 0);
     const bool pxc_hit = kJac && s_pxc_tag == pxc_tag;
-    int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;  // tile walked incrementally (no per-tile division)
-    const int step_y = gridDim.x / ntx, step_x = gridDim.x % ntx;
-    for (int it = 0; ty < nty; tx += step_x, ty += step_y, ++it) {
-        if (tx >= ntx) {
-            tx -= ntx;
-            ++ty;
-            if (ty >= nty) break;
-        }
-        const int u = tx * kTileW + (threadIdx.x % kTileW);
-        const int v = ty * kTileH + (threadIdx.x / kTileW);
-        if (u >= K.w || v >= K.h) continue;
+    auto pixel = [&](const int u, const int v, const int it) {
         const int p = v * K.w + u;
         // Every per-pixel input is loaded up front (depth, mask, intensity),
         // so only the hash slot and voxel gathers are dependent round trips.
@@ -326,6 +319,36 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
         if (!kJac && write_res) {
             F.res_sq[p] = rs;
             F.res_valid[p] = rv;
+        }
+    };
+    // A level with at most RF_TRACK_SPREAD steps of the grid's pixels is spread
+    // evenly: ceil(npx / G) consecutive pixels per CTA (a strip of rows),
+    // instead of whole 16x24 tiles on part of the CTAs (640x480: 800 / 200 / 50
+    // tiles for 148 CTAs). B200, frames 5..104: tiles everywhere 1519 frames/s,
+    // coarsest level spread 1565, two coarsest 1577, all levels 1581 (default).
+    const int npx = K.w * K.h;
+    if (npx <= RF_TRACK_SPREAD * int(gridDim.x) * kTrackThreads) {
+#ifndef RF_SPREAD_ALIGN
+#define RF_SPREAD_ALIGN 1
+#endif
+        const int per = ((npx + int(gridDim.x) - 1) / int(gridDim.x) + RF_SPREAD_ALIGN - 1) / RF_SPREAD_ALIGN * RF_SPREAD_ALIGN;
+        for (int it = 0, q = int(threadIdx.x); q < per; ++it, q += kTrackThreads) {
+            const int p = int(blockIdx.x) * per + q;
+            if (p < npx) pixel(p % K.w, p / K.w, it);
+        }
+    } else {
+        int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;  // tile walked incrementally (no per-tile division)
+        const int step_y = gridDim.x / ntx, step_x = gridDim.x % ntx;
+        for (int it = 0; ty < nty; tx += step_x, ty += step_y, ++it) {
+            if (tx >= ntx) {
+                tx -= ntx;
+                ++ty;
+                if (ty >= nty) break;
+            }
+            const int u = tx * kTileW + (threadIdx.x % kTileW);
+            const int v = ty * kTileH + (threadIdx.x / kTileW);
+            if (u >= K.w || v >= K.h) continue;
+            pixel(u, v, it);
         }
     }
     if (tr) {
