@@ -89,6 +89,10 @@ __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned 
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+#ifndef RF_POLL_ACQ
+#define RF_POLL_ACQ 0
+#endif
+
 struct NoHook {
     __device__ void operator()() const {}
 };
@@ -114,10 +118,17 @@ __device__ __forceinline__ void grid_arrive_wait(const GridCtx& g, unsigned int 
     // Relaxed polling, then one acquire. Bounded: a co-residency bug must
     // fail loudly, never hang the GPU.
     unsigned long long spins = 0;
+#if RF_POLL_ACQ
+    // acquire polling: the load that sees the target is the acquire (no extra L2 trip)
+    while (!__all_sync(0xffffffffu, ld_acquire_u64(cnt) >= target)) {
+        if (++spins > (1ull << 26)) __trap();
+    }
+#else
     while (!__all_sync(0xffffffffu, ld_relaxed_u64(cnt) >= target)) {
         if (++spins > (1ull << 26)) __trap();
     }
     (void)ld_acquire_u64(cnt);
+#endif
     if (lane == 0) s_grid_bar = bar + 1u;
 }
 
