@@ -657,6 +657,19 @@ __device__ __forceinline__ void ff_enqueue3x3(int* base, int ntx, int nty, int t
     }
 }
 
+// Flag worklists (RF_FF_FLAGS, default): F.ffstamp holds three per-tile flag
+// arrays, round r reading array r % 3 (tiles that changed in round r - 1, or
+// seeded ones for r = 0), setting array (r + 1) % 3 with plain stores and
+// zeroing array (r + 2) % 3 (read in round r - 1). Every CTA builds the same
+// tile list -- the 3x3 dilation of the flags, compacted in tile order -- in
+// its dynamic shared memory, so a round costs one flag load instead of the
+// count / list loads and the returning atomics of the queue.
+#ifndef RF_FF_FLAGS
+#define RF_FF_FLAGS 1
+#endif
+constexpr int kFfMaxFlagTiles = int((kTrackDynSmem - 16) / 3);  // nft bytes + nft uint16 in the pixel cache
+__device__ __forceinline__ bool ff_flag_mode(int nft) { return RF_FF_FLAGS && nft <= kFfMaxFlagTiles; }
+
 // Kogge-Stone fills of a 32-bit row: every pixel reachable from `g` by
 // moves of one pixel in the given direction through pixels whose entry bit
 // (`p`) is set, in five steps.
@@ -713,15 +726,60 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint32_t* planes,
     auto at = [&](int gx, int gy) -> uint32_t {  // mask bit of an image pixel (0 outside)
         return (gx >= 0 && gx < w && gy >= 0 && gy < h) ? uint32_t(__ldcg(m + size_t(gy) * w + gx) != 0) : 0u;
     };
+    const bool flags = ff_flag_mode(nft);
+    uint8_t* s_flag = reinterpret_cast<uint8_t*>(s_dyn);  // (the pixel cache is refilled after the mask)
+    uint16_t* s_list = reinterpret_cast<uint16_t*>(s_dyn + ((nft + 15) & ~15));
+    __shared__ int s_wcount[kTrackThreads / 32];
+    if (flags && threadIdx.x == 0) s_pxc_tag = 0;
     int rounds = 0;
     while (true) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) *ff_count(wl, nft, rounds + 2) = 0u;  // not touched this round
         if (a.trace && rounds < 8 && blockIdx.x == 0 && threadIdx.x == 0)
             a.trace[8 * (kTracePasses - 3) + rounds] = global_ns();
-        const int nq = int(__ldcg(ff_count(wl, nft, rounds)));
-        const int* list = ff_list(wl, nft, rounds);
+        int nq;
+        const int* list = nullptr;
+        if (flags) {
+            const int* fr = wl + nft * (rounds % 3);
+            for (int t = threadIdx.x; t < nft; t += blockDim.x) s_flag[t] = __ldcg(fr + t) != 0;
+            if (blockIdx.x == 0)
+                for (int t = threadIdx.x; t < nft; t += blockDim.x) wl[nft * ((rounds + 2) % 3) + t] = 0;
+            __syncthreads();
+            nq = 0;
+            for (int c0 = 0; c0 < nft; c0 += blockDim.x) {  // queued = 3x3 dilation, compacted in tile order
+                const int t = c0 + int(threadIdx.x);
+                bool q = false;
+                if (t < nft) {
+                    const int tx = t % ntx, ty = t / ntx;
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            const int nx = tx + dx, ny = ty + dy;
+                            q |= nx >= 0 && nx < ntx && ny >= 0 && ny < nty && s_flag[ny * ntx + nx];
+                        }
+                }
+                const unsigned b = __ballot_sync(0xffffffffu, q);
+                if (lane == 0) s_wcount[warp] = __popc(b);
+                __syncthreads();
+                int before = 0, total = 0;
+                for (int k = 0; k < nwarps; ++k) {
+                    const int c = s_wcount[k];
+                    before += k < warp ? c : 0;
+                    total += c;
+                }
+                if (q) s_list[nq + before + __popc(b & ((1u << lane) - 1u))] = uint16_t(t);
+                nq += total;
+                __syncthreads();
+            }
+            if (nq == 0) {  // nothing changed in the last round: fixpoint reached
+                if (a.trace && rounds < 8 && threadIdx.x == 0)
+                    atomicMax(a.trace + 8 * (kTracePasses - 4) + rounds, global_ns());  // (the empty round's end)
+                break;
+            }
+        } else {
+            if (blockIdx.x == 0 && threadIdx.x == 0) *ff_count(wl, nft, rounds + 2) = 0u;  // not touched this round
+            nq = int(__ldcg(ff_count(wl, nft, rounds)));
+            list = ff_list(wl, nft, rounds);
+        }
         for (int qi = warp * G + blockIdx.x; qi < nq; qi += G * nwarps) {  // one tile per warp
-            const int t = __ldcg(list + qi);
+            const int t = flags ? int(s_list[qi]) : __ldcg(list + qi);
             const int tx = t % ntx, ty = t / ntx, x0 = tx * kFfW, y0 = ty * kFfH;
             const int gy = y0 + lane;
             // row words: mask, validity, growth planes (x = bit)
@@ -789,12 +847,18 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint32_t* planes,
                 grew &= grew - 1u;
             }
             if (a.trace && lane == 0) atomicAdd(a.trace + 8 * (kTracePasses - 2), 1ull);  // tile visits
-            if (changed) ff_enqueue3x3(wl, ntx, nty, tx, ty, rounds + 1);
+            if (changed) {
+                if (flags) {
+                    if (lane == 0) wl[nft * ((rounds + 1) % 3) + t] = 1;
+                } else {
+                    ff_enqueue3x3(wl, ntx, nty, tx, ty, rounds + 1);
+                }
+            }
         }
         if (a.trace && rounds < 8 && threadIdx.x == 0) atomicMax(a.trace + 8 * (kTracePasses - 4) + rounds, global_ns());
         grid_barrier(a.grid);
         ++rounds;
-        if (__ldcg(ff_count(wl, nft, rounds)) == 0u) break;  // nothing queued: fixpoint reached
+        if (!flags && __ldcg(ff_count(wl, nft, rounds)) == 0u) break;  // nothing queued: fixpoint reached
     }
     return rounds;
 }
@@ -835,7 +899,10 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
             if (stages & 4) {  // the floodfill's growth bits (same 32x32 tiling) and round-0 worklist
                 grow_tile(F.depth0, reinterpret_cast<uint32_t*>(F.grow), w, h, t % ntx, t / ntx, M.theta,
                           M.connectivity);
-                if (__syncthreads_or(nseed)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
+                if (__syncthreads_or(nseed)) {
+                    if (!ff_flag_mode(ntx * nty)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
+                    else if (threadIdx.x == 0) F.ffstamp[t] = 1;  // round 0's flags
+                }
             }
         }
     } else {  // wide windows: threshold, then separable passes through global memory
@@ -858,7 +925,10 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
                 const int gx = x0 + i % kMorphTile, gy = y0 + i / kMorphTile;
                 any |= (gx < w && gy < h && __ldcg(seeds + gy * w + gx)) ? 1 : 0;
             }
-            if (__syncthreads_or(any)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
+            if (__syncthreads_or(any)) {
+                if (!ff_flag_mode(ntx * nty)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
+                else if (threadIdx.x == 0) F.ffstamp[t] = 1;
+            }
         }
     }
     grid_barrier(a.grid);
@@ -900,7 +970,7 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
     if ((a.mode == kModeFrame && a.dynamics) || a.mode == kModeMask) {  // floodfill worklists (ff_list)
         const int nft = ((a.F.K[0].w + kFfW - 1) / kFfW) * ((a.F.K[0].h + kFfH - 1) / kFfH);
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * nft + kFfCounts; i += gridDim.x * blockDim.x)
-            a.F.ffstamp[i] = i < nft ? -1 : 0;
+            a.F.ffstamp[i] = (i < nft && !ff_flag_mode(nft)) ? -1 : 0;
     }
 
     if (a.mode == kModeLinearize || a.mode == kModeEvalDepth || a.mode == kModeEvalColor) {
