@@ -464,3 +464,32 @@ def test_pipeline_tracking_loss_single_and_batch():
         assert np.array_equal(pg, bposes[i])
     assert bstats[4]["tracking_lost"] == 1 and np.array_equal(bposes[4], bposes[3])
     assert ga.tracking_losses() == gb.tracking_losses() == 1
+
+
+def test_pipeline_nonfinite_and_negative_depth():
+    """Depth pixels that are NaN, +inf, -inf, negative or zero are invalid
+    (image.hpp:68 DepthValid: d > 0 and finite) everywhere on the path --
+    allocation, integration, pyramid and registration -- so a frame sequence
+    salted with them tracks and fuses as the oracle does, and the batched call
+    matches the single calls."""
+    s = O.Scene(scenes.room_script(with_mover=False, width=160, height=120, frames=6))
+    frames = [s.render(i) for i in range(len(s))]
+    rng = np.random.default_rng(7)
+    bad = np.array([np.nan, np.inf, -np.inf, -1.0, 0.0], np.float32)
+    for i in range(1, len(frames)):
+        d = frames[i]["depth"].copy()
+        idx = rng.choice(d.size, size=d.size // 20, replace=False)
+        d.reshape(-1)[idx] = bad[rng.integers(0, len(bad), size=idx.size)]
+        frames[i] = dict(frames[i], depth=d)
+    vc = O.vol_cfg(voxel_size=0.02, max_blocks=200000)
+    op = O.Pipeline(O.pipe_cfg(refine=False, volume=vc, reg=O.reg_cfg(threads=8)))
+    cfg = G.pipeline_config(refine=False, volume=gcfg(vc))
+    ga, gb = G.Pipeline(cfg), G.Pipeline(cfg)
+    gframes = [frame(s.k, f["depth"], f["rgb"], f["timestamp"]) for f in frames]
+    bstats, bposes = gb.process_frames(gframes)
+    for i, f in enumerate(frames):
+        so, po = op.process_frame(f["depth"], f["rgb"], s.k, f["timestamp"])
+        sg, pg = ga.process_frame(gframes[i])
+        assert so["tracking_lost"] == sg["tracking_lost"] == bstats[i]["tracking_lost"] == 0, i
+        assert max(pose_error(po, pg)) <= 1e-4, i
+        assert np.array_equal(pg, bposes[i]), i
