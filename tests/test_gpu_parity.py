@@ -493,3 +493,27 @@ def test_pipeline_nonfinite_and_negative_depth():
         assert so["tracking_lost"] == sg["tracking_lost"] == bstats[i]["tracking_lost"] == 0, i
         assert max(pose_error(po, pg)) <= 1e-4, i
         assert np.array_equal(pg, bposes[i]), i
+
+
+@pytest.mark.parametrize("h,w", [(1, 1), (33, 45), (67, 101), (130, 37)])
+def test_mask_stages_bitexact_ragged(h, w):
+    """The mask stages on image sizes that are not multiples of the 32x32
+    floodfill tile or of 4 bytes (the byte-wise row path), down to 1x1."""
+    rng = np.random.default_rng(h * 1000 + w)
+    depth = (1.0 + 0.5 * (rng.random((h, w)) < 0.3) + 0.003 * rng.standard_normal((h, w))).astype(np.float32)
+    depth[rng.random((h, w)) < 0.05] = 0
+    sq = (rng.random((h, w)) * 0.01).astype(np.float32)
+    valid = (rng.random((h, w)) < 0.9).astype(np.uint8)
+    for cfg in (O.mask_cfg(), O.mask_cfg(erode_radius=1, dilate_radius=3, connectivity=8, theta=0.02)):
+        gc = G.mask_config(gamma=cfg.gamma, truncation=cfg.truncation, theta=cfg.theta,
+                           erode_radius=cfg.erode_radius, dilate_radius=cfg.dilate_radius,
+                           connectivity=cfg.connectivity)
+        assert (O.build_mask(sq, valid, depth, cfg) == G.build_mask(sq, valid, depth, gc)).all()
+    seeds = (rng.random((h, w)) < 0.02).astype(np.uint8)
+    for theta in (0.007, 0.6):
+        for conn in (4, 8):
+            assert (O.floodfill(seeds, depth, theta, conn) == G.floodfill_depth(seeds, depth, theta, conn)).all()
+    m = (rng.random((h, w)) < 0.6).astype(np.uint8)
+    for r in (1, 3):
+        assert (O.erode(m, r) == G.erode(m, r)).all()
+        assert (O.dilate(m, r) == G.dilate(m, r)).all()
