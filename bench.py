@@ -18,6 +18,9 @@ Arms:
   --impl reference : the reference algorithm on the host CPU (the oracle
                      restatement, all host threads; the C++ reference itself
                      cannot be built here — DESIGN.md §Oracle).
+The default line carries a `parity` block: the GPU arm's per-frame poses and
+counts (registrations, LM iterations, masked pixels) against the cpu_baseline
+leg's over the frames both processed (same bytes, same order).
 Multi-GPU (torchrun): independent sequences per GPU (replicas, no collective).
 """
 from __future__ import annotations
@@ -68,52 +71,123 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock and throttle reasons sampled through NVML every 0.5 ms while
+    the timed region runs (one sample is always taken on entry and on exit,
+    so even a 20 ms region has samples)."""
+
+    NAMES = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
         self.rows = []
-        self.proc = None
+        self.h = None
+        self.stop = threading.Event()
+
+    def _sample(self):
+        import pynvml as N
+        try:
+            sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+            mx = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.rows.append((sm, mx, rs))
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self.stop.wait(0.0005):
+            self._sample()
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[self.index].isdigit() else self.index
+            self.h = N.nvmlDeviceGetHandleByIndex(idx)
+            self._sample()
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
         except Exception:
-            self.proc = None
+            self.h = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        if self.h is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
+            self._sample()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            if len(r) >= 7:
-                for n, v in zip(names, r[3:7]):
-                    if v.lower() == "active":
-                        reasons.add(n)
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({n for r in self.rows for n, bit in self.NAMES.items() if r[2] & bit})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(r[1] for r in self.rows) if sm else None,
+                "reasons": reasons, "samples": len(sm), "source": "nvml, 0.5 ms polling inside the timed region"}
+
+
+# ----------------------------------------------------------------------------- workload
+DATA = ("synthetic: the {cfg} scene script rendered by RenderFrame (synth.cpp:136-203, oracle restatement, "
+        "mt19937 depth noise 0.001*z^2, seed {seed}); identical bytes in both arms")
+
+
+def render_sequence(script: str):
+    """The workload generator, outside every timed region: all frames of a
+    scene script through RenderFrame on the host cores (frames are independent:
+    each seeds its own mt19937, synth.cpp:185). Returns (intrinsics, depth
+    [F,H,W] f32, rgb [F,H,W,3] u8, timestamps)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    from oracle import oracle as O
+
+    scene = O.Scene(script)
+    k = scene.k
+    F = len(scene)
+    depth = np.empty((F, k.height, k.width), dtype=np.float32)
+    rgb = np.empty((F, k.height, k.width, 3), dtype=np.uint8)
+    ts = np.empty(F)
+
+    def one(i):
+        f = scene.render(i)
+        depth[i], rgb[i], ts[i] = f["depth"], f["rgb"], f["timestamp"]
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:  # ctypes releases the GIL
+        list(ex.map(one, range(F)))
+    return k, depth, rgb, ts
+
+
+def workload_config(W, H, F):
+    """The `config` object of both arms (identical by construction)."""
+    return {"workload": f"{CONFIG}: synthetic room with 2 moving boxes, {W}x{H} RGB-D, 1 cm voxels, "
+                        f"{F}-frame ping-pong sequence, refine_depth off",
+            "resolution": [W, H], "voxel_size": 0.01, "frames_in_sequence": F,
+            "l2": "bricks (~20k, 80 MB) L2-resident by design; the frames (430 MB) exceed L2"}
+
+
+def parity_block(gpu, cpu):
+    """Per-frame comparison of the GPU arm's steps with the cpu_baseline leg
+    over the frames both processed (step s = frame seq_index(s) of the same
+    sequence from the same bootstrap): pose difference (translation, m;
+    rotation angle, rad) and count mismatches."""
+    import numpy as np
+
+    n = min(len(gpu), len(cpu))
+    worst_t = worst_r = 0.0
+    mism = {"registrations": 0, "iterations": 0, "masked_pixels": 0, "tracking_lost": 0}
+    max_masked = 0
+    for s in range(1, n):  # step 0 is the identity bootstrap in both
+        (gs, gp), (cs, cp) = gpu[s], cpu[s]
+        worst_t = max(worst_t, float(np.abs(gp[9:] - cp[9:]).max()))
+        Rd = gp[:9].reshape(3, 3) @ cp[:9].reshape(3, 3).T
+        axis = np.array([Rd[2, 1] - Rd[1, 2], Rd[0, 2] - Rd[2, 0], Rd[1, 0] - Rd[0, 1]])  # 2 sin(theta) * axis
+        worst_r = max(worst_r, float(np.arctan2(0.5 * np.linalg.norm(axis), 0.5 * (np.trace(Rd) - 1.0))))
+        for key in mism:
+            if int(gs[key]) != int(cs[key]):
+                mism[key] += 1
+        max_masked = max(max_masked, abs(int(gs["masked_pixels"]) - int(cs["masked_pixels"])))
+    return {"frames_compared": max(0, n - 1), "worst_pose_m": worst_t, "worst_pose_rad": worst_r,
+            "mismatched_frames": mism, "max_masked_pixel_diff": max_masked,
+            "bar": "pose <= 1e-4 m / 1e-4 rad (north_star)"}
 
 
 # ----------------------------------------------------------------------------- ours
@@ -122,7 +196,7 @@ def run_ours(args):
     import torch
 
     from paper_1905_02082_b200 import _lib as L
-    from paper_1905_02082_b200 import api, replicas, scenes, synth
+    from paper_1905_02082_b200 import api, replicas, scenes
 
     R = replicas.env()
     rank, world, local = R.rank, R.world, R.local
@@ -131,17 +205,14 @@ def run_ours(args):
     lib = L.load()
     cfgd = scenes.BENCH_CONFIGS[CONFIG]
     seed = replicas.sequence_seed(cfgd["seed"], R)  # independent sequence per replica
-    scene = synth.parse(scenes.config_script(CONFIG, seed=seed))
-    k = scene.intrinsics
-    H, W, F = k.height, k.width, len(scene)
-    depth = torch.empty((F, H, W), dtype=torch.float32, device="cuda")
-    rgb = torch.empty((F, H, W, 3), dtype=torch.uint8, device="cuda")
-    labels = torch.empty((F, H, W), dtype=torch.uint8, device="cuda")
-    for i in range(F):
-        synth.render(scene, i, depth[i], rgb[i], labels[i], device=local)
+    ok, depth_np, rgb_np, _ = render_sequence(scenes.config_script(CONFIG, seed=seed))
+    k = api.intrinsics(ok.fx, ok.fy, ok.cx, ok.cy, ok.width, ok.height, ok.depth_scale)
+    F, H, W = depth_np.shape
+    depth_h = torch.from_numpy(depth_np).pin_memory()
+    rgb_h = torch.from_numpy(rgb_np).pin_memory()
+    depth = depth_h.to("cuda")
+    rgb = rgb_h.to("cuda")
     torch.cuda.synchronize()
-    depth_h = depth.cpu().pin_memory()
-    rgb_h = rgb.cpu().pin_memory()
 
     cfg = api.pipeline_config(refine=False)
 
@@ -186,8 +257,10 @@ def run_ours(args):
     pv = api.Pipeline(cfg, device=local)
     dev_frames = make_frames(True)
     # warm-up through the same batched call as the timed steps
+    wst = (L.rf_frame_stats * max(1, args.warmup))()
+    wposes = (C.c_double * (12 * max(1, args.warmup)))()
     L.check(lib.rf_pipeline_process_frames(pv.h, batch(dev_frames, 0, args.warmup), C.c_uint64(args.warmup),
-                                           None, None))
+                                           wst, wposes))
     sptr = C.c_void_p()
     L.check(lib.rf_pipeline_stream(pv.h, C.byref(sptr)))
     stream = torch.cuda.ExternalStream(sptr.value)
@@ -211,6 +284,12 @@ def run_ours(args):
     agg = {"lost": sum(x.tracking_lost for x in st_arr), "iters": sum(x.iterations for x in st_arr),
            "regs": sum(x.registrations for x in st_arr), "masked": sum(x.masked_pixels for x in st_arr)}
     num_blocks = pv.volume().num_blocks()
+    gpu_steps = []  # (stats, pose) per step of the value run, warm-up included (parity block)
+    for j in range(args.warmup + args.steps):
+        sa, pa, jj = (wst, wposes, j) if j < args.warmup else (st_arr, poses, j - args.warmup)
+        gpu_steps.append(({"registrations": sa[jj].registrations, "iterations": sa[jj].iterations,
+                           "masked_pixels": sa[jj].masked_pixels, "tracking_lost": sa[jj].tracking_lost},
+                          np.array(pa[12 * jj:12 * jj + 12])))
 
     # ---- per-stage device times and work counters (roofline): the same steps
     # frame by frame with CUDA events between the kernels
@@ -277,13 +356,10 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": n,
         "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / n, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (GPU-rendered acceptance room + 2 moving boxes, depth noise 0.001*z^2)",
-        "config": {"workload": f"{CONFIG}: synthetic room with 2 moving boxes, 640x480 RGB-D, 1 cm voxels, "
-                               f"200-frame ping-pong sequence, refine_depth off",
-                   "resolution": [W, H], "voxel_size": 0.01, "frames_in_sequence": F,
-                   "parallelism": f"replicas x{world} (independent sequences, no collective)",
-                   "api": "rf_pipeline_process_frames (RunSequence: up to 64 frames enqueued back to back)",
-                   "l2": "working set (~20k bricks, 80 MB) L2-resident by design; frames > L2 in total"},
+        "data": DATA.format(cfg=CONFIG, seed=seed),
+        "config": workload_config(W, H, F),
+        "parallelism": f"replicas x{world} (independent sequences, no collective)",
+        "api": "rf_pipeline_process_frames (RunSequence: up to 64 frames enqueued back to back)",
         "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": P0 * 4 + P0 * 3,
                 "d2h_bytes_per_step": 192 + 32},
         "gpu_launches": int(gpu_launches),
@@ -300,37 +376,43 @@ def run_ours(args):
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(depth_h, rgb_h, k, args.cpu_sample_seconds)
+        line["cpu_baseline"], cpu_steps = cpu_baseline(depth_np, rgb_np, ok, args.cpu_sample_seconds)
+        line["parity"] = parity_block(gpu_steps, cpu_steps)
     print(json.dumps(line), flush=True)
     replicas.finish(R)
 
 
-def oracle_rate(depth_list, rgb_list, k, budget_s, threads, max_frames=None):
+def oracle_rate(frame, k, budget_s, threads, max_frames=None):
     """Oracle pipeline over a frame sample: bootstrap on frame 0 (untimed, as
-    the reference's fps excludes frame 0), then time frames until budget_s."""
+    the reference's fps excludes frame 0), then time frames until budget_s.
+    Returns the rate and every step's (stats, pose) for the parity block."""
     from oracle import oracle as O
 
-    ok = O.OIntr(k.fx, k.fy, k.cx, k.cy, k.width, k.height, k.depth_scale)
     p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads)))
-    p.process_frame(depth_list(0), rgb_list(0), ok, 0.0)
+    d, c = frame(0)
+    st, pose = p.process_frame(d, c, k, 0.0)
+    steps = [(st, pose)]
     spent, n = 0.0, 0
     while spent < budget_s and (max_frames is None or n < max_frames):
         i = n + 1
+        d, c = frame(i)
         t0 = time.perf_counter()
-        p.process_frame(depth_list(i), rgb_list(i), ok, i / 30.0)
+        st, pose = p.process_frame(d, c, k, i / 30.0)
         spent += time.perf_counter() - t0
+        steps.append((st, pose))
         n += 1
-    return n / spent, n, spent
+    return n / spent, n, spent, steps
 
 
-def cpu_baseline(depth_h, rgb_h, k, budget_s):
+def cpu_baseline(depth_np, rgb_np, k, budget_s):
     threads = os.cpu_count() or 1
-    F = depth_h.shape[0]
-    rate, n, spent = oracle_rate(lambda i: depth_h[seq_index(i, F)].numpy(), lambda i: rgb_h[seq_index(i, F)].numpy(),
-                                 k, budget_s, threads)
-    return {"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"oracle ProcessFrame on frames 1..{n} of the same {CONFIG} sequence ({spent:.1f} s, "
-                      f"{threads} threads for integrate/carve and registration)"}
+    F = depth_np.shape[0]
+    rate, n, spent, steps = oracle_rate(lambda i: (depth_np[seq_index(i, F)], rgb_np[seq_index(i, F)]), k,
+                                        budget_s, threads)
+    return ({"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
+             "sample": f"oracle ProcessFrame on steps 1..{n} of the same {CONFIG} ping-pong sequence and the same "
+                       f"frame bytes as the GPU arm ({spent:.1f} s, {threads} threads for integrate/carve and "
+                       f"registration)"}, steps)
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -346,24 +428,19 @@ def run_reference(args):
     from oracle import oracle as O
     from paper_1905_02082_b200 import scenes
 
-    scene = O.Scene(scenes.config_script(CONFIG))
-    F = len(scene)
-    cache = {}
+    seed = scenes.BENCH_CONFIGS[CONFIG]["seed"]
+    k, depth_np, rgb_np, _ = render_sequence(scenes.config_script(CONFIG, seed=seed))  # the GPU arm's bytes
+    F, H, W = depth_np.shape
 
     def frame(i):
         j = seq_index(i, F)
-        if j not in cache:
-            cache[j] = scene.render(j)
-        return cache[j]
+        return {"depth": depth_np[j], "rgb": rgb_np[j]}
 
     threads = os.cpu_count() or 1
-    k = scene.k
     p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads)))
     for i in range(args.warmup):
         f = frame(i)
         p.process_frame(f["depth"], f["rgb"], k, i / 30.0)
-    for i in range(args.warmup, args.warmup + args.steps):  # render outside the timed loop
-        frame(i)
     t0 = time.perf_counter()
     for i in range(args.warmup, args.warmup + args.steps):
         f = frame(i)
@@ -374,10 +451,8 @@ def run_reference(args):
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-        "data": "synthetic (oracle-rendered acceptance room + 2 moving boxes, mt19937 depth noise)",
-        "config": {"workload": f"{CONFIG}: synthetic room with 2 moving boxes, 640x480 RGB-D, 1 cm voxels, "
-                               f"200-frame ping-pong sequence, refine_depth off",
-                   "resolution": [k.width, k.height], "voxel_size": 0.01},
+        "data": DATA.format(cfg=CONFIG, seed=seed),
+        "config": workload_config(W, H, F),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"oracle ProcessFrame, steps {args.warmup}..{args.warmup + args.steps - 1} of the "
                                    f"{CONFIG} sequence, {threads} threads"},

@@ -524,6 +524,14 @@ class Scene:
         lib().o_scene_camera(self.s, C.c_uint64(i), C.byref(t), _p(pose))
         return t.value, pose
 
+    def world_to_object(self, prim, t):
+        """World-to-object pose of primitive `prim` at time t (synth.cpp:155-158)."""
+        L = lib()
+        L.o_scene_w2o.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_void_p]
+        pose = np.zeros(12)
+        L.o_scene_w2o(self.s, C.c_uint64(prim), C.c_double(t), _p(pose))
+        return pose
+
     def render(self, i):
         h, w = self.k.height, self.k.width
         depth = np.zeros((h, w), dtype=np.float32)

@@ -504,6 +504,11 @@ void o_scene_camera(void* s, uint64_t i, double* t, double pose[12]) {
     *t = c.first;
     c.second.ToArray(pose);
 }
+// World-to-object pose of primitive i at time t (RenderFrame's views, synth.cpp:155-158).
+uint64_t o_scene_num_prims(void* s) { return static_cast<Scene*>(s)->prims.size(); }
+void o_scene_w2o(void* s, uint64_t i, double t, double pose[12]) {
+    static_cast<Scene*>(s)->prims[i].PoseAt(t).Inverse().ToArray(pose);
+}
 int o_render(void* sp, uint64_t i, float* depth, uint8_t* rgb, float* true_depth, uint8_t* labels) {
     return Guard([&] {
         const Rendered r = RenderFrame(*static_cast<Scene*>(sp), i);

@@ -44,44 +44,67 @@ class Scene:
         return len(self.camera)
 
 
-def _quat_to_R(w, x, y, z):  # Quaterniond::toRotationMatrix after normalize
-    n = math.sqrt(w * w + x * x + y * y + z * z)
-    w, x, y, z = w / n, x / n, y / n, z / n
-    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
-                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
-                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+# Pose arithmetic in the reference's operation order (Eigen's Quaterniond
+# normalized / toRotationMatrix / slerp / quaternion-from-matrix and the 3x3
+# products, as synth.cpp and geometry.hpp use them), so the renderer sees the
+# same double-precision poses as RenderFrame (synth.cpp:136-203).
+def _normalized(w, x, y, z):
+    n = math.sqrt(((x * x + y * y) + z * z) + w * w)
+    return w / n, x / n, y / n, z / n
 
 
-def _R_to_quat(R):
-    t = np.trace(R)
-    if t > 0:
-        s = math.sqrt(t + 1.0) * 2
-        return np.array([0.25 * s, (R[2, 1] - R[1, 2]) / s, (R[0, 2] - R[2, 0]) / s, (R[1, 0] - R[0, 1]) / s])
-    i = int(np.argmax(np.diag(R)))
+def _quat_to_R(w, x, y, z):  # geometry.hpp:78-79: q.normalized().toRotationMatrix()
+    w, x, y, z = _normalized(w, x, y, z)
+    tx, ty, tz = 2.0 * x, 2.0 * y, 2.0 * z
+    twx, twy, twz = tx * w, ty * w, tz * w
+    txx, txy, txz = tx * x, ty * x, tz * x
+    tyy, tyz, tzz = ty * y, tz * y, tz * z
+    return np.array([[1.0 - (tyy + tzz), txy - twz, txz + twy],
+                     [txy + twz, 1.0 - (txx + tzz), tyz - twx],
+                     [txz - twy, tyz + twx, 1.0 - (txx + tyy)]])
+
+
+def _R_to_quat(m):  # Eigen's quaternion-from-matrix (Shepperd), as (w, x, y, z)
+    m = [[float(m[i][j]) for j in range(3)] for i in range(3)]
+    t = (m[0][0] + m[1][1]) + m[2][2]
+    if t > 0.0:
+        t = math.sqrt(t + 1.0)
+        w = 0.5 * t
+        t = 0.5 / t
+        return (w, (m[2][1] - m[1][2]) * t, (m[0][2] - m[2][0]) * t, (m[1][0] - m[0][1]) * t)
+    i = 0
+    if m[1][1] > m[0][0]:
+        i = 1
+    if m[2][2] > m[i][i]:
+        i = 2
     j, k = (i + 1) % 3, (i + 2) % 3
-    s = math.sqrt(R[i, i] - R[j, j] - R[k, k] + 1.0) * 2
-    q = np.zeros(4)
-    q[0] = (R[k, j] - R[j, k]) / s
-    q[1 + i] = 0.25 * s
-    q[1 + j] = (R[j, i] + R[i, j]) / s
-    q[1 + k] = (R[k, i] + R[i, k]) / s
-    return q
+    t = math.sqrt(((m[i][i] - m[j][j]) - m[k][k]) + 1.0)
+    c = [0.0, 0.0, 0.0]
+    c[i] = 0.5 * t
+    t = 0.5 / t
+    w = (m[k][j] - m[j][k]) * t
+    c[j] = (m[j][i] + m[i][j]) * t
+    c[k] = (m[k][i] + m[i][k]) * t
+    return (w, c[0], c[1], c[2])
 
 
-def _slerp(q0, q1, t):
-    d = float(np.dot(q0, q1))
-    if abs(d) >= 1 - 1e-15:
-        s0, s1 = 1 - t, t
+def _slerp(a, t, b):  # Eigen QuaternionBase::slerp; quaternions as (w, x, y, z)
+    one = 1.0 - 2.220446049250313e-16
+    d = ((a[1] * b[1] + a[2] * b[2]) + a[3] * b[3]) + a[0] * b[0]
+    absd = abs(d)
+    if absd >= one:
+        s0, s1 = 1.0 - t, t
     else:
-        th = math.acos(abs(d))
-        s0, s1 = math.sin((1 - t) * th) / math.sin(th), math.sin(t * th) / math.sin(th)
+        theta = math.acos(absd)
+        st = math.sin(theta)
+        s0, s1 = math.sin((1.0 - t) * theta) / st, math.sin(t * theta) / st
     if d < 0:
         s1 = -s1
-    return s0 * q0 + s1 * q1
+    return tuple(s0 * a[i] + s1 * b[i] for i in range(4))
 
 
 def _pose_at(prim: Primitive, time: float):
-    """Primitive::PoseAt (synth.cpp:35-45): object-to-world (R, t)."""
+    """Primitive::PoseAt (synth.cpp:26-45): object-to-world (R, t)."""
     kf = prim.keyframes
     if not kf:
         return np.eye(3), np.zeros(3)
@@ -94,8 +117,16 @@ def _pose_at(prim: Primitive, time: float):
         hi += 1
     (t0, R0, p0), (t1, R1, p1) = kf[hi - 1], kf[hi]
     al = (time - t0) / (t1 - t0)
-    q = _slerp(_R_to_quat(R0), _R_to_quat(R1), al)
-    return _quat_to_R(*q), (1 - al) * p0 + al * p1
+    q = _slerp(_R_to_quat(R0), al, _R_to_quat(R1))
+    t = np.array([(1.0 - al) * float(p0[i]) + al * float(p1[i]) for i in range(3)])
+    return _quat_to_R(*q), t
+
+
+def _inverse(R, t):
+    """Pose::Inverse (geometry.hpp:93-96): (R^T, -(R^T t)), rows summed left to right."""
+    Rt = [[float(R[j][i]) for j in range(3)] for i in range(3)]
+    ti = [-((Rt[i][0] * float(t[0]) + Rt[i][1] * float(t[1])) + Rt[i][2] * float(t[2])) for i in range(3)]
+    return np.array(Rt), np.array(ti)
 
 
 def parse(text: str) -> Scene:
@@ -140,11 +171,11 @@ def parse(text: str) -> Scene:
             name, t = tok[1], float(tok[2])
             tx, ty, tz, qx, qy, qz, qw = (float(x) for x in tok[3:10])
             target = next(p for p in prims if p.name == name)
-            target.keyframes.append((t, _quat_to_R(qw, qx, qy, qz), np.array([tx, ty, tz])))
+            target.keyframes.append((t, _quat_to_R(*_normalized(qw, qx, qy, qz)), np.array([tx, ty, tz])))
         elif d == "camera":
             t = float(tok[1])
             tx, ty, tz, qx, qy, qz, qw = (float(x) for x in tok[2:9])
-            pose = np.concatenate([_quat_to_R(qw, qx, qy, qz).reshape(9), [tx, ty, tz]])
+            pose = np.concatenate([_quat_to_R(*_normalized(qw, qx, qy, qz)).reshape(9), [tx, ty, tz]])
             camera.append((t, pose))
         else:
             raise ValueError(f"scene line {no}: unknown directive '{d}'")
@@ -165,9 +196,8 @@ def render(scene: Scene, index: int, depth, rgb, labels, device: int = 0):
     t, cam = scene.camera[index]
     arr = (_Prim * len(scene.prims))()
     for i, p in enumerate(scene.prims):
-        R, tr = _pose_at(p, t)
-        Rt = R.T
-        w2o = np.concatenate([Rt.reshape(9), -(Rt @ tr)])
+        Rw, tw = _inverse(*_pose_at(p, t))
+        w2o = np.concatenate([Rw.reshape(9), tw])
         q = arr[i]
         q.shape, q.dynamic, q.checker = p.shape, int(p.dynamic), int(p.checker)
         q.a[:] = list(p.a)
