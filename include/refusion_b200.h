@@ -21,6 +21,13 @@
  *  - Calls are synchronous like the reference (results are on the host when
  *    they return). Handles are not thread-safe, matching the reference's
  *    volume concurrency contract (tsdf_volume.hpp:64-66).
+ *  - Device-memory inputs (rf_frame.memory == RF_MEMORY_DEVICE, and the
+ *    device-pointer variants of the evaluation calls) are read on the
+ *    library's own CUDA streams, which are not ordered after the caller's
+ *    streams: the work that produced them must be complete when the call is
+ *    made (synchronise the producing stream first; the Python layer does).
+ *    rf_pipeline_stream() exposes the pipeline's stream for callers that want
+ *    to order against it with events instead.
  *  - block_side must be 8 (the reference default); other values return
  *    RF_UNSUPPORTED.
  */
@@ -55,7 +62,8 @@ typedef struct {
 } rf_intrinsics;
 
 /* VolumeConfig (tsdf_volume.hpp:14-29); hash_capacity 0 = next power of two
- * >= 4/3 * max_blocks (the load bound of spatial_hash.hpp:51). */
+ * >= 4/3 * max_blocks (the load bound of spatial_hash.hpp:51), at least 2^18
+ * (an overflowing allocation holds its not-yet-numbered keys in the table). */
 typedef struct {
     double voxel_size, truncation;
     int32_t block_side, max_weight, carve_weight, reserved0;
@@ -165,11 +173,26 @@ rf_status rf_volume_set_voxels(rf_volume* v, const int32_t* voxel_coords, uint64
 rf_status rf_volume_export_blocks(const rf_volume* v, int32_t* coords, uint8_t* voxels, uint64_t capacity,
                                   uint64_t* count);
 rf_status rf_volume_hash_occupancy(const rf_volume* v, uint8_t* bitmap);                  /* hash_capacity bytes */
+/* FindBlock (tsdf_volume.cpp:59-62): one hash probe on the device and one brick
+ * copied back; *found = 0 when the block is not allocated. voxels (512 x 8 B,
+ * x fastest) may be NULL. */
+rf_status rf_volume_find_block(const rf_volume* v, const int32_t block_coord[3], uint8_t* voxels, int32_t* found);
+/* Writes one allocated brick's 512 voxels (the write-back of the host layer's
+ * mutable VoxelHandle mirror, tsdf_volume.cpp:89-91); *found = 0 when absent. */
+rf_status rf_volume_write_block(rf_volume* v, const int32_t block_coord[3], const uint8_t* voxels, int32_t* found);
 rf_status rf_volume_reset(rf_volume* v);
 rf_status rf_volume_save(const rf_volume* v, const char* path);                           /* Save (TSDFVOL v1) */
 rf_status rf_volume_load(const char* path, int device, rf_volume** out);                  /* Load */
 
 /* ---- registration (registration.hpp:42-85) ----------------------------- */
+/* BuildPyramid (registration.hpp:42, registration.cpp:119-182) on the GPU.
+ * Outputs hold all levels back to back, level 0 first; level l has
+ * (width >> l) * (height >> l) pixels. depth: f32; intensity: f32, ToIntensity
+ * at level 0 then 2x2 means (requires f->rgb); mask_out: u8, any-of-2x2
+ * (requires mask). Any output may be NULL; k_out (levels records) receives
+ * CameraIntrinsics::Scaled(l). RF_INVALID_ARGUMENT when a level is empty. */
+rf_status rf_build_pyramid(const rf_frame* f, const uint8_t* mask, int32_t levels, int device, float* depth,
+                           float* intensity, uint8_t* mask_out, rf_intrinsics* k_out);
 rf_status rf_linearize(const rf_volume* v, const rf_frame* f, const double pose[12],
                        const rf_registration_config* cfg, const uint8_t* mask, rf_linearize_result* out);
 rf_status rf_evaluate_depth_error(const rf_volume* v, const rf_frame* f, const double pose[12],

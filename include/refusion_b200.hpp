@@ -20,6 +20,8 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <memory>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -276,6 +278,16 @@ struct Mesh {  // mesh.hpp:14-18
     std::vector<Vec3i> faces;
 };
 
+// Voxel access follows the reference: FindBlock returns a block pointer and
+// VoxelHandle a (const or mutable) voxel pointer (tsdf_volume.cpp:59-91).
+// The voxels live on the GPU, so the host layer keeps a lazy mirror of the
+// bricks a caller touches: a brick is fetched with one hash probe
+// (rf_volume_find_block) on first access, writes through a mutable handle
+// mark it dirty, and every GPU operation on the volume first writes dirty
+// bricks back (rf_volume_write_block) and then invalidates the mirror. A
+// pointer stays valid (the brick's storage is never freed while the volume
+// lives); after a GPU operation its contents are refreshed by the next
+// FindBlock / VoxelHandle of that brick.
 class TsdfVolume {
   public:
     explicit TsdfVolume(VolumeConfig config, int device = 0) : config_(config), owned_(true) {
@@ -288,7 +300,10 @@ class TsdfVolume {
     }
     TsdfVolume(const TsdfVolume&) = delete;
     TsdfVolume& operator=(const TsdfVolume&) = delete;
-    TsdfVolume(TsdfVolume&& o) noexcept : config_(o.config_), h_(o.h_), owned_(o.owned_) { o.h_ = nullptr; }
+    TsdfVolume(TsdfVolume&& o) noexcept
+        : config_(o.config_), h_(o.h_), owned_(o.owned_), mirror_(std::move(o.mirror_)), generation_(o.generation_) {
+        o.h_ = nullptr;
+    }
 
     const VolumeConfig& config() const { return config_; }
     rf_volume* handle() const { return h_; }
@@ -302,6 +317,7 @@ class TsdfVolume {
     void AllocateForFrame(const DepthImage& depth, const CameraIntrinsics& k, const Pose& camera_to_world,
                           const PixelMask* mask = nullptr) {
         detail::RequireSize(depth, k);
+        Sync();
         const rf_frame f = detail::ToC(depth, k);
         Check(rf_volume_allocate_for_frame(h_, &f, camera_to_world.data(), detail::MaskPtr(mask, k.width, k.height)));
     }
@@ -310,6 +326,7 @@ class TsdfVolume {
         if (!frame.SizesConsistent() && !(frame.color.Empty() && frame.depth.SameSize(frame.intrinsics.width,
                                                                                       frame.intrinsics.height)))
             throw std::invalid_argument("frame sizes are inconsistent");
+        Sync();
         const rf_frame f = detail::ToC(frame);
         Check(rf_volume_integrate(h_, &f, camera_to_world.data(),
                                   detail::MaskPtr(mask, frame.intrinsics.width, frame.intrinsics.height)));
@@ -317,12 +334,14 @@ class TsdfVolume {
     void CarveFreeSpace(const DepthImage& depth, const CameraIntrinsics& k, const Pose& camera_to_world,
                         int /*threads*/ = 1) {
         detail::RequireSize(depth, k);
+        Sync();
         const rf_frame f = detail::ToC(depth, k);
         Check(rf_volume_carve(h_, &f, camera_to_world.data()));
     }
 
     // Batched sampling (one launch for all points); single-point forms below.
     std::vector<SdfGradientSample> Sample(int mode, const std::vector<Vec3>& points) const {
+        Sync();
         const std::size_t n = points.size();
         std::vector<double> val(n), grad(3 * n);
         std::vector<std::uint8_t> ok(n);
@@ -341,19 +360,27 @@ class TsdfVolume {
     SdfGradientSample SampleIntensityWithGradient(const Vec3& p) const { return Sample(3, {p})[0]; }
     SdfGradientSample SampleSdfGradient(const Vec3& p) const { return Sample(4, {p})[0]; }
 
-    // VoxelHandle: the GPU owns the voxels, so reads return a copy and writes
-    // go through SetVoxel (the reference's mutable handle).
-    std::optional<Voxel> VoxelHandle(const Vec3i& voxel) const {
-        Voxel v;
-        std::uint8_t found = 0;
-        Check(rf_volume_get_voxels(h_, voxel.data(), 1, reinterpret_cast<std::uint8_t*>(&v), &found));
-        if (!found) return std::nullopt;
-        return v;
+    // FindBlock (tsdf_volume.cpp:59-62): nullptr when the block is not allocated.
+    const VoxelBlock* FindBlock(const Vec3i& block_coord) const {
+        const Mirror* m = Fetch(block_coord);
+        return m ? &m->block : nullptr;
+    }
+    // VoxelHandle (tsdf_volume.cpp:79-91): nullptr when the voxel's block is not allocated.
+    const Voxel* VoxelHandle(const Vec3i& voxel) const {
+        Mirror* m = Fetch(BlockOf(voxel));
+        return m ? &m->block.voxels[LocalIndex(voxel)] : nullptr;
+    }
+    Voxel* VoxelHandle(const Vec3i& voxel) {
+        Mirror* m = Fetch(BlockOf(voxel));
+        if (!m) return nullptr;
+        m->dirty = true;  // written back before the next GPU operation
+        return &m->block.voxels[LocalIndex(voxel)];
     }
     bool SetVoxel(const Vec3i& voxel, const Voxel& value) {
-        std::uint64_t missing = 0;
-        Check(rf_volume_set_voxels(h_, voxel.data(), 1, reinterpret_cast<const std::uint8_t*>(&value), &missing));
-        return missing == 0;
+        Voxel* v = VoxelHandle(voxel);
+        if (!v) return false;
+        *v = value;
+        return true;
     }
     Vec3 VoxelCenter(const Vec3i& v) const {
         return {(v[0] + 0.5) * config_.voxel_size, (v[1] + 0.5) * config_.voxel_size,
@@ -362,17 +389,14 @@ class TsdfVolume {
     double block_extent() const { return config_.block_side * config_.voxel_size; }
 
     bool AllocateBlock(const Vec3i& block_coord) {
+        Sync();
         std::int32_t created = 0;
         Check(rf_volume_allocate_blocks(h_, block_coord.data(), 1, &created));
-        return created != 0;
-    }
-    std::optional<VoxelBlock> FindBlock(const Vec3i& block_coord) const {
-        for (VoxelBlock& b : blocks())
-            if (b.coord == block_coord) return std::move(b);
-        return std::nullopt;
+        return created == 1;
     }
     // blocks() in allocation order (a device -> host copy).
     std::vector<VoxelBlock> blocks() const {
+        Sync();
         std::uint64_t n = 0;
         Check(rf_volume_export_blocks(h_, nullptr, nullptr, 0, &n));
         std::vector<std::int32_t> c(3 * n);
@@ -387,7 +411,10 @@ class TsdfVolume {
         return out;
     }
 
-    void Save(const std::string& path) const { Check(rf_volume_save(h_, path.c_str())); }
+    void Save(const std::string& path) const {
+        Sync();
+        Check(rf_volume_save(h_, path.c_str()));
+    }
     static TsdfVolume Load(const std::string& path, int device = 0) {
         rf_volume* h = nullptr;
         Check(rf_volume_load(path.c_str(), device, &h));
@@ -395,10 +422,50 @@ class TsdfVolume {
     }
     static TsdfVolume Borrow(rf_volume* h) { return TsdfVolume(h, false); }
 
+    // Writes back bricks modified through mutable VoxelHandles and invalidates
+    // the mirror; every GPU operation on the volume calls it first.
+    void Sync() const {
+        for (auto& [coord, m] : mirror_) {
+            if (!m->dirty) continue;
+            std::int32_t found = 0;
+            Check(rf_volume_write_block(h_, coord.data(), reinterpret_cast<const std::uint8_t*>(m->block.voxels.data()),
+                                        &found));
+            m->dirty = false;
+        }
+        ++generation_;
+    }
+
   private:
+    struct Mirror {
+        VoxelBlock block;
+        bool dirty = false;
+        std::uint64_t generation = 0;
+    };
     TsdfVolume(rf_volume* h, bool owned) : h_(h), owned_(owned) {
         // Config travels with the handle only through Save/Load; callers of
         // Borrow/Load that need it use the pipeline's config.
+    }
+    static int FloorDiv8(int a) { return a >= 0 ? a / 8 : -((-a + 7) / 8); }  // FloorDiv (tsdf_volume.hpp:136-140)
+    static Vec3i BlockOf(const Vec3i& v) { return {FloorDiv8(v[0]), FloorDiv8(v[1]), FloorDiv8(v[2])}; }
+    static std::size_t LocalIndex(const Vec3i& v) {
+        const Vec3i b = BlockOf(v);
+        return (std::size_t(v[2] - 8 * b[2]) * 8 + std::size_t(v[1] - 8 * b[1])) * 8 + std::size_t(v[0] - 8 * b[0]);
+    }
+    Mirror* Fetch(const Vec3i& bc) const {
+        auto it = mirror_.find(bc);
+        if (it != mirror_.end() && it->second->generation == generation_) return it->second.get();
+        std::vector<Voxel> vox(512);
+        std::int32_t found = 0;
+        Check(rf_volume_find_block(h_, bc.data(), reinterpret_cast<std::uint8_t*>(vox.data()), &found));
+        if (!found) return nullptr;
+        if (it == mirror_.end()) it = mirror_.emplace(bc, std::make_unique<Mirror>()).first;
+        Mirror& m = *it->second;
+        m.block.coord = bc;
+        if (m.block.voxels.size() != 512) m.block.voxels.resize(512);
+        std::memcpy(m.block.voxels.data(), vox.data(), 512 * sizeof(Voxel));  // in place: handed-out pointers stay valid
+        m.dirty = false;
+        m.generation = generation_;
+        return &m;
     }
     SdfSample Value(int mode, const Vec3& p) const {
         const SdfGradientSample s = Sample(mode, {p})[0];
@@ -407,6 +474,8 @@ class TsdfVolume {
     VolumeConfig config_;
     rf_volume* h_ = nullptr;
     bool owned_ = false;
+    mutable std::map<Vec3i, std::unique_ptr<Mirror>> mirror_;
+    mutable std::uint64_t generation_ = 1;
 };
 
 // ---------------------------------------------------------------- registration (registration.hpp:13-85)
@@ -444,8 +513,55 @@ struct RegistrationResult {
     ResidualImage residuals;
 };
 
+using IntensityImage = Image<float>;
+
+struct PyramidLevel {  // registration.hpp:32-37
+    CameraIntrinsics intrinsics;
+    DepthImage depth;
+    IntensityImage intensity;  // empty when the frame has no color
+    PixelMask mask;            // empty when no pixels are excluded
+};
+
+// BuildPyramid (registration.hpp:42): level 0 is the input, each level halves
+// the previous one (closest valid depth, mean intensity, any-of mask).
+inline std::vector<PyramidLevel> BuildPyramid(const Frame& frame, const PixelMask* mask, int levels, int device = 0) {
+    if (levels < 1) throw std::invalid_argument("pyramid needs at least one level");
+    const int w = frame.intrinsics.width, h = frame.intrinsics.height;
+    std::size_t total = 0;
+    for (int l = 0; l < levels; ++l) total += std::size_t(w >> l) * std::size_t(h >> l);
+    const bool color = !frame.color.Empty();
+    const std::uint8_t* m = detail::MaskPtr(mask, w, h);
+    std::vector<float> depth(total), inten(color ? total : 0);
+    std::vector<std::uint8_t> mout(m ? total : 0);
+    std::vector<rf_intrinsics> k(levels);
+    const rf_frame f = detail::ToC(frame);
+    Check(rf_build_pyramid(&f, m, levels, device, depth.data(), color ? inten.data() : nullptr,
+                           m ? mout.data() : nullptr, k.data()));
+    std::vector<PyramidLevel> out(levels);
+    std::size_t off = 0;
+    for (int l = 0; l < levels; ++l) {
+        const int lw = w >> l, lh = h >> l;
+        const std::size_t n = std::size_t(lw) * lh;
+        PyramidLevel& L = out[l];
+        L.intrinsics = frame.intrinsics.Scaled(l);
+        L.depth = DepthImage(lw, lh);
+        std::memcpy(L.depth.data(), depth.data() + off, n * sizeof(float));
+        if (color) {
+            L.intensity = IntensityImage(lw, lh);
+            std::memcpy(L.intensity.data(), inten.data() + off, n * sizeof(float));
+        }
+        if (m) {
+            L.mask = PixelMask(lw, lh);
+            std::memcpy(L.mask.data(), mout.data() + off, n);
+        }
+        off += n;
+    }
+    return out;
+}
+
 inline LinearizeResult Linearize(const TsdfVolume& volume, const Frame& frame, const Pose& pose,
                                  const RegistrationConfig& config, const PixelMask* mask = nullptr) {
+    volume.Sync();
     const rf_frame f = detail::ToC(frame);
     const rf_registration_config c = config.c();
     rf_linearize_result r{};
@@ -465,6 +581,7 @@ inline LinearizeResult Linearize(const TsdfVolume& volume, const Frame& frame, c
 inline std::pair<double, ResidualImage> EvaluateDepthError(const TsdfVolume& volume, const Frame& frame,
                                                            const Pose& pose, const PixelMask* mask = nullptr,
                                                            int /*threads*/ = 1) {
+    volume.Sync();
     const int w = frame.intrinsics.width, h = frame.intrinsics.height;
     const rf_frame f = detail::ToC(frame);
     ResidualImage res{Image<float>(w, h), PixelMask(w, h)};
@@ -476,6 +593,7 @@ inline std::pair<double, ResidualImage> EvaluateDepthError(const TsdfVolume& vol
 
 inline double EvaluateColorError(const TsdfVolume& volume, const Frame& frame, const Pose& pose,
                                  const PixelMask* mask = nullptr, int /*threads*/ = 1) {
+    volume.Sync();
     const rf_frame f = detail::ToC(frame);
     double e = 0.0;
     Check(rf_evaluate_color_error(volume.handle(), &f, pose.data(),
@@ -485,6 +603,7 @@ inline double EvaluateColorError(const TsdfVolume& volume, const Frame& frame, c
 
 inline RegistrationResult Register(const TsdfVolume& volume, const Frame& frame, const Pose& initial_pose,
                                    const PixelMask* mask, const RegistrationConfig& config) {
+    volume.Sync();
     const int w = frame.intrinsics.width, h = frame.intrinsics.height;
     const rf_frame f = detail::ToC(frame);
     const rf_registration_config c = config.c();
@@ -550,6 +669,7 @@ inline PixelMask BuildMask(const ResidualImage& r, const DepthImage& depth, cons
 // Ray-march of RenderVirtualDepth (depth_refinement.cpp:32-79) over `volume`.
 inline DepthImage Raycast(const TsdfVolume& volume, const Pose& view_pose, const CameraIntrinsics& k,
                           int bisection_iterations = 8) {
+    volume.Sync();
     DepthImage out(k.width, k.height);
     const rf_intrinsics ck = k.c();
     Check(rf_raycast(volume.handle(), view_pose.data(), &ck, bisection_iterations, out.data()));
@@ -557,6 +677,7 @@ inline DepthImage Raycast(const TsdfVolume& volume, const Pose& view_pose, const
 }
 
 inline Mesh ExtractMesh(const TsdfVolume& volume, int min_weight = 2, int /*threads*/ = 1) {
+    volume.Sync();
     rf_mesh* m = nullptr;
     Check(rf_volume_extract_mesh(volume.handle(), min_weight, &m));
     Mesh out;
@@ -656,6 +777,7 @@ class Pipeline {
         if (!frame.depth.SameSize(frame.intrinsics.width, frame.intrinsics.height) ||
             (!frame.color.Empty() && !frame.color.SameSize(frame.depth)))
             throw std::invalid_argument("frame sizes are inconsistent");
+        volume_->Sync();
         const rf_frame f = detail::ToC(frame);
         rf_frame_stats s{};
         double pose[12];
@@ -682,12 +804,14 @@ class Pipeline {
         }
         std::vector<rf_frame_stats> st(frames.size());
         std::vector<double> poses(12 * frames.size());
+        volume_->Sync();
         Check(rf_pipeline_process_frames(h_, cf.data(), cf.size(), st.data(), poses.data()));
         for (std::size_t i = 0; i < frames.size(); ++i)
             out.push_back(Record(frames[i].timestamp, st[i], poses.data() + 12 * i));
         return out;
     }
     void Finalize() {  // pipeline.cpp:133-135 (IntegrateFront until the window is empty)
+        volume_->Sync();
         if (!debug_sink_) {
             Check(rf_pipeline_finalize(h_));
             return;

@@ -392,6 +392,34 @@ class Volume:
         _check(lib().o_raycast(self.v, _p(_f64(pose)), C.byref(k), bisections, threads, _p(out)))
         return out
 
+    def save(self, path):
+        """TsdfVolume::Save (tsdf_volume.cpp:375-403)."""
+        lib().ov_save.argtypes = [C.c_void_p, C.c_char_p]
+        _check(lib().ov_save(self.v, str(path).encode()))
+
+    @classmethod
+    def load(cls, path):
+        """TsdfVolume::Load (tsdf_volume.cpp:405-449)."""
+        lib().ov_load.restype = C.c_void_p
+        lib().ov_load.argtypes = [C.c_char_p]
+        h = lib().ov_load(str(path).encode())
+        if not h:
+            raise OracleError(OTHER, lib().o_last_error().decode())
+        self = cls.__new__(cls)
+        self.v, self.owned = C.c_void_p(h), True
+        self._cfg = vol_cfg()
+        lib().ov_config(self.v, C.byref(self._cfg))
+        return self
+
+    def write_ply(self, path, min_weight=2, threads=1):
+        """ExtractMesh then WritePly (mesh.cpp:149-225)."""
+        m = C.c_void_p(lib().o_mesh_extract(self.v, min_weight, threads))
+        lib().o_mesh_write_ply.argtypes = [C.c_void_p, C.c_char_p]
+        try:
+            _check(lib().o_mesh_write_ply(m, str(path).encode()))
+        finally:
+            lib().o_mesh_free(m)
+
     def extract_mesh(self, min_weight=2, threads=1):
         m = C.c_void_p(lib().o_mesh_extract(self.v, min_weight, threads))
         nv, nf = C.c_uint64(), C.c_uint64()

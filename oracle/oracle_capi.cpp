@@ -1,6 +1,8 @@
 // ORACLE — test infrastructure only (see oracle.hpp). Flat C ABI over the
 // restatement so pytest (ctypes) can drive it. Pose arrays are 12 doubles:
 // row-major rotation then translation, camera-to-world.
+#include <fstream>
+#include <memory>
 #include <cstring>
 #include <memory>
 
@@ -468,6 +470,121 @@ int o_render_virtual_depth(int n, const float* const* depths, const uint8_t* con
             const DepthImage r = RefineDepth(window[0].frame.depth, v, far_value);
             std::memcpy(refined, r.d.data(), sizeof(float) * r.d.size());
         }
+    });
+}
+
+void ov_config(void* vp, OVolCfg* o) {
+    const VolumeConfig& c = static_cast<Volume*>(vp)->config();
+    o->voxel_size = c.voxel_size;
+    o->truncation = c.truncation;
+    o->block_side = c.block_side;
+    o->max_weight = c.max_weight;
+    o->carve_weight = c.carve_weight;
+    o->min_depth = c.min_depth;
+    o->max_depth = c.max_depth;
+    o->carve_clip = c.carve_clip;
+    o->max_blocks = c.max_blocks;
+}
+// TsdfVolume::Save (tsdf_volume.cpp:375-403): "TSDFVOL\0", u32 version 1, the
+// config, u64 block count, then per block in allocation order i32[3] + voxels.
+int ov_save(void* vp, const char* path) {
+    return Guard([&] {
+        const Volume* v = static_cast<Volume*>(vp);
+        const VolumeConfig& c = v->config();
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw std::runtime_error(std::string("cannot open for writing: ") + path);
+        auto w = [&](const auto& x) { out.write(reinterpret_cast<const char*>(&x), sizeof(x)); };
+        out.write("TSDFVOL\0", 8);
+        w(uint32_t(1));
+        w(c.voxel_size);
+        w(c.truncation);
+        w(int32_t(c.block_side));
+        w(int32_t(c.max_weight));
+        w(int32_t(c.carve_weight));
+        w(c.min_depth);
+        w(c.max_depth);
+        w(c.carve_clip);
+        w(uint64_t(c.max_blocks));
+        w(uint64_t(v->blocks().size()));
+        for (const VoxelBlock& b : v->blocks()) {
+            const int32_t cc[3] = {b.coord.x, b.coord.y, b.coord.z};
+            out.write(reinterpret_cast<const char*>(cc), sizeof(cc));
+            out.write(reinterpret_cast<const char*>(b.voxels.data()), std::streamsize(b.voxels.size() * sizeof(Voxel)));
+        }
+        if (!out) throw std::runtime_error(std::string("write failed: ") + path);
+    });
+}
+// TsdfVolume::Load (tsdf_volume.cpp:405-449): AllocateBlock in file order.
+void* ov_load(const char* path) {
+    Volume* vol = nullptr;
+    const int s = Guard([&] {
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw std::runtime_error(std::string("cannot open volume snapshot: ") + path);
+        char magic[8];
+        in.read(magic, 8);
+        if (!in || std::memcmp(magic, "TSDFVOL\0", 8) != 0) throw std::runtime_error("not a volume snapshot");
+        auto r = [&](auto& x) { in.read(reinterpret_cast<char*>(&x), sizeof(x)); };
+        uint32_t version = 0;
+        r(version);
+        if (version != 1) throw std::runtime_error("unsupported volume snapshot version");
+        VolumeConfig c;
+        int32_t bs = 0, mw = 0, cw = 0;
+        uint64_t mb = 0, nb = 0;
+        r(c.voxel_size);
+        r(c.truncation);
+        r(bs);
+        r(mw);
+        r(cw);
+        r(c.min_depth);
+        r(c.max_depth);
+        r(c.carve_clip);
+        r(mb);
+        r(nb);
+        if (!in) throw std::runtime_error("truncated volume snapshot");
+        c.block_side = bs;
+        c.max_weight = mw;
+        c.carve_weight = cw;
+        c.max_blocks = mb;
+        auto v = std::make_unique<Volume>(c);
+        for (uint64_t i = 0; i < nb; ++i) {
+            int32_t cc[3];
+            in.read(reinterpret_cast<char*>(cc), sizeof(cc));
+            v->AllocateBlock(V3i{cc[0], cc[1], cc[2]});
+            VoxelBlock& b = v->blocks_mut().back();
+            in.read(reinterpret_cast<char*>(b.voxels.data()), std::streamsize(b.voxels.size() * sizeof(Voxel)));
+            if (!in) throw std::runtime_error("truncated volume snapshot");
+        }
+        vol = v.release();
+    });
+    return s == O_OK ? vol : nullptr;
+}
+
+// WritePly (mesh.cpp:192-225): ASCII header, binary little-endian body; the
+// colour properties only when the mesh has colours.
+int o_mesh_write_ply(void* mp, const char* path) {
+    return Guard([&] {
+        const Mesh* m = static_cast<Mesh*>(mp);
+        const size_t nv = m->vertices.size() / 3, nf = m->faces.size() / 3;
+        const bool colored = !m->colors.empty();
+        std::ofstream out(path, std::ios::binary);
+        if (!out) throw std::runtime_error(std::string("cannot open for writing: ") + path);
+        out << "ply\nformat binary_little_endian 1.0\n";
+        out << "element vertex " << nv << "\n";
+        out << "property float x\nproperty float y\nproperty float z\n";
+        if (colored) out << "property uchar red\nproperty uchar green\nproperty uchar blue\n";
+        out << "element face " << nf << "\n";
+        out << "property list uchar int vertex_indices\n";
+        out << "end_header\n";
+        for (size_t i = 0; i < nv; ++i) {
+            out.write(reinterpret_cast<const char*>(&m->vertices[3 * i]), 12);
+            if (colored) out.write(reinterpret_cast<const char*>(&m->colors[3 * i]), 3);
+        }
+        for (size_t i = 0; i < nf; ++i) {
+            const uint8_t three = 3;
+            out.write(reinterpret_cast<const char*>(&three), 1);
+            out.write(reinterpret_cast<const char*>(&m->faces[3 * i]), 12);
+        }
+        if (!out) throw std::runtime_error(std::string("write failed: ") + path);
     });
 }
 

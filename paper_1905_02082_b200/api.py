@@ -92,6 +92,11 @@ class Frame:
         dev = _is_cuda(self.depth)
         f.memory = L.RF_MEMORY_DEVICE if dev else L.RF_MEMORY_HOST
         if dev:
+            k = self.intrinsics
+            _check_device_tensor(self.depth, "float32", (k.height, k.width), "depth")
+            if self.rgb is not None:
+                _check_device_tensor(self.rgb, "uint8", (k.height, k.width, 3), "rgb", self.depth.device)
+            _producer_done(self.depth)
             f.depth = self.depth.data_ptr()
             f.rgb = None if self.rgb is None else self.rgb.data_ptr()
             self._keep = ()
@@ -108,10 +113,34 @@ def _is_cuda(x):
     return hasattr(x, "is_cuda") and x.is_cuda
 
 
+def _check_device_tensor(t, dtype, shape, name, device=None):
+    """A CUDA tensor handed to the C ABI as a raw pointer: exact dtype, dense
+    row-major layout, the expected size, on the frame's device."""
+    if str(t.dtype) != "torch." + dtype:
+        raise ValueError(f"{name}: expected a torch.{dtype} tensor, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: tensor must be contiguous")
+    if tuple(t.shape) != tuple(shape) and t.numel() != int(np.prod(shape)):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: tensor is on {t.device}, the frame on {device}")
+
+
+def _producer_done(t):
+    """The library reads device inputs on its own streams (refusion_b200.h):
+    finish the work torch has queued for them first."""
+    import torch
+
+    torch.cuda.current_stream(t.device).synchronize()
+
+
 def _mask_ptr(mask, frame: Frame):
     if mask is None:
         return None, None
     if _is_cuda(frame.depth):
+        k = frame.intrinsics
+        _check_device_tensor(mask, "uint8", (k.height, k.width), "mask", frame.depth.device)
+        _producer_done(mask)
         return C.c_void_p(mask.data_ptr()), mask
     m = np.ascontiguousarray(mask, dtype=np.uint8)
     return C.c_void_p(m.ctypes.data), m
@@ -211,6 +240,23 @@ class TsdfVolume:
         L.check(_lib().rf_volume_export_blocks(self.h, _p(coords), _p(vox), C.c_uint64(n), C.byref(cnt)))
         return coords, vox
 
+    def find_block(self, block_coord):
+        """FindBlock (tsdf_volume.cpp:59-62): the brick's 512 voxels (x fastest)
+        or None when the block is not allocated (one hash probe on the device)."""
+        c = _i32(block_coord).reshape(3)
+        vox = np.zeros(512, dtype=VOXEL_DTYPE)
+        found = C.c_int32()
+        L.check(_lib().rf_volume_find_block(self.h, _p(c), _p(vox), C.byref(found)))
+        return vox if found.value else None
+
+    def write_block(self, block_coord, voxels) -> bool:
+        """Writes an allocated brick's 512 voxels; False when it does not exist."""
+        c = _i32(block_coord).reshape(3)
+        v = np.ascontiguousarray(voxels, dtype=VOXEL_DTYPE).reshape(512)
+        found = C.c_int32()
+        L.check(_lib().rf_volume_write_block(self.h, _p(c), _p(v), C.byref(found)))
+        return bool(found.value)
+
     def hash_occupancy(self) -> np.ndarray:
         bm = np.zeros(self.hash_capacity(), dtype=np.uint8)
         L.check(_lib().rf_volume_hash_occupancy(self.h, _p(bm)))
@@ -239,7 +285,8 @@ class TsdfVolume:
         out = L.rf_linearize_result()
         L.check(_lib().rf_linearize(self.h, C.byref(f), _p(_f64(pose)), C.byref(cfg), mp, C.byref(out)))
         return dict(H=np.array(out.H).reshape(6, 6), b=np.array(out.b), depth_error=out.depth_error,
-                    color_error=out.color_error, error=out.error, valid=out.valid_count)
+                    color_error=out.color_error, error=out.error, valid=out.valid_count,
+                    degenerate=bool(out.degenerate))
 
     def evaluate_depth_error(self, frame: Frame, pose, mask=None):
         f = frame.c()
@@ -294,6 +341,30 @@ class TsdfVolume:
         finally:
             _lib().rf_mesh_destroy(m)
         return v, c, f
+
+
+def build_pyramid(frame: Frame, mask=None, levels=3, device=0):
+    """BuildPyramid (registration.hpp:42, registration.cpp:119-182) on the GPU:
+    one dict per level {intrinsics, depth, intensity (None without colour),
+    mask (None without a mask)}, level 0 first."""
+    k = frame.intrinsics
+    sizes = [(k.width >> l) * (k.height >> l) for l in range(max(levels, 0))]
+    tot = max(sum(sizes), 1)
+    f = frame.c()
+    mp, _keep = _mask_ptr(mask, frame)
+    depth = np.zeros(tot, np.float32)
+    inten = np.zeros(tot, np.float32) if frame.rgb is not None else None
+    mout = np.zeros(tot, np.uint8) if mask is not None else None
+    ks = (L.rf_intrinsics * max(levels, 1))()
+    L.check(_lib().rf_build_pyramid(C.byref(f), mp, int(levels), device, _p(depth), _p(inten), _p(mout), ks))
+    out, off = [], 0
+    for l, n in enumerate(sizes):
+        w, h = k.width >> l, k.height >> l
+        out.append(dict(intrinsics=ks[l], depth=depth[off:off + n].reshape(h, w),
+                        intensity=None if inten is None else inten[off:off + n].reshape(h, w),
+                        mask=None if mout is None else mout[off:off + n].reshape(h, w)))
+        off += n
+    return out
 
 
 # ------------------------------------------------------------------ refinement
@@ -514,7 +585,10 @@ def nearest_distances(queries, reference, device=0):
         import torch
         q = queries.reshape(-1, 3).to(torch.float32).contiguous()
         r = reference.reshape(-1, 3).to(torch.float32).contiguous()
+        if r.device != q.device:
+            raise ValueError("queries and reference must be on the same device")
         out = torch.empty(q.shape[0], dtype=torch.float64, device=q.device)
+        _producer_done(q)  # the conversions above ran on torch's stream
         L.check(_lib().rf_nearest_distances(C.c_void_p(q.data_ptr()), C.c_uint64(q.shape[0]),
                                             C.c_void_p(r.data_ptr()), C.c_uint64(r.shape[0]),
                                             L.RF_MEMORY_DEVICE, q.device.index or 0, C.c_void_p(out.data_ptr())))
@@ -534,6 +608,7 @@ def distance_cdf(distances, bin_edges, device=0):
     out = np.zeros(len(e))
     if _is_cuda(distances):
         d = distances.reshape(-1).double().contiguous()
+        _producer_done(d)
         L.check(_lib().rf_distance_cdf(C.c_void_p(d.data_ptr()), C.c_uint64(d.numel()), L.RF_MEMORY_DEVICE,
                                        d.device.index or 0, _p(e), C.c_uint64(len(e)), _p(out)))
         return out

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -27,10 +28,16 @@ namespace rfb {
 struct FrameSignal {
     TrackOut out;
     uint32_t counters[kNumCounters];
+    unsigned long long t_start;  // %globaltimer before the batch's first frame (record 0 only)
+    unsigned long long t_end;    // %globaltimer when the frame's work completed
     unsigned long long seq;
 };
+__global__ void k_stamp(FrameSignal* sig) {
+    if (threadIdx.x == 0) sig->t_start = global_ns();
+}
 __global__ void k_signal(const TrackOut* out, const uint32_t* counters, FrameSignal* sig, unsigned long long seq) {
     pdl_enter();
+    if (threadIdx.x == 0) sig->t_end = global_ns();
     const uint32_t* src = reinterpret_cast<const uint32_t*>(out);
     uint32_t* dst = reinterpret_cast<uint32_t*>(&sig->out);
     for (int i = threadIdx.x; i < int(sizeof(TrackOut) / 4); i += blockDim.x) dst[i] = __ldcg(src + i);
@@ -51,6 +58,50 @@ __global__ void k_import(VolumeView V, const int* coords, uint32_t n, uint32_t b
     while (atomicCAS(&V.slots[idx].key, kEmptyKey, key) != kEmptyKey) idx = (idx + 1) & V.hash_mask;
     V.slots[idx].value = base + i;
     V.coords[base + i] = make_int4(x, y, z, int(idx));
+}
+// Start of an allocation (AllocateForFrame / AllocateBlock batch): snapshot
+// the brick count (assign_new numbers new bricks from it) and clear the
+// per-allocation counters. The per-frame path does this inside k_track.
+__global__ void k_alloc_begin(uint32_t* c, uint32_t max_blocks) {
+    if (threadIdx.x == 0) {
+        c[kBlocksBefore] = min(c[kNumBlocks], max_blocks);
+        c[kOverflow] = 0;
+        c[kVisible] = 0;
+        c[kDdaVisits] = 0;
+        c[kNewBlocks] = 0;
+    }
+}
+// FindBlock (tsdf_volume.cpp:59-62): one probe, then the brick's 512 voxels
+// (one per thread) copied to / from `io`.
+__global__ void k_block_rw(VolumeView V, int x, int y, int z, uint2* io, int* found, int write) {
+    __shared__ uint32_t b;
+    if (threadIdx.x == 0) {
+        b = hash_find(V, x, y, z);
+        *found = b != kInvalid;
+    }
+    __syncthreads();
+    if (b == kInvalid) return;
+    uint2* vox = reinterpret_cast<uint2*>(V.voxels + size_t(b) * kBrickVoxels) + threadIdx.x;
+    if (write) *vox = io[threadIdx.x];
+    else io[threadIdx.x] = *vox;
+}
+// Sticky halt of the model volume when the refinement temp volume overflowed
+// (RenderVirtualDepth throws before anything else of the frame runs).
+__global__ void k_halt_if(const uint32_t* src, uint32_t* halt) {
+    if (threadIdx.x == 0 && *src) *halt = 1u;
+}
+// Re-inserts bricks [0, n) into an emptied table (after an overflow left
+// pending keys behind): the occupied-slot set is again exactly the allocated
+// keys', as in the reference, whose AllocateBlock threw before inserting.
+__global__ void k_rehash(VolumeView V, uint32_t n) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n) return;
+    const int4 c = V.coords[b];
+    const unsigned long long key = pack_key(c.x, c.y, c.z);
+    uint32_t idx = hash_coord(c.x, c.y, c.z) & V.hash_mask;
+    while (atomicCAS(&V.slots[idx].key, kEmptyKey, key) != kEmptyKey) idx = (idx + 1) & V.hash_mask;
+    V.slots[idx].value = b;
+    V.coords[b].w = int(idx);
 }
 }  // namespace rfb
 
@@ -101,6 +152,8 @@ struct Workspace {
     int track_grid = 0;
     int parity = 0;  // alternates the grid-barrier counter between cooperative launches
     DevBuf depth, rgb, mask_in, pose, res_sq, res_valid, mwork, levels, gsync, partials, result, out, list;
+    DevBuf ll;                // the all-reduce's flagged lines (rf_grid.cuh block_grid_allreduce)
+    uint32_t ll_seq = 0;      // launch sequence number of the flags
     DevBuf trace;            // per-pass timeline when RF_TRACE_FILE is set (diagnostics)
     std::string trace_path;
     TrackOut* h_out = nullptr;
@@ -133,6 +186,8 @@ struct Workspace {
         gsync.ensure(sizeof(GridSync));
         CK(cudaMemset(gsync.p, 0, sizeof(GridSync)));
         partials.ensure(2 * size_t(track_grid) * kRedStride * sizeof(double));
+        ll.ensure(2 * size_t(track_grid) * 32 * sizeof(uint4));
+        CK(cudaMemset(ll.p, 0, ll.n));
         result.ensure(kRedStride * sizeof(double));
         out.ensure(sizeof(TrackOut));
         pose.ensure(12 * sizeof(double));
@@ -148,7 +203,7 @@ struct Workspace {
     }
     void destroy() {
         for (DevBuf* b : {&depth, &rgb, &mask_in, &pose, &res_sq, &res_valid, &mwork, &levels, &gsync, &partials,
-                          &result, &out, &list, &trace})
+                          &result, &out, &list, &trace, &ll})
             b->release();
         if (h_out) cudaFreeHost(h_out);
         if (h_counters) cudaFreeHost(h_counters);
@@ -185,6 +240,25 @@ struct Workspace {
         L = levels_needed;
     }
     void sync() { CK(cudaStreamSynchronize(stream)); }
+    // Grid-sync state for one cooperative launch: the barrier counters of this
+    // launch's parity, and a fresh flag sequence number for the all-reduce
+    // lines (after 2^20 - 1 launches the lines are cleared so no stale flag
+    // can ever match).
+    GridCtx grid() {
+        GridCtx g{};
+        g.sync = gsync.as<GridSync>();
+        g.partials = partials.as<double>();
+        g.result = result.as<double>();
+        g.parity = parity;
+        parity ^= 1;
+        g.ll = ll.as<uint4>();
+        if (++ll_seq >= (1u << 20)) {
+            CK(cudaMemsetAsync(ll.p, 0, ll.n, stream));
+            ll_seq = 1;
+        }
+        g.seq = ll_seq;
+        return g;
+    }
     // Enqueues k_signal after the frame's work: the frame's results land in
     // record `slot`, tagged with a new sequence number (returned).
     unsigned long long signal(const TrackOut* d_out, const uint32_t* d_counters, int slot) {
@@ -266,6 +340,7 @@ struct rf_volume {
     rf_volume_config cfg{};
     uint64_t cap = 0;
     DevBuf slots, coords, voxels, links, counters;
+    DevBuf ord, newlist;  // allocation order (model volumes only, VolumeView::ord)
     DevBuf win_first;  // refinement temp volume: first window entry per hash slot
     VolumeView view{};
     Workspace ws;
@@ -333,6 +408,35 @@ struct rf_volume {
         }
         CK(cudaMemsetAsync(view.counters, 0, kNumCounters * sizeof(uint32_t), ws.stream));
     }
+    void begin_alloc() {
+        k_alloc_begin<<<1, 32, 0, ws.stream>>>(view.counters, uint32_t(cfg.max_blocks));
+        CK(cudaGetLastError());
+    }
+    // Standalone allocation epilogue: pool indices for the claimed keys (model
+    // volumes), then link records.
+    void assign(int* created = nullptr) {
+        if (view.ord) {
+            k_assign<<<148, 256, 0, ws.stream>>>(view, created);
+            CK(cudaGetLastError());
+        }
+        link();
+    }
+    // After an allocation overflowed (the host is about to throw
+    // ResourceLimitError): the kept bricks are the first max_blocks in
+    // allocation order already; drop the pending keys by rebuilding the table
+    // from the bricks, relink, clear the sticky halt. Stream must be idle.
+    void recover_overflow() {
+        const uint64_t nb = num_blocks();
+        CK(cudaMemsetAsync(slots.p, 0xFF, cap * sizeof(HashSlot), ws.stream));
+        CK(cudaMemsetAsync(links.p, 0xFF, cap * kLinkStride * sizeof(uint32_t), ws.stream));
+        if (ord.p) CK(cudaMemsetAsync(ord.p, 0xFF, cap * sizeof(unsigned long long), ws.stream));
+        if (nb) k_rehash<<<unsigned((nb + 255) / 256), 256, 0, ws.stream>>>(view, uint32_t(nb));
+        CK(cudaGetLastError());
+        CK(cudaMemsetAsync(view.counters + kNewBlocks, 0, 4 * 4, ws.stream));  // kNewBlocks, kLinked, kLinkDone, kHalt
+        CK(cudaMemsetAsync(view.counters + kOverflow, 0, 4, ws.stream));
+        link();
+        ws.sync();
+    }
     // RenderVirtualDepth's temp-volume fusion (depth_refinement.cpp:25-30) of
     // n same-size entries, front to back, kMaxWin entries per alloc / cull /
     // fuse triple (rf_volume.cuh WindowArgs).
@@ -387,7 +491,8 @@ struct rf_volume {
         CK(cudaGetLastError());
     }
     void fuse(const float* d, const uint8_t* rgb, const uint8_t* mask, const rf_intrinsics& k, const double* pose,
-              const int* lost, bool carve, bool integrate, bool carve_only_before, bool reset_visible = true) {
+              const int* lost, bool carve, bool integrate, bool carve_only_before, bool reset_visible = true,
+              bool assign = false) {
         // The visible list is appended to from counters[kVisible]; the frame
         // path's tracking kernel already zeroed it.
         if (reset_visible) reset_counter(kVisible);
@@ -400,6 +505,7 @@ struct rf_volume {
         ca.do_carve = carve;
         ca.do_integrate = integrate;
         ca.carve_only_before = carve_only_before;
+        ca.assign = assign && view.ord != nullptr;
         launch(k_cull, 4 * 148, 256, 0, ws.stream, false, ca);
         if (prof) CK(cudaEventRecord(prof[3], ws.stream));
         FuseArgs fa{};
@@ -442,9 +548,6 @@ struct rf_volume {
         for (int i = 0; i < 3; ++i) a.F.mwork[i] = ws.mwork.as<uint8_t>() + i * n;
         a.F.grow = ws.mwork.as<uint8_t>() + (3 * n + 255) / 256 * 256;
         a.F.ffstamp = ws.ffstamp();
-        a.grid.sync = ws.gsync.as<GridSync>();
-        a.grid.partials = ws.partials.as<double>();
-        a.grid.result = ws.result.as<double>();
         a.pose_state = ws.pose.as<double>();
         a.out = ws.out.as<TrackOut>();
         a.reg.levels = levels;
@@ -462,8 +565,7 @@ struct rf_volume {
     }
     void launch_track(TrackArgs& a) {
         if (a.trace) CK(cudaMemsetAsync(a.trace, 0, kTracePasses * 8 * sizeof(unsigned long long), ws.stream));
-        a.grid.parity = ws.parity;
-        ws.parity ^= 1;
+        a.grid = ws.grid();
         launch(k_track, ws.track_grid, kTrackThreads, kTrackDynSmem, ws.stream, true, a);
     }
     TrackOut fetch_out() {
@@ -511,14 +613,19 @@ void check_frame_dims(const rf_frame* f) {
     require(f->intrinsics.width > 0 && f->intrinsics.height > 0, RF_INVALID_ARGUMENT, "bad image size");
 }
 
-void create_volume(const rf_volume_config* cfg, int device, rf_volume** out) {
+void create_volume(const rf_volume_config* cfg, int device, rf_volume** out, bool ordered = true) {
     require(cfg && out, RF_INVALID_ARGUMENT, "null argument");
     validate_volume_config(*cfg);
     CK(cudaSetDevice(device));
     auto v = std::make_unique<rf_volume>();
     v->device = device;
     v->cfg = *cfg;
-    v->cap = cfg->hash_capacity ? cfg->hash_capacity : next_pow2((cfg->max_blocks * 4 + 2) / 3);
+    // Default capacity: the reference's load bound (spatial_hash.hpp:51) for a
+    // full pool, but at least 2^18 slots: an allocation that overflows keeps
+    // its pending keys in the table until the pool indices are assigned, so the
+    // table must hold one frame's distinct keys even when max_blocks is tiny.
+    v->cap = cfg->hash_capacity ? cfg->hash_capacity
+                                : std::max<uint64_t>(next_pow2((cfg->max_blocks * 4 + 2) / 3), uint64_t(1) << 18);
     require((v->cap & (v->cap - 1)) == 0 && v->cap <= (1ull << 31), RF_INVALID_ARGUMENT,
             "hash_capacity must be a power of two <= 2^31");
     require(v->cap >= cfg->max_blocks, RF_INVALID_ARGUMENT, "hash_capacity must be >= max_blocks");
@@ -527,7 +634,12 @@ void create_volume(const rf_volume_config* cfg, int device, rf_volume** out) {
     v->voxels.ensure(cfg->max_blocks * kBrickVoxels * sizeof(Voxel));
     v->links.ensure(v->cap * kLinkStride * sizeof(uint32_t));  // one record per hash slot
     v->counters.ensure(kNumCounters * sizeof(uint32_t));
+    if (ordered) {
+        v->ord.ensure(v->cap * sizeof(unsigned long long));
+        v->newlist.ensure(v->cap * sizeof(uint32_t));
+    }
     v->ws.init(device);
+    if (ordered) CK(cudaMemsetAsync(v->ord.p, 0xFF, v->cap * sizeof(unsigned long long), v->ws.stream));
     CK(cudaMemsetAsync(v->slots.p, 0xFF, v->cap * sizeof(HashSlot), v->ws.stream));
     CK(cudaMemsetAsync(v->links.p, 0xFF, v->cap * kLinkStride * sizeof(uint32_t), v->ws.stream));
     CK(cudaMemsetAsync(v->voxels.p, 0, cfg->max_blocks * kBrickVoxels * sizeof(Voxel), v->ws.stream));
@@ -541,6 +653,8 @@ void create_volume(const rf_volume_config* cfg, int device, rf_volume** out) {
     V.voxels = v->voxels.as<Voxel>();
     V.links = v->links.as<uint32_t>();
     V.counters = v->counters.as<uint32_t>();
+    V.ord = ordered ? v->ord.as<unsigned long long>() : nullptr;
+    V.newlist = ordered ? v->newlist.as<uint32_t>() : nullptr;
     V.voxel_size = cfg->voxel_size;
     V.inv_voxel_size = 1.0 / cfg->voxel_size;
     V.truncation = cfg->truncation;
@@ -587,6 +701,9 @@ void rf_volume_destroy(rf_volume* v) {
     v->voxels.release();
     v->links.release();
     v->counters.release();
+    v->ord.release();
+    v->newlist.release();
+    v->win_first.release();
     delete v;
 }
 
@@ -608,23 +725,27 @@ rf_status rf_volume_hash_capacity(const rf_volume* v, uint64_t* out) {
 rf_status rf_volume_allocate_blocks(rf_volume* v, const int32_t* coords, uint64_t n, int32_t* created) {
     return guard([&] {
         require(v && (coords || n == 0), RF_INVALID_ARGUMENT, "null argument");
+        require(n < (1ull << 31), RF_INVALID_ARGUMENT, "too many coordinates in one call");
         if (n == 0) return;
         CK(cudaSetDevice(v->device));
         DevBuf dc, dr;
         dc.ensure(n * 12);
         dr.ensure(n * 4);
         CK(cudaMemcpyAsync(dc.p, coords, n * 12, cudaMemcpyHostToDevice, v->ws.stream));
-        v->reset_counter(kOverflow);
+        CK(cudaMemsetAsync(dr.p, 0, n * 4, v->ws.stream));
+        v->begin_alloc();
         k_alloc_coords<<<unsigned((n + 255) / 256), 256, 0, v->ws.stream>>>(v->view, dc.as<int>(), int(n),
                                                                              dr.as<int>());
         CK(cudaGetLastError());
-        v->link();
+        v->assign(dr.as<int>());  // AllocateBlock in coordinate order (tsdf_volume.cpp:64-77)
         if (created) CK(cudaMemcpyAsync(created, dr.p, n * 4, cudaMemcpyDeviceToHost, v->ws.stream));
         v->ws.sync();
         dc.release();
         dr.release();
-        require(v->overflow() == 0, RF_RESOURCE_LIMIT,
-                "voxel block budget exhausted (" + std::to_string(v->cfg.max_blocks) + " blocks)");
+        if (v->overflow()) {
+            v->recover_overflow();
+            throw Error{RF_RESOURCE_LIMIT, "voxel block budget exhausted (" + std::to_string(v->cfg.max_blocks) + " blocks)"};
+        }
     });
 }
 
@@ -636,13 +757,14 @@ rf_status rf_volume_allocate_for_frame(rf_volume* v, const rf_frame* f, const do
         const float* d = v->depth_of(f);
         const uint8_t* m = v->mask_of(f, mask);
         v->upload_pose(pose);
-        v->reset_counter(kDdaVisits);
-        v->reset_counter(kOverflow);
+        v->begin_alloc();
         v->allocate(d, m, f->intrinsics, v->ws.pose.as<double>(), nullptr);
-        v->link();
+        v->assign();
         v->ws.sync();
-        require(v->overflow() == 0, RF_RESOURCE_LIMIT,
-                "voxel block budget exhausted (" + std::to_string(v->cfg.max_blocks) + " blocks)");
+        if (v->overflow()) {
+            v->recover_overflow();
+            throw Error{RF_RESOURCE_LIMIT, "voxel block budget exhausted (" + std::to_string(v->cfg.max_blocks) + " blocks)"};
+        }
     });
 }
 
@@ -782,6 +904,7 @@ rf_status rf_volume_reset(rf_volume* v) {
         CK(cudaMemsetAsync(v->slots.p, 0xFF, v->cap * sizeof(HashSlot), v->ws.stream));
         CK(cudaMemsetAsync(v->voxels.p, 0, nb * kBrickVoxels * sizeof(Voxel), v->ws.stream));
         CK(cudaMemsetAsync(v->links.p, 0xFF, v->cap * kLinkStride * sizeof(uint32_t), v->ws.stream));
+        if (v->ord.p) CK(cudaMemsetAsync(v->ord.p, 0xFF, v->cap * sizeof(unsigned long long), v->ws.stream));
         CK(cudaMemsetAsync(v->counters.p, 0, kNumCounters * sizeof(uint32_t), v->ws.stream));
         v->ws.sync();
     });
@@ -885,7 +1008,133 @@ rf_status rf_volume_load(const char* path, int device, rf_volume** out) {
     });
 }
 
+static rf_status block_rw(const rf_volume* cv, const int32_t c[3], uint8_t* io, int32_t* found, bool write) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && c && found && (io || !write), RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(v->device));
+        DevBuf d;
+        d.ensure(kBrickVoxels * sizeof(Voxel) + 16);
+        int* dfound = reinterpret_cast<int*>(d.as<uint8_t>() + kBrickVoxels * sizeof(Voxel));
+        if (write) CK(cudaMemcpyAsync(d.p, io, kBrickVoxels * sizeof(Voxel), cudaMemcpyHostToDevice, v->ws.stream));
+        k_block_rw<<<1, kBrickVoxels, 0, v->ws.stream>>>(v->view, c[0], c[1], c[2], d.as<uint2>(), dfound, write);
+        CK(cudaGetLastError());
+        int f = 0;
+        CK(cudaMemcpyAsync(&f, dfound, 4, cudaMemcpyDeviceToHost, v->ws.stream));
+        v->ws.sync();
+        *found = f;
+        if (f && !write && io) CK(cudaMemcpy(io, d.p, kBrickVoxels * sizeof(Voxel), cudaMemcpyDeviceToHost));
+    });
+}
+
+rf_status rf_volume_find_block(const rf_volume* v, const int32_t c[3], uint8_t* voxels, int32_t* found) {
+    return block_rw(v, c, voxels, found, false);
+}
+
+rf_status rf_volume_write_block(rf_volume* v, const int32_t c[3], const uint8_t* voxels, int32_t* found) {
+    return block_rw(v, c, const_cast<uint8_t*>(voxels), found, true);
+}
+
 // ---------------------------------------------------------------- registration
+namespace {
+// LinearizeResult::degenerate (registration.cpp:136-138): the eigenvalues of
+// the symmetric 6x6 H (cyclic Jacobi rotations to convergence, in place of
+// Eigen's SelfAdjointEigenSolver) and min(ev) <= 1e-12 * max(max |ev|, 1).
+bool hessian_degenerate(const double* Hin, uint64_t valid) {
+    if (valid == 0) return true;
+    double A[6][6];
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) A[i][j] = Hin[6 * i + j];
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        double off = 0.0, diag = 0.0;
+        for (int i = 0; i < 6; ++i) {
+            diag += A[i][i] * A[i][i];
+            for (int j = i + 1; j < 6; ++j) off += A[i][j] * A[i][j];
+        }
+        if (off <= 1e-34 * diag || off == 0.0) break;
+        for (int p = 0; p < 5; ++p)
+            for (int q = p + 1; q < 6; ++q) {
+                if (A[p][q] == 0.0) continue;
+                // rotation zeroing A[p][q]: tan(2 phi) = 2 A_pq / (A_qq - A_pp), smaller root
+                const double zeta = (A[q][q] - A[p][p]) / (2.0 * A[p][q]);
+                const double t = std::copysign(1.0, zeta) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+                const double c = 1.0 / std::sqrt(1.0 + t * t), sn = t * c;
+                for (int k = 0; k < 6; ++k) {  // columns p, q
+                    const double kp = A[k][p], kq = A[k][q];
+                    A[k][p] = c * kp - sn * kq;
+                    A[k][q] = sn * kp + c * kq;
+                }
+                for (int k = 0; k < 6; ++k) {  // rows p, q
+                    const double pk = A[p][k], qk = A[q][k];
+                    A[p][k] = c * pk - sn * qk;
+                    A[q][k] = sn * pk + c * qk;
+                }
+            }
+    }
+    double mn = A[0][0], mx = std::fabs(A[0][0]);
+    for (int i = 1; i < 6; ++i) {
+        mn = std::min(mn, A[i][i]);
+        mx = std::max(mx, std::fabs(A[i][i]));
+    }
+    return mn <= 1e-12 * std::max(mx, 1.0);
+}
+}  // namespace
+
+rf_status rf_build_pyramid(const rf_frame* f, const uint8_t* mask, int32_t levels, int device, float* depth,
+                           float* intensity, uint8_t* mask_out, rf_intrinsics* k_out) {
+    return guard([&] {
+        require(levels >= 1, RF_INVALID_ARGUMENT, "pyramid needs at least one level");
+        check_frame_dims(f);
+        require(levels <= kMaxLevels, RF_UNSUPPORTED, "pyramid_levels > 6");
+        for (int l = 1; l < levels; ++l)
+            require((f->intrinsics.width >> l) >= 1 && (f->intrinsics.height >> l) >= 1, RF_INVALID_ARGUMENT,
+                    "image too small for pyramid level");
+        require(!intensity || f->rgb, RF_INVALID_ARGUMENT, "intensity levels need colour");
+        require(!mask_out || mask, RF_INVALID_ARGUMENT, "mask levels need a mask");
+        CK(cudaSetDevice(device));
+        Workspace& ws = device_ws(device);
+        const int w = f->intrinsics.width, h = f->intrinsics.height;
+        ws.ensure_frame(w, h, levels);
+        const size_t n = size_t(w) * h;
+        const cudaMemcpyKind kind = f->memory == RF_MEMORY_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        CK(cudaMemcpyAsync(ws.depth.p, f->depth, n * 4, kind, ws.stream));
+        if (f->rgb) CK(cudaMemcpyAsync(ws.rgb.p, f->rgb, n * 3, kind, ws.stream));
+        uint8_t* base = ws.levels.as<uint8_t>();
+        TrackArgs a{};
+        a.mode = kModePyramid;
+        a.reg.levels = levels;
+        a.F.depth0 = ws.depth.as<float>();
+        a.F.rgb0 = f->rgb ? ws.rgb.as<uint8_t>() : nullptr;
+        for (int l = 0; l < levels; ++l) {
+            a.F.K[l] = level_intr(f->intrinsics, l);
+            a.F.depth[l] = reinterpret_cast<float*>(base + ws.lvl_off_depth[l]);
+            a.F.inten[l] = reinterpret_cast<float*>(base + ws.lvl_off_inten[l]);
+            a.F.mask[l] = base + ws.lvl_off_mask[l];
+        }
+        if (mask) {
+            CK(cudaMemcpyAsync(a.F.mask[0], mask, n, kind, ws.stream));
+            a.use_mask = 1;
+        }
+        a.grid = ws.grid();
+        a.out = ws.out.as<TrackOut>();
+        void* args[] = {&a};
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, kTrackDynSmem,
+                                       ws.stream));
+        size_t off = 0;
+        for (int l = 0; l < levels; ++l) {
+            const size_t nl = size_t(w >> l) * size_t(h >> l);
+            if (k_out) k_out[l] = rf_intrinsics{a.F.K[l].fx, a.F.K[l].fy, a.F.K[l].cx, a.F.K[l].cy, a.F.K[l].w,
+                                                 a.F.K[l].h, f->intrinsics.depth_scale};
+            if (depth) CK(cudaMemcpyAsync(depth + off, l ? (const void*)a.F.depth[l] : ws.depth.p, nl * 4,
+                                          cudaMemcpyDeviceToHost, ws.stream));
+            if (intensity) CK(cudaMemcpyAsync(intensity + off, a.F.inten[l], nl * 4, cudaMemcpyDeviceToHost, ws.stream));
+            if (mask_out) CK(cudaMemcpyAsync(mask_out + off, a.F.mask[l], nl, cudaMemcpyDeviceToHost, ws.stream));
+            off += nl;
+        }
+        ws.sync();
+    });
+}
+
 static void run_pass(rf_volume* v, const rf_frame* f, const double pose[12], const uint8_t* mask, int mode,
                      double cw, TrackOut& out) {
     v->prepare(f);
@@ -918,7 +1167,7 @@ rf_status rf_linearize(const rf_volume* cv, const rf_frame* f, const double pose
         out->color_error = o.acc[28];
         out->error = o.acc[27] + cfg->color_weight * o.acc[28];
         out->valid_count = uint64_t(o.acc[29]);
-        out->degenerate = 0;  // informational only; computed by the host layer
+        out->degenerate = hessian_degenerate(out->H, out->valid_count) ? 1 : 0;
     });
 }
 
@@ -1012,11 +1261,7 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
         a.F.grow = ws.mwork.as<uint8_t>() + (3 * n + 255) / 256 * 256;
         a.F.ffstamp = ws.ffstamp();
         a.F.mask[0] = ws.mask_in.as<uint8_t>();
-        a.grid.sync = ws.gsync.as<GridSync>();
-        a.grid.partials = ws.partials.as<double>();
-        a.grid.result = ws.result.as<double>();
-        a.grid.parity = ws.parity;
-        ws.parity ^= 1;
+        a.grid = ws.grid();
         a.out = ws.out.as<TrackOut>();
         void* args[] = {&a};
         CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, kTrackDynSmem,
@@ -1066,7 +1311,7 @@ rf_status rf_render_virtual_depth(const rf_frame* frames, const double* poses, c
                         frames[i].intrinsics.height == frames[0].intrinsics.height,
                     RF_INVALID_ARGUMENT, "window frames must share one size");
         rf_volume* t = nullptr;
-        create_volume(vcfg, device, &t);
+        create_volume(vcfg, device, &t, false);  // the throw-away volume: brick order unobservable
         std::unique_ptr<rf_volume, void (*)(rf_volume*)> hold(t, rf_volume_destroy);
         // every entry resident at once (the window kernels read them together)
         const size_t nf = size_t(frames[0].intrinsics.width) * frames[0].intrinsics.height;
@@ -1199,7 +1444,9 @@ rf_status rf_mesh_write_ply(const rf_mesh* m, const char* path) {
         out << "ply\nformat binary_little_endian 1.0\n";
         out << "element vertex " << m->nv << "\n";
         out << "property float x\nproperty float y\nproperty float z\n";
-        out << "property uchar red\nproperty uchar green\nproperty uchar blue\n";
+        // ExtractMesh colours every vertex, so WritePly's `colored` (mesh.cpp:197)
+        // is false only for an empty mesh
+        if (m->nv) out << "property uchar red\nproperty uchar green\nproperty uchar blue\n";
         out << "element face " << m->nf << "\n";
         out << "property list uchar int vertex_indices\n";
         out << "end_header\n";
@@ -1348,10 +1595,13 @@ void ensure_window(rf_pipeline* p, int w, int h) {
     p->off_rgb = align256(4 * n);
     p->off_mask = p->off_rgb + align256(3 * n);
     p->slot_bytes = p->off_mask + align256(n);
-    p->win.ensure(size_t(p->cfg.refine_window) * p->slot_bytes);
-    p->win_lists.ensure(size_t(p->cfg.refine_window) * rf_pipeline::kSlotBricks * sizeof(int4));
-    p->win_counts.ensure(size_t(p->cfg.refine_window) * sizeof(uint32_t));
-    p->win_pose.ensure(size_t(p->cfg.refine_window) * 96);
+    // window + 1 slots: the entry IntegrateFront pops keeps its slot while the
+    // current frame is staged, so it can go back to the window if the frame throws
+    const size_t slots = size_t(p->cfg.refine_window) + 1;
+    p->win.ensure(slots * p->slot_bytes);
+    p->win_lists.ensure(slots * rf_pipeline::kSlotBricks * sizeof(int4));
+    p->win_counts.ensure(slots * sizeof(uint32_t));
+    p->win_pose.ensure(slots * 96);
     p->virt.ensure(4 * n);
     p->refined.ensure(4 * n);
     p->win_w = w;
@@ -1363,7 +1613,7 @@ void ensure_window(rf_pipeline* p, int w, int h) {
 // from the front pose with RefineDepth fused in (only raw-depth holes are
 // marched), then CarveAndIntegrate the refined front frame into the model.
 // All on the pipeline's stream; no host sync.
-void integrate_front(rf_pipeline* p) {
+WinEntry integrate_front(rf_pipeline* p) {
     rf_volume* v = p->vol;
     rf_volume* t = p->temp;
     cudaStream_t s = v->ws.stream;
@@ -1378,6 +1628,11 @@ void integrate_front(rf_pipeline* p) {
     t->fuse_window(in.data(), int(in.size()));
     p->launches += 4 * ((in.size() + kMaxWin - 1) / kMaxWin);
     CK(cudaMemcpyAsync(p->h_front + 1, t->view.counters + kOverflow, 4, cudaMemcpyDeviceToHost, s));
+    // A temp-volume overflow throws inside RenderVirtualDepth: nothing else of
+    // this frame may run (the front's CarveAndIntegrate below is gated by the
+    // temp overflow word, the frame's tracking by the halt).
+    k_halt_if<<<1, 32, 0, s>>>(t->view.counters + kOverflow, v->view.counters + kHalt);
+    const int* temp_overflow = reinterpret_cast<const int*>(t->view.counters + kOverflow);
     const WinEntry f = p->window.front();
     RaycastArgs a{};
     a.V = t->view;
@@ -1395,21 +1650,36 @@ void integrate_front(rf_pipeline* p) {
     // CarveAndIntegrate (pipeline.cpp:25-29) of the refined front frame.
     const float* rd = p->refined.as<float>();
     const uint8_t* m = f.has_mask ? slot_mask(p, f.slot) : nullptr;
-    CK(cudaMemcpyAsync(v->view.counters + kBlocksBefore, v->view.counters + kNumBlocks, 4, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemsetAsync(v->view.counters + kVisible, 0, 3 * 4, s));
-    v->allocate(rd, m, f.k, slot_pose(p, f.slot), nullptr);
-    v->fuse(rd, f.has_rgb ? slot_rgb(p, f.slot) : nullptr, m, f.k, slot_pose(p, f.slot), nullptr, true, true, true);
+    v->begin_alloc();
+    v->allocate(rd, m, f.k, slot_pose(p, f.slot), temp_overflow);
+    v->fuse(rd, f.has_rgb ? slot_rgb(p, f.slot) : nullptr, m, f.k, slot_pose(p, f.slot), temp_overflow, true, true,
+            true, false, true);
     CK(cudaMemcpyAsync(p->h_front, v->view.counters + kOverflow, 4, cudaMemcpyDeviceToHost, s));
-    p->launches += 5;
+    p->launches += 7;
     p->has_refinement = true;
     p->refined_index = f.index;
-    p->window.pop_front();
+    p->window.pop_front();  // WindowEntry entry = window_.PopFront() (pipeline.cpp:40)
+    return f;
 }
 
-void check_front_overflow(rf_pipeline* p) {  // after a stream sync
-    if (p->h_front[1]) p->temp_full_reset = true;
-    require(p->h_front[1] == 0 && p->h_front[0] == 0, RF_RESOURCE_LIMIT,
-            "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)");
+// After the stream is idle: the frame that ran IntegrateFront throws when the
+// window re-fusion (temp volume) or the front's CarveAndIntegrate (model
+// volume) ran out of bricks, before its own registration (pipeline.cpp:77).
+// A temp overflow happens before PopFront, so the entry goes back to the front.
+void check_front_overflow(rf_pipeline* p, const WinEntry& popped) {
+    const std::string msg = "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)";
+    if (p->h_front[1]) {
+        p->temp_full_reset = true;
+        p->window.push_front(popped);
+        p->has_refinement = false;
+        CK(cudaMemsetAsync(p->vol->view.counters + kHalt, 0, 4, p->vol->ws.stream));
+        p->vol->ws.sync();
+        throw Error{RF_RESOURCE_LIMIT, msg};
+    }
+    if (p->h_front[0]) {
+        p->vol->recover_overflow();
+        throw Error{RF_RESOURCE_LIMIT, msg};
+    }
 }
 
 }  // namespace
@@ -1430,8 +1700,8 @@ rf_status rf_pipeline_create(const rf_pipeline_config* cfg, int device, rf_pipel
             rf_volume_config sc = p->cfg.volume;  // per-entry brick lists: bounded scratch volume
             sc.max_blocks = std::min<uint64_t>(sc.max_blocks, rf_pipeline::kSlotBricks);
             sc.hash_capacity = 0;
-            create_volume(&p->cfg.volume, device, &p->temp);
-            create_volume(&sc, device, &p->scratch);
+            create_volume(&p->cfg.volume, device, &p->temp, false);  // brick order unobservable: unordered
+            create_volume(&sc, device, &p->scratch, false);
             for (rf_volume* t : {p->temp, p->scratch}) {
                 cudaStreamDestroy(t->ws.stream);  // work runs on the pipeline's stream
                 t->ws.stream = p->vol->ws.stream;
@@ -1484,13 +1754,13 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
         if (p->first) {  // bootstrap at the identity (pipeline.cpp:66-76)
             static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
             CK(cudaMemcpyAsync(pose_state, kIdentity, 96, cudaMemcpyHostToDevice, ws.stream));
-            CK(cudaMemsetAsync(v->view.counters + kOverflow, 0, 5 * 4, ws.stream));
+            v->begin_alloc();
             if (v->prof) CK(cudaEventRecord(p->ev[1], ws.stream));
             v->allocate(d, nullptr, f->intrinsics, pose_state, nullptr);
             if (v->prof) CK(cudaEventRecord(p->ev[2], ws.stream));
-            v->fuse(d, rgb, nullptr, f->intrinsics, pose_state, nullptr, false, true, false);
+            v->fuse(d, rgb, nullptr, f->intrinsics, pose_state, nullptr, false, true, false, true, true);
             if (v->prof) CK(cudaEventRecord(p->ev[4], ws.stream));
-            p->launches += 4;
+            p->launches += 5;
             ws.signal_wait(ws.out.as<TrackOut>(), v->view.counters);
             st.converged = 1;
             std::memcpy(p->last.pose, kIdentity, 96);
@@ -1501,10 +1771,11 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
         } else {
             const bool refine = p->cfg.refine_enabled != 0;
             bool fronted = false;
+            WinEntry popped{};
             if (refine) {
                 ensure_window(p, f->intrinsics.width, f->intrinsics.height);
                 if (int(p->window.size()) >= p->cfg.refine_window) {  // pipeline.cpp:77
-                    integrate_front(p);
+                    popped = integrate_front(p);
                     fronted = true;
                 }
             }
@@ -1520,7 +1791,11 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             const int* lost = &ws.out.as<TrackOut>()->lost;
             int slot = -1;
             if (refine) {  // window.Push (pipeline.cpp:111-113), committed below unless tracking was lost
-                slot = p->window.empty() ? 0 : (p->window.back().slot + 1) % p->cfg.refine_window;
+                for (slot = 0;; ++slot) {  // a free slot: not in the window, not the entry just popped
+                    bool used = fronted && popped.slot == slot;
+                    for (const WinEntry& e : p->window) used = used || e.slot == slot;
+                    if (!used) break;
+                }
                 const size_t n = size_t(f->intrinsics.width) * f->intrinsics.height;
                 CK(cudaMemcpyAsync(slot_depth(p, slot), d, 4 * n, cudaMemcpyDeviceToDevice, ws.stream));
                 if (rgb) CK(cudaMemcpyAsync(slot_rgb(p, slot), rgb, 3 * n, cudaMemcpyDeviceToDevice, ws.stream));
@@ -1544,12 +1819,13 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             } else {
                 v->allocate(d, mask, f->intrinsics, pose_state, lost);
                 if (v->prof) CK(cudaEventRecord(p->ev[2], ws.stream));
-                v->fuse(d, rgb, mask, f->intrinsics, pose_state, lost, true, true, true, false);
+                v->fuse(d, rgb, mask, f->intrinsics, pose_state, lost, true, true, true, false, true);
                 if (v->prof) CK(cudaEventRecord(p->ev[4], ws.stream));
                 p->launches += 4;
             }
             p->launches += 1;
             ws.signal_wait(ws.out.as<TrackOut>(), v->view.counters);
+            if (fronted) check_front_overflow(p, popped);  // throws before this frame's registration counts
             p->last = *ws.h_out;
             v->dump_trace();
             const TrackOut& o = p->last;
@@ -1562,7 +1838,6 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             st.final_error = o.final_error;
             p->has_mask = !o.lost && p->cfg.dynamics_enabled;
             if (o.lost) ++p->losses;
-            if (fronted) check_front_overflow(p);
             if (refine && !o.lost) {
                 WinEntry e;
                 e.slot = slot;
@@ -1575,10 +1850,21 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             }
         }
         std::memcpy(p->last_counters, ws.h_counters, sizeof(p->last_counters));
-        p->traj_t.push_back(f->timestamp);
+        const bool overflow = ws.h_counters[kOverflow] != 0;
+        if (overflow && p->first) {  // AllocateForFrame threw during the bootstrap: nothing recorded (pipeline.cpp:69-74)
+            v->prof = nullptr;
+            v->recover_overflow();
+            throw Error{RF_RESOURCE_LIMIT, "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)"};
+        }
+        p->traj_t.push_back(f->timestamp);  // pushed before CarveAndIntegrate (pipeline.cpp:101-102)
         p->traj_p.insert(p->traj_p.end(), p->last.pose, p->last.pose + 12);
         if (pose_out) std::memcpy(pose_out, p->last.pose, 96);
         p->first = false;
+        if (overflow) {  // CarveAndIntegrate threw: no FrameStats, frame_count unchanged (pipeline.cpp:127-130)
+            v->prof = nullptr;
+            v->recover_overflow();
+            throw Error{RF_RESOURCE_LIMIT, "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)"};
+        }
         if (v->prof) {  // all events completed: the stream was synchronised above
             for (int i = 0; i < 4; ++i) {
                 float ms = 0.f;
@@ -1598,8 +1884,6 @@ rf_status rf_pipeline_process_frame(rf_pipeline* p, const rf_frame* f, rf_frame_
             s.pixel_passes += c.pixel_passes;
             v->prof = nullptr;
         }
-        require(ws.h_counters[kOverflow] == 0, RF_RESOURCE_LIMIT,
-                "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)");
         st.runtime_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         ++p->frame_count;
         if (stats) *stats = st;
@@ -1631,10 +1915,10 @@ unsigned long long enqueue_frame(rf_pipeline* p, const rf_frame* f, int slot, bo
     if (first) {  // bootstrap at the identity (pipeline.cpp:66-76)
         static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
         CK(cudaMemcpyAsync(pose_state, kIdentity, 96, cudaMemcpyHostToDevice, ws.stream));
-        CK(cudaMemsetAsync(v->view.counters + kOverflow, 0, 5 * 4, ws.stream));
+        v->begin_alloc();
         v->allocate(d, nullptr, f->intrinsics, pose_state, nullptr);
-        v->fuse(d, rgb, nullptr, f->intrinsics, pose_state, nullptr, false, true, false);
-        p->launches += 4;
+        v->fuse(d, rgb, nullptr, f->intrinsics, pose_state, nullptr, false, true, false, true, true);
+        p->launches += 5;
     } else {
         TrackArgs a = v->track_args(f, d, rgb, L);
         a.mode = kModeFrame;
@@ -1647,7 +1931,7 @@ unsigned long long enqueue_frame(rf_pipeline* p, const rf_frame* f, int slot, bo
         const uint8_t* mask = p->cfg.dynamics_enabled ? a.F.mask[0] : nullptr;
         const int* lost = &ws.out.as<TrackOut>()->lost;
         v->allocate(d, mask, f->intrinsics, pose_state, lost);
-        v->fuse(d, rgb, mask, f->intrinsics, pose_state, lost, true, true, true, false);
+        v->fuse(d, rgb, mask, f->intrinsics, pose_state, lost, true, true, true, false, true);
         p->launches += 5;
     }
     return ws.signal(ws.out.as<TrackOut>(), v->view.counters, slot);
@@ -1684,10 +1968,18 @@ rf_frame stage_upload(rf_pipeline* p, const rf_frame* f, int u) {
 // (already read into h_out / h_counters).
 void finish_frame(rf_pipeline* p, const rf_frame* f, bool first, rf_frame_stats* stats, double pose_out[12]) {
     Workspace& ws = p->vol->ws;
+    const std::string overflow_msg =
+        "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)";
+    const bool overflow = ws.h_counters[kOverflow] != 0;
+    std::memcpy(p->last_counters, ws.h_counters, sizeof(p->last_counters));
     rf_frame_stats st{};
     st.frame_index = p->frame_count;
     st.timestamp = f->timestamp;
     if (first) {
+        if (overflow) {  // the bootstrap's AllocateForFrame threw: nothing recorded; later frames were halted
+            p->vol->recover_overflow();
+            throw Error{RF_RESOURCE_LIMIT, overflow_msg};
+        }
         static const double kIdentity[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
         st.converged = 1;
         std::memcpy(p->last.pose, kIdentity, 96);
@@ -1708,15 +2000,16 @@ void finish_frame(rf_pipeline* p, const rf_frame* f, bool first, rf_frame_stats*
         p->has_mask = !o.lost && p->cfg.dynamics_enabled;
         if (o.lost) ++p->losses;
     }
-    std::memcpy(p->last_counters, ws.h_counters, sizeof(p->last_counters));
     p->traj_t.push_back(f->timestamp);
     p->traj_p.insert(p->traj_p.end(), p->last.pose, p->last.pose + 12);
     if (pose_out) std::memcpy(pose_out, p->last.pose, 96);
     p->first = false;
+    if (overflow) {  // CarveAndIntegrate threw: trajectory kept, no stats (pipeline.cpp:101-130); the
+        p->vol->recover_overflow();  // rest of the batch was halted on the device (kHalt)
+        throw Error{RF_RESOURCE_LIMIT, overflow_msg};
+    }
     ++p->frame_count;
     if (stats) *stats = st;
-    require(ws.h_counters[kOverflow] == 0, RF_RESOURCE_LIMIT,
-            "voxel block budget exhausted (" + std::to_string(p->cfg.volume.max_blocks) + " blocks)");
 }
 }  // namespace
 
@@ -1740,6 +2033,8 @@ rf_status rf_pipeline_process_frames(rf_pipeline* p, const rf_frame* frames, uin
             const uint64_t m = std::min<uint64_t>(Workspace::kSigSlots, n - c0);
             const bool first0 = p->first;
             unsigned long long last_seq = 0;
+            k_stamp<<<1, 32, 0, ws.stream>>>(ws.d_sig);
+            CK(cudaGetLastError());
             for (uint64_t j = 0; j < m; ++j) {
                 const rf_frame* f = &frames[c0 + j];
                 if (f->memory != RF_MEMORY_DEVICE) {
@@ -1754,12 +2049,13 @@ rf_status rf_pipeline_process_frames(rf_pipeline* p, const rf_frame* frames, uin
             }
             ws.wait_signal(int(m - 1), last_seq);  // stream order: every earlier record is complete too
             for (uint64_t j = 0; j < m; ++j) {
-                const auto t0 = std::chrono::steady_clock::now();
                 ws.read_signal(int(j));
                 finish_frame(p, &frames[c0 + j], first0 && j == 0, stats ? &stats[c0 + j] : nullptr,
                              poses ? poses + 12 * (c0 + j) : nullptr);
-                if (stats) stats[c0 + j].runtime_ms = std::chrono::duration<double, std::milli>(
-                                                          std::chrono::steady_clock::now() - t0).count();
+                // FrameStats::runtime_ms (pipeline.cpp:61, 125-127) of a frame in a back-to-back
+                // batch: device time from the previous frame's completion to this one's
+                const unsigned long long t1 = ws.h_sig[j].t_end, t0 = j ? ws.h_sig[j - 1].t_end : ws.h_sig[0].t_start;
+                if (stats) stats[c0 + j].runtime_ms = 1e-6 * double(t1 - t0);
             }
         }
     });
@@ -1770,9 +2066,9 @@ rf_status rf_pipeline_finalize(rf_pipeline* p) {  // Finalize (pipeline.cpp:133-
         require(p, RF_INVALID_ARGUMENT, "null argument");
         CK(cudaSetDevice(p->vol->device));
         while (!p->window.empty()) {
-            integrate_front(p);
+            const WinEntry e = integrate_front(p);
             p->vol->ws.sync();
-            check_front_overflow(p);
+            check_front_overflow(p, e);
         }
     });
 }
@@ -1782,9 +2078,9 @@ rf_status rf_pipeline_finalize_one(rf_pipeline* p) {
         require(p, RF_INVALID_ARGUMENT, "null argument");
         CK(cudaSetDevice(p->vol->device));
         if (p->window.empty()) return;
-        integrate_front(p);
+        const WinEntry e = integrate_front(p);
         p->vol->ws.sync();
-        check_front_overflow(p);
+        check_front_overflow(p, e);
     });
 }
 
@@ -1976,17 +2272,12 @@ extern "C" rf_status rf_diag_grid_barrier(int device, int32_t iters, int32_t red
         require(us_per_call && iters > 0, RF_INVALID_ARGUMENT, "bad argument");
         CK(cudaSetDevice(device));
         Workspace& ws = device_ws(device);
-        GridCtx g{};
-        g.sync = ws.gsync.as<GridSync>();
-        g.partials = ws.partials.as<double>();
-        g.result = ws.result.as<double>();
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
         float best = 1e30f;
         for (int rep = 0; rep < 3; ++rep) {
-            g.parity = ws.parity;
-            ws.parity ^= 1;
+            GridCtx g = ws.grid();
             void* args[] = {&g, &iters, &reduce};
             CK(cudaEventRecord(e0, ws.stream));
             CK(cudaLaunchCooperativeKernel((void*)k_grid_bench, dim3(ws.track_grid), dim3(kTrackThreads), args, 0,

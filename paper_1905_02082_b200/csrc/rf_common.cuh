@@ -64,6 +64,12 @@ struct VolumeView {
     uint32_t* links;     // kLinkStride per HASH SLOT: [0] the slot's brick, [q] the brick at +(q&1, q>>1&1, q>>2)
     uint32_t* counters;  // see VolumeCounters
     uint32_t* win_first; // refinement temp volume only: per hash slot, first window entry that allocated it
+    // Allocation order (model volumes; null for the refinement scratch/temp
+    // volumes, whose brick order is unobservable): per hash slot the smallest
+    // allocation ordinal that visited a pending key, and the slots claimed
+    // since the last assignment (see hash_insert_ordered / assign_new).
+    unsigned long long* ord;
+    uint32_t* newlist;
     double voxel_size, truncation;
     double inv_voxel_size;  // 1.0 / voxel_size (the reference's inv_s, tsdf_volume.cpp:336)
     int max_weight, carve_weight;
@@ -77,10 +83,11 @@ enum VolumeCounters : int {
     kBlocksBefore = 2,  // snapshot of kNumBlocks before this frame's allocation
     kVisible = 3,       // compacted visible-brick count for carve/integrate
     kDdaVisits = 4,     // cells visited by the allocation walk (bytes model)
-    kNewBlocks = 5,
+    kNewBlocks = 5,     // keys claimed by the current allocation (pending until assign_new)
     kLinked = 6,        // bricks [0, kLinked) have link records
-    kLinkDone = 7,      // k_link completion counter (last CTA advances kLinked)
-    kNumCounters = 8
+    kLinkDone = 7,      // link pass completion counter (last CTA advances kLinked)
+    kHalt = 8,          // sticky: an allocation overflowed; later frames of a batch do nothing
+    kNumCounters = 9
 };
 
 // ---------------------------------------------------------------- math
@@ -224,6 +231,106 @@ __device__ __forceinline__ int hash_insert(const VolumeView& V, int x, int y, in
     }
     atomicOr(&V.counters[kOverflow], 4u);
     return -1;
+}
+
+// AllocateBlock's insertion in allocation order (tsdf_volume.cpp:64-77,
+// 93-113). The first visitor of a key claims its slot with atomicCAS and lists
+// the slot; every visit of a still-pending key (value kInvalid: not yet a
+// brick) folds its ordinal into ord[slot] with atomicMin. assign_new later
+// hands out pool indices by ordinal, so the pool order -- blocks(), Save --
+// is the reference's serial order whatever the thread schedule. A pending key
+// is invisible to every lookup (hash_find treats kInvalid as absent).
+__device__ __forceinline__ void hash_insert_ordered(const VolumeView& V, int x, int y, int z,
+                                                    unsigned long long ordinal) {
+    if (!coord_in_range(x, y, z)) {
+        atomicOr(&V.counters[kOverflow], 2u);
+        atomicOr(&V.counters[kHalt], 1u);
+        return;
+    }
+    const unsigned long long key = pack_key(x, y, z);
+    uint32_t idx = hash_coord(x, y, z) & V.hash_mask;
+    for (uint32_t probe = 0; probe <= V.hash_mask; ++probe) {
+        unsigned long long k = *reinterpret_cast<volatile unsigned long long*>(&V.slots[idx].key);
+        if (k == kEmptyKey) {
+            k = atomicCAS(&V.slots[idx].key, kEmptyKey, key);
+            if (k == kEmptyKey) {
+                V.newlist[atomicAdd(&V.counters[kNewBlocks], 1u)] = idx;  // <= one entry per slot
+                atomicMin(&V.ord[idx], ordinal);
+                return;
+            }
+        }
+        if (k == key) {
+            if (*reinterpret_cast<volatile uint32_t*>(&V.slots[idx].value) == kInvalid) atomicMin(&V.ord[idx], ordinal);
+            return;
+        }
+        idx = (idx + 1) & V.hash_mask;
+    }
+    atomicOr(&V.counters[kOverflow], 4u);
+    atomicOr(&V.counters[kHalt], 1u);
+}
+
+__host__ __device__ __forceinline__ int4 unpack_key(unsigned long long k, uint32_t slot) {
+    return make_int4(int(uint32_t(k & 0x1FFFFFu)) - kCoordBias, int(uint32_t((k >> 21) & 0x1FFFFFu)) - kCoordBias,
+                     int(uint32_t((k >> 42) & 0x1FFFFFu)) - kCoordBias, int(slot));
+}
+
+// Pool indices for the keys claimed since the last assignment: key i gets
+// before + rank(i), rank = the number of claimed keys whose first visit came
+// earlier (ordinals are unique per key: a pixel walks distinct cells). Keys
+// ranked past max_blocks get no brick -- the reference throws at the first of
+// them (tsdf_volume.cpp:66-69) -- and stay pending until the host rebuilds
+// the table (rf_capi.cu recover_overflow). `on_new(b, coord)` runs for each
+// assigned brick; created[ordinal] (explicit AllocateBlock batches, whose
+// ordinal is the coordinate's index) receives 1, or -1 past the budget.
+// Grid-stride over the claimed keys; each CTA streams all ordinals through
+// shared memory in tiles. Reads counters[kBlocksBefore] (== the brick count
+// when the allocation started) and counters[kNewBlocks]; CTA 0 publishes
+// counters[kNumBlocks] and the overflow flags.
+template <class OnNew>
+__device__ __forceinline__ void assign_new(const VolumeView& V, OnNew on_new, int* created = nullptr) {
+    constexpr int kTile = 256;
+    __shared__ unsigned long long s_ord[kTile];
+    const uint32_t n = V.counters[kNewBlocks];
+    const uint32_t before = V.counters[kBlocksBefore];
+    const uint32_t budget = V.max_blocks > before ? V.max_blocks - before : 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        V.counters[kNumBlocks] = before + min(n, budget);
+        if (n > budget) {
+            atomicOr(&V.counters[kOverflow], 1u);
+            atomicOr(&V.counters[kHalt], 1u);
+        }
+    }
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += stride) {  // CTA-uniform trip count
+        const uint32_t i = i0 + threadIdx.x;
+        uint32_t slot = 0;
+        unsigned long long mine = 0;
+        if (i < n) {
+            slot = __ldcg(V.newlist + i);
+            mine = __ldcg(V.ord + slot);
+        }
+        uint32_t rank = 0;
+        for (uint32_t t0 = 0; t0 < n; t0 += kTile) {
+            __syncthreads();
+            const uint32_t m = min(uint32_t(kTile), n - t0);
+            for (uint32_t k = threadIdx.x; k < m; k += blockDim.x) s_ord[k] = __ldcg(V.ord + __ldcg(V.newlist + t0 + k));
+            __syncthreads();
+            for (uint32_t j = 0; j < m; ++j) rank += s_ord[j] < mine;
+        }
+        if (i < n) {
+            if (rank < budget) {
+                const uint32_t b = before + rank;
+                const int4 c = unpack_key(__ldcg(&V.slots[slot].key), slot);
+                V.coords[b] = c;
+                V.slots[slot].value = b;  // (ord[slot] stays: other CTAs may still be ranking against it;
+                                          // an assigned slot never becomes pending again)
+                if (created) created[mine] = 1;
+                on_new(b, c);
+            } else if (created) {
+                created[mine] = -1;
+            }
+        }
+    }
 }
 
 __device__ __forceinline__ const Voxel* brick_ptr(const VolumeView& V, uint32_t b) {

@@ -23,9 +23,13 @@ struct GridCtx {
     double* partials;    // 2 * gridDim.x * kRedStride (double-buffered)
     double* result;      // unused by the current barrier (kept for ABI stability)
     int parity;          // which counter this launch uses (host alternates)
+    uint4* ll;           // all-reduce lines: 2 * gridDim.x * 32 (double-buffered), see block_grid_allreduce
+    uint32_t seq;        // launch sequence number (host, 1..2^20-1): flags are (seq << 12) | reduce index
 };
 
 __shared__ unsigned int s_grid_bar;  // barriers completed by this CTA in this launch
+__shared__ unsigned int s_ll_bar;    // all-reduces completed by this CTA in this launch
+__shared__ double s_fold[32][32];    // per-chunk sums of the all-reduce fold
 
 __device__ __forceinline__ unsigned long long* grid_counter(const GridCtx& g, int parity, int lane) {
     return &g.sync->lane[parity][lane][0];
@@ -33,7 +37,10 @@ __device__ __forceinline__ unsigned long long* grid_counter(const GridCtx& g, in
 
 // Call once at kernel start, before any barrier, from all threads.
 __device__ __forceinline__ void grid_init(const GridCtx& g) {
-    if (threadIdx.x == 0) s_grid_bar = 0;
+    if (threadIdx.x == 0) {
+        s_grid_bar = 0;
+        s_ll_bar = 0;
+    }
     if (blockIdx.x == 0 && threadIdx.x < kArriveLanes)
         *grid_counter(g, g.parity ^ 1, threadIdx.x) = 0ull;  // next launch's counters
     __syncthreads();
@@ -56,25 +63,6 @@ __device__ __forceinline__ double warp_transpose_reduce(double (&v)[32]) {
     return v[0];
 }
 
-// CTA sum of NV (<= 32) doubles per thread. Result in `out` (smem) for all
-// threads after return; `scratch` holds (blockDim/32) * 32 doubles.
-template <int NV>
-__device__ __forceinline__ void block_reduce(const double (&in)[NV], double* scratch, double* out) {
-    static_assert(NV <= 32, "block_reduce handles up to 32 values");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    double v[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = i < NV ? in[i] : 0.0;
-    scratch[warp * 32 + lane] = warp_transpose_reduce(v);
-    __syncthreads();
-    if (threadIdx.x < NV) {
-        double s = 0.0;
-        for (int w = 0; w < nw; ++w) s += scratch[w * 32 + threadIdx.x];
-        out[threadIdx.x] = s;
-    }
-    __syncthreads();
-}
-
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -88,10 +76,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-
-#ifndef RF_POLL_ACQ
-#define RF_POLL_ACQ 0
-#endif
 
 struct NoHook {
     __device__ void operator()() const {}
@@ -118,108 +102,127 @@ __device__ __forceinline__ void grid_arrive_wait(const GridCtx& g, unsigned int 
     // Relaxed polling, then one acquire. Bounded: a co-residency bug must
     // fail loudly, never hang the GPU.
     unsigned long long spins = 0;
-#if RF_POLL_ACQ
-    // acquire polling: the load that sees the target is the acquire (no extra L2 trip)
-    while (!__all_sync(0xffffffffu, ld_acquire_u64(cnt) >= target)) {
-        if (++spins > (1ull << 26)) __trap();
-    }
-#else
     while (!__all_sync(0xffffffffu, ld_relaxed_u64(cnt) >= target)) {
         if (++spins > (1ull << 26)) __trap();
     }
     (void)ld_acquire_u64(cnt);
-#endif
     if (lane == 0) s_grid_bar = bar + 1u;
 }
 
-// All threads, after grid_arrive_wait: `out` (smem) = the sum of every CTA's
-// partial, folded in CTA index order.
-template <int NV>
-__device__ __forceinline__ void grid_fold(const double* buf, double* out) {
-    const int G = gridDim.x;
-    __shared__ double red[32][32];
-    const int j = threadIdx.x & 31, c = threadIdx.x >> 5, nchunk = blockDim.x >> 5;
-    double s = 0.0;
-    if (j < NV) {
-        // chunk c folds CTA rows c, c+nchunk, ... in order; all of the
-        // chunk's loads are issued before the first add (one L2 latency).
-        constexpr int kRows = 24;
-        double v[kRows];
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) {
-            const int i = c + r * nchunk;
-            v[r] = i < G ? __ldcg(buf + i * kRedStride + j) : 0.0;
-        }
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) s += v[r];
-        for (int i = c + kRows * nchunk; i < G; i += nchunk) s += __ldcg(buf + i * kRedStride + j);
-    }
-    red[c][j] = s;
-    __syncthreads();
-    if (threadIdx.x < NV) {
-        double t = 0.0;
-        for (int cc = 0; cc < nchunk; ++cc) t += red[cc][threadIdx.x];
-        out[threadIdx.x] = t;
-    }
-}
-
-// All CTAs call with their CTA vector `mine` (smem, NV entries). On return
-// `out` (smem) holds the sum over CTAs folded in CTA index order (identical
-// in every CTA, independent of arrival order). NV == 0 is a plain barrier.
-// Inlined at every call site: as a __noinline__ call the ABI spilled live state
-// to the stack around each barrier (912 B stack, 1413 vs 1532 frames/s).
-#ifndef RF_GRID_NOINLINE
-#define RF_GRID_NOINLINE 0
-#endif
-#if RF_GRID_NOINLINE
-#define RF_GRID_INLINE __noinline__
-#else
-#define RF_GRID_INLINE __forceinline__
-#endif
-template <int NV>
-__device__ RF_GRID_INLINE void grid_allreduce(const GridCtx& g, const double* mine, double* out) {
-    const int G = gridDim.x;
+// Grid-wide barrier with release/acquire semantics (global writes before it
+// are visible to every CTA after it): warp 0 arrives on the launch's counter
+// and polls it. Inlined at every call site (a __noinline__ call spilled live
+// state around each barrier).
+__device__ __forceinline__ void grid_barrier(const GridCtx& g) {
     const unsigned int bar = s_grid_bar;  // read before thread 0 advances it
-    double* buf = g.partials + size_t(bar & 1u) * G * kRedStride;
-    if (NV > 0 && threadIdx.x < NV) __stcg(buf + blockIdx.x * kRedStride + threadIdx.x, mine[threadIdx.x]);
     __syncthreads();
     if (threadIdx.x < 32) grid_arrive_wait(g, bar);
     __syncthreads();
-    if (NV > 0) grid_fold<NV>(buf, out);
-    __syncthreads();
 }
 
-// Block sum + grid all-reduce of NV (<= 30) per-thread doubles in one: warp
-// partials by the transpose reduce, then warp 0 sums them (fixed warp order)
-// and stores the CTA vector straight into its grid slot before arriving, with
-// no CTA-wide barrier between the block sum and the arrival. Same sums, same
-// order as block_reduce + grid_allreduce.
-template <int NV, class Hook = NoHook>
+// Flagged lines (the low-latency protocol of NCCL's LL transport): a double
+// travels as one 16-byte store {lo32, flag, hi32, flag}; each 8-byte half is
+// single-copy atomic, so a reader that sees the expected flag in both halves
+// holds the complete value. No fence, no counter, no acquire round trip.
+__device__ __forceinline__ void st_line(uint4* p, double v, uint32_t flag) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(uint32_t(b)), "r"(flag),
+                 "r"(uint32_t(b >> 32)), "r"(flag)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ld_line(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ bool line_ready(const uint4& v, uint32_t flag) { return v.y == flag && v.w == flag; }
+__device__ __forceinline__ double line_value(const uint4& v) {
+    return __longlong_as_double((long long)(((unsigned long long)v.z << 32) | v.x));
+}
+
+// Block sum + grid all-reduce of NV (<= 30) per-thread doubles. Warp
+// partials by the transpose reduce, warp 0 sums them (fixed warp order) and
+// stores the CTA's vector as flagged lines; then every CTA folds all CTAs'
+// lines in CTA index order as they arrive (chunk c of 32 threads folds rows
+// c, c + nchunk, ...; each thread polls only the rows it still misses).
+// Deterministic: the sums do not depend on arrival order. The critical path is
+// the partials' one-way trip to L2 plus one polling round trip.
+// kPublish: the CTAs wrote global data before this call that others read after
+// it (residual images, masks): the partial store then acts as a release
+// (fence after the CTA barrier) and the observation of all partials as an
+// acquire. `hook` runs on thread 0 right after its CTA's partial is stored.
+// Double buffering by the reduce index is safe: a CTA writes reduce i + 2 only
+// after every CTA's partial of i + 1, i.e. after every CTA finished folding i.
+template <int NV, bool kPublish = true, class Hook = NoHook>
 __device__ __forceinline__ void block_grid_allreduce(const GridCtx& g, const double (&in)[NV], double* scratch,
                                                      double* out, const Hook& hook = Hook()) {
     static_assert(NV <= 32, "one warp holds the CTA vector");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int G = gridDim.x;
     double v[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = i < NV ? in[i] : 0.0;
     scratch[warp * 32 + lane] = warp_transpose_reduce(v);
-    const unsigned int bar = s_grid_bar;  // read before warp 0 advances it (it does so after the barrier)
-    double* buf = g.partials + size_t(bar & 1u) * gridDim.x * kRedStride;
+    const unsigned int bar = s_ll_bar;  // read before lane 0 of warp 0 advances it (after the barrier below)
+    const uint32_t flag = (g.seq << 12) | (bar & 0xFFFu);
+    uint4* buf = g.ll + size_t(bar & 1u) * G * 32;
     __syncthreads();
     if (warp == 0) {
-        if (lane < NV) {
-            double s = 0.0;
-            for (int w = 0; w < nw; ++w) s += scratch[w * 32 + lane];
-            __stcg(buf + blockIdx.x * kRedStride + lane, s);
+        double sum = 0.0;
+        if (lane < NV)
+            for (int w = 0; w < nw; ++w) sum += scratch[w * 32 + lane];
+        if (kPublish) __threadfence();  // release: the CTA's writes (ordered by the barrier above) first
+        if (lane < NV) st_line(buf + blockIdx.x * 32 + lane, sum, flag);
+        if (lane == 0) {
+            hook();
+            s_ll_bar = bar + 1u;
         }
-        __syncwarp();  // orders the lanes' partial stores before lane 0's release
-        grid_arrive_wait(g, bar, hook);
     }
+    const int j = lane, c = warp;
+    double s = 0.0;
+    if (j < NV) {
+        constexpr int kRows = 13;  // rows per chunk in flight (148 CTAs / 12 warps)
+        uint4 r[kRows];
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) {
+            const int i = c + k * nw;
+            r[k] = i < G ? ld_line(buf + i * 32 + j) : make_uint4(0u, flag, 0u, flag);
+        }
+        unsigned long long spins = 0;
+        for (;;) {
+            bool all = true;
+#pragma unroll
+            for (int k = 0; k < kRows; ++k) {
+                if (!line_ready(r[k], flag)) {
+                    all = false;
+                    r[k] = ld_line(buf + (c + k * nw) * 32 + j);
+                }
+            }
+            if (all) break;
+            if (++spins > (1ull << 26)) __trap();  // a co-residency bug fails loudly, never hangs
+        }
+#pragma unroll
+        for (int k = 0; k < kRows; ++k) s += line_value(r[k]);  // rows past G hold +0.0
+        for (int i = c + kRows * nw; i < G; i += nw) {
+            uint4 t = ld_line(buf + i * 32 + j);
+            for (unsigned long long sp = 0; !line_ready(t, flag); t = ld_line(buf + i * 32 + j))
+                if (++sp > (1ull << 26)) __trap();
+            s += line_value(t);
+        }
+        if (kPublish) __threadfence();  // acquire: the other CTAs' writes before their partials
+    }
+    s_fold[c][j] = s;
     __syncthreads();
-    grid_fold<NV>(buf, out);
+    if (threadIdx.x < NV) {
+        double t = 0.0;
+        for (int cc = 0; cc < nw; ++cc) t += s_fold[cc][threadIdx.x];
+        out[threadIdx.x] = t;
+    }
     __syncthreads();
 }
 
-__device__ __forceinline__ void grid_barrier(const GridCtx& g) { grid_allreduce<0>(g, nullptr, nullptr); }
 
 }  // namespace rfb

@@ -359,17 +359,10 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
             if (blockIdx.x == 0) tr[1] = now;
         }
     }
-#ifndef RF_FUSED_REDUCE
-#define RF_FUSED_REDUCE 1
-#endif
-#if RF_FUSED_REDUCE
-    block_grid_allreduce<kAccN>(a.grid, acc, scratch, out, hook);
+    // Jacobian passes write nothing global; a value pass's residual image is
+    // read across CTAs by the mask that follows (publish).
+    block_grid_allreduce<kAccN, !kJac>(a.grid, acc, scratch, out, hook);
     if (kJac && threadIdx.x == 0) s_pxc_tag = pxc_tag;  // (every thread read it before the barriers above)
-#else
-    block_reduce<kAccN>(acc, scratch, blk);  // (its barriers: every thread has read s_pxc_tag)
-    if (kJac && threadIdx.x == 0) s_pxc_tag = pxc_tag;
-    grid_allreduce<kAccN>(a.grid, blk, out);
-#endif
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = global_ns();
     if (a.trace && threadIdx.x == 0) ++s_trace_pass;
 }
@@ -998,6 +991,24 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
         return;
     }
 
+    if (a.mode == kModeFrame && a.vol_counters && __ldcg(a.vol_counters + kHalt)) {
+        // An earlier frame of this batch overflowed the block budget: the host
+        // throws ResourceLimitError at that frame, so this one must leave no
+        // trace (no pose update, no allocation / integration: lost = 2 gates
+        // the launches that follow).
+        if (lead) a.out->lost = 2;
+        return;
+    }
+    if (a.mode == kModePyramid) {  // BuildPyramid (registration.cpp:144-182) as a public entry point
+        const FrameView& F = a.F;
+        if (F.rgb0)  // LevelZero: ToIntensity (registration.cpp:119-126, image.hpp:85-91)
+            for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < F.K[0].w * F.K[0].h; p += gridDim.x * blockDim.x) {
+                const uint8_t* c = F.rgb0 + 3 * size_t(p);
+                F.inten[0][p] = float(luma(__ldg(c), __ldg(c + 1), __ldg(c + 2)));
+            }
+        build_pyramid(a, true, a.use_mask);
+        return;
+    }
     Pose init;
     for (int i = 0; i < 9; ++i) init.R[i] = a.pose_state[i];
     for (int i = 0; i < 3; ++i) init.t[i] = a.pose_state[9 + i];
@@ -1069,6 +1080,7 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
             a.vol_counters[kBlocksBefore] = a.vol_counters[kNumBlocks];
             a.vol_counters[kVisible] = 0;
             a.vol_counters[kDdaVisits] = 0;
+            a.vol_counters[kNewBlocks] = 0;
             a.vol_counters[kOverflow] = 0;
         }
     }
@@ -1117,13 +1129,18 @@ namespace rfb {
 // Back-to-back grid all-reduces (no pixel work): the fixed per-pass cost of
 // the persistent tracking kernel's barrier. reduce = 0 is a bare barrier.
 __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_grid_bench(GridCtx g, int iters, int reduce) {
-    __shared__ double blk[32], red[32];
+    __shared__ double blk[32], red[32], scratch[(kTrackThreads / 32) * 32];
     grid_init(g);
     if (threadIdx.x < 32) blk[threadIdx.x] = double(blockIdx.x + threadIdx.x);
     __syncthreads();
     for (int i = 0; i < iters; ++i) {
-        if (reduce) grid_allreduce<kAccN>(g, blk, red);
-        else grid_barrier(g);
+        if (reduce) {
+            double v[kAccN];
+            for (int k = 0; k < kAccN; ++k) v[k] = blk[k % 32];
+            block_grid_allreduce<kAccN, false>(g, v, scratch, red);
+        } else {
+            grid_barrier(g);
+        }
     }
 }
 

@@ -80,6 +80,7 @@ enum TrackMode : int {
     kModeEvalColor = 4,  // value pass at level 0, colour error (EvaluateColorError)
     kModeMask = 5,       // BuildMask stages on given residuals
     kModePassBench = 6,  // diagnostics: bench_iters Jacobian passes at bench_level (timeline in out)
+    kModePyramid = 7,    // BuildPyramid only (level-0 intensity included), for rf_build_pyramid
 };
 
 struct TrackArgs {

@@ -103,43 +103,58 @@ __global__ void k_alloc(AllocArgs a) {
     if (p < a.K.w * a.K.h) {
         // The walk runs one cell ahead of the inserts: the first hash slot of
         // the next cell is loaded while the current one is checked, and a cell
-        // whose key already sits in its first slot (almost all of them once the
-        // scene is mapped) needs no atomic. Same key set as inserting every
-        // visited cell (hash_insert of a present key is a no-op).
+        // whose brick already sits in its first slot (almost all of them once
+        // the scene is mapped) needs no atomic. Same key set as inserting every
+        // visited cell (inserting a present key is a no-op). Model volumes
+        // insert in allocation order: the ordinal of a visit is (pixel, step),
+        // AllocateForFrame's raster order (tsdf_volume.cpp:96-111).
+        const bool ordered = a.V.ord != nullptr;
         auto first_slot = [&](const int (&c)[3]) -> uint4 {
             if (!coord_in_range(c[0], c[1], c[2])) return make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
             return __ldg(reinterpret_cast<const uint4*>(a.V.slots + (hash_coord(c[0], c[1], c[2]) & a.V.hash_mask)));
         };
-        auto settle = [&](const int (&c)[3], uint4 sl) {
+        auto settle = [&](const int (&c)[3], uint4 sl, unsigned step) {
             const unsigned long long k = (unsigned long long)sl.x | ((unsigned long long)sl.y << 32);
-            if (!(coord_in_range(c[0], c[1], c[2]) && k == pack_key(c[0], c[1], c[2]) && sl.z < kOverflowed))
-                hash_insert(a.V, c[0], c[1], c[2]);
+            if (coord_in_range(c[0], c[1], c[2]) && k == pack_key(c[0], c[1], c[2]) && sl.z < kOverflowed) return;
+            if (ordered) hash_insert_ordered(a.V, c[0], c[1], c[2], ((unsigned long long)p << 32) | step);
+            else hash_insert(a.V, c[0], c[1], c[2]);
         };
         int cur[3] = {0, 0, 0};
         uint4 cur_sl = make_uint4(0, 0, 0, 0);
-        bool have = false;
+        unsigned step = 0;
         visits = walk_pixel(a.V, a.depth, a.mask, a.K, a.pose, p, [&](const int (&c)[3]) {
             const uint4 next_sl = first_slot(c);
-            if (have) settle(cur, cur_sl);
+            if (step) settle(cur, cur_sl, step - 1);
             cur[0] = c[0];
             cur[1] = c[1];
             cur[2] = c[2];
             cur_sl = next_sl;
-            have = true;
+            ++step;
         });
-        if (have) settle(cur, cur_sl);
+        if (step) settle(cur, cur_sl, step - 1);
     }
     // warp-aggregated visit counter (for the algorithmic-bytes model)
     for (int o = 16; o > 0; o >>= 1) visits += __shfl_down_sync(0xffffffffu, visits, o);
     if ((threadIdx.x & 31) == 0 && visits) atomicAdd(&a.V.counters[kDdaVisits], visits);
 }
 
-// Explicit AllocateBlock (tsdf_volume.cpp:64-77) for a batch of coordinates.
+// Explicit AllocateBlock (tsdf_volume.cpp:64-77) for a batch of coordinates,
+// in index order on model volumes (ordinal = index; created[] is filled by
+// k_assign), else unordered with created[i] = 1 / 0 / -1.
 __global__ void k_alloc_coords(VolumeView V, const int* coords, int n, int* created) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    if (V.ord) {
+        hash_insert_ordered(V, coords[3 * i], coords[3 * i + 1], coords[3 * i + 2], (unsigned long long)i);
+        return;
+    }
     const int r = hash_insert(V, coords[3 * i], coords[3 * i + 1], coords[3 * i + 2]);
     if (created) created[i] = r;
+}
+
+// Pool indices for an allocation's claimed keys (assign_new), standalone.
+__global__ void k_assign(VolumeView V, int* created) {
+    assign_new(V, [](uint32_t, int4) {}, created);
 }
 
 // ---------------------------------------------------------------- culling
@@ -177,48 +192,72 @@ __device__ __forceinline__ FrustumTest frustum_test(const double cc[8][3], const
     return {min_z, max_u < -0.5 || min_u > K.w - 0.5 || max_v < -0.5 || min_v > K.h - 0.5};
 }
 
+__device__ __forceinline__ void cull_brick(const CullArgs& a, const Pose& W, double ext, int4 c, bool carve,
+                                           bool integrate, uint32_t& flags) {
+    double cc[8][3];
+    for (int k = 0; k < 8; ++k) {
+        const double x = (double(c.x) + double(k & 1)) * ext;
+        const double y = (double(c.y) + double((k >> 1) & 1)) * ext;
+        const double z = (double(c.z) + double(k >> 2)) * ext;
+        pose_apply(W, x, y, z, cc[k]);
+    }
+    const FrustumTest ft = frustum_test(cc, a.K);
+    if (carve && !ft.outside(a.V.carve_clip)) flags |= kFlagCarve;
+    if (integrate && !ft.outside(a.V.max_depth + a.V.truncation)) flags |= kFlagIntegrate;
+}
+
+// Appends the brick of every lane with flags to the visible list (one atomic per warp).
+__device__ __forceinline__ void append_visible(const CullArgs& a, uint32_t b, uint32_t flags) {
+    const unsigned vote = __ballot_sync(0xffffffffu, flags != 0);
+    if (vote) {  // lanes take consecutive slots
+        const int lane = threadIdx.x & 31;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&a.V.counters[kVisible], uint32_t(__popc(vote)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (flags) a.list[base + __popc(vote & ((1u << lane) - 1u))] = b | flags;
+    }
+}
+
 __global__ void k_cull(CullArgs a) {
     pdl_enter();
     if (a.lost && *a.lost) return;
-    const uint32_t nb = min(a.V.counters[kNumBlocks], a.V.max_blocks);
-    const uint32_t before = a.carve_only_before ? min(a.V.counters[kBlocksBefore], nb) : nb;
+    // With `assign`, this frame's allocation (k_alloc) left its new keys
+    // pending: they receive their pool indices here (assign_new) and are culled
+    // by the thread that assigns them, while the other threads cull the bricks
+    // that existed before the frame. An overflowing allocation integrates
+    // nothing (AllocateForFrame throws before Integrate, tsdf_volume.cpp:66-69;
+    // the carve already happened, pipeline.cpp:26-28).
+    const uint32_t old_n = a.assign ? a.V.counters[kBlocksBefore] : min(a.V.counters[kNumBlocks], a.V.max_blocks);
+    const uint32_t before = a.carve_only_before ? min(a.V.counters[kBlocksBefore], old_n) : old_n;
+    bool overflow = a.V.counters[kOverflow] != 0;
+    if (a.assign) {
+        const uint32_t n = a.V.counters[kNewBlocks];
+        overflow = overflow || n > (a.V.max_blocks > old_n ? a.V.max_blocks - old_n : 0u);
+    }
+    const bool integrate = a.do_integrate && !overflow;
     Pose P;
     for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = __ldg(a.pose + i);
     const Pose W = pose_inverse(P);
     const double ext = double(kSide) * a.V.voxel_size;
+    if (a.assign)
+        assign_new(a.V, [&](uint32_t b, int4 c) {
+            uint32_t flags = 0;
+            cull_brick(a, W, ext, c, false, integrate, flags);  // new bricks: integrate only
+            if (flags) a.list[atomicAdd(&a.V.counters[kVisible], 1u)] = b | flags;
+        });
     const uint32_t stride = gridDim.x * blockDim.x;
     // warp-uniform trip count so the whole warp can aggregate its appends
-    for (uint32_t b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b0 < nb; b0 += stride) {
+    for (uint32_t b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b0 < old_n; b0 += stride) {
         const uint32_t b = b0 + (threadIdx.x & 31u);
         uint32_t flags = 0;
-        if (b < nb) {
-            const int4 c = a.V.coords[b];
-            double cc[8][3];
-            for (int k = 0; k < 8; ++k) {
-                const double x = (double(c.x) + double(k & 1)) * ext;
-                const double y = (double(c.y) + double((k >> 1) & 1)) * ext;
-                const double z = (double(c.z) + double(k >> 2)) * ext;
-                pose_apply(W, x, y, z, cc[k]);
-            }
-            const FrustumTest ft = frustum_test(cc, a.K);
-            if (a.do_carve && b < before && !ft.outside(a.V.carve_clip)) flags |= kFlagCarve;
-            if (a.do_integrate && !ft.outside(a.V.max_depth + a.V.truncation)) flags |= kFlagIntegrate;
-        }
-        const unsigned vote = __ballot_sync(0xffffffffu, flags != 0);
-        if (vote) {  // one atomic per warp, lanes take consecutive slots
-            const int lane = threadIdx.x & 31;
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(&a.V.counters[kVisible], uint32_t(__popc(vote)));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (flags) a.list[base + __popc(vote & ((1u << lane) - 1u))] = b | flags;
-        }
+        if (b < old_n) cull_brick(a, W, ext, a.V.coords[b], a.do_carve && b < before, integrate, flags);
+        append_visible(a, b, flags);
     }
-    link_new(a.V);  // index this frame's new bricks for the next frame's tracking
 }
 
 // Link records for bricks allocated since the last link pass: grid-stride
-// over [kLinked, num_blocks). The next kernel on the stream commits the range
-// (commit_links), so no completion atomics are needed here.
+// over [kLinked, num_blocks). The range is committed afterwards (commit_links
+// in the next kernel on the stream, or link_new_commit's completion count).
 // One thread per (brick, neighbour q, direction): the 14 hash probes of a
 // brick's record run in parallel instead of as one thread's serial chain.
 __device__ void link_new(const VolumeView& V) {
@@ -231,6 +270,24 @@ __device__ void link_new(const VolumeView& V) {
 
 __device__ __forceinline__ void commit_links(const VolumeView& V) {
     if (blockIdx.x == 0 && threadIdx.x == 0) V.counters[kLinked] = min(V.counters[kNumBlocks], V.max_blocks);
+}
+
+// link_new, then the last CTA to finish advances kLinked (kernels that cannot
+// leave the commit to a successor).
+__device__ void link_new_commit(const VolumeView& V) {
+    __shared__ bool s_last;
+    const uint32_t hi = min(V.counters[kNumBlocks], V.max_blocks);
+    if (V.counters[kLinked] >= hi) return;  // nothing new (CTA-uniform)
+    link_new(V);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // this CTA's link records before its arrival
+        s_last = atomicAdd(&V.counters[kLinkDone], 1u) == gridDim.x - 1;
+        if (s_last) {
+            V.counters[kLinked] = hi;
+            V.counters[kLinkDone] = 0;
+        }
+    }
 }
 
 __global__ void k_link(VolumeView V) { link_new(V); }
@@ -281,8 +338,8 @@ __device__ __forceinline__ unsigned long long colour_magic(uint32_t d) {  // cei
 
 __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
     pdl_enter();
-    commit_links(a.V);  // k_cull (previous launch) linked this frame's new bricks
     if (a.lost && *a.lost) return;
+    link_new_commit(a.V);  // index the bricks k_cull assigned, for the next frame's tracking
     __shared__ Pose W;
     __shared__ double s_rcp[512];  // RN(1 / i): i = w + 1 (integrate) or w + carve_weight (carve), <= 510
     __shared__ unsigned long long s_cdiv[257];  // colour_avg multipliers by d = w + 1

@@ -25,6 +25,7 @@ struct CullArgs {
     uint32_t* list;
     int do_carve, do_integrate;
     int carve_only_before;  // carve only bricks allocated before this frame
+    int assign;             // assign + cull the preceding k_alloc's pending bricks (assign_new)
 };
 
 struct FuseArgs {
@@ -105,6 +106,7 @@ __global__ void k_link_commit(VolumeView V);
 __global__ void k_alloc(AllocArgs a);
 __global__ void k_raycast(RaycastArgs a);
 __global__ void k_alloc_coords(VolumeView V, const int* coords, int n, int* created);
+__global__ void k_assign(VolumeView V, int* created);
 __global__ void k_cull(CullArgs a);
 __global__ void k_fuse(FuseArgs a);
 __global__ void k_sample(VolumeView V, const double* pts, int n, int mode, double* value, double* grad,
