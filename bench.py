@@ -3,9 +3,12 @@
 
 metric : frames/s of Pipeline::ProcessFrame (track + mask + carve + allocate +
          integrate, pipeline.cpp:57-131) at 640x480 with 1 cm voxels.
-workload: BASELINE.json configs[1] ("C2"): the acceptance room with two moving
-         boxes, 200 frames at 30 Hz, replayed forwards then backwards (a
-         continuous ping-pong sequence) so any step count keeps tracking.
+workload: BASELINE.json configs[1] ("C2", the default): the acceptance room
+         with two moving boxes, 200 frames at 30 Hz, replayed forwards then
+         backwards (a continuous ping-pong sequence) so any step count keeps
+         tracking. --config C1|C3|C4 runs the other BASELINE.json workloads
+         (C3: large room at 0.5 cm with a 2^22 hash; C4: 1280x720 with the
+         mesh export timed after the run).
          Frames are synthetic, rendered on the GPU before timing.
 One step = one ProcessFrame on one frame.
 
@@ -39,7 +42,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "frames/sec (track+integrate, 640x480, 1cm voxels) per B200 + HBM roofline frac"
 UNIT = "frames/s"
-CONFIG = "C2"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
@@ -51,6 +53,8 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"],
+                    help="BASELINE.json workload (C2 is the headline)")
     return ap.parse_args()
 
 
@@ -129,11 +133,11 @@ DATA = ("synthetic: the {cfg} scene script rendered by RenderFrame (synth.cpp:13
         "mt19937 depth noise 0.001*z^2, seed {seed}); identical bytes in both arms")
 
 
-def render_sequence(script: str):
-    """The workload generator, outside every timed region: all frames of a
-    scene script through RenderFrame on the host cores (frames are independent:
-    each seeds its own mt19937, synth.cpp:185). Returns (intrinsics, depth
-    [F,H,W] f32, rgb [F,H,W,3] u8, timestamps)."""
+def render_sequence(script: str, count: int | None = None):
+    """The workload generator, outside every timed region: the first `count`
+    frames (default all) of a scene script through RenderFrame on the host
+    cores (frames are independent: each seeds its own mt19937, synth.cpp:185).
+    Returns (intrinsics, depth [F,H,W] f32, rgb [F,H,W,3] u8, timestamps)."""
     from concurrent.futures import ThreadPoolExecutor
 
     import numpy as np
@@ -142,7 +146,7 @@ def render_sequence(script: str):
 
     scene = O.Scene(script)
     k = scene.k
-    F = len(scene)
+    F = len(scene) if count is None else min(count, len(scene))
     depth = np.empty((F, k.height, k.width), dtype=np.float32)
     rgb = np.empty((F, k.height, k.width, 3), dtype=np.uint8)
     ts = np.empty(F)
@@ -156,12 +160,35 @@ def render_sequence(script: str):
     return k, depth, rgb, ts
 
 
-def workload_config(W, H, F):
+WORKLOADS = {
+    "C1": "C1: synthetic static room (acceptance RoomScript), {W}x{H} RGB-D, 1 cm voxels",
+    "C2": "C2: synthetic room with 2 moving boxes, {W}x{H} RGB-D, 1 cm voxels",
+    "C3": "C3: synthetic large scene (12 x 4 x 12 m room + props), {W}x{H} RGB-D, 0.5 cm voxels, 2^22-entry hash",
+    "C4": "C4: synthetic room with 2 moving boxes, {W}x{H} RGB-D (K 1050/639.5/359.5), 1 cm voxels, 3 levels, "
+          "mesh export after the run",
+}
+L2_NOTE = {
+    "C3": "bricks (~1e5-1e6, 0.5-4 GB) exceed the 126 MB L2: fuse/alloc stream from HBM",
+    "C4": "bricks L2-resident; frames (6.4 MB each) stream from HBM",
+}
+
+
+def workload_config(name, W, H, F):
     """The `config` object of both arms (identical by construction)."""
-    return {"workload": f"{CONFIG}: synthetic room with 2 moving boxes, {W}x{H} RGB-D, 1 cm voxels, "
-                        f"{F}-frame ping-pong sequence, refine_depth off",
-            "resolution": [W, H], "voxel_size": 0.01, "frames_in_sequence": F,
-            "l2": "bricks (~20k, 80 MB) L2-resident by design; the frames (430 MB) exceed L2"}
+    from paper_1905_02082_b200 import scenes
+
+    return {"workload": WORKLOADS[name].format(W=W, H=H) + f", {F}-frame sequence (ping-pong past its end), "
+                                                            "refine_depth off",
+            "resolution": [W, H], "voxel_size": scenes.BENCH_CONFIGS[name]["voxel"], "frames_in_sequence": F,
+            "l2": L2_NOTE.get(name, "bricks (~20k, 80 MB) L2-resident by design; the frames (430 MB) exceed L2")}
+
+
+def volume_params(name):
+    """VolumeConfig of a workload: (voxel_size, max_blocks, hash_capacity)."""
+    from paper_1905_02082_b200 import scenes
+
+    c = scenes.BENCH_CONFIGS[name]
+    return c["voxel"], c.get("max_blocks", 1000000), c.get("hash_capacity", 0)
 
 
 def parity_block(gpu, cpu):
@@ -195,30 +222,36 @@ def run_ours(args):
     import numpy as np
     import torch
 
+    from oracle import oracle as O
     from paper_1905_02082_b200 import _lib as L
     from paper_1905_02082_b200 import api, replicas, scenes
 
+    name = args.config
     R = replicas.env()
     rank, world, local = R.rank, R.world, R.local
     torch.cuda.set_device(local)
     R = replicas.init("nccl")
     lib = L.load()
-    cfgd = scenes.BENCH_CONFIGS[CONFIG]
+    cfgd = scenes.BENCH_CONFIGS[name]
     seed = replicas.sequence_seed(cfgd["seed"], R)  # independent sequence per replica
-    ok, depth_np, rgb_np, _ = render_sequence(scenes.config_script(CONFIG, seed=seed))
+    script = scenes.config_script(name, seed=seed)
+    F = cfgd["frames"]
+    ok, depth_np, rgb_np, _ = render_sequence(script, min(F, args.warmup + args.steps))  # the frames the run uses
     k = api.intrinsics(ok.fx, ok.fy, ok.cx, ok.cy, ok.width, ok.height, ok.depth_scale)
-    F, H, W = depth_np.shape
+    Fr, H, W = depth_np.shape
     depth_h = torch.from_numpy(depth_np).pin_memory()
     rgb_h = torch.from_numpy(rgb_np).pin_memory()
     depth = depth_h.to("cuda")
     rgb = rgb_h.to("cuda")
     torch.cuda.synchronize()
 
-    cfg = api.pipeline_config(refine=False)
+    voxel, max_blocks, cap = volume_params(name)
+    cfg = api.pipeline_config(refine=False, volume=api.volume_config(voxel_size=voxel, max_blocks=max_blocks,
+                                                                     hash_capacity=cap))
 
     def make_frames(dev_resident):
         frames = []
-        for i in range(F):
+        for i in range(Fr):
             f = L.rf_frame()
             f.intrinsics = k
             if dev_resident:
@@ -228,15 +261,11 @@ def run_ours(args):
             frames.append(f)
         return frames
 
-    def run_steps(p, frames, start, n, stats, pose, record=None):
-        for s in range(start, start + n):
-            f = frames[seq_index(s, F)]
-            f.timestamp = s / 30.0
-            code = lib.rf_pipeline_process_frame(p.h, C.byref(f), C.byref(stats), pose)
-            if code != 0:
-                L.check(code)
-            if record is not None:
-                record(p)
+    def run_steps(p, frames, start, n, stats, pose):
+        for st in range(start, start + n):
+            f = frames[seq_index(st, F)]
+            f.timestamp = st / 30.0
+            L.check(lib.rf_pipeline_process_frame(p.h, C.byref(f), C.byref(stats), pose))
 
     def barrier():
         replicas.barrier(R)
@@ -290,6 +319,14 @@ def run_ours(args):
         gpu_steps.append(({"registrations": sa[jj].registrations, "iterations": sa[jj].iterations,
                            "masked_pixels": sa[jj].masked_pixels, "tracking_lost": sa[jj].tracking_lost},
                           np.array(pa[12 * jj:12 * jj + 12])))
+    mesh = None
+    if name == "C4":  # ExtractMesh of the run's model (mesh.cpp:149-181), timed apart from the frames
+        vol = pv.volume()
+        vol.extract_mesh()  # loads the mesh kernels' module
+        t0 = time.perf_counter()
+        v_, c_, f_ = vol.extract_mesh()
+        mesh = {"ms": round(1e3 * (time.perf_counter() - t0), 3), "vertices": len(v_), "faces": len(f_),
+                "bricks": num_blocks, "includes": "device extraction + D2H of vertices, colours and faces"}
 
     # ---- per-stage device times and work counters (roofline): the same steps
     # frame by frame with CUDA events between the kernels
@@ -303,7 +340,8 @@ def run_ours(args):
     sums = L.rf_frame_counters()
     L.check(lib.rf_pipeline_profile_counters(pp.h, C.byref(sums)))
     agg.update(pixel_passes=sums.pixel_passes, visible=sums.visible_bricks, dda=sums.dda_visits,
-               new=sums.new_blocks, ff_rounds=sums.floodfill_rounds)
+               new=sums.new_blocks, ff_rounds=sums.floodfill_rounds, passes=sums.passes)
+    del pp
 
     # ---- e2e: pinned host frames through the same public call, wall clock
     # (each step's H2D copy and its result read-back inside the timed region)
@@ -317,6 +355,7 @@ def run_ours(args):
     L.check(lib.rf_pipeline_process_frames(pe.h, timed_h, C.c_uint64(args.steps), st_arr, poses))
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    del pe
 
     # ---- max over ranks
     sec, e2e_sec = replicas.max_over_ranks(R, [ms / 1000.0, e2e_s])
@@ -327,7 +366,7 @@ def run_ours(args):
         replicas.finish(R)
         return
 
-    # ---- roofline of the dominant kernel (SURVEY §8d bytes model)
+    # ---- rooflines (SURVEY §8d bytes model): every kernel, the dominant one first
     n = args.steps
     P0 = W * H
     stage_ms = [stage[i] / max(1, nprof.value) for i in range(4)]
@@ -344,29 +383,47 @@ def run_ours(args):
     names = ["track", "allocate", "cull", "fuse"]
     dom = max(range(4), key=lambda i: stage_ms[i])
     peak, peak_kind = measured_peaks()
-    achieved = bytes_per_frame[names[dom]] / (stage_ms[dom] / 1e3) / 1e9
+    achieved = {nm: bytes_per_frame[nm] / (stage_ms[i] / 1e3) / 1e9 for i, nm in enumerate(names)}
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             traffic = json.load(f).get(names[dom])
     except Exception:
         pass
+    # k_track is bound by its chain of dependent passes, not by bytes: the
+    # latency model puts the measured grid all-reduce floor and the LM step of
+    # every pass against the kernel's time (the rest is the pixel phases).
+    us_red, cyc = C.c_double(), (C.c_double * 3)()
+    L.check(lib.rf_diag_grid_barrier(local, 500, 1, C.byref(us_red)))
+    L.check(lib.rf_diag_lm_step(local, 200, cyc))
+    sm_mhz = clocks.summary().get("sm_mhz") or 1965.0
+    passes = agg["passes"] / max(1, nprof.value)
+    fixed_us = passes * (us_red.value + cyc[2] / sm_mhz)
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": n,
         "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / n, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": DATA.format(cfg=CONFIG, seed=seed),
-        "config": workload_config(W, H, F),
+        "data": DATA.format(cfg=name, seed=seed),
+        "config": workload_config(name, W, H, F),
         "parallelism": f"replicas x{world} (independent sequences, no collective)",
         "api": "rf_pipeline_process_frames (RunSequence: up to 64 frames enqueued back to back)",
         "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": P0 * 4 + P0 * 3,
                 "d2h_bytes_per_step": 192 + 32},
         "gpu_launches": int(gpu_launches),
-        "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved, 2), "peak": peak,
-                     "peak_source": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 5),
+        "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": round(achieved[names[dom]], 2), "peak": peak,
+                     "peak_source": peak_kind, "unit": "GB/s", "frac": round(achieved[names[dom]] / peak, 5),
                      "traffic": traffic, "bytes_per_launch": round(bytes_per_frame[names[dom]]),
                      "launch_ms": round(stage_ms[dom], 5)},
+        "roofline_by_kernel": {nm: {"launch_ms": round(stage_ms[i], 5), "bytes_per_launch": round(bytes_per_frame[nm]),
+                                    "achieved_gbs": round(achieved[nm], 1), "frac": round(achieved[nm] / peak, 4)}
+                               for i, nm in enumerate(names)},
+        "latency_model": {"kernel": "track", "passes_per_frame": round(passes, 2),
+                          "allreduce_us": round(us_red.value, 3), "lm_step_us": round(cyc[2] / sm_mhz, 3),
+                          "fixed_us_per_frame": round(fixed_us, 1),
+                          "frac_of_track": round(fixed_us / (stage_ms[0] * 1e3), 3),
+                          "note": "passes x (grid all-reduce floor + one-thread LM step), measured in-process; the "
+                                  "remainder of k_track is the pixel phases, mask and pyramid"},
         "stages_ms_per_frame": {nm: round(stage_ms[i], 5) for i, nm in enumerate(names)},
         "workload_stats": {"lm_iterations_per_frame": agg["iters"] / n, "registrations_per_frame": agg["regs"] / n,
                            "masked_pixels_per_frame": agg["masked"] / n, "lost_frames": agg["lost"],
@@ -375,25 +432,40 @@ def run_ours(args):
                            "floodfill_rounds_per_frame": agg["ff_rounds"] / n},
         "clocks": clocks.summary(),
     }
+    if mesh:
+        line["mesh_export"] = mesh
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"], cpu_steps = cpu_baseline(depth_np, rgb_np, ok, args.cpu_sample_seconds)
+        scene = O.Scene(script)
+        cache = {}
+
+        def frame(st):  # the bench's bytes, rendered on demand past the GPU run's frames
+            j = seq_index(st, F)
+            if j < Fr:
+                return depth_np[j], rgb_np[j]
+            if j not in cache:
+                r = scene.render(j)
+                cache[j] = (r["depth"], r["rgb"])
+            return cache[j]
+
+        line["cpu_baseline"], cpu_steps = cpu_baseline(frame, ok, args.cpu_sample_seconds, name)
         line["parity"] = parity_block(gpu_steps, cpu_steps)
     print(json.dumps(line), flush=True)
     replicas.finish(R)
 
 
-def oracle_rate(frame, k, budget_s, threads, max_frames=None):
+def oracle_rate(frame, k, budget_s, threads, vol):
     """Oracle pipeline over a frame sample: bootstrap on frame 0 (untimed, as
     the reference's fps excludes frame 0), then time frames until budget_s.
     Returns the rate and every step's (stats, pose) for the parity block."""
     from oracle import oracle as O
 
-    p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads)))
+    p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads),
+                              volume=O.vol_cfg(voxel_size=vol[0], max_blocks=vol[1])))
     d, c = frame(0)
     st, pose = p.process_frame(d, c, k, 0.0)
     steps = [(st, pose)]
     spent, n = 0.0, 0
-    while spent < budget_s and (max_frames is None or n < max_frames):
+    while spent < budget_s or n < 2:
         i = n + 1
         d, c = frame(i)
         t0 = time.perf_counter()
@@ -404,15 +476,13 @@ def oracle_rate(frame, k, budget_s, threads, max_frames=None):
     return n / spent, n, spent, steps
 
 
-def cpu_baseline(depth_np, rgb_np, k, budget_s):
+def cpu_baseline(frame, k, budget_s, name):
     threads = os.cpu_count() or 1
-    F = depth_np.shape[0]
-    rate, n, spent, steps = oracle_rate(lambda i: (depth_np[seq_index(i, F)], rgb_np[seq_index(i, F)]), k,
-                                        budget_s, threads)
+    rate, n, spent, steps = oracle_rate(frame, k, budget_s, threads, volume_params(name))
     return ({"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
-             "sample": f"oracle ProcessFrame on steps 1..{n} of the same {CONFIG} ping-pong sequence and the same "
-                       f"frame bytes as the GPU arm ({spent:.1f} s, {threads} threads for integrate/carve and "
-                       f"registration)"}, steps)
+             "sample": f"oracle ProcessFrame on steps 1..{n} of the same {name} sequence and the same frame bytes "
+                       f"as the GPU arm ({spent:.1f} s, {threads} threads for integrate/carve and registration)"},
+            steps)
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -423,21 +493,24 @@ def run_reference(args):
     rank, world = R.rank, R.world
     if rank != 0:  # rank 0 alone times the host CPU path; the others exit 0
         return
-    import numpy as np
-
     from oracle import oracle as O
     from paper_1905_02082_b200 import scenes
 
-    seed = scenes.BENCH_CONFIGS[CONFIG]["seed"]
-    k, depth_np, rgb_np, _ = render_sequence(scenes.config_script(CONFIG, seed=seed))  # the GPU arm's bytes
-    F, H, W = depth_np.shape
+    name = args.config
+    seed = scenes.BENCH_CONFIGS[name]["seed"]
+    F = scenes.BENCH_CONFIGS[name]["frames"]
+    k, depth_np, rgb_np, _ = render_sequence(scenes.config_script(name, seed=seed),
+                                             min(F, args.warmup + args.steps))  # the GPU arm's bytes
+    Fr, H, W = depth_np.shape
 
     def frame(i):
         j = seq_index(i, F)
         return {"depth": depth_np[j], "rgb": rgb_np[j]}
 
     threads = os.cpu_count() or 1
-    p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads)))
+    vox, mb, _ = volume_params(name)
+    p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads),
+                              volume=O.vol_cfg(voxel_size=vox, max_blocks=mb)))
     for i in range(args.warmup):
         f = frame(i)
         p.process_frame(f["depth"], f["rgb"], k, i / 30.0)
@@ -451,11 +524,11 @@ def run_reference(args):
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
-        "data": DATA.format(cfg=CONFIG, seed=seed),
-        "config": workload_config(W, H, F),
+        "data": DATA.format(cfg=name, seed=seed),
+        "config": workload_config(name, W, H, F),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"oracle ProcessFrame, steps {args.warmup}..{args.warmup + args.steps - 1} of the "
-                                   f"{CONFIG} sequence, {threads} threads"},
+                                   f"{name} sequence, {threads} threads"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -163,6 +163,7 @@ struct Workspace {
     FrameSignal* d_sig = nullptr;
     unsigned long long sig_seq = 0;
     int W = 0, H = 0, L = 0;
+    int pxc_steps = 0, dyn_bytes = 16;  // the tracking kernel's dynamic shared memory for this frame size
     size_t lvl_off_depth[kMaxLevels] = {}, lvl_off_inten[kMaxLevels] = {}, lvl_off_mask[kMaxLevels] = {};
 
     void init(int dev) {
@@ -173,14 +174,10 @@ struct Workspace {
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         // The tracking passes gather voxels through L1: leave it as much of the
         // unified L1/shared array as the kernel's static shared memory allows.
-        static const int carveout = [] {
-            const char* e = std::getenv("RF_TRACK_CARVEOUT");
-            return e ? std::atoi(e) : int(cudaSharedmemCarveoutMaxL1);
-        }();
-        CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTrackDynSmem)));
-        if (carveout >= 0)
-            CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributePreferredSharedMemoryCarveout, carveout));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_track, kTrackThreads, kTrackDynSmem));
+        CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTrackMaxDynSmem)));
+        CK(cudaFuncSetAttribute((const void*)k_track, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                int(cudaSharedmemCarveoutMaxL1)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_track, kTrackThreads, kTrackMaxDynSmem));
         require(per > 0, RF_CUDA_ERROR, "tracking kernel does not fit on an SM");
         track_grid = sms * per;
         gsync.ensure(sizeof(GridSync));
@@ -216,6 +213,16 @@ struct Workspace {
     }
     void ensure_frame(int w, int h, int levels_needed) {
         if (w == W && h == H && levels_needed <= L) return;
+        {  // pixel cache: one entry per pixel step of the finest level (the coarser ones need fewer);
+           // at least the floodfill's tile flags (ff_flag_mode); the excess of huge frames reloads
+            const size_t npx = size_t(w) * h, per = (npx + track_grid - 1) / track_grid;
+            const size_t steps = (per + kTrackThreads - 1) / kTrackThreads;
+            const size_t nft = size_t((w + 31) / 32) * ((h + 31) / 32);
+            size_t bytes = std::max(steps * kTrackThreads * 8, ((nft + 15) & ~size_t(15)) + 2 * nft);
+            bytes = std::min((bytes + 15) & ~size_t(15), kTrackMaxDynSmem);
+            pxc_steps = int(std::min(steps, bytes / (size_t(kTrackThreads) * 8)));
+            dyn_bytes = int(bytes);
+        }
         const size_t n = size_t(w) * h;
         depth.ensure(n * 4);
         rgb.ensure(n * 3);
@@ -472,12 +479,11 @@ struct rf_volume {
                 wa.bcount[j] = in[c0 + j].bcount;
             }
             if (c0 > 0) k_win_first_reset<<<148, 256, 0, ws.stream>>>(view);
-            bool lists = false, walks = false;
-            for (int j = 0; j < m; ++j) (in[c0 + j].bcount ? lists : walks) = true;
+            bool lists = false;
+            for (int j = 0; j < m; ++j) lists = lists || in[c0 + j].bcount;
             if (lists) k_insert_window<<<2 * 148, 256, 0, ws.stream>>>(wa);
             // entries without a list (or whose list overflowed: decided on the device) walk their pixels
             const long long total = (long long)in[c0].k.width * in[c0].k.height * m;
-            (void)walks;
             k_alloc_window<<<unsigned((total + 255) / 256), 256, 0, ws.stream>>>(wa);
             reset_counter(kVisible);
             k_cull_window<<<4 * 148, 256, 0, ws.stream>>>(wa);
@@ -552,6 +558,8 @@ struct rf_volume {
         a.out = ws.out.as<TrackOut>();
         a.reg.levels = levels;
         a.trace = ws.trace.as<unsigned long long>();
+        a.pxc_steps = ws.pxc_steps;
+        a.dyn_bytes = ws.dyn_bytes;
         return a;
     }
     void dump_trace() {  // appends one frame's per-pass timeline (binary u64) to RF_TRACE_FILE
@@ -566,7 +574,7 @@ struct rf_volume {
     void launch_track(TrackArgs& a) {
         if (a.trace) CK(cudaMemsetAsync(a.trace, 0, kTracePasses * 8 * sizeof(unsigned long long), ws.stream));
         a.grid = ws.grid();
-        launch(k_track, ws.track_grid, kTrackThreads, kTrackDynSmem, ws.stream, true, a);
+        launch(k_track, ws.track_grid, kTrackThreads, size_t(a.dyn_bytes), ws.stream, true, a);
     }
     TrackOut fetch_out() {
         CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));
@@ -1115,10 +1123,12 @@ rf_status rf_build_pyramid(const rf_frame* f, const uint8_t* mask, int32_t level
             CK(cudaMemcpyAsync(a.F.mask[0], mask, n, kind, ws.stream));
             a.use_mask = 1;
         }
+        a.pxc_steps = ws.pxc_steps;
+        a.dyn_bytes = ws.dyn_bytes;
         a.grid = ws.grid();
         a.out = ws.out.as<TrackOut>();
         void* args[] = {&a};
-        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, kTrackDynSmem,
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, size_t(a.dyn_bytes),
                                        ws.stream));
         size_t off = 0;
         for (int l = 0; l < levels; ++l) {
@@ -1261,10 +1271,12 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
         a.F.grow = ws.mwork.as<uint8_t>() + (3 * n + 255) / 256 * 256;
         a.F.ffstamp = ws.ffstamp();
         a.F.mask[0] = ws.mask_in.as<uint8_t>();
+        a.pxc_steps = ws.pxc_steps;
+        a.dyn_bytes = ws.dyn_bytes;
         a.grid = ws.grid();
         a.out = ws.out.as<TrackOut>();
         void* args[] = {&a};
-        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, kTrackDynSmem,
+        CK(cudaLaunchCooperativeKernel((void*)k_track, dim3(ws.track_grid), dim3(kTrackThreads), args, size_t(a.dyn_bytes),
                                        ws.stream));
         CK(cudaMemcpyAsync(out, ws.mask_in.p, n, cudaMemcpyDeviceToHost, ws.stream));
         CK(cudaMemcpyAsync(ws.h_out, ws.out.p, sizeof(TrackOut), cudaMemcpyDeviceToHost, ws.stream));

@@ -576,10 +576,7 @@ __device__ __forceinline__ bool sample_point(const VolumeView& V, const double p
 // partial vector, the last CTA to arrive folds all partials in CTA order
 // (fixed order => run-to-run deterministic) and publishes the result, then
 // releases the others. One L2 round trip per waiting CTA.
-#ifndef RF_ARRIVE_LANES
-#define RF_ARRIVE_LANES 8
-#endif
-constexpr int kArriveLanes = RF_ARRIVE_LANES;  // (<= 32) arrival counters on separate 128-B lines (parallel L2 atomics)
+constexpr int kArriveLanes = 8;  // (<= 32) arrival counters on separate 128-B lines (parallel L2 atomics)
 struct GridSync {
     unsigned long long lane[2][kArriveLanes][16];  // [launch parity][lane][0] = arrivals, rest padding
 };

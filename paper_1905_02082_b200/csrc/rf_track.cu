@@ -21,17 +21,13 @@ constexpr double kRelDecreaseTol = 1e-6;         // registration.cpp:26
 __device__ __forceinline__ int hidx(int i, int j) { return i * 6 - (i * (i - 1)) / 2 + (j - i); }
 
 __shared__ int s_trace_pass;  // per-CTA pass counter for the optional timeline
-// Per-thread copy of the first kTrackPxCache pixels' inputs {depth (0: skip),
+// Per-thread copy of the first a.pxc_steps pixels' inputs {depth (0: skip),
 // intensity} for the Jacobian passes: a thread sees the same pixels in every
 // pass at a level, so after the first pass they come from shared memory
-// instead of an L2 round trip (dynamic shared memory, kTrackDynSmem).
+// instead of an L2 round trip (dynamic shared memory, TrackArgs::dyn_bytes).
 extern __shared__ __align__(16) unsigned char s_dyn[];
 __device__ __forceinline__ float2* pxc_base() { return reinterpret_cast<float2*>(s_dyn); }
 __shared__ int s_pxc_tag;  // (level + 1) | 16 * use_mask of the cached inputs, 0: none
-#ifdef RF_LM_PROFILE
-__shared__ long long s_lmp[5];  // [1..4]: steps, judge->solve-done, solve, expmap+compose; [0]: warm repeat
-__shared__ volatile double s_lmp_sink;
-#endif
 __shared__ int s_passes;   // Accumulate passes run (CTA 0; TrackOut.passes / pixel_passes)
 __shared__ double s_pixel_passes;
 __shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (see voxel_luma_lut)
@@ -47,6 +43,12 @@ struct RegState {
     double cur_err, tol, lam_acc, lam_rej;
     int small_step;
     int total, converged, lost, go, brk, level_it;
+    // The next candidate if the trial in flight is rejected: it depends only
+    // on the current normal equations and the raised damping, so it is solved
+    // during the trial's pass (on a thread with slack) instead of after it.
+    Pose cand_rej;
+    double dnorm_rej;
+    int rej_ok;
 };
 
 // ------------------------------------------------------------------ math
@@ -211,19 +213,17 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
 
 // ------------------------------------------------------------------ pixel pass
 // One Accumulate (registration.cpp:49-117) over pyramid level `level`.
-#ifndef RF_TRACK_SPREAD
-#define RF_TRACK_SPREAD 64
-#endif
-template <bool kJac, bool kColor, class Hook>
+// `pre` runs on the CTA's last thread after its pixels when that thread has
+// fewer pixels than the busiest ones (its slack hides the work).
+template <bool kJac, bool kColor, class Hook, class Pre>
 __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
-                           double* scratch, double* blk, double* out, const Hook& hook) {
+                           double* scratch, double* blk, double* out, const Hook& hook, const Pre& pre) {
     const FrameView& F = a.F;
     const Intr K = F.K[level];
     const double min_depth = a.V.min_depth, max_depth = a.V.max_depth;
     double acc[kAccN];
 #pragma unroll
     for (int i = 0; i < kAccN; ++i) acc[i] = 0.0;
-    const int ntx = (K.w + kTileW - 1) / kTileW, nty = (K.h + kTileH - 1) / kTileH;
     const float* depth = level == 0 ? F.depth0 : F.depth[level];
     const uint8_t* mask = use_mask ? F.mask[level] : nullptr;
     unsigned long long* tr = (a.trace && s_trace_pass < kTracePasses) ? a.trace + 8 * s_trace_pass : nullptr;
@@ -242,7 +242,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
         float d;
         bool masked;
         float inten = 0.f;  // ToIntensity (image.hpp:85-91) at level 0, the pyramid's f32 above
-        if (pxc_hit && it < kTrackPxCache) {
+        if (pxc_hit && it < a.pxc_steps) {
             const float2 c = pxc_base()[it * kTrackThreads + threadIdx.x];
             d = c.x;
             inten = c.y;
@@ -258,7 +258,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
                     inten = __ldcg(F.inten[level] + p);
                 }
             }
-            if (kJac && it < kTrackPxCache) pxc_base()[it * kTrackThreads + threadIdx.x] = make_float2(masked ? 0.f : d, inten);
+            if (kJac && it < a.pxc_steps) pxc_base()[it * kTrackThreads + threadIdx.x] = make_float2(masked ? 0.f : d, inten);
         }
         float rs = 0.f;
         uint8_t rv = 0;
@@ -321,35 +321,19 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
             F.res_valid[p] = rv;
         }
     };
-    // A level with at most RF_TRACK_SPREAD steps of the grid's pixels is spread
-    // evenly: ceil(npx / G) consecutive pixels per CTA (a strip of rows),
-    // instead of whole 16x24 tiles on part of the CTAs (640x480: 800 / 200 / 50
-    // tiles for 148 CTAs). B200, frames 5..104: tiles everywhere 1519 frames/s,
-    // coarsest level spread 1565, two coarsest 1577, all levels 1581 (default).
     const int npx = K.w * K.h;
-    if (npx <= RF_TRACK_SPREAD * int(gridDim.x) * kTrackThreads) {
-#ifndef RF_SPREAD_ALIGN
-#define RF_SPREAD_ALIGN 1
-#endif
-        const int per = ((npx + int(gridDim.x) - 1) / int(gridDim.x) + RF_SPREAD_ALIGN - 1) / RF_SPREAD_ALIGN * RF_SPREAD_ALIGN;
-        for (int it = 0, q = int(threadIdx.x); q < per; ++it, q += kTrackThreads) {
+    // The level's pixels spread evenly: ceil(npx / G) consecutive pixels per
+    // CTA (a strip of rows), 384 per step (640x480: 2076 / 519 / 130 per CTA
+    // at levels 0 / 1 / 2), instead of whole 16x24 tiles on part of the CTAs
+    // (B200, frames 5..104: 1519 -> 1581 frames/s).
+    {
+        const int per = (npx + int(gridDim.x) - 1) / int(gridDim.x);
+        int it = 0;
+        for (int q = int(threadIdx.x); q < per; ++it, q += kTrackThreads) {
             const int p = int(blockIdx.x) * per + q;
             if (p < npx) pixel(p % K.w, p / K.w, it);
         }
-    } else {
-        int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;  // tile walked incrementally (no per-tile division)
-        const int step_y = gridDim.x / ntx, step_x = gridDim.x % ntx;
-        for (int it = 0; ty < nty; tx += step_x, ty += step_y, ++it) {
-            if (tx >= ntx) {
-                tx -= ntx;
-                ++ty;
-                if (ty >= nty) break;
-            }
-            const int u = tx * kTileW + (threadIdx.x % kTileW);
-            const int v = ty * kTileH + (threadIdx.x / kTileW);
-            if (u >= K.w || v >= K.h) continue;
-            pixel(u, v, it);
-        }
+        if (threadIdx.x == kTrackThreads - 1 && it < (per + kTrackThreads - 1) / kTrackThreads) pre();
     }
     if (tr) {
         __syncthreads();
@@ -369,16 +353,17 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
 
 // `hook` runs on thread 0 once the CTA has arrived at the pass's all-reduce
 // (work that must not delay the CTA's own pixels or arrival).
-template <bool kJac, class Hook = NoHook>
+template <bool kJac, class Hook = NoHook, class Pre = NoHook>
 __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res,
-                                     double cw, double* scratch, double* blk, double* out, const Hook& hook = Hook()) {
+                                     double cw, double* scratch, double* blk, double* out, const Hook& hook = Hook(),
+                                     const Pre& pre = Pre()) {
     const bool color = cw > 0.0 && a.F.rgb0 != nullptr;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         s_passes += 1;  // CTA 0's tally, published once at kernel exit (no global RMW on the pass path)
         s_pixel_passes += double(a.F.K[level].w) * double(a.F.K[level].h);
     }
-    if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook);
-    else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook);
+    if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook, pre);
+    else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook, pre);
 }
 
 // ------------------------------------------------------------------ Register
@@ -418,9 +403,6 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
         bool judge = false;  // a trial was evaluated since the last solve
         for (;;) {
             if (threadIdx.x == 0) {
-#ifdef RF_LM_PROFILE
-                const long long cj = clock64();
-#endif
                 double lambda = st.lambda;
                 int brk = st.brk, level_it = st.level_it, total = st.total, converged = st.converged, ci = st.ci;
                 const double* tr = st.buf[ci ^ 1];
@@ -444,19 +426,25 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
                         }
                     }
                 }
-#ifdef RF_LM_PROFILE
-                long long c0 = clock64(), c1 = c0;
-#endif
                 int go = 0;
-                while (!brk && level_it < R.max_iterations) {
+                bool rejected = false;
+                if (judge) rejected = !(tr[29] >= min_valid && tr[27] + cw * tr[28] < st.cur_err);
+                if (rejected && !brk && level_it < R.max_iterations && st.rej_ok) {
+                    // the solve this loop would run now (same buffer, same damping): done during the pass
+                    ++level_it;
+                    ++total;
+                    st.cand = st.cand_rej;
+                    st.dnorm = st.dnorm_rej;
+                    go = 1;
+                }
+                if (judge && a.trace && blockIdx.x == 0 && s_trace_pass > 0 && s_trace_pass <= kTracePasses)
+                    a.trace[8 * (s_trace_pass - 1) + 6] |= rejected ? 0x200ull : 0x100ull;  // the trial's verdict
+                while (!go && !brk && level_it < R.max_iterations) {
                     ++level_it;
                     ++total;
                     const Pose P0 = st.pose;
                     double delta[6];  // in registers: ExpMap and the norm read it straight from the solve
                     const bool solved = lm_solve(st.buf[ci], lambda, delta);
-#ifdef RF_LM_PROFILE
-                    c1 = clock64();
-#endif
                     if (!solved) {
                         lambda = fmin(lambda * R.lambda_up, 1e12);  // NumericalIssue: damp more, retry
                         continue;
@@ -478,27 +466,7 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
                 st.converged = converged;
                 st.ci = ci;
                 st.go = go;
-#ifdef RF_LM_PROFILE
-                {
-                    const long long c2 = clock64();
-                    if (judge) {
-                        s_lmp[1] += 1;
-                        s_lmp[2] += c2 - cj;
-                        s_lmp[3] += c1 - c0;
-                        s_lmp[4] += c2 - c1;
-                        // the same solve + ExpMap + compose again, now with warm caches
-                        const long long h0 = clock64();
-                        double d2[6];
-                        const bool ok2 = lm_solve(st.buf[st.ci], st.lambda, d2);
-                        Pose e2;
-                        expmap(d2, e2);
-                        const Pose c2p = pose_mul(e2, st.pose);
-                        const long long h1 = clock64();
-                        s_lmp_sink = c2p.t[0] + (ok2 ? 1.0 : 0.0);
-                        s_lmp[0] += h1 - h0;
-                    }
-                }
-#endif
+                st.rej_ok = 0;
                 if (a.trace && blockIdx.x == 0 && s_trace_pass < kTracePasses)
                     a.trace[8 * s_trace_pass + 7] = global_ns();  // solve done (next pass's record)
             }
@@ -512,6 +480,23 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
                 st.lam_acc = fmax(st.lambda / R.lambda_down, 1e-12);
                 st.lam_rej = fmin(st.lambda * R.lambda_up, 1e12);
                 st.small_step = sqrt(st.dnorm) < R.eps;
+            }, [&] {
+                // registration.cpp:265-271 then :240-249 on rejection: lambda
+                // raised (a level that reaches 1e12 converges instead)
+                const double lam = fmin(st.lambda * R.lambda_up, 1e12);
+                if (!(lam >= 1e12)) {
+                    double delta[6];
+                    if (lm_solve(st.cur(), lam, delta)) {
+                        Pose e;
+                        expmap(delta, e);
+                        st.cand_rej = pose_mul(e, st.pose);
+                        double dn = 0.0;
+#pragma unroll
+                        for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
+                        st.dnorm_rej = dn;
+                        st.rej_ok = 1;
+                    }
+                }
             });
             judge = true;
         }
@@ -650,18 +635,18 @@ __device__ __forceinline__ void ff_enqueue3x3(int* base, int ntx, int nty, int t
     }
 }
 
-// Flag worklists (RF_FF_FLAGS, default): F.ffstamp holds three per-tile flag
+// Flag worklists (when the tile flags fit in the launch's dynamic shared
+// memory; the atomic queue above otherwise): F.ffstamp holds three per-tile flag
 // arrays, round r reading array r % 3 (tiles that changed in round r - 1, or
 // seeded ones for r = 0), setting array (r + 1) % 3 with plain stores and
 // zeroing array (r + 2) % 3 (read in round r - 1). Every CTA builds the same
 // tile list -- the 3x3 dilation of the flags, compacted in tile order -- in
 // its dynamic shared memory, so a round costs one flag load instead of the
-// count / list loads and the returning atomics of the queue.
-#ifndef RF_FF_FLAGS
-#define RF_FF_FLAGS 1
-#endif
-constexpr int kFfMaxFlagTiles = int((kTrackDynSmem - 16) / 3);  // nft bytes + nft uint16 in the pixel cache
-__device__ __forceinline__ bool ff_flag_mode(int nft) { return RF_FF_FLAGS && nft <= kFfMaxFlagTiles; }
+// count / list loads and the returning atomics of the queue (1336 -> 1340
+// frames/s).
+__device__ __forceinline__ bool ff_flag_mode(int nft, int dyn_bytes) {  // nft flag bytes + nft uint16 list
+    return ((nft + 15) & ~15) + 2 * nft <= dyn_bytes;
+}
 
 // Kogge-Stone fills of a 32-bit row: every pixel reachable from `g` by
 // moves of one pixel in the given direction through pixels whose entry bit
@@ -719,7 +704,7 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint32_t* planes,
     auto at = [&](int gx, int gy) -> uint32_t {  // mask bit of an image pixel (0 outside)
         return (gx >= 0 && gx < w && gy >= 0 && gy < h) ? uint32_t(__ldcg(m + size_t(gy) * w + gx) != 0) : 0u;
     };
-    const bool flags = ff_flag_mode(nft);
+    const bool flags = ff_flag_mode(nft, a.dyn_bytes);
     uint8_t* s_flag = reinterpret_cast<uint8_t*>(s_dyn);  // (the pixel cache is refilled after the mask)
     uint16_t* s_list = reinterpret_cast<uint16_t*>(s_dyn + ((nft + 15) & ~15));
     __shared__ int s_wcount[kTrackThreads / 32];
@@ -876,7 +861,6 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
     uint8_t* seeds = F.mwork[1];
     const double thr = M.gamma * M.truncation * M.truncation;  // ThresholdResiduals (dynamics_mask.cpp:9-18)
     const bool do_thr = stages & 1;
-    int dummy = 0;
     if (re <= kMorphMaxR) {
         for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
             int nseed = 0;
@@ -893,7 +877,7 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
                 grow_tile(F.depth0, reinterpret_cast<uint32_t*>(F.grow), w, h, t % ntx, t / ntx, M.theta,
                           M.connectivity);
                 if (__syncthreads_or(nseed)) {
-                    if (!ff_flag_mode(ntx * nty)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
+                    if (!ff_flag_mode(ntx * nty, a.dyn_bytes)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
                     else if (threadIdx.x == 0) F.ffstamp[t] = 1;  // round 0's flags
                 }
             }
@@ -919,7 +903,7 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
                 any |= (gx < w && gy < h && __ldcg(seeds + gy * w + gx)) ? 1 : 0;
             }
             if (__syncthreads_or(any)) {
-                if (!ff_flag_mode(ntx * nty)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
+                if (!ff_flag_mode(ntx * nty, a.dyn_bytes)) ff_enqueue3x3(F.ffstamp, ntx, nty, t % ntx, t / ntx, 0);
                 else if (threadIdx.x == 0) F.ffstamp[t] = 1;
             }
         }
@@ -963,7 +947,7 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
     if ((a.mode == kModeFrame && a.dynamics) || a.mode == kModeMask) {  // floodfill worklists (ff_list)
         const int nft = ((a.F.K[0].w + kFfW - 1) / kFfW) * ((a.F.K[0].h + kFfH - 1) / kFfH);
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 3 * nft + kFfCounts; i += gridDim.x * blockDim.x)
-            a.F.ffstamp[i] = (i < nft && !ff_flag_mode(nft)) ? -1 : 0;
+            a.F.ffstamp[i] = (i < nft && !ff_flag_mode(nft, a.dyn_bytes)) ? -1 : 0;
     }
 
     if (a.mode == kModeLinearize || a.mode == kModeEvalDepth || a.mode == kModeEvalColor) {
@@ -1100,9 +1084,6 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
     if (threadIdx.x == 0) {
         s_trace_pass = 0;
         s_pxc_tag = 0;
-#ifdef RF_LM_PROFILE
-        for (int i = 0; i < 5; ++i) s_lmp[i] = 0;
-#endif
     }
     for (int i = threadIdx.x; i < 768; i += blockDim.x) {
         const double w = i < 256 ? 0.2126 : (i < 512 ? 0.7152 : 0.0722);  // image.hpp:80-83
@@ -1114,12 +1095,6 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
         a.out->passes = s_passes;
         a.out->pixel_passes = s_pixel_passes;
     }
-#ifdef RF_LM_PROFILE
-    if (lead && a.trace) {  // diagnostic variant: record 251 = {steps, judge..solved, solve, expmap+compose, warm repeat}
-        for (int i = 0; i < 4; ++i) a.trace[8 * 251 + i] = (unsigned long long)s_lmp[i + 1];
-        a.trace[8 * 251 + 4] = (unsigned long long)s_lmp[0];
-    }
-#endif
 }
 
 }  // namespace rfb
@@ -1134,10 +1109,43 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_grid_bench(G
     if (threadIdx.x < 32) blk[threadIdx.x] = double(blockIdx.x + threadIdx.x);
     __syncthreads();
     for (int i = 0; i < iters; ++i) {
-        if (reduce) {
+        if (reduce == 1) {
             double v[kAccN];
             for (int k = 0; k < kAccN; ++k) v[k] = blk[k % 32];
             block_grid_allreduce<kAccN, false>(g, v, scratch, red);
+        } else if (reduce == 2) {  // the CTA-local part only: transpose reduce + warp-0 sum
+            double v[32];
+            for (int k = 0; k < 32; ++k) v[k] = k < kAccN ? blk[k] : 0.0;
+            scratch[(threadIdx.x >> 5) * 32 + (threadIdx.x & 31)] = warp_transpose_reduce(v);
+            __syncthreads();
+            if (threadIdx.x < kAccN) {
+                double t = 0.0;
+                for (int w = 0; w < int(blockDim.x >> 5); ++w) t += scratch[w * 32 + threadIdx.x];
+                red[threadIdx.x] = t;
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) blk[threadIdx.x] = red[threadIdx.x] * 1e-30 + blk[threadIdx.x];
+            __syncthreads();
+        } else if (reduce == 3) {  // one value: the grid exchange without the 30-wide fold
+            double v[1] = {blk[0]};
+            block_grid_allreduce<1, false>(g, v, scratch, red);
+        } else if (reduce == 4) {  // the exchange alone: thread 0 stores a line, every CTA polls all lines
+            const unsigned int bar = s_ll_bar;
+            const uint32_t flag = (g.seq << 12) | (bar & 0xFFFu);
+            uint4* buf = g.ll + size_t(bar & 1u) * gridDim.x * 32;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                st_line(buf + blockIdx.x * 32, blk[0], flag);
+                s_ll_bar = bar + 1u;
+            }
+            double acc = 0.0;
+            for (int i = threadIdx.x; i < int(gridDim.x); i += blockDim.x) {
+                uint4 t = ld_line(buf + i * 32);
+                while (!line_ready(t, flag)) t = ld_line(buf + i * 32);
+                acc += line_value(t);
+            }
+            if (acc == 12345.0) blk[1] = acc;
+            __syncthreads();
         } else {
             grid_barrier(g);
         }

@@ -7,23 +7,14 @@
 namespace rfb {
 
 constexpr int kMaxLevels = 6;
-#ifndef RF_TRACK_THREADS
-#define RF_TRACK_THREADS 384  // 12 warps at <= 168 registers (tools/pass_bench.py: 16.6 vs 19.9 us per L0 pass at 256)
-#endif
-#ifndef RF_TRACK_MIN_BLOCKS
-#define RF_TRACK_MIN_BLOCKS 1  // one CTA per SM: 148 grid partials
-#endif
-constexpr int kTrackThreads = RF_TRACK_THREADS;
-constexpr int kTrackMinBlocks = RF_TRACK_MIN_BLOCKS;
-constexpr int kTileW = 16, kTileH = kTrackThreads / kTileW;  // pixel tile per CTA step, 1 px per thread
-// Per-thread cache of the Jacobian passes' pixel inputs {depth, intensity},
-// one entry per tile step (a thread meets the same pixels in every pass of a
-// level), in dynamic shared memory: 8 steps cover 640x480 (<= 6 steps per CTA).
-#ifndef RF_TRACK_PXC
-#define RF_TRACK_PXC 8
-#endif
-constexpr int kTrackPxCache = RF_TRACK_PXC;
-constexpr size_t kTrackDynSmem = size_t(kTrackPxCache) * kTrackThreads * 8;
+constexpr int kTrackThreads = 384;  // 12 warps at <= 168 registers (tools/pass_bench.py: 16.6 vs 19.9 us per L0 pass at 256)
+constexpr int kTrackMinBlocks = 1;  // one CTA per SM: 148 grid partials
+// Per-thread cache of the Jacobian passes' pixel inputs {depth, intensity}:
+// one 8-byte entry per pixel step (a thread meets the same pixels in every
+// pass of a level), in dynamic shared memory sized per launch from the frame
+// (TrackArgs::pxc_steps): 6 steps at 640x480, 17 at 1280x720. The floodfill's
+// tile flags reuse the same bytes after the registrations.
+constexpr size_t kTrackMaxDynSmem = 96 * 1024;
 
 struct RegParams {  // RegistrationConfig, registration.hpp:13-23
     double color_weight;
@@ -98,6 +89,8 @@ struct TrackArgs {
     TrackOut* out;
     uint32_t* vol_counters;  // kModeFrame: snapshot kNumBlocks -> kBlocksBefore
     int bench_iters, bench_level;  // kModePassBench
+    int pxc_steps;       // pixel-cache entries per thread (dynamic shared memory)
+    int dyn_bytes;       // dynamic shared memory of this launch
 };
 
 }  // namespace rfb

@@ -17,12 +17,8 @@ namespace rfb {
 // quotient comes out +0 where a / b gives -0; the walk only floors and
 // subtracts these values, where the two zeros agree.
 __device__ __forceinline__ double div_rn(double a, double b, double rb) {
-#ifdef RF_WALK_IEEE_DIV
-    return a / b;
-#else
     const double q = a * rb;
     return __fma_rn(__fma_rn(-q, b, a), rb, q);
-#endif
 }
 
 // The ray segment of pixel p (AllocateForFrame, tsdf_volume.cpp:93-113):
@@ -614,10 +610,7 @@ __global__ void k_cull_window(WindowArgs a) {
 // Integrate (tsdf_volume.cpp:155-202) of the chunk's entries, in order, into
 // each listed brick: the voxel is read once, updated by every entry whose bit
 // is set, and written once.
-#ifndef RF_WIN_MINB
-#define RF_WIN_MINB 2
-#endif
-__global__ void __launch_bounds__(kBrickVoxels, RF_WIN_MINB) k_fuse_window(WindowArgs a) {
+__global__ void __launch_bounds__(kBrickVoxels, 2) k_fuse_window(WindowArgs a) {
     commit_links(a.V);
     __shared__ Pose Ws[kMaxWin];
     __shared__ double s_rcp[512];  // RN(1 / i) for the running averages (see div_f32)
@@ -648,10 +641,7 @@ __global__ void __launch_bounds__(kBrickVoxels, RF_WIN_MINB) k_fuse_window(Windo
         // Entries in groups of kGroup: the frame reads of a group (projection
         // only depends on the entry's pose) are all issued before the first
         // update, then the updates run in window order.
-#ifndef RF_WIN_GROUP
-#define RF_WIN_GROUP 4
-#endif
-        constexpr int kGroup = RF_WIN_GROUP;
+        constexpr int kGroup = 4;
         for (uint32_t m = bits; m;) {
             int jj[kGroup];
             float dd[kGroup];

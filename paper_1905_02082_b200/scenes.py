@@ -86,6 +86,40 @@ def bench_script(dynamic=True, width=640, height=480, frames=200, noise=0.001, s
     return s
 
 
+def large_scene_script(frames=500, width=640, height=480, noise=0.001, seed=45):
+    """BASELINE.json configs[2] (C3): a scaled room,
+    box half-extents 6 x 2 x 6 m, with props (12 pillars, crates, spheres) and
+    500 frames at 30 Hz along half of a 2.5 m circle looking outward and a little down
+    (walls 3.5-6 m away, props 1-3 m, the floor in view). Run with 0.5 cm voxels and a 2^22-entry hash: about
+    a million 8^3 bricks (4 GB), far beyond the 126 MB L2."""
+    f = 525.0 * width / 640.0
+    s = "intrinsics %.6f %.6f %.6f %.6f %d %d 5000\n" % (f, f, width / 2.0 - 0.5, height / 2.0 - 0.5, width, height)
+    s += "noise %g 0.0\n" % noise
+    s += "seed %d\n" % seed
+    s += "primitive hall static box 0 0 0 6 2 6 albedo checker 0.5 220 220 210 50 50 60\n"
+    for i in range(12):  # pillars on a 4 m circle, 30 degrees apart: always some in view
+        a = 2.0 * math.pi * (i + 0.5) / 12.0
+        s += ("primitive pillar%d static box %.4f 0 %.4f 0.18 2 0.18 albedo checker 0.2 %d 90 90 60 60 %d\n"
+              % (i, 4.0 * math.sin(a), 4.0 * math.cos(a), 120 + 10 * i, 110 + 10 * i))
+    for i in range(6):  # crates on the floor and spheres at eye height between the path and the walls
+        a = 2.0 * math.pi * i / 6.0
+        if i % 2:
+            s += ("primitive ball%d static sphere %.4f %.4f %.4f 0.45 albedo checker 0.25 240 200 60 60 90 200\n"
+                  % (i, 3.4 * math.sin(a), 0.2 + 0.1 * i, 3.4 * math.cos(a)))
+        else:
+            s += ("primitive crate%d static box %.4f 1.4 %.4f 0.5 0.6 0.4 albedo checker 0.3 90 210 120 40 60 40\n"
+                  % (i, 3.4 * math.sin(a), 3.4 * math.cos(a)))
+    for i in range(frames):
+        t = i / 30.0
+        th = math.pi * i / 500.0  # half a turn in 500 frames: ~1.6 cm and ~0.5 degree per frame
+        p = (2.5 * math.sin(th), 0.3 + 0.1 * math.sin(0.13 * i), 2.5 * math.cos(th))
+        yaw = th + 0.15 * math.sin(0.02 * i)
+        pitch = (8.0 + 3.0 * math.sin(0.3 * i)) * math.pi / 180.0  # looking a little down: floor in view
+        q = _quat_mul(_quat_axis_angle([0, 1, 0], yaw), _quat_axis_angle([1, 0, 0], pitch))
+        s += _camera_line(t, p, q)
+    return s
+
+
 def corner_scene():
     """proj/tests/test_registration.cpp:157-162."""
     return ("intrinsics 40 40 31.5 23.5 64 48 5000\n"
@@ -107,17 +141,25 @@ def pipeline_static_scene(frames=7):
 
 BENCH_CONFIGS = {
     # RoomScript(false) at 640x480 with the default K, its path extended to 50 frames
-    "C1": dict(dynamic=False, frames=50, seed=42),
+    "C1": dict(dynamic=False, frames=50, seed=42, voxel=0.01),
     # the acceptance room + 2 crossing boxes on a closed 200-frame orbit
-    "C2": dict(dynamic=True, frames=200, seed=43),
+    "C2": dict(dynamic=True, frames=200, seed=43, voxel=0.01),
+    # large scene at 0.5 cm with the 4M-entry hash (large_scene_script)
+    "C3": dict(dynamic=False, frames=500, seed=45, voxel=0.005, hash_capacity=1 << 22, max_blocks=4000000),
+    # 1280x720, K = (1050, 1050, 639.5, 359.5), 3 levels, mesh export at the end
+    "C4": dict(dynamic=True, frames=1000, seed=44, voxel=0.01, width=1280, height=720),
 }
 
 
 def config_script(name: str, seed: int | None = None) -> str:
-    """Scene script of BASELINE.json workload `name` (C1 or C2); `seed`
+    """Scene script of BASELINE.json workload `name` (C1..C4); `seed`
     overrides the noise seed (independent replicas)."""
     c = BENCH_CONFIGS[name]
     s = c["seed"] if seed is None else seed
     if name == "C1":
         return room_script(False, 640, 480, frames=c["frames"], seed=s)
+    if name == "C3":
+        return large_scene_script(frames=c["frames"], seed=s)
+    if name == "C4":
+        return bench_script(dynamic=True, width=c["width"], height=c["height"], frames=c["frames"], seed=s)
     return bench_script(dynamic=c["dynamic"], frames=c["frames"], seed=s)

@@ -115,3 +115,29 @@ def test_cpp_host_voxel_handles(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAIL" not in r.stdout and r.stdout.count("ok") >= 14
+
+
+def test_device_frames_checked_and_ordered():
+    """CUDA-tensor frames go to the library as raw pointers: wrong dtype,
+    layout or device is refused, and work torch queued for them is complete
+    before the library's own stream reads them (refusion_b200.h stream contract)."""
+    import torch
+
+    s_k = O.small_intrinsics(64, 48, 50.0)
+    k = G.intrinsics(s_k.fx, s_k.fy, s_k.cx, s_k.cy, s_k.width, s_k.height, s_k.depth_scale)
+    d = torch.full((48, 64), 0.5, dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        G.Frame(d.double(), None, k).c()
+    with pytest.raises(ValueError):
+        G.Frame(torch.full((64, 48), 0.5, device="cuda").t(), None, k).c()  # non-contiguous
+    with pytest.raises(ValueError):
+        G.Frame(d, torch.zeros((48, 64, 3), dtype=torch.float32, device="cuda"), k).c()
+    # produced on torch's stream right before the call: the volume sees the final values
+    ov, gv = plane_pair()
+    big = torch.empty((48, 64), dtype=torch.float32, device="cuda")
+    for _ in range(50):
+        big.fill_(0.1)
+    big.fill_(0.5)
+    g = gv.linearize(G.Frame(big, None, k), O.IDENTITY, G.registration_config(color_weight=0.0))
+    o = ov.linearize(np.full((48, 64), 0.5, np.float32), None, s_k, O.IDENTITY, O.reg_cfg(color_weight=0.0))
+    assert g["valid"] == o["valid"] and g["depth_error"] == pytest.approx(o["depth_error"], rel=1e-12, abs=1e-18)

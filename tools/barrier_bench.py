@@ -6,7 +6,7 @@ sys.path.insert(0, ".")
 from paper_1905_02082_b200 import _lib as L  # noqa: E402
 
 lib = L.load()
-for reduce in (0, 1):
+for reduce in (0, 1, 2, 3, 4):  # barrier, 30-value all-reduce, CTA-local part, 1-value all-reduce, bare exchange
     us = C.c_double()
     L.check(lib.rf_diag_grid_barrier(0, 2000, reduce, C.byref(us)))
     print(f"{L.LIB_PATH.split('/')[-1]} reduce={reduce}: {us.value:.3f} us per call")

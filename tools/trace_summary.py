@@ -10,6 +10,7 @@ import numpy as np
 def main(path, skip=3):
     raw = np.fromfile(path, dtype=np.uint64).reshape(-1, 256, 8)[skip:]
     per = defaultdict(list)
+    verdicts = defaultdict(lambda: [0, 0, 0])
     frame_tot = []
     mask = raw[:, 255, :7].astype(np.float64)
     mask = mask[mask[:, 0] > 0]
@@ -42,6 +43,9 @@ def main(path, skip=3):
             start, lead_done, slow_done, red_done, level, px, jac, _ = (int(x) for x in p[:8])
             nxt = int(passes[i + 1, 0]) if i + 1 < len(passes) else red_done
             solved = int(passes[i + 1, 7]) if i + 1 < len(passes) and int(passes[i + 1, 7]) > red_done else 0
+            verdict = jac >> 8  # 1 accepted, 2 rejected, 0 not a trial (first pass of a level)
+            jac &= 0xFF
+            verdicts[(level, px, jac)][verdict] += 1
             key = (level, px, jac)
             per[key].append((slow_done - start, red_done - slow_done, max(0, nxt - red_done), lead_done - start,
                              (solved - red_done) if solved else np.nan, (nxt - solved) if solved else np.nan))
@@ -52,7 +56,8 @@ def main(path, skip=3):
         a = np.array(per[key]) / 1e3
         print(f"{key[0]:5d} {key[1]:7d} {key[2]:3d} {len(a) / len(frame_tot):10.1f} "
               f"{a[:, 0].mean():14.2f} {a[:, 1].mean():14.2f} {a[:, 2].mean():6.2f} {a[:, 3].mean():10.2f}  "
-              f"[{np.nanmean(a[:, 4]):.2f} + {np.nanmean(a[:, 5]):.2f}]")
+              f"[{np.nanmean(a[:, 4]):.2f} + {np.nanmean(a[:, 5]):.2f}]  "
+              f"trials accepted/rejected per frame {verdicts[key][1] / len(frame_tot):.1f}/{verdicts[key][2] / len(frame_tot):.1f}")
 
 
 if __name__ == "__main__":
