@@ -300,6 +300,11 @@ rf_status rf_diag_grid_barrier(int device, int32_t iters, int32_t reduce, double
 rf_status rf_diag_pass_bench(rf_volume* v, const rf_frame* f, const double pose[12], int32_t level, int32_t iters,
                              double color_weight, double* us_per_pass, double* acc);  /* acc: 30 doubles or NULL */
 rf_status rf_diag_lm_step(int device, int32_t iters, double cycles[3]);
+/* Structural invariants of a volume, as error counts (all zero when consistent):
+ * [0] occupied slots with a value that is neither a brick nor pending, [1] bricks
+ * whose slot does not hold their key and index, [2] duplicated keys, [3] link
+ * records that disagree with a hash probe, [4] pending (claimed, unnumbered) keys. */
+rf_status rf_diag_volume_check(const rf_volume* v, uint64_t errors[5]);
 
 rf_status rf_synth_render(const void* prims, int32_t nprims, const double cam_pose[12], const rf_intrinsics* k,
                           double noise_sigma_scale, double dropout, uint64_t seed, uint64_t frame_index,

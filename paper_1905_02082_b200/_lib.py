@@ -92,7 +92,7 @@ EXPORTS = [
     "rf_mesh_write_ply", "rf_mesh_destroy", "rf_render_virtual_depth", "rf_pipeline_window_size",
     "rf_pipeline_set_debug_images", "rf_pipeline_last_refinement", "rf_pipeline_finalize_one", "rf_diag_pass_bench", "rf_pipeline_process_frames",
     "rf_ate_rmse", "rf_rpe_over_time", "rf_nearest_distances", "rf_distance_cdf", "rf_build_pyramid",
-    "rf_volume_find_block", "rf_volume_write_block",
+    "rf_volume_find_block", "rf_volume_write_block", "rf_diag_volume_check",
 ]
 
 _lib = None

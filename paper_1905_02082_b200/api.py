@@ -257,6 +257,12 @@ class TsdfVolume:
         L.check(_lib().rf_volume_write_block(self.h, _p(c), _p(v), C.byref(found)))
         return bool(found.value)
 
+    def check(self):
+        """rf_diag_volume_check: {name: count} of structural invariant violations (all 0 expected)."""
+        e = (C.c_uint64 * 5)()
+        L.check(_lib().rf_diag_volume_check(self.h, e))
+        return dict(zip(("bad_value", "bad_brick_slot", "duplicate_key", "bad_link", "pending_key"), e))
+
     def hash_occupancy(self) -> np.ndarray:
         bm = np.zeros(self.hash_capacity(), dtype=np.uint8)
         L.check(_lib().rf_volume_hash_occupancy(self.h, _p(bm)))

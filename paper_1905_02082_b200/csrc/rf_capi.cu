@@ -348,6 +348,7 @@ struct rf_volume {
     uint64_t cap = 0;
     DevBuf slots, coords, voxels, links, counters;
     DevBuf ord, newlist;  // allocation order (model volumes only, VolumeView::ord)
+    DevBuf mesh_scratch;  // ExtractMesh's per-cell state, kept between calls
     DevBuf win_first;  // refinement temp volume: first window entry per hash slot
     VolumeView view{};
     Workspace ws;
@@ -711,6 +712,7 @@ void rf_volume_destroy(rf_volume* v) {
     v->counters.release();
     v->ord.release();
     v->newlist.release();
+    v->mesh_scratch.release();
     v->win_first.release();
     delete v;
 }
@@ -1388,12 +1390,11 @@ rf_status rf_volume_extract_mesh(const rf_volume* cv, int32_t min_weight, rf_mes
         m->device = v->device;
         const uint32_t n = uint32_t(v->num_blocks());
         if (n) {
-            DevBuf scratch;
             const size_t bytes = mesh_scratch_bytes(n);
-            scratch.ensure(bytes);
+            v->mesh_scratch.ensure(bytes);
             uint32_t* totals = v->ws.h_counters;  // pinned, idle between calls
             MeshArgs a{};
-            CK(mesh_prepare(v->view, n, min_weight, v->ws.stream, scratch.p, bytes, totals, &a));
+            CK(mesh_prepare(v->view, n, min_weight, v->ws.stream, v->mesh_scratch.p, v->mesh_scratch.n, totals, &a));
             v->ws.sync();
             m->nv = totals[0];
             m->nf = totals[1];
@@ -2261,6 +2262,23 @@ extern "C" rf_status rf_diag_pass_bench(rf_volume* v, const rf_frame* f, const d
         const TrackOut o = v->fetch_out();
         *us_per_pass = o.final_error;
         if (acc) std::memcpy(acc, o.acc, sizeof(o.acc));
+    });
+}
+
+// Structural invariants of a volume (k_volume_check): five error counts, all
+// zero for a consistent table, pool and link-record set.
+extern "C" rf_status rf_diag_volume_check(const rf_volume* cv, uint64_t errors[5]) {
+    return guard([&] {
+        rf_volume* v = const_cast<rf_volume*>(cv);
+        require(v && errors, RF_INVALID_ARGUMENT, "null argument");
+        CK(cudaSetDevice(v->device));
+        DevBuf e;
+        e.ensure(5 * sizeof(unsigned long long));
+        CK(cudaMemsetAsync(e.p, 0, 5 * sizeof(unsigned long long), v->ws.stream));
+        k_volume_check<<<4 * 148, 256, 0, v->ws.stream>>>(v->view, e.as<unsigned long long>());
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(errors, e.p, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, v->ws.stream));
+        v->ws.sync();
     });
 }
 

@@ -7,7 +7,25 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Bounds / invariant checks of the checked build (tools/checked_build.sh:
+// build --variant checked -DRF_CHECKED, run the GPU suite with RF_LIB_PATH).
+// The GPU pool has no compute-sanitizer, so the hot kernels assert their own
+// index ranges; a violation prints and traps (the test run fails loudly).
+#ifdef RF_CHECKED
+#define RF_ASSERT(c)                                                                       \
+    do {                                                                                   \
+        if (!(c)) {                                                                        \
+            printf("RF_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+                   int(blockIdx.x), int(threadIdx.x));                                     \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define RF_ASSERT(c) ((void)0)
+#endif
 
 namespace rfb {
 
@@ -254,7 +272,9 @@ __device__ __forceinline__ void hash_insert_ordered(const VolumeView& V, int x, 
         if (k == kEmptyKey) {
             k = atomicCAS(&V.slots[idx].key, kEmptyKey, key);
             if (k == kEmptyKey) {
-                V.newlist[atomicAdd(&V.counters[kNewBlocks], 1u)] = idx;  // <= one entry per slot
+                const uint32_t at = atomicAdd(&V.counters[kNewBlocks], 1u);
+                RF_ASSERT(at <= V.hash_mask);
+                V.newlist[at] = idx;  // <= one entry per slot
                 atomicMin(&V.ord[idx], ordinal);
                 return;
             }
@@ -307,7 +327,9 @@ __device__ __forceinline__ void assign_new(const VolumeView& V, OnNew on_new, in
         unsigned long long mine = 0;
         if (i < n) {
             slot = __ldcg(V.newlist + i);
+            RF_ASSERT(slot <= V.hash_mask);
             mine = __ldcg(V.ord + slot);
+            RF_ASSERT(mine != ~0ull);  // every claimed key has a first visit
         }
         uint32_t rank = 0;
         for (uint32_t t0 = 0; t0 < n; t0 += kTile) {
@@ -318,8 +340,10 @@ __device__ __forceinline__ void assign_new(const VolumeView& V, OnNew on_new, in
             for (uint32_t j = 0; j < m; ++j) rank += s_ord[j] < mine;
         }
         if (i < n) {
+            RF_ASSERT(rank < n);
             if (rank < budget) {
                 const uint32_t b = before + rank;
+                RF_ASSERT(b < V.max_blocks);
                 const int4 c = unpack_key(__ldcg(&V.slots[slot].key), slot);
                 V.coords[b] = c;
                 V.slots[slot].value = b;  // (ord[slot] stays: other CTAs may still be ranking against it;
@@ -334,6 +358,7 @@ __device__ __forceinline__ void assign_new(const VolumeView& V, OnNew on_new, in
 }
 
 __device__ __forceinline__ const Voxel* brick_ptr(const VolumeView& V, uint32_t b) {
+    RF_ASSERT(b < V.max_blocks);
     return V.voxels + size_t(b) * kBrickVoxels;
 }
 
@@ -417,7 +442,9 @@ __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int 
 // One word of link_brick: dir 0 fills own[q] (q = 0: the brick itself),
 // dir 1 points the "-q" neighbour's record at b.
 __device__ __forceinline__ void link_brick_item(const VolumeView& V, uint32_t b, int q, int dir) {
+    RF_ASSERT(b < V.max_blocks);
     const int4 c = V.coords[b];
+    RF_ASSERT(uint32_t(c.w) <= V.hash_mask);
     if (dir == 0) {
         V.links[size_t(uint32_t(c.w)) * kLinkStride + q] =
             q == 0 ? b : hash_find(V, c.x + (q & 1), c.y + ((q >> 1) & 1), c.z + (q >> 2));

@@ -237,6 +237,8 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
     const bool pxc_hit = kJac && s_pxc_tag == pxc_tag;
     auto pixel = [&](const int u, const int v, const int it) {
         const int p = v * K.w + u;
+        RF_ASSERT(u >= 0 && u < K.w && v >= 0 && v < K.h);
+        RF_ASSERT(it >= a.pxc_steps || (it + 1) * kTrackThreads * 8 <= a.dyn_bytes);
         // Every per-pixel input is loaded up front (depth, mask, intensity),
         // so only the hash slot and voxel gathers are dependent round trips.
         float d;
@@ -756,8 +758,10 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint32_t* planes,
             nq = int(__ldcg(ff_count(wl, nft, rounds)));
             list = ff_list(wl, nft, rounds);
         }
+        RF_ASSERT(nq <= nft);
         for (int qi = warp * G + blockIdx.x; qi < nq; qi += G * nwarps) {  // one tile per warp
             const int t = flags ? int(s_list[qi]) : __ldcg(list + qi);
+            RF_ASSERT(t >= 0 && t < nft);
             const int tx = t % ntx, ty = t / ntx, x0 = tx * kFfW, y0 = ty * kFfH;
             const int gy = y0 + lane;
             // row words: mask, validity, growth planes (x = bit)

@@ -210,6 +210,7 @@ __device__ __forceinline__ void append_visible(const CullArgs& a, uint32_t b, ui
         uint32_t base = 0;
         if (lane == 0) base = atomicAdd(&a.V.counters[kVisible], uint32_t(__popc(vote)));
         base = __shfl_sync(0xffffffffu, base, 0);
+        RF_ASSERT(!flags || base + __popc(vote & ((1u << lane) - 1u)) < a.V.max_blocks);
         if (flags) a.list[base + __popc(vote & ((1u << lane) - 1u))] = b | flags;
     }
 }
@@ -239,7 +240,11 @@ __global__ void k_cull(CullArgs a) {
         assign_new(a.V, [&](uint32_t b, int4 c) {
             uint32_t flags = 0;
             cull_brick(a, W, ext, c, false, integrate, flags);  // new bricks: integrate only
-            if (flags) a.list[atomicAdd(&a.V.counters[kVisible], 1u)] = b | flags;
+            if (flags) {
+                const uint32_t at = atomicAdd(&a.V.counters[kVisible], 1u);
+                RF_ASSERT(at < a.V.max_blocks);
+                a.list[at] = b | flags;
+            }
         });
     const uint32_t stride = gridDim.x * blockDim.x;
     // warp-uniform trip count so the whole warp can aggregate its appends
@@ -365,9 +370,11 @@ __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
         c_nx = a.V.coords[e_nx & kIndexMask];
         v_nx = *reinterpret_cast<const uint2*>(a.V.voxels + size_t(e_nx & kIndexMask) * kBrickVoxels + threadIdx.x);
     }
+    RF_ASSERT(nvis <= a.V.max_blocks);
     for (; i < nvis; i += G) {
         const uint32_t e = e_nx;
         const uint32_t b = e & kIndexMask;
+        RF_ASSERT(b < min(a.V.counters[kNumBlocks], a.V.max_blocks));
         const int4 c = c_nx;
         uint2 raw = v_nx;
         e_nx = e_nx2;
@@ -487,6 +494,47 @@ __global__ void k_voxel_rw(VolumeView V, const int* vc, int n, Voxel* io, uint8_
     Voxel* v = V.voxels + size_t(b) * kBrickVoxels + (((z & 7) * 8 + (y & 7)) * 8 + (x & 7));
     if (write) *v = io[i];
     else io[i] = *v;
+}
+
+// Structural invariants of a volume (the race detector for the lock-free
+// inserts, the ranked assignment and the concurrent link writers; the GPU
+// pool has no compute-sanitizer). err[] counts:
+//  [0] occupied slots holding a value that is neither a brick < num_blocks nor pending
+//  [1] bricks whose recorded slot does not hold their key and index
+//  [2] keys stored twice (a probe from the key's home slot finds another slot first)
+//  [3] link records that disagree with a fresh hash probe of the neighbour
+//  [4] pending keys (claimed, no brick) outside an allocation in progress
+__global__ void k_volume_check(VolumeView V, unsigned long long* err) {
+    const uint32_t nb = min(V.counters[kNumBlocks], V.max_blocks);
+    const uint32_t linked = min(V.counters[kLinked], nb);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    unsigned long long e[5] = {0, 0, 0, 0, 0};
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= V.hash_mask; i += stride) {
+        const HashSlot sl = V.slots[i];
+        if (sl.key == kEmptyKey) continue;
+        if (sl.value == kInvalid) {
+            ++e[4];
+            continue;
+        }
+        if (sl.value >= nb) ++e[0];
+        const int4 c = unpack_key(sl.key, i);
+        if (hash_find_slot(V, c.x, c.y, c.z) != i) ++e[2];
+    }
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride) {
+        const int4 c = V.coords[b];
+        const uint32_t slot = uint32_t(c.w);
+        if (slot > V.hash_mask || V.slots[slot].key != pack_key(c.x, c.y, c.z) || V.slots[slot].value != b) {
+            ++e[1];
+            continue;
+        }
+        if (b >= linked) continue;
+        const uint32_t* rec = V.links + size_t(slot) * kLinkStride;
+        if (rec[0] != b) ++e[3];
+        for (int q = 1; q < 8; ++q)
+            if (rec[q] != hash_find(V, c.x + (q & 1), c.y + ((q >> 1) & 1), c.z + (q >> 2))) ++e[3];
+    }
+    for (int k = 0; k < 5; ++k)
+        if (e[k]) atomicAdd(err + k, e[k]);
 }
 
 // Occupied-slot bitmap (for bit-exact hash-occupancy parity).

@@ -113,6 +113,7 @@ __global__ void k_sample(VolumeView V, const double* pts, int n, int mode, doubl
                          uint8_t* valid);
 __global__ void k_voxel_rw(VolumeView V, const int* vc, int n, Voxel* io, uint8_t* found, int write);
 __global__ void k_occupancy(VolumeView V, uint8_t* bitmap);
+__global__ void k_volume_check(VolumeView V, unsigned long long* err);
 __global__ void k_vol_clear(VolumeView V, bool voxels);  // voxels=false: hash only
 __global__ void k_win_first_reset(VolumeView V);
 __global__ void k_alloc_window(WindowArgs a);

@@ -72,6 +72,7 @@ def test_whole_sequence_free_running(name, n):
     assert worst <= 1e-4, worst
     assert mism == {k: 0 for k in COUNTS}, mism
     assert gp.tracking_losses() == op.losses() == 0
+    assert all(v == 0 for v in gp.volume().check().values())
     assert len(gp.trajectory()[0]) == n
 
 
@@ -84,6 +85,7 @@ def test_c3_large_scene_half_centimetre_4m_hash():
     oc, _ = ov.export(False)
     gc, _ = gv.export(False)
     assert (oc == gc).all()  # pool (allocation) order too
+    assert all(v == 0 for v in gv.check().values()) and all(v == 0 for v in gp.volume().check().values())
     assert worst <= 1e-4, worst
     assert mism == {k: 0 for k in COUNTS}, mism
 

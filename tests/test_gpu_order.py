@@ -26,6 +26,14 @@ from tests.test_gpu_parity import frame, gcfg, pair, pose_error, wavy_frame
 pytestmark = pytest.mark.gpu
 
 
+def assert_consistent(gv):
+    """rf_diag_volume_check: table, pool and link records agree (the lock-free
+    inserts, the ranked assignment and the concurrent link writers left no
+    inconsistency)."""
+    errs = gv.check()
+    assert all(v == 0 for v in errs.values()), errs
+
+
 def assert_same_pool(ov, gv, occupancy=True):
     oc, ovox = ov.export()
     gc, gvox = gv.export()
@@ -34,6 +42,7 @@ def assert_same_pool(ov, gv, occupancy=True):
     assert ovox.tobytes() == gvox.tobytes(), "voxels differ"
     if occupancy:
         assert (ov.hash_occupancy(gv.hash_capacity()) == gv.hash_occupancy()).all()
+    assert_consistent(gv)
 
 
 def lockstep(n=8, mover=True, vc=None):
@@ -184,6 +193,7 @@ def test_pipeline_overflow_stops_at_the_frame(batched):
     gc, _ = gp.volume().export(False)
     assert (np.sort(oc.view("i4,i4,i4"), axis=0) == np.sort(gc.view("i4,i4,i4"), axis=0)).all()
     assert (ov.hash_occupancy(gp.volume().hash_capacity()) == gp.volume().hash_occupancy()).all()
+    assert_consistent(gp.volume())
     # the pipeline keeps working after the exception (the next frame throws again: no room)
     with pytest.raises(G.ResourceLimitError):
         gp.process_frame(gfr[j + 1])
@@ -210,6 +220,7 @@ def test_pipeline_rerun_snapshot_bytes(tmp_path):
         gp.volume().save(p)
         paths.append(p)
     assert np.array_equal(trajs[0], trajs[1])
+    assert_consistent(gp.volume())
     assert open(paths[0], "rb").read() == open(paths[1], "rb").read()
     # the refine-off batched run differs in content, but is itself rerun-stable
     gp = G.Pipeline(G.pipeline_config(refine=False, volume=cfg.volume))
