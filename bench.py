@@ -18,9 +18,13 @@ Arms:
                      pipeline's stream, max over ranks); `e2e` = the same through
                      rf_pipeline_process_frame with pinned HOST buffers (H2D of
                      depth+RGB and the D2H of stats+pose inside the timed loop).
-  --impl reference : the reference algorithm on the host CPU (the oracle
-                     restatement, all host threads; the C++ reference itself
-                     cannot be built here — DESIGN.md §Oracle).
+  --impl reference : the reference itself on the host CPU: /root/reference's
+                     unmodified C++ sources built into oracle/_ref against the
+                     Eigen / doctest / libpng stand-ins of oracle/ref_shim
+                     (`make -C oracle ref`; the library travels to the GPU box),
+                     all host threads. Falls back to the oracle restatement
+                     (bit-identical to it, tests/test_reference_build.py) when
+                     oracle/_ref was not built.
 The default line carries a `parity` block: the GPU arm's per-frame poses and
 counts (registrations, LM iterations, masked pixels) against the cpu_baseline
 leg's over the frames both processed (same bytes, same order).
@@ -458,14 +462,25 @@ def run_ours(args):
     replicas.finish(R)
 
 
+def cpu_impl():
+    """(module, kind): the reference build when present, else the oracle port."""
+    from oracle import oracle as O
+    from oracle import reference as Rf
+
+    if Rf.available():
+        return Rf, "reference"
+    return O, "port"
+
+
 def oracle_rate(frame, k, budget_s, threads, vol):
     """Oracle pipeline over a frame sample: bootstrap on frame 0 (untimed, as
     the reference's fps excludes frame 0), then time frames until budget_s.
     Returns the rate and every step's (stats, pose) for the parity block."""
     from oracle import oracle as O
 
-    p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads),
-                              volume=O.vol_cfg(voxel_size=vol[0], max_blocks=vol[1])))
+    impl, _ = cpu_impl()
+    p = impl.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads),
+                                 volume=O.vol_cfg(voxel_size=vol[0], max_blocks=vol[1])))
     d, c = frame(0)
     st, pose = p.process_frame(d, c, k, 0.0)
     steps = [(st, pose)]
@@ -484,9 +499,12 @@ def oracle_rate(frame, k, budget_s, threads, vol):
 def cpu_baseline(frame, k, budget_s, name):
     threads = os.cpu_count() or 1
     rate, n, spent, steps = oracle_rate(frame, k, budget_s, threads, volume_params(name))
-    return ({"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": "port",
-             "sample": f"oracle ProcessFrame on steps 1..{n} of the same {name} sequence and the same frame bytes "
-                       f"as the GPU arm ({spent:.1f} s, {threads} threads for integrate/carve and registration)"},
+    _, kind = cpu_impl()
+    what = "the reference's Pipeline::ProcessFrame (oracle/_ref build)" if kind == "reference" else \
+        "the oracle restatement of ProcessFrame"
+    return ({"value": round(rate, 4), "unit": UNIT, "cores": threads, "kind": kind,
+             "sample": f"{what} on steps 1..{n} of the same {name} sequence and the same frame bytes as the GPU arm "
+                       f"({spent:.1f} s, {threads} threads for integrate/carve and registration)"},
             steps)
 
 
@@ -514,8 +532,9 @@ def run_reference(args):
 
     threads = os.cpu_count() or 1
     vox, mb, _ = volume_params(name)
-    p = O.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads),
-                              volume=O.vol_cfg(voxel_size=vox, max_blocks=mb)))
+    impl, kind = cpu_impl()
+    p = impl.Pipeline(O.pipe_cfg(refine=False, threads=threads, reg=O.reg_cfg(threads=threads),
+                                 volume=O.vol_cfg(voxel_size=vox, max_blocks=mb)))
     for i in range(args.warmup):
         f = frame(i)
         p.process_frame(f["depth"], f["rgb"], k, i / 30.0)
@@ -531,8 +550,9 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
         "data": DATA.format(cfg=name, seed=seed),
         "config": workload_config(name, W, H, F),
-        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"oracle ProcessFrame, steps {args.warmup}..{args.warmup + args.steps - 1} of the "
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{'reference (oracle/_ref build)' if kind == 'reference' else 'oracle'} "
+                                   f"ProcessFrame, steps {args.warmup}..{args.warmup + args.steps - 1} of the "
                                    f"{name} sequence, {threads} threads"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
