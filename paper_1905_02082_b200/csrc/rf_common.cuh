@@ -537,8 +537,12 @@ __device__ __forceinline__ void interp_cell(const VolumeView& V, const uint2 (&c
 
 // Exact integer Rec.709 luma times 1e4 (2126 r + 7152 g + 722 b < 2^22) as a
 // double, without a conversion instruction: OR into the mantissa of 2^52.
+// The weights split into bytes (2126 = 8 * 256 + 78, 7152 = 27 * 256 + 240,
+// 722 = 2 * 256 + 210) make the sum two byte dot products: L = 256 dp4a(v, hi)
+// + dp4a(v, lo) over the bytes {weight, r, g, b} (weight's multiplier 0).
 __device__ __forceinline__ double voxel_luma_e4(uint2 v) {
-    const unsigned int L = 2126u * ((v.y >> 8) & 0xFFu) + 7152u * ((v.y >> 16) & 0xFFu) + 722u * (v.y >> 24);
+    constexpr unsigned kHi = (2u << 24) | (27u << 16) | (8u << 8), kLo = (210u << 24) | (240u << 16) | (78u << 8);
+    const unsigned int L = (__dp4a(v.y, kHi, 0u) << 8) + __dp4a(v.y, kLo, 0u);
     return __longlong_as_double(0x4330000000000000ll | (long long)L) - 4503599627370496.0;
 }
 

@@ -18,6 +18,10 @@ namespace {
 constexpr double kIntensityScale = 1.0 / 255.0;  // registration.cpp:22
 constexpr double kRelDecreaseTol = 1e-6;         // registration.cpp:26
 
+// The thread that judges each trial and solves the next LM step: the CTA's
+// last thread, which also pre-solves the reject path during the pass (its
+// SMSP's instruction cache then holds the solve).
+constexpr int kLmThread = kTrackThreads - 1;
 __device__ __forceinline__ int hidx(int i, int j) { return i * 6 - (i * (i - 1)) / 2 + (j - i); }
 
 __shared__ int s_trace_pass;  // per-CTA pass counter for the optional timeline
@@ -330,10 +334,18 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
     // (B200, frames 5..104: 1519 -> 1581 frames/s).
     {
         const int per = (npx + int(gridDim.x) - 1) / int(gridDim.x);
+        const int end = min(npx, (int(blockIdx.x) + 1) * per);
+        int p = int(blockIdx.x) * per + int(threadIdx.x);
+        int v = p / K.w, u = p - v * K.w;  // then stepped: no division per pixel
         int it = 0;
         for (int q = int(threadIdx.x); q < per; ++it, q += kTrackThreads) {
-            const int p = int(blockIdx.x) * per + q;
-            if (p < npx) pixel(p % K.w, p / K.w, it);
+            if (p < end) pixel(u, v, it);
+            p += kTrackThreads;
+            u += kTrackThreads;
+            while (u >= K.w) {
+                u -= K.w;
+                ++v;
+            }
         }
         if (threadIdx.x == kTrackThreads - 1 && it < (per + kTrackThreads - 1) / kTrackThreads) pre();
     }
@@ -393,18 +405,18 @@ __device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask
             return;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == kLmThread) {  // the LM thread's own state: no barrier needed before it reads it
             st.lambda = R.lambda_init;
             st.converged = 0;
             st.brk = 0;
             st.level_it = 0;
         }
-        // One barrier per LM iteration: thread 0 judges the last trial and
+        // One barrier per LM iteration: kLmThread judges the last trial and
         // solves for the next candidate in one straight-line section on
         // local copies of its state (registration.cpp:233-272).
         bool judge = false;  // a trial was evaluated since the last solve
         for (;;) {
-            if (threadIdx.x == 0) {
+            if (threadIdx.x == kLmThread) {
                 double lambda = st.lambda;
                 int brk = st.brk, level_it = st.level_it, total = st.total, converged = st.converged, ci = st.ci;
                 const double* tr = st.buf[ci ^ 1];
