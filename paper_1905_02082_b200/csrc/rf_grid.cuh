@@ -157,16 +157,28 @@ __device__ __forceinline__ double line_value(const uint4& v) {
 // acquire. `hook` runs on thread 0 right after its CTA's partial is stored.
 // Double buffering by the reduce index is safe: a CTA writes reduce i + 2 only
 // after every CTA's partial of i + 1, i.e. after every CTA finished folding i.
+// `warp_active` false: the warp's values are all zero (no pixels); it skips
+// the transpose and contributes zeros (the same sums bit for bit: x + 0.0 = x).
 template <int NV, bool kPublish = true, class Hook = NoHook>
 __device__ __forceinline__ void block_grid_allreduce(const GridCtx& g, const double (&in)[NV], double* scratch,
-                                                     double* out, const Hook& hook = Hook()) {
+                                                     double* out, const Hook& hook = Hook(),
+                                                     bool warp_active = true) {
     static_assert(NV <= 32, "one warp holds the CTA vector");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int G = gridDim.x;
-    double v[32];
+    if (NV == 1) {  // one value: a plain butterfly (fixed tree, deterministic)
+        double t = in[0];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = i < NV ? in[i] : 0.0;
-    scratch[warp * 32 + lane] = warp_transpose_reduce(v);
+        for (int o = 16; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        scratch[warp * 32 + lane] = lane == 0 ? t : 0.0;
+    } else if (warp_active) {
+        double v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = i < NV ? in[i] : 0.0;
+        scratch[warp * 32 + lane] = warp_transpose_reduce(v);
+    } else {
+        scratch[warp * 32 + lane] = 0.0;
+    }
     const unsigned int bar = s_ll_bar;  // read before lane 0 of warp 0 advances it (after the barrier below)
     const uint32_t flag = (g.seq << 12) | (bar & 0xFFFu);
     uint4* buf = g.ll + size_t(bar & 1u) * G * 32;

@@ -358,8 +358,10 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
         }
     }
     // Jacobian passes write nothing global; a value pass's residual image is
-    // read across CTAs by the mask that follows (publish).
-    block_grid_allreduce<kAccN, !kJac>(a.grid, acc, scratch, out, hook);
+    // read across CTAs by the mask that follows (publish). Warps without
+    // pixels (most of them at the coarsest level) skip their transpose.
+    const bool warp_has_pixels = (int(threadIdx.x) & ~31) < (npx + int(gridDim.x) - 1) / int(gridDim.x);
+    block_grid_allreduce<kAccN, !kJac>(a.grid, acc, scratch, out, hook, warp_has_pixels);
     if (kJac && threadIdx.x == 0) s_pxc_tag = pxc_tag;  // (every thread read it before the barriers above)
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = global_ns();
     if (a.trace && threadIdx.x == 0) ++s_trace_pass;
