@@ -17,6 +17,8 @@
 namespace rfb {
 
 constexpr int kRedStride = 32;  // doubles per CTA partial slot
+constexpr int kGridThreads = 384;  // CTA size of the cooperative kernels that use these primitives
+constexpr int kGridWarps = kGridThreads / 32;
 
 struct GridCtx {
     GridSync* sync;      // counters live here (zero-initialised once)
@@ -61,6 +63,25 @@ __device__ __forceinline__ double warp_transpose_reduce(double (&v)[32]) {
         }
     }
     return v[0];
+}
+
+// Fixed-shape pairwise sums (deterministic, log-depth dependency chains
+// instead of one add per term): N values in registers, and the first n <= N
+// values at stride `stride` (missing terms are 0.0).
+template <int N>
+__device__ __forceinline__ double tree_sum_regs(double (&v)[N]) {
+#pragma unroll
+    for (int h = 1; h < N; h *= 2)
+#pragma unroll
+        for (int i = 0; i + h < N; i += 2 * h) v[i] += v[i + h];
+    return v[0];
+}
+template <int N>
+__device__ __forceinline__ double tree_sum(const double* p, int stride, int n) {
+    double v[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = i < n ? p[i * stride] : 0.0;
+    return tree_sum_regs(v);
 }
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -164,7 +185,7 @@ __device__ __forceinline__ void block_grid_allreduce(const GridCtx& g, const dou
                                                      double* out, const Hook& hook = Hook(),
                                                      bool warp_active = true) {
     static_assert(NV <= 32, "one warp holds the CTA vector");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kGridWarps;
     const int G = gridDim.x;
     if (NV == 1) {  // one value: a plain butterfly (fixed tree, deterministic)
         double t = in[0];
@@ -185,8 +206,7 @@ __device__ __forceinline__ void block_grid_allreduce(const GridCtx& g, const dou
     __syncthreads();
     if (warp == 0) {
         double sum = 0.0;
-        if (lane < NV)
-            for (int w = 0; w < nw; ++w) sum += scratch[w * 32 + lane];
+        if (lane < NV) sum = tree_sum<kGridWarps>(scratch + lane, 32, nw);
         if (kPublish) __threadfence();  // release: the CTA's writes (ordered by the barrier above) first
         if (lane < NV) st_line(buf + blockIdx.x * 32 + lane, sum, flag);
         if (lane == 0) {
@@ -217,8 +237,10 @@ __device__ __forceinline__ void block_grid_allreduce(const GridCtx& g, const dou
             if (!missing) break;
             if (++spins > (1ull << 26)) __trap();  // a co-residency bug fails loudly, never hangs
         }
+        double v[kRows];
 #pragma unroll
-        for (int k = 0; k < kRows; ++k) s += line_value(r[k]);  // rows past G hold +0.0
+        for (int k = 0; k < kRows; ++k) v[k] = line_value(r[k]);  // rows past G hold +0.0
+        s = tree_sum_regs(v);
         for (int i = c + kRows * nw; i < G; i += nw) {
             uint4 t = ld_line(buf + i * 32 + j);
             for (unsigned long long sp = 0; !line_ready(t, flag); t = ld_line(buf + i * 32 + j))
@@ -229,11 +251,7 @@ __device__ __forceinline__ void block_grid_allreduce(const GridCtx& g, const dou
     }
     s_fold[c][j] = s;
     __syncthreads();
-    if (threadIdx.x < NV) {
-        double t = 0.0;
-        for (int cc = 0; cc < nw; ++cc) t += s_fold[cc][threadIdx.x];
-        out[threadIdx.x] = t;
-    }
+    if (threadIdx.x < NV) out[threadIdx.x] = tree_sum<kGridWarps>(&s_fold[0][threadIdx.x], 32, nw);
     __syncthreads();
 }
 

@@ -35,6 +35,13 @@ __shared__ int s_pxc_tag;  // (level + 1) | 16 * use_mask of the cached inputs, 
 __shared__ int s_passes;   // Accumulate passes run (CTA 0; TrackOut.passes / pixel_passes)
 __shared__ double s_pixel_passes;
 __shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (see voxel_luma_lut)
+// This CTA's pixel range per pyramid level (set at kernel start): ceil(npx /
+// G) consecutive pixels from (ubase, vbase), so a pass starts without an
+// integer division on every thread's path to its first pixel.
+struct LevelRange {
+    int per, end, ubase, vbase;
+};
+__shared__ LevelRange s_lvl[kMaxLevels];
 
 struct RegState {
     Pose pose, cand;
@@ -327,16 +334,19 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
             F.res_valid[p] = rv;
         }
     };
-    const int npx = K.w * K.h;
     // The level's pixels spread evenly: ceil(npx / G) consecutive pixels per
     // CTA (a strip of rows), 384 per step (640x480: 2076 / 519 / 130 per CTA
     // at levels 0 / 1 / 2), instead of whole 16x24 tiles on part of the CTAs
     // (B200, frames 5..104: 1519 -> 1581 frames/s).
     {
-        const int per = (npx + int(gridDim.x) - 1) / int(gridDim.x);
-        const int end = min(npx, (int(blockIdx.x) + 1) * per);
+        const LevelRange R = s_lvl[level];
+        const int per = R.per, end = R.end;
         int p = int(blockIdx.x) * per + int(threadIdx.x);
-        int v = p / K.w, u = p - v * K.w;  // then stepped: no division per pixel
+        int u = R.ubase + int(threadIdx.x), v = R.vbase;  // then stepped: no division per pixel
+        while (u >= K.w) {
+            u -= K.w;
+            ++v;
+        }
         int it = 0;
         for (int q = int(threadIdx.x); q < per; ++it, q += kTrackThreads) {
             if (p < end) pixel(u, v, it);
@@ -360,7 +370,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
     // Jacobian passes write nothing global; a value pass's residual image is
     // read across CTAs by the mask that follows (publish). Warps without
     // pixels (most of them at the coarsest level) skip their transpose.
-    const bool warp_has_pixels = (int(threadIdx.x) & ~31) < (npx + int(gridDim.x) - 1) / int(gridDim.x);
+    const bool warp_has_pixels = (int(threadIdx.x) & ~31) < s_lvl[level].per;
     block_grid_allreduce<kAccN, !kJac>(a.grid, acc, scratch, out, hook, warp_has_pixels);
     if (kJac && threadIdx.x == 0) s_pxc_tag = pxc_tag;  // (every thread read it before the barriers above)
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = global_ns();
@@ -1102,6 +1112,14 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
     if (threadIdx.x == 0) {
         s_trace_pass = 0;
         s_pxc_tag = 0;
+    }
+    if (threadIdx.x < kMaxLevels) {
+        const int l = threadIdx.x, npx = a.F.K[l].w * a.F.K[l].h, per = (npx + int(gridDim.x) - 1) / int(gridDim.x);
+        const int start = min(npx, int(blockIdx.x) * per);
+        s_lvl[l].per = per;
+        s_lvl[l].end = min(npx, start + per);
+        s_lvl[l].vbase = a.F.K[l].w > 0 ? start / a.F.K[l].w : 0;
+        s_lvl[l].ubase = start - s_lvl[l].vbase * a.F.K[l].w;
     }
     for (int i = threadIdx.x; i < 768; i += blockDim.x) {
         const double w = i < 256 ? 0.2126 : (i < 512 ? 0.7152 : 0.0722);  // image.hpp:80-83

@@ -7,7 +7,7 @@
 namespace rfb {
 
 constexpr int kMaxLevels = 6;
-constexpr int kTrackThreads = 384;  // 12 warps at <= 168 registers (tools/pass_bench.py: 16.6 vs 19.9 us per L0 pass at 256)
+constexpr int kTrackThreads = kGridThreads;  // 12 warps at <= 168 registers (tools/pass_bench.py: 16.6 vs 19.9 us per L0 pass at 256)
 constexpr int kTrackMinBlocks = 1;  // one CTA per SM: 148 grid partials
 // Per-thread cache of the Jacobian passes' pixel inputs {depth, intensity}:
 // one 8-byte entry per pixel step (a thread meets the same pixels in every
