@@ -72,18 +72,30 @@ typedef struct {
     uint64_t hash_capacity;
 } rf_volume_config;
 
-/* RegistrationConfig (registration.hpp:13-23); `threads` is accepted and ignored */
+/* RegistrationConfig (registration.hpp:13-23); `threads` is accepted and ignored.
+ * Extension (not in the reference, off by default): Huber weighting of the
+ * depth (huber_depth, metres) and colour (huber_color, scaled intensity)
+ * residuals in the LM normal equations and cost; 0 = plain least squares as
+ * the reference (registration.cpp:72-95), bit for bit. */
 typedef struct {
     double color_weight;
     int32_t pyramid_levels, max_iterations;
     double lm_lambda_init, lm_lambda_up, lm_lambda_down, convergence_eps;
     int32_t min_valid_residuals, threads;
+    double huber_depth, huber_color;
 } rf_registration_config;
 
-/* MaskConfig (dynamics_mask.hpp:10-17) */
+/* MaskConfig (dynamics_mask.hpp:10-17).
+ * Extension (not in the reference, off by default): free_space > 0 also
+ * seeds the mask with pixels whose measured point lies at least free_space
+ * metres in front of the model surface (signed residual > free_space: the
+ * model holds that space as free). 0 = the reference's threshold, bit for bit.
+ * The residual images then carry the sign in bit 1 of `valid` (3 = valid and
+ * positive); rf_mask_stages reads it the same way. */
 typedef struct {
     double gamma, truncation, theta;
     int32_t erode_radius, dilate_radius, connectivity, reserved0;
+    double free_space;
 } rf_mask_config;
 
 /* PipelineConfig (config.hpp:12-24) with RefinementConfig (depth_refinement.hpp:12-17) */

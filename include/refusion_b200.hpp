@@ -484,10 +484,11 @@ struct RegistrationConfig {
     int pyramid_levels = 3, max_iterations = 20;
     double lm_lambda_init = 1e-4, lm_lambda_up = 10.0, lm_lambda_down = 2.0, convergence_eps = 1e-5;
     int min_valid_residuals = 100, threads = 1;
+    double huber_depth = 0.0, huber_color = 0.0;  // extension, off by default (see rf_registration_config)
     rf_registration_config c() const {
         return rf_registration_config{color_weight,   pyramid_levels, max_iterations, lm_lambda_init,
                                       lm_lambda_up,   lm_lambda_down, convergence_eps, min_valid_residuals,
-                                      threads};
+                                      threads,        huber_depth,    huber_color};
     }
 };
 
@@ -624,8 +625,9 @@ inline RegistrationResult Register(const TsdfVolume& volume, const Frame& frame,
 struct MaskConfig {
     double gamma = 0.5, truncation = 0.1, theta = 0.007;
     int erode_radius = 2, dilate_radius = 2, connectivity = 4;
+    double free_space = 0.0;  // extension, off by default (see rf_mask_config)
     rf_mask_config c() const {
-        return rf_mask_config{gamma, truncation, theta, erode_radius, dilate_radius, connectivity, 0};
+        return rf_mask_config{gamma, truncation, theta, erode_radius, dilate_radius, connectivity, 0, free_space};
     }
 };
 

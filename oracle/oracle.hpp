@@ -368,6 +368,16 @@ struct RegistrationConfig {
     double convergence_eps = 1e-5;
     int min_valid_residuals = 100;
     int threads = 1;
+    // Extensions (not in the reference; 0 / false reproduce it): Huber
+    // weighting of the depth / colour residuals, and the residual sign in
+    // bit 1 of ResidualImage::valid (set by the pipeline when the mask's
+    // free-space term is on).
+    double huber_depth = 0.0, huber_color = 0.0;
+    bool residual_sign = false;
+};
+struct Robust {  // the extensions Accumulate applies
+    double huber_depth = 0.0, huber_color = 0.0;
+    bool residual_sign = false;
 };
 struct ResidualImage {
     Image<float> squared;
@@ -395,7 +405,8 @@ struct RegistrationResult {
 };
 std::vector<PyramidLevel> BuildPyramid(const Frame& f, const Mask* mask, int levels);
 Accum Accumulate(const Volume& vol, const PyramidLevel& level, const Pose& pose, double cw,
-                 bool with_jacobian, bool use_mask, int threads, ResidualImage* out);
+                 bool with_jacobian, bool use_mask, int threads, ResidualImage* out,
+                 const Robust& rb = Robust());
 PyramidLevel LevelZero(const Frame& f, const Mask* mask);
 RegistrationResult Register(const Volume& vol, const Frame& f, const Pose& init, const Mask* mask,
                             const RegistrationConfig& cfg);
@@ -409,6 +420,7 @@ bool Degenerate(const Accum& acc);  // registration.cpp:128-139
 struct MaskConfig {
     double gamma = 0.5, truncation = 0.1, theta = 0.007;
     int erode_radius = 2, dilate_radius = 2, connectivity = 4;
+    double free_space = 0.0;  // extension (0: off): positive residuals > free_space also seed the mask
 };
 Mask ThresholdResiduals(const ResidualImage& r, const MaskConfig& c);
 Mask Erode(const Mask& m, int radius);

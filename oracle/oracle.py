@@ -41,13 +41,14 @@ class OVolCfg(C.Structure):
 class ORegCfg(C.Structure):
     _fields_ = [("color_weight", C.c_double), ("pyramid_levels", C.c_int32), ("max_iterations", C.c_int32),
                 ("lm_lambda_init", C.c_double), ("lm_lambda_up", C.c_double), ("lm_lambda_down", C.c_double),
-                ("convergence_eps", C.c_double), ("min_valid_residuals", C.c_int32), ("threads", C.c_int32)]
+                ("convergence_eps", C.c_double), ("min_valid_residuals", C.c_int32), ("threads", C.c_int32),
+                ("huber_depth", C.c_double), ("huber_color", C.c_double)]
 
 
 class OMaskCfg(C.Structure):
     _fields_ = [("gamma", C.c_double), ("truncation", C.c_double), ("theta", C.c_double),
                 ("erode_radius", C.c_int32), ("dilate_radius", C.c_int32), ("connectivity", C.c_int32),
-                ("pad0", C.c_int32)]
+                ("pad0", C.c_int32), ("free_space", C.c_double)]
 
 
 class OPipeCfg(C.Structure):
@@ -153,14 +154,14 @@ def vol_cfg(**kw) -> OVolCfg:
 
 
 def reg_cfg(**kw) -> ORegCfg:
-    c = ORegCfg(0.025, 3, 20, 1e-4, 10.0, 2.0, 1e-5, 100, 1)
+    c = ORegCfg(0.025, 3, 20, 1e-4, 10.0, 2.0, 1e-5, 100, 1, 0.0, 0.0)
     for k, v in kw.items():
         setattr(c, k, v)
     return c
 
 
 def mask_cfg(**kw) -> OMaskCfg:
-    c = OMaskCfg(0.5, 0.1, 0.007, 2, 2, 4, 0)
+    c = OMaskCfg(0.5, 0.1, 0.007, 2, 2, 4, 0, 0.0)
     for k, v in kw.items():
         setattr(c, k, v)
     return c

@@ -28,10 +28,12 @@ struct ORegCfg {
     int32_t pyramid_levels, max_iterations;
     double lm_lambda_init, lm_lambda_up, lm_lambda_down, convergence_eps;
     int32_t min_valid_residuals, threads;
+    double huber_depth, huber_color;  // extension (0: the reference)
 };
 struct OMaskCfg {
     double gamma, truncation, theta;
     int32_t erode_radius, dilate_radius, connectivity, pad0;
+    double free_space;  // extension (0: the reference)
 };
 struct OPipeCfg {
     OVolCfg volume;
@@ -104,12 +106,14 @@ RegistrationConfig ToReg(const ORegCfg* c) {
     r.lm_lambda_up = c->lm_lambda_up; r.lm_lambda_down = c->lm_lambda_down;
     r.convergence_eps = c->convergence_eps; r.min_valid_residuals = c->min_valid_residuals;
     r.threads = c->threads;
+    r.huber_depth = c->huber_depth; r.huber_color = c->huber_color;
     return r;
 }
 MaskConfig ToMask(const OMaskCfg* c) {
     MaskConfig m;
     m.gamma = c->gamma; m.truncation = c->truncation; m.theta = c->theta;
     m.erode_radius = c->erode_radius; m.dilate_radius = c->dilate_radius; m.connectivity = c->connectivity;
+    m.free_space = c->free_space;
     return m;
 }
 DepthImage ToDepth(const float* d, int w, int h) {
@@ -344,7 +348,7 @@ int o_linearize(void* vp, const float* depth, const uint8_t* rgb, const OIntr* k
         if (mask) m = ToMaskImg(mask, k->width, k->height);
         const PyramidLevel level = LevelZero(f, mask ? &m : nullptr);
         const Accum acc = Accumulate(*static_cast<Volume*>(vp), level, Pose::FromArray(pose), cfg->color_weight,
-                                     true, true, cfg->threads, nullptr);
+                                     true, true, cfg->threads, nullptr, Robust{cfg->huber_depth, cfg->huber_color, false});
         std::memcpy(H, acc.H, sizeof(acc.H));
         std::memcpy(b, acc.b, sizeof(acc.b));
         errs[0] = acc.depth_error;

@@ -383,7 +383,7 @@ Accum CombineAccum(Accum a, const Accum& b) {  // registration.cpp:36-43
 
 Accum Accumulate(const Volume& vol, const PyramidLevel& level, const Pose& pose, double cw,
                  bool with_jacobian, bool use_mask, int threads,
-                 ResidualImage* out) {  // registration.cpp:49-117
+                 ResidualImage* out, const Robust& rb) {  // registration.cpp:49-117
     const bool use_color = cw > 0.0 && !level.intensity.Empty();
     const bool has_mask = use_mask && !level.mask.Empty();
     const double min_depth = vol.config().min_depth, max_depth = vol.config().max_depth;
@@ -409,20 +409,27 @@ Accum Accumulate(const Volume& vol, const PyramidLevel& level, const Pose& pose,
                 const double r_d = sdf.value;
                 const V3d yg = Cross(y, sdf.gradient);
                 const double J[6] = {sdf.gradient.x, sdf.gradient.y, sdf.gradient.z, yg.x, yg.y, yg.z};
+                // Huber extension: weight hd / |r| and cost 2 hd |r| - hd^2 beyond the threshold
+                const double hd = rb.huber_depth, ad = std::fabs(r_d);
+                const bool out_d = hd > 0.0 && ad > hd;
+                const double wd = out_d ? hd / ad : 1.0;
                 for (int i = 0; i < 6; ++i)
-                    for (int j = 0; j < 6; ++j) acc.H[6 * i + j] += J[i] * J[j];
-                for (int i = 0; i < 6; ++i) acc.b[i] += J[i] * r_d;
-                acc.depth_error += r_d * r_d;
+                    for (int j = 0; j < 6; ++j) acc.H[6 * i + j] += out_d ? wd * (J[i] * J[j]) : J[i] * J[j];
+                for (int i = 0; i < 6; ++i) acc.b[i] += out_d ? wd * (J[i] * r_d) : J[i] * r_d;
+                acc.depth_error += out_d ? 2.0 * hd * ad - hd * hd : r_d * r_d;
                 if (use_color) {
                     const Sample in = vol.SampleIntensityWithGradient(y);
                     const double r_c = (in.value - double(level.intensity(u, v))) * kIntensityScale;
                     const V3d yi = Cross(y, in.gradient);
                     double Jc[6] = {in.gradient.x, in.gradient.y, in.gradient.z, yi.x, yi.y, yi.z};
                     for (double& e : Jc) e *= kIntensityScale;
+                    const double hc = rb.huber_color, ac = std::fabs(r_c);
+                    const bool out_c = hc > 0.0 && ac > hc;
+                    const double cwc = out_c ? cw * (hc / ac) : cw;
                     for (int i = 0; i < 6; ++i)
-                        for (int j = 0; j < 6; ++j) acc.H[6 * i + j] += cw * (Jc[i] * Jc[j]);
-                    for (int i = 0; i < 6; ++i) acc.b[i] += cw * (Jc[i] * r_c);
-                    acc.color_error += r_c * r_c;
+                        for (int j = 0; j < 6; ++j) acc.H[6 * i + j] += cwc * (Jc[i] * Jc[j]);
+                    for (int i = 0; i < 6; ++i) acc.b[i] += cwc * (Jc[i] * r_c);
+                    acc.color_error += out_c ? 2.0 * hc * ac - hc * hc : r_c * r_c;
                 }
                 ++acc.valid;
                 if (out) {
@@ -435,7 +442,7 @@ Accum Accumulate(const Volume& vol, const PyramidLevel& level, const Pose& pose,
                 const double r_d = sdf.value;
                 if (out) {
                     out->squared(u, v) = float(r_d * r_d);
-                    out->valid(u, v) = 1;
+                    out->valid(u, v) = (rb.residual_sign && r_d > 0.0) ? 3 : 1;
                 }
                 if (masked) continue;
                 acc.depth_error += r_d * r_d;
@@ -630,7 +637,8 @@ RegistrationResult Register(const Volume& vol, const Frame& f, const Pose& init,
         const PyramidLevel& level = pyr[li];
         const size_t min_valid =
             std::max<size_t>(size_t(std::max(cfg.min_valid_residuals, 1)) >> (2 * li), 16);
-        current = Accumulate(vol, level, pose, cfg.color_weight, true, true, cfg.threads, nullptr);
+        const Robust rb{cfg.huber_depth, cfg.huber_color, false};
+        current = Accumulate(vol, level, pose, cfg.color_weight, true, true, cfg.threads, nullptr, rb);
         if (current.valid < min_valid)
             throw TrackingLostError("only " + std::to_string(current.valid) +
                                     " valid residuals at pyramid level " + std::to_string(li));
@@ -654,7 +662,7 @@ RegistrationResult Register(const Volume& vol, const Frame& f, const Pose& init,
                 continue;
             }
             const Pose cand = ExpMap(delta) * pose;
-            const Accum trial = Accumulate(vol, level, cand, cfg.color_weight, true, true, cfg.threads, nullptr);
+            const Accum trial = Accumulate(vol, level, cand, cfg.color_weight, true, true, cfg.threads, nullptr, rb);
             const double cur_err = current.depth_error + cfg.color_weight * current.color_error;
             const double trial_err = trial.depth_error + cfg.color_weight * trial.color_error;
             if (trial.valid >= min_valid && trial_err < cur_err) {
@@ -685,7 +693,9 @@ RegistrationResult Register(const Volume& vol, const Frame& f, const Pose& init,
     res.final_error = current.depth_error + cfg.color_weight * current.color_error;
     PyramidLevel full = pyr[0];
     full.mask = Mask();
-    Accumulate(vol, full, pose, 0.0, false, false, cfg.threads, &res.residuals);
+    Robust sign;
+    sign.residual_sign = cfg.residual_sign;
+    Accumulate(vol, full, pose, 0.0, false, false, cfg.threads, &res.residuals, sign);
     return res;
 }
 
@@ -697,7 +707,9 @@ Mask ThresholdResiduals(const ResidualImage& r, const MaskConfig& c) {
     Mask m(r.squared.w, r.squared.h, 0);
     for (int y = 0; y < m.h; ++y)
         for (int x = 0; x < m.w; ++x)
-            if (r.valid(x, y) && double(r.squared(x, y)) > thr) m(x, y) = 1;
+            if ((r.valid(x, y) && double(r.squared(x, y)) > thr) ||
+                (c.free_space > 0.0 && (r.valid(x, y) & 2) && double(r.squared(x, y)) > c.free_space * c.free_space))
+                m(x, y) = 1;  // the second clause: the free-space extension (off by default)
     return m;
 }
 
@@ -906,7 +918,9 @@ FrameStats Pipeline::ProcessFrame(const Frame& f) {  // pipeline.cpp:57-131
         if (cfg_.refinement.enabled && int(window_.size()) >= cfg_.refinement.window) IntegrateFront();
         Mask mask;
         try {
-            RegistrationResult reg = Register(volume_, f, current_, nullptr, cfg_.registration);
+            RegistrationConfig rc = cfg_.registration;
+            rc.residual_sign = cfg_.mask.free_space > 0.0;  // the free-space extension reads the sign
+            RegistrationResult reg = Register(volume_, f, current_, nullptr, rc);
             st.registrations = 1;
             st.iterations = reg.iterations;
             if (cfg_.dynamics_enabled) {
@@ -915,7 +929,7 @@ FrameStats Pipeline::ProcessFrame(const Frame& f) {  // pipeline.cpp:57-131
                 for (uint8_t v : mask.d) n += v != 0;
                 st.masked_pixels = n;
                 if (n > 0) {
-                    RegistrationResult r2 = Register(volume_, f, reg.pose, &mask, cfg_.registration);
+                    RegistrationResult r2 = Register(volume_, f, reg.pose, &mask, rc);
                     st.registrations = 2;
                     st.iterations += r2.iterations;
                     reg = std::move(r2);

@@ -35,10 +35,12 @@ struct RRegCfg {
     int32_t pyramid_levels, max_iterations;
     double lm_lambda_init, lm_lambda_up, lm_lambda_down, convergence_eps;
     int32_t min_valid_residuals, threads;
+    double huber_depth, huber_color;  // the oracle's extension knobs: layout only, the reference has none
 };
 struct RMaskCfg {
     double gamma, truncation, theta;
     int32_t erode_radius, dilate_radius, connectivity, pad0;
+    double free_space;  // (layout only, as above)
 };
 struct RPipeCfg {
     RVolCfg volume;

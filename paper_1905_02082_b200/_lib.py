@@ -28,13 +28,14 @@ class rf_volume_config(C.Structure):
 class rf_registration_config(C.Structure):
     _fields_ = [("color_weight", C.c_double), ("pyramid_levels", C.c_int32), ("max_iterations", C.c_int32),
                 ("lm_lambda_init", C.c_double), ("lm_lambda_up", C.c_double), ("lm_lambda_down", C.c_double),
-                ("convergence_eps", C.c_double), ("min_valid_residuals", C.c_int32), ("threads", C.c_int32)]
+                ("convergence_eps", C.c_double), ("min_valid_residuals", C.c_int32), ("threads", C.c_int32),
+                ("huber_depth", C.c_double), ("huber_color", C.c_double)]
 
 
 class rf_mask_config(C.Structure):
     _fields_ = [("gamma", C.c_double), ("truncation", C.c_double), ("theta", C.c_double),
                 ("erode_radius", C.c_int32), ("dilate_radius", C.c_int32), ("connectivity", C.c_int32),
-                ("reserved0", C.c_int32)]
+                ("reserved0", C.c_int32), ("free_space", C.c_double)]
 
 
 class rf_pipeline_config(C.Structure):

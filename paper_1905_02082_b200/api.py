@@ -48,16 +48,18 @@ def volume_config(**kw) -> L.rf_volume_config:
 
 
 def registration_config(**kw) -> L.rf_registration_config:
-    """RegistrationConfig (registration.hpp:13-23) defaults."""
-    c = L.rf_registration_config(0.025, 3, 20, 1e-4, 10.0, 2.0, 1e-5, 100, 1)
+    """RegistrationConfig (registration.hpp:13-23) defaults; huber_depth /
+    huber_color > 0 turn on the Huber-weighted extension (off = reference)."""
+    c = L.rf_registration_config(0.025, 3, 20, 1e-4, 10.0, 2.0, 1e-5, 100, 1, 0.0, 0.0)
     for k, v in kw.items():
         setattr(c, k, v)
     return c
 
 
 def mask_config(**kw) -> L.rf_mask_config:
-    """MaskConfig (dynamics_mask.hpp:10-17) defaults."""
-    c = L.rf_mask_config(0.5, 0.1, 0.007, 2, 2, 4, 0)
+    """MaskConfig (dynamics_mask.hpp:10-17) defaults; free_space > 0 turns on
+    the free-space seed extension (off = reference)."""
+    c = L.rf_mask_config(0.5, 0.1, 0.007, 2, 2, 4, 0, 0.0)
     for k, v in kw.items():
         setattr(c, k, v)
     return c

@@ -338,6 +338,7 @@ void check_reg_config(const rf_registration_config& r) {
     require(r.pyramid_levels >= 1, RF_INVALID_ARGUMENT, "pyramid_levels must be >= 1");
     require(r.pyramid_levels <= kMaxLevels, RF_UNSUPPORTED, "pyramid_levels > 6");
     require(r.max_iterations >= 1, RF_INVALID_ARGUMENT, "max_iterations must be >= 1");
+    require(r.huber_depth >= 0 && r.huber_color >= 0, RF_INVALID_ARGUMENT, "huber thresholds must be >= 0");
 }
 
 }  // namespace
@@ -603,6 +604,8 @@ RegParams to_reg(const rf_registration_config& c, int levels) {
     r.lambda_down = c.lm_lambda_down;
     r.eps = c.convergence_eps;
     r.min_valid = c.min_valid_residuals;
+    r.huber_d = c.huber_depth;
+    r.huber_c = c.huber_color;
     return r;
 }
 
@@ -614,6 +617,7 @@ MaskParams to_mask(const rf_mask_config& c) {
     m.erode_radius = c.erode_radius;
     m.dilate_radius = c.dilate_radius;
     m.connectivity = c.connectivity;
+    m.free_space = c.free_space;
     return m;
 }
 
@@ -1148,7 +1152,7 @@ rf_status rf_build_pyramid(const rf_frame* f, const uint8_t* mask, int32_t level
 }
 
 static void run_pass(rf_volume* v, const rf_frame* f, const double pose[12], const uint8_t* mask, int mode,
-                     double cw, TrackOut& out) {
+                     double cw, TrackOut& out, const rf_registration_config* cfg = nullptr) {
     v->prepare(f);
     const float* d = v->depth_of(f);
     const uint8_t* rgb = v->rgb_of(f);
@@ -1161,6 +1165,10 @@ static void run_pass(rf_volume* v, const rf_frame* f, const double pose[12], con
     a.mode = mode;
     a.reg.color_weight = cw;
     a.reg.levels = 1;
+    if (cfg) {
+        a.reg.huber_d = cfg->huber_depth;
+        a.reg.huber_c = cfg->huber_color;
+    }
     v->launch_track(a);
     out = v->fetch_out();
 }
@@ -1171,7 +1179,8 @@ rf_status rf_linearize(const rf_volume* cv, const rf_frame* f, const double pose
         rf_volume* v = const_cast<rf_volume*>(cv);
         require(v && pose && cfg && out, RF_INVALID_ARGUMENT, "null argument");
         TrackOut o;
-        run_pass(v, f, pose, mask, kModeLinearize, cfg->color_weight, o);
+        require(cfg->huber_depth >= 0 && cfg->huber_color >= 0, RF_INVALID_ARGUMENT, "huber thresholds must be >= 0");
+        run_pass(v, f, pose, mask, kModeLinearize, cfg->color_weight, o, cfg);
         for (int i = 0, k = 0; i < 6; ++i)
             for (int j = i; j < 6; ++j, ++k) out->H[6 * i + j] = out->H[6 * j + i] = o.acc[k];
         for (int i = 0; i < 6; ++i) out->b[i] = o.acc[21 + i];
@@ -1249,6 +1258,7 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
     return guard([&] {
         require(res_valid && depth && cfg && out && w > 0 && h > 0, RF_INVALID_ARGUMENT, "null argument");
         require(!(stages & 1) || res_sq, RF_INVALID_ARGUMENT, "threshold stage needs residuals");
+        require(cfg->free_space >= 0, RF_INVALID_ARGUMENT, "free_space must be >= 0");
         require(cfg->connectivity == 4 || cfg->connectivity == 8, RF_INVALID_ARGUMENT,
                 "connectivity must be 4 or 8");
         CK(cudaSetDevice(device));
@@ -1575,6 +1585,7 @@ void validate_pipeline_config(rf_pipeline_config c) {  // PipelineConfig::Sync (
             "morphology radii must be non-negative");
     require(c.mask.connectivity == 4 || c.mask.connectivity == 8, RF_INVALID_ARGUMENT,
             "connectivity must be 4 or 8");
+    require(c.mask.free_space >= 0, RF_INVALID_ARGUMENT, "free_space must be >= 0");
     require(c.registration.color_weight >= 0, RF_INVALID_ARGUMENT, "color_weight must be non-negative");
     check_reg_config(c.registration);
     require(c.registration.lm_lambda_init > 0 && c.registration.lm_lambda_up > 1 && c.registration.lm_lambda_down > 1,

@@ -226,7 +226,7 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
 // One Accumulate (registration.cpp:49-117) over pyramid level `level`.
 // `pre` runs on the CTA's last thread after its pixels when that thread has
 // fewer pixels than the busiest ones (its slack hides the work).
-template <bool kJac, bool kColor, class Hook, class Pre>
+template <bool kJac, bool kColor, bool kRobust, class Hook, class Pre>
 __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
                            double* scratch, double* blk, double* out, const Hook& hook, const Pre& pre) {
     const FrameView& F = a.F;
@@ -287,7 +287,44 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
                 if (sample_point<kJac, kColor, !kJac>(a.V, y, cs, s_luma_lut)) {
                     const double r_d = cs.sdf;
                     const double I = kColor ? double(inten) : 0.0;
-                    if (kJac) {
+                    if (kJac && kRobust) {
+                        // Huber extension (off by default; not in the reference): rows
+                        // of a residual beyond the threshold weighted by hd / |r|, its
+                        // cost 2 hd |r| - hd^2 (continuous with r^2). A weight of 1.0
+                        // multiplies exactly, so inliers add what the plain path adds.
+                        const double hd = a.reg.huber_d, ad = fabs(r_d);
+                        const bool out_d = hd > 0.0 && ad > hd;
+                        const double wd = out_d ? hd / ad : 1.0;
+                        const double J[6] = {cs.gs[0], cs.gs[1], cs.gs[2], y[1] * cs.gs[2] - y[2] * cs.gs[1],
+                                             y[2] * cs.gs[0] - y[0] * cs.gs[2], y[0] * cs.gs[1] - y[1] * cs.gs[0]};
+#pragma unroll
+                        for (int i = 0; i < 6; ++i)
+#pragma unroll
+                            for (int j = i; j < 6; ++j) acc[hidx(i, j)] = __fma_rn(wd * J[i], J[j], acc[hidx(i, j)]);
+#pragma unroll
+                        for (int i = 0; i < 6; ++i) acc[21 + i] = __fma_rn(wd * J[i], r_d, acc[21 + i]);
+                        acc[27] = out_d ? acc[27] + (2.0 * hd * ad - hd * hd) : __fma_rn(r_d, r_d, acc[27]);
+                        if (kColor) {
+                            const double r_c = (cs.inten - I) * kIntensityScale;
+                            const double hc = a.reg.huber_c, ac = fabs(r_c);
+                            const bool out_c = hc > 0.0 && ac > hc;
+                            const double cwc = cw * (out_c ? hc / ac : 1.0);
+                            const double Jc[6] = {cs.gi[0] * kIntensityScale, cs.gi[1] * kIntensityScale,
+                                                  cs.gi[2] * kIntensityScale,
+                                                  (y[1] * cs.gi[2] - y[2] * cs.gi[1]) * kIntensityScale,
+                                                  (y[2] * cs.gi[0] - y[0] * cs.gi[2]) * kIntensityScale,
+                                                  (y[0] * cs.gi[1] - y[1] * cs.gi[0]) * kIntensityScale};
+#pragma unroll
+                            for (int i = 0; i < 6; ++i)
+#pragma unroll
+                                for (int j = i; j < 6; ++j)
+                                    acc[hidx(i, j)] = __fma_rn(cwc * Jc[i], Jc[j], acc[hidx(i, j)]);
+#pragma unroll
+                            for (int i = 0; i < 6; ++i) acc[21 + i] = __fma_rn(cwc * Jc[i], r_c, acc[21 + i]);
+                            acc[28] = out_c ? acc[28] + (2.0 * hc * ac - hc * hc) : __fma_rn(r_c, r_c, acc[28]);
+                        }
+                        acc[29] += 1.0;
+                    } else if (kJac) {
                         const double J[6] = {cs.gs[0], cs.gs[1], cs.gs[2], y[1] * cs.gs[2] - y[2] * cs.gs[1],
                                              y[2] * cs.gs[0] - y[0] * cs.gs[2], y[0] * cs.gs[1] - y[1] * cs.gs[0]};
 #pragma unroll
@@ -316,7 +353,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
                         acc[29] += 1.0;
                     } else {
                         rs = float(r_d * r_d);
-                        rv = 1;
+                        rv = (a.mp.free_space > 0.0 && r_d > 0.0) ? 3 : 1;  // bit 1: the free-space extension's sign
                         if (!masked) {
                             acc[27] += r_d * r_d;
                             if (kColor) {
@@ -388,8 +425,15 @@ __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& 
         s_passes += 1;  // CTA 0's tally, published once at kernel exit (no global RMW on the pass path)
         s_pixel_passes += double(a.F.K[level].w) * double(a.F.K[level].h);
     }
-    if (color) accumulate<kJac, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook, pre);
-    else accumulate<kJac, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook, pre);
+    const bool robust = kJac && (a.reg.huber_d > 0.0 || a.reg.huber_c > 0.0);
+    if (robust) {
+        if (color) accumulate<kJac, true, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook, pre);
+        else accumulate<kJac, false, true>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook, pre);
+    } else if (color) {
+        accumulate<kJac, true, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook, pre);
+    } else {
+        accumulate<kJac, false, false>(a, level, P, use_mask, write_res, cw, scratch, blk, out, hook, pre);
+    }
 }
 
 // ------------------------------------------------------------------ Register
@@ -888,6 +932,10 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
     const uint8_t* input = F.mwork[0];
     uint8_t* seeds = F.mwork[1];
     const double thr = M.gamma * M.truncation * M.truncation;  // ThresholdResiduals (dynamics_mask.cpp:9-18)
+    // free-space extension (off: 0): a valid residual whose signed sdf is
+    // positive (bit 1 of valid, set by the residual pass only when enabled)
+    // and whose square exceeds free_space^2 also seeds the mask
+    const double fs2 = M.free_space > 0.0 ? M.free_space * M.free_space : INFINITY;
     const bool do_thr = stages & 1;
     if (re <= kMorphMaxR) {
         for (int t = blockIdx.x; t < ntx * nty; t += gridDim.x) {
@@ -898,7 +946,7 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
                                  if (!do_thr) return __ldcg(input + p) != 0;
                                  const uint8_t valid = __ldcg(F.res_valid + p);
                                  const float sq = __ldcg(F.res_sq + p);
-                                 return (valid != 0) & (double(sq) > thr);
+                                 return ((valid != 0) & (double(sq) > thr)) | ((valid & 2) != 0 && double(sq) > fs2);
                              },
                              seeds, nseed);
             if (stages & 4) {  // the floodfill's growth bits (same 32x32 tiling) and round-0 worklist
@@ -913,7 +961,8 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
     } else {  // wide windows: threshold, then separable passes through global memory
         uint8_t* thr_img = F.mwork[2];
         for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride)
-            thr_img[p] = do_thr ? ((__ldcg(F.res_valid + p) && double(__ldcg(F.res_sq + p)) > thr) ? 1 : 0)
+            thr_img[p] = do_thr ? (((__ldcg(F.res_valid + p) && double(__ldcg(F.res_sq + p)) > thr) ||
+                                    ((__ldcg(F.res_valid + p) & 2) && double(__ldcg(F.res_sq + p)) > fs2)) ? 1 : 0)
                                 : __ldcg(input + p);
         grid_barrier(a.grid);
         morph_pass(thr_img, F.grow, w, h, re, true, true);

@@ -21,11 +21,13 @@ struct RegParams {  // RegistrationConfig, registration.hpp:13-23
     int levels, max_iterations;
     double lambda_init, lambda_up, lambda_down, eps;
     int min_valid;
+    double huber_d, huber_c;  // Huber extension (0: off, the reference's least squares)
 };
 
 struct MaskParams {  // MaskConfig, dynamics_mask.hpp:10-17
     double gamma, truncation, theta;
     int erode_radius, dilate_radius, connectivity;
+    double free_space;  // free-space seed extension (0: off)
 };
 
 // Device images of one frame and its pyramid. Level 0 depth/rgb are the
