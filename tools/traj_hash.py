@@ -1,3 +1,8 @@
+"""Fingerprint of the CUDA pipeline's trajectory on the first 40 C2 frames
+(SHA-1 of the pose bytes): two library builds that print the same digest
+track bit-identically (RF_LIB_PATH selects a variant). Used to check that a
+kernel change which should not alter arithmetic (e.g. the default-off
+extensions, a reordered but equivalent computation) does not."""
 import hashlib, sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np
