@@ -378,7 +378,7 @@ struct CellSample {
 // so its load is issued together with the slot's, before the key compare:
 // one dependent L2 round trip (slot + record) instead of two, and every
 // lane runs the same code.
-__device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int by, int bz, uint2 c[8]) {
+__device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int by, int bz, uint2 (&c)[8]) {
     const int lx = bx & 7, ly = by & 7, lz = bz & 7;
     const int cx = bx >> 3, cy = by >> 3, cz = bz >> 3;  // arithmetic shift == FloorDiv by 8
     if (!coord_in_range(cx, cy, cz)) return false;
@@ -392,12 +392,9 @@ __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int 
         r1 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(idx) * kLinkStride) + 1);
     }
     const unsigned long long k = (unsigned long long)s.x | ((unsigned long long)s.y << 32);
-    uint32_t b0;
-    if (k == key) {
-        b0 = s.z >= kOverflowed ? kInvalid : s.z;
-    } else if (k == kEmptyKey) {
-        return false;
-    } else {  // collision: continue the probe, then the record of the slot found (rare)
+    uint32_t b0 = s.z;
+    if (k != key) {  // empty slot, or a collision: continue the probe (rare)
+        if (k == kEmptyKey) return false;
         idx = hash_find_slot_from(V, key, idx);
         if (idx == kInvalid) return false;
         b0 = __ldg(&V.slots[idx].value);
@@ -406,7 +403,6 @@ __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int 
             r1 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(idx) * kLinkStride) + 1);
         }
     }
-    if (b0 >= kOverflowed) return false;
     uint32_t n[8];
     n[0] = b0;
     if (smask) {
@@ -415,6 +411,11 @@ __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int 
 #pragma unroll
         for (int q = 1; q < 8; ++q) n[q] = b0;
     }
+    // Straight-line from here: an absent or overflowed brick (index >= kOverflowed)
+    // is remembered in `bad` and its corner loaded from brick 0 instead (a mapped
+    // address), so the 8 loads issue back to back without a branch between them;
+    // the cell is rejected once, after the loads. Same result as returning early.
+    bool bad = false;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
         const int dx = kk & 1, dy = (kk >> 1) & 1, dz = kk >> 2;  // compile-time corner offset
@@ -424,14 +425,15 @@ __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int 
 #pragma unroll
         for (int q = 1; q < 8; ++q)
             if ((q & ~kbits) == 0) b = (code == q) ? n[q] : b;
-        if (b >= kOverflowed) return false;
+        bad |= b >= kOverflowed;
+        b = b >= kOverflowed ? 0u : b;
         const int ox = (lx + dx) & 7, oy = (ly + dy) & 7, oz = (lz + dz) & 7;
         c[kk] = __ldg(reinterpret_cast<const uint2*>(brick_ptr(V, b)) + ((oz * 8 + oy) * 8 + ox));
     }
+    bool ok = !bad;
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk)
-        if ((c[kk].y & 0xFFu) == 0u) return false;  // weight byte
-    return true;
+    for (int kk = 0; kk < 8; ++kk) ok = ok && (c[kk].y & 0xFFu) != 0u;  // weight byte
+    return ok;
 }
 
 // Link records (tsdf_volume.hpp:149-185 allocates; this only indexes): the
