@@ -378,6 +378,17 @@ struct CellSample {
 // so its load is issued together with the slot's, before the key compare:
 // one dependent L2 round trip (slot + record) instead of two, and every
 // lane runs the same code.
+// n[Q | subset of K's bits], choosing each bit of K by its straddle flag.
+template <int K, int Q = 0>
+__device__ __forceinline__ uint32_t corner_brick(const uint32_t (&n)[8], bool sx, bool sy, bool sz) {
+    if constexpr (K == 0) {
+        return n[Q];
+    } else {
+        constexpr int top = (K & 4) ? 4 : ((K & 2) ? 2 : 1);
+        const bool s = top == 4 ? sz : (top == 2 ? sy : sx);
+        return s ? corner_brick<K & ~top, Q | top>(n, sx, sy, sz) : corner_brick<K & ~top, Q>(n, sx, sy, sz);
+    }
+}
 __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int by, int bz, uint2 (&c)[8]) {
     const int lx = bx & 7, ly = by & 7, lz = bz & 7;
     const int cx = bx >> 3, cy = by >> 3, cz = bz >> 3;  // arithmetic shift == FloorDiv by 8
@@ -403,28 +414,31 @@ __device__ __forceinline__ bool gather_corners(const VolumeView& V, int bx, int 
             r1 = __ldg(reinterpret_cast<const uint4*>(V.links + size_t(idx) * kLinkStride) + 1);
         }
     }
-    uint32_t n[8];
-    n[0] = b0;
-    if (smask) {
-        n[1] = r0.y; n[2] = r0.z; n[3] = r0.w; n[4] = r1.x; n[5] = r1.y; n[6] = r1.z; n[7] = r1.w;
-    } else {
-#pragma unroll
-        for (int q = 1; q < 8; ++q) n[q] = b0;
-    }
-    // Straight-line from here: an absent or overflowed brick (index >= kOverflowed)
-    // is remembered in `bad` and its corner loaded from brick 0 instead (a mapped
-    // address), so the 8 loads issue back to back without a branch between them;
-    // the cell is rejected once, after the loads. Same result as returning early.
+    // The brick of corner (dx, dy, dz) is n[q], q = (dx & sx) | (dy & sy) << 1 |
+    // (dz & sz) << 2 with s* the straddle flags: a select tree on the three
+    // flags over the corner's own axes (19 selects for the 8 corners, no
+    // compare per candidate). Unloaded record words are never selected.
+    const uint32_t n[8] = {b0, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    const bool sx = lx == 7, sy = ly == 7, sz = lz == 7;
     bool bad = false;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
         const int dx = kk & 1, dy = (kk >> 1) & 1, dz = kk >> 2;  // compile-time corner offset
-        const int kbits = dx | (dy << 1) | (dz << 2);
-        const int code = kbits & smask;                          // which neighbour holds this corner
-        uint32_t b = b0;
-#pragma unroll
-        for (int q = 1; q < 8; ++q)
-            if ((q & ~kbits) == 0) b = (code == q) ? n[q] : b;
+        uint32_t b;
+        switch (kk) {
+            case 0: b = corner_brick<0>(n, sx, sy, sz); break;
+            case 1: b = corner_brick<1>(n, sx, sy, sz); break;
+            case 2: b = corner_brick<2>(n, sx, sy, sz); break;
+            case 3: b = corner_brick<3>(n, sx, sy, sz); break;
+            case 4: b = corner_brick<4>(n, sx, sy, sz); break;
+            case 5: b = corner_brick<5>(n, sx, sy, sz); break;
+            case 6: b = corner_brick<6>(n, sx, sy, sz); break;
+            default: b = corner_brick<7>(n, sx, sy, sz); break;
+        }
+        // Straight-line from here: an absent or overflowed brick (index >=
+        // kOverflowed) is remembered in `bad` and its corner loaded from brick 0
+        // instead (a mapped address), so the 8 loads issue back to back without
+        // a branch between them; the cell is rejected once, after the loads.
         bad |= b >= kOverflowed;
         b = b >= kOverflowed ? 0u : b;
         const int ox = (lx + dx) & 7, oy = (ly + dy) & 7, oz = (lz + dz) & 7;
