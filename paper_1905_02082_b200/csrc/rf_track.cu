@@ -35,13 +35,19 @@ __shared__ int s_pxc_tag;  // (level + 1) | 16 * use_mask of the cached inputs, 
 __shared__ int s_passes;   // Accumulate passes run (CTA 0; TrackOut.passes / pixel_passes)
 __shared__ double s_pixel_passes;
 __shared__ double s_luma_lut[768];  // w_c * x for the three Rec.709 weights (see voxel_luma_lut)
-// This CTA's pixel range per pyramid level (set at kernel start): ceil(npx /
-// G) consecutive pixels from (ubase, vbase), so a pass starts without an
-// integer division on every thread's path to its first pixel.
-struct LevelRange {
+// Per pyramid level (set at kernel start): the intrinsics and image pointers
+// (shared memory, so no code indexes the kernel parameters with a run-time
+// level, which would copy them to local memory), and this CTA's pixel range:
+// ceil(npx / G) consecutive pixels from (ubase, vbase), so a pass starts
+// without an integer division on every thread's path to its first pixel.
+struct LevelInfo {
+    Intr K;
+    float* depth;  // level 0: the input depth (read only)
+    float* inten;  // level 0: unused (intensity from rgb0 on the fly)
+    uint8_t* mask;
     int per, end, ubase, vbase;
 };
-__shared__ LevelRange s_lvl[kMaxLevels];
+__shared__ LevelInfo s_lvl[kMaxLevels];
 
 struct RegState {
     Pose pose, cand;
@@ -145,7 +151,10 @@ __device__ bool lm_solve(const double* acc, double lambda, double* delta) {
     // cycles), one multiply and one FMA per pivot sit on the dependency
     // chain. Rounding differs from Eigen's divisions in the last bits only;
     // the normal equations already differ at that level through the
-    // reduction order, so parity is held at the pose level.
+    // reduction order, so parity is held at the pose level. (A 2x2 block
+    // elimination over the 3x3 translation / rotation blocks with adjugate
+    // inverses measured 797 vs 840 cycles in isolation and no difference in
+    // the pipeline.)
     double L[6][6], inv_d[6];
     bool pivots_ok = true;  // no early exit: one basic block, so later pivots' work can be hoisted
 #pragma unroll
@@ -188,7 +197,9 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
     const FrameView& F = a.F;
     const int stride = gridDim.x * blockDim.x;
     for (int l = 1; l < a.reg.levels; ++l) {
-        const int w = F.K[l].w, h = F.K[l].h, pw = F.K[l - 1].w;
+        const LevelInfo& L0 = s_lvl[l - 1];
+        const LevelInfo& L1 = s_lvl[l];
+        const int w = L1.K.w, h = L1.K.h, pw = L0.K.w;
         for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < w * h; p += stride) {
             const int x = p % w, y = p / w;
             float closest = 0.f, isum = 0.f;
@@ -197,7 +208,7 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
                 for (int dx = 0; dx < 2; ++dx) {
                     const int sp = (2 * y + dy) * pw + (2 * x + dx);
                     if (images) {
-                        const float d = (l == 1) ? __ldg(F.depth0 + sp) : __ldcg(F.depth[l - 1] + sp);
+                        const float d = (l == 1) ? __ldg(F.depth0 + sp) : __ldcg(L0.depth + sp);
                         if (depth_valid(d) && (!depth_valid(closest) || d < closest)) closest = d;
                         if (F.rgb0) {
                             float iv;
@@ -205,18 +216,18 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
                                 const uint8_t* c = F.rgb0 + 3 * size_t(sp);
                                 iv = float(luma(__ldg(c), __ldg(c + 1), __ldg(c + 2)));  // image.hpp:85-91
                             } else {
-                                iv = __ldcg(F.inten[l - 1] + sp);
+                                iv = __ldcg(L0.inten + sp);
                             }
                             isum += iv;
                         }
                     }
-                    if (masks && __ldcg(F.mask[l - 1] + sp)) masked = 1;
+                    if (masks && __ldcg(L0.mask + sp)) masked = 1;
                 }
             if (images) {
-                F.depth[l][p] = closest;
-                if (F.rgb0) F.inten[l][p] = isum * 0.25f;
+                L1.depth[p] = closest;
+                if (F.rgb0) L1.inten[p] = isum * 0.25f;
             }
-            if (masks) F.mask[l][p] = masked;
+            if (masks) L1.mask[p] = masked;
         }
         grid_barrier(a.grid);
     }
@@ -230,13 +241,14 @@ template <bool kJac, bool kColor, bool kRobust, class Hook, class Pre>
 __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
                            double* scratch, double* blk, double* out, const Hook& hook, const Pre& pre) {
     const FrameView& F = a.F;
-    const Intr K = F.K[level];
+    const LevelInfo& LI = s_lvl[level];
+    const Intr K = LI.K;
     const double min_depth = a.V.min_depth, max_depth = a.V.max_depth;
     double acc[kAccN];
 #pragma unroll
     for (int i = 0; i < kAccN; ++i) acc[i] = 0.0;
-    const float* depth = level == 0 ? F.depth0 : F.depth[level];
-    const uint8_t* mask = use_mask ? F.mask[level] : nullptr;
+    const float* depth = LI.depth;
+    const uint8_t* mask = use_mask ? LI.mask : nullptr;
     unsigned long long* tr = (a.trace && s_trace_pass < kTracePasses) ? a.trace + 8 * s_trace_pass : nullptr;
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
         tr[0] = global_ns();
@@ -268,7 +280,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
                     const uint8_t* c = F.rgb0 + 3 * size_t(p);
                     inten = float(luma(__ldg(c), __ldg(c + 1), __ldg(c + 2)));
                 } else {
-                    inten = __ldcg(F.inten[level] + p);
+                    inten = __ldcg(LI.inten + p);
                 }
             }
             if (kJac && it < a.pxc_steps) pxc_base()[it * kTrackThreads + threadIdx.x] = make_float2(masked ? 0.f : d, inten);
@@ -376,7 +388,7 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
     // at levels 0 / 1 / 2), instead of whole 16x24 tiles on part of the CTAs
     // (B200, frames 5..104: 1519 -> 1581 frames/s).
     {
-        const LevelRange R = s_lvl[level];
+        const LevelInfo& R = s_lvl[level];
         const int per = R.per, end = R.end;
         int p = int(blockIdx.x) * per + int(threadIdx.x);
         int u = R.ubase + int(threadIdx.x), v = R.vbase;  // then stepped: no division per pixel
@@ -423,7 +435,7 @@ __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& 
     const bool color = cw > 0.0 && a.F.rgb0 != nullptr;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         s_passes += 1;  // CTA 0's tally, published once at kernel exit (no global RMW on the pass path)
-        s_pixel_passes += double(a.F.K[level].w) * double(a.F.K[level].h);
+        s_pixel_passes += double(s_lvl[level].K.w) * double(s_lvl[level].K.h);
     }
     const bool robust = kJac && (a.reg.huber_d > 0.0 || a.reg.huber_c > 0.0);
     if (robust) {
@@ -439,8 +451,10 @@ __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& 
 // ------------------------------------------------------------------ Register
 // registration.cpp:211-286. All CTAs run the same state machine on the same
 // reduced vectors; thread 0 of each CTA updates the shared state.
-__device__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask, RegState& st, double* scratch,
-                             double* blk) {
+// Inlined at both call sites: as an out-of-line function its `const
+// TrackArgs&` would force a copy of the kernel parameters to local memory.
+__device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& init, bool use_mask, RegState& st,
+                                             double* scratch, double* blk) {
     const RegParams& R = a.reg;
     const double cw = R.color_weight;
     if (threadIdx.x == 0) {
@@ -1162,14 +1176,21 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
         s_trace_pass = 0;
         s_pxc_tag = 0;
     }
-    if (threadIdx.x < kMaxLevels) {
-        const int l = threadIdx.x, npx = a.F.K[l].w * a.F.K[l].h, per = (npx + int(gridDim.x) - 1) / int(gridDim.x);
-        const int start = min(npx, int(blockIdx.x) * per);
-        s_lvl[l].per = per;
-        s_lvl[l].end = min(npx, start + per);
-        s_lvl[l].vbase = a.F.K[l].w > 0 ? start / a.F.K[l].w : 0;
-        s_lvl[l].ubase = start - s_lvl[l].vbase * a.F.K[l].w;
-    }
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l)  // static indices into the kernel parameters
+        if (threadIdx.x == l) {
+            LevelInfo& L = s_lvl[l];
+            L.K = a.F.K[l];
+            L.depth = l == 0 ? const_cast<float*>(a.F.depth0) : a.F.depth[l];
+            L.inten = a.F.inten[l];
+            L.mask = a.F.mask[l];
+            const int npx = L.K.w * L.K.h, per = (npx + int(gridDim.x) - 1) / int(gridDim.x);
+            const int start = min(npx, int(blockIdx.x) * per);
+            L.per = per;
+            L.end = min(npx, start + per);
+            L.vbase = L.K.w > 0 ? start / L.K.w : 0;
+            L.ubase = start - L.vbase * L.K.w;
+        }
     for (int i = threadIdx.x; i < 768; i += blockDim.x) {
         const double w = i < 256 ? 0.2126 : (i < 512 ? 0.7152 : 0.0722);  // image.hpp:80-83
         s_luma_lut[i] = w * double(i & 255);
