@@ -481,16 +481,27 @@ __device__ __forceinline__ double voxel_luma_lut(uint2 v, const double* lut) {
     return (lut[(v.y >> 8) & 0xFFu] + lut[256 + ((v.y >> 16) & 0xFFu)]) + lut[512 + (v.y >> 24)];
 }
 
-// CellOf (tsdf_volume.cpp:279-283). kExact divides like the reference; the
+// a / b correctly rounded from rb = RN(1 / b): q = RN(a rb) is within an ulp,
+// the FMA residual is exact, and one correction step rounds correctly
+// (Markstein); no IEEE division sequence on the walk's setup chain. A zero
+// quotient comes out +0 where a / b gives -0; the walk only floors and
+// subtracts these values, where the two zeros agree.
+__device__ __forceinline__ double div_rn(double a, double b, double rb) {
+    const double q = a * rb;
+    return __fma_rn(__fma_rn(-q, b, a), rb, q);
+}
+
+// CellOf (tsdf_volume.cpp:279-283). kExact divides like the reference (the
+// quotient correctly rounded through the reciprocal, div_rn); the
 // tracking passes multiply by the precomputed reciprocal (last-bit
 // differences only; parity there is held on the normal equations and poses).
 template <bool kExact>
 __device__ __forceinline__ void cell_of(double px, double py, double pz, const VolumeView& V, int base[3], double f[3]) {
     double g[3];
     if (kExact) {
-        g[0] = px / V.voxel_size - 0.5;
-        g[1] = py / V.voxel_size - 0.5;
-        g[2] = pz / V.voxel_size - 0.5;
+        g[0] = div_rn(px, V.voxel_size, V.inv_voxel_size) - 0.5;
+        g[1] = div_rn(py, V.voxel_size, V.inv_voxel_size) - 0.5;
+        g[2] = div_rn(pz, V.voxel_size, V.inv_voxel_size) - 0.5;
     } else {
         g[0] = px * V.inv_voxel_size - 0.5;
         g[1] = py * V.inv_voxel_size - 0.5;

@@ -291,8 +291,8 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
             if (!(masked && !write_res)) {
                 const double dd = double(d);
                 // Backproject (geometry.hpp:41-43); Jacobian passes use reciprocals
-                const double x0 = kJac ? (double(u) - K.cx) * K.ifx * dd : (double(u) - K.cx) / K.fx * dd;
-                const double x1 = kJac ? (double(v) - K.cy) * K.ify * dd : (double(v) - K.cy) / K.fy * dd;
+                const double x0 = kJac ? (double(u) - K.cx) * K.ifx * dd : div_rn(double(u) - K.cx, K.fx, K.ifx) * dd;
+                const double x1 = kJac ? (double(v) - K.cy) * K.ify * dd : div_rn(double(v) - K.cy, K.fy, K.ify) * dd;
                 double y[3];
                 pose_apply(P, x0, x1, dd, y);
                 CellSample cs;

@@ -11,16 +11,6 @@ namespace rfb {
 // tsdf_volume.hpp:149-185), one thread per pixel, all cells inserted with
 // atomicCAS. The set of inserted keys, and so the occupied-slot set of the
 // linear-probing table, is independent of thread order.
-// a / b correctly rounded from rb = RN(1 / b): q = RN(a rb) is within an ulp,
-// the FMA residual is exact, and one correction step rounds correctly
-// (Markstein); no IEEE division sequence on the walk's setup chain. A zero
-// quotient comes out +0 where a / b gives -0; the walk only floors and
-// subtracts these values, where the two zeros agree.
-__device__ __forceinline__ double div_rn(double a, double b, double rb) {
-    const double q = a * rb;
-    return __fma_rn(__fma_rn(-q, b, a), rb, q);
-}
-
 // The ray segment of pixel p (AllocateForFrame, tsdf_volume.cpp:93-113):
 // [max(d - tau, 1e-4), d + tau] along the pixel's ray, walked through the
 // block grid (WalkGridSegment, tsdf_volume.hpp:149-185); `visit(cell)` for
