@@ -192,6 +192,41 @@ __device__ __forceinline__ void cull_brick(const CullArgs& a, const Pose& W, dou
     if (integrate && !ft.outside(a.V.max_depth + a.V.truncation)) flags |= kFlagIntegrate;
 }
 
+// The same test with the brick's 8 corners on 8 consecutive lanes (corner k
+// on lane k of the group): each lane projects its corner, the group combines
+// the flags and extremes with shuffles (min / max / or are exact and order
+// free), so a brick costs one corner's chain instead of eight. Every lane of
+// the group returns the brick's flags.
+__device__ __forceinline__ uint32_t cull_brick_lanes(const CullArgs& a, const Pose& W, double ext, int4 c, int k,
+                                                     bool carve, bool integrate) {
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    double cc[3];
+    pose_apply(W, (double(c.x) + double(k & 1)) * ext, (double(c.y) + double((k >> 1) & 1)) * ext,
+               (double(c.z) + double(k >> 2)) * ext, cc);
+    bool behind = cc[2] <= 1e-9, front = cc[2] > 1e-9;
+    double min_z = fmin(inf, cc[2]), min_u = inf, max_u = -inf, min_v = inf, max_v = -inf;
+    if (front) {
+        min_u = max_u = a.K.fx * cc[0] / cc[2] + a.K.cx;  // (as frustum_test)
+        min_v = max_v = a.K.fy * cc[1] / cc[2] + a.K.cy;
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        behind = __shfl_xor_sync(0xffffffffu, behind, o) || behind;
+        front = __shfl_xor_sync(0xffffffffu, front, o) || front;
+        min_z = fmin(min_z, __shfl_xor_sync(0xffffffffu, min_z, o));
+        min_u = fmin(min_u, __shfl_xor_sync(0xffffffffu, min_u, o));
+        max_u = fmax(max_u, __shfl_xor_sync(0xffffffffu, max_u, o));
+        min_v = fmin(min_v, __shfl_xor_sync(0xffffffffu, min_v, o));
+        max_v = fmax(max_v, __shfl_xor_sync(0xffffffffu, max_v, o));
+    }
+    const FrustumTest ft{min_z, behind ? !front
+                                       : (max_u < -0.5 || min_u > a.K.w - 0.5 || max_v < -0.5 || min_v > a.K.h - 0.5)};
+    uint32_t flags = 0;
+    if (carve && !ft.outside(a.V.carve_clip)) flags |= kFlagCarve;
+    if (integrate && !ft.outside(a.V.max_depth + a.V.truncation)) flags |= kFlagIntegrate;
+    return flags;
+}
+
 // Appends the brick of every lane with flags to the visible list (one atomic per warp).
 __device__ __forceinline__ void append_visible(const CullArgs& a, uint32_t b, uint32_t flags) {
     const unsigned vote = __ballot_sync(0xffffffffu, flags != 0);
@@ -237,12 +272,16 @@ __global__ void k_cull(CullArgs a) {
             }
         });
     const uint32_t stride = gridDim.x * blockDim.x;
-    // warp-uniform trip count so the whole warp can aggregate its appends
-    for (uint32_t b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b0 < old_n; b0 += stride) {
-        const uint32_t b = b0 + (threadIdx.x & 31u);
-        uint32_t flags = 0;
-        if (b < old_n) cull_brick(a, W, ext, a.V.coords[b], a.do_carve && b < before, integrate, flags);
-        append_visible(a, b, flags);
+    // 8 lanes per brick (one per corner), warp-uniform trip count so the whole
+    // warp can aggregate its appends (the group's corner-0 lane appends)
+    const uint64_t items = uint64_t(old_n) * 8u;
+    for (uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); i0 < items; i0 += stride) {
+        const uint64_t i = i0 + (threadIdx.x & 31u);
+        const uint32_t b = uint32_t(i >> 3);
+        const bool live = i < items;
+        const uint32_t fl = cull_brick_lanes(a, W, ext, a.V.coords[live ? b : 0u], int(i & 7u),
+                                             a.do_carve && b < before, integrate);
+        append_visible(a, b, (live && (i & 7u) == 0) ? fl : 0u);
     }
 }
 
