@@ -50,8 +50,17 @@ struct LevelInfo {
 __shared__ LevelInfo s_lvl[kMaxLevels];
 
 struct RegState {
-    Pose pose, cand;
-    double lambda, dnorm;
+    // Three pose slots, by index (an accepted or pre-solved candidate changes an
+    // index instead of copying 12 doubles on the LM thread's critical path):
+    // P[ip] the current pose, P[ic] the candidate of the pass in flight (dn[ic]
+    // its squared step), P[3 - ip - ic] the reject-path pre-solve.
+    Pose P[3];
+    double dn[3];
+    int ip, ic;
+    __device__ Pose& pose() { return P[ip]; }
+    __device__ const Pose& pose() const { return P[ip]; }
+    __device__ Pose& cand() { return P[ic]; }
+    double lambda;
     double buf[2][kAccN];  // normal equations at the current pose / at the candidate
     int ci;                // buf[ci]: current, buf[ci ^ 1]: trial; swapped on an accepted step (no copy)
     __device__ double* cur() { return buf[ci]; }
@@ -60,11 +69,9 @@ struct RegState {
     double cur_err, tol, lam_acc, lam_rej;
     int small_step;
     int total, converged, lost, go, brk, level_it;
-    // The next candidate if the trial in flight is rejected: it depends only
-    // on the current normal equations and the raised damping, so it is solved
-    // during the trial's pass (on a thread with slack) instead of after it.
-    Pose cand_rej;
-    double dnorm_rej;
+    // The next candidate if the trial in flight is rejected (in the free slot):
+    // it depends only on the current normal equations and the raised damping,
+    // so it is solved during the trial's pass (on a thread with slack).
     int rej_ok;
 };
 
@@ -458,7 +465,9 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
     const RegParams& R = a.reg;
     const double cw = R.color_weight;
     if (threadIdx.x == 0) {
-        st.pose = init;
+        st.P[0] = init;
+        st.ip = 0;
+        st.ic = 1;
         st.total = 0;
         st.converged = 0;
         st.lost = 0;
@@ -468,7 +477,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
     for (int l = R.levels - 1; l >= 0; --l) {
         const long long mv = (long long)(max(R.min_valid, 1)) >> (2 * l);
         const double min_valid = double(mv > 16 ? mv : 16);
-        pass<true>(a, l, st.pose, use_mask, false, cw, scratch, blk, st.cur());
+        pass<true>(a, l, st.pose(), use_mask, false, cw, scratch, blk, st.cur());
         if (st.cur()[29] < min_valid) {
             if (threadIdx.x == 0) st.lost = 1;
             __syncthreads();
@@ -489,13 +498,17 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
             if (threadIdx.x == kLmThread) {
                 double lambda = st.lambda;
                 int brk = st.brk, level_it = st.level_it, total = st.total, converged = st.converged, ci = st.ci;
+                const int ip0 = st.ip, ic0 = st.ic;
+                int ip = ip0, ic = ic0;  // the solve below writes slot ic
                 const double* tr = st.buf[ci ^ 1];
+                bool rejected = false;
                 if (judge) {
                     const double cur_err = st.cur_err;
                     const double trial_err = tr[27] + cw * tr[28];
                     if (tr[29] >= min_valid && trial_err < cur_err) {
                         const double decrease = cur_err - trial_err;
-                        st.pose = st.cand;
+                        ip = ic0;  // the candidate becomes the pose; its old slot takes the next candidate
+                        ic = ip0;
                         ci ^= 1;
                         lambda = st.lam_acc;
                         if (st.small_step || decrease < st.tol) {
@@ -503,6 +516,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                             brk = 1;
                         }
                     } else {
+                        rejected = true;
                         lambda = st.lam_rej;
                         if (lambda >= 1e12) {
                             converged = 1;
@@ -511,14 +525,11 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                     }
                 }
                 int go = 0;
-                bool rejected = false;
-                if (judge) rejected = !(tr[29] >= min_valid && tr[27] + cw * tr[28] < st.cur_err);
                 if (rejected && !brk && level_it < R.max_iterations && st.rej_ok) {
                     // the solve this loop would run now (same buffer, same damping): done during the pass
                     ++level_it;
                     ++total;
-                    st.cand = st.cand_rej;
-                    st.dnorm = st.dnorm_rej;
+                    ic = 3 - ip0 - ic0;
                     go = 1;
                 }
                 if (judge && a.trace && blockIdx.x == 0 && s_trace_pass > 0 && s_trace_pass <= kTracePasses)
@@ -526,7 +537,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                 while (!go && !brk && level_it < R.max_iterations) {
                     ++level_it;
                     ++total;
-                    const Pose P0 = st.pose;
+                    const Pose P0 = st.P[ip];
                     double delta[6];  // in registers: ExpMap and the norm read it straight from the solve
                     const bool solved = lm_solve(st.buf[ci], lambda, delta);
                     if (!solved) {
@@ -535,14 +546,16 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                     }
                     Pose e;
                     expmap(delta, e);
-                    st.cand = pose_mul(e, P0);
+                    st.P[ic] = pose_mul(e, P0);
                     double dn = 0.0;
 #pragma unroll
                     for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
-                    st.dnorm = dn;  // squared; the sqrt is taken off the critical path below
+                    st.dn[ic] = dn;  // squared; the sqrt is taken off the critical path below
                     go = 1;
                     break;
                 }
+                st.ip = ip;
+                st.ic = ic;
                 st.lambda = lambda;
                 st.brk = brk;
                 st.level_it = level_it;
@@ -558,12 +571,12 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
             if (!st.go) break;
             // everything of the judge but the trial's error, on thread 0 while the
             // all-reduce's arrivals propagate (off every critical path)
-            pass<true>(a, l, st.cand, use_mask, false, cw, scratch, blk, st.trial(), [&] {
+            pass<true>(a, l, st.cand(), use_mask, false, cw, scratch, blk, st.trial(), [&] {
                 st.cur_err = st.cur()[27] + cw * st.cur()[28];
                 st.tol = kRelDecreaseTol * st.cur_err;
                 st.lam_acc = fmax(st.lambda / R.lambda_down, 1e-12);
                 st.lam_rej = fmin(st.lambda * R.lambda_up, 1e12);
-                st.small_step = sqrt(st.dnorm) < R.eps;
+                st.small_step = sqrt(st.dn[st.ic]) < R.eps;
             }, [&] {
                 // registration.cpp:265-271 then :240-249 on rejection: lambda
                 // raised (a level that reaches 1e12 converges instead)
@@ -573,11 +586,12 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                     if (lm_solve(st.cur(), lam, delta)) {
                         Pose e;
                         expmap(delta, e);
-                        st.cand_rej = pose_mul(e, st.pose);
+                        const int fr = 3 - st.ip - st.ic;  // the free slot
+                        st.P[fr] = pose_mul(e, st.pose());
                         double dn = 0.0;
 #pragma unroll
                         for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
-                        st.dnorm_rej = dn;
+                        st.dn[fr] = dn;
                         st.rej_ok = 1;
                     }
                 }
@@ -587,7 +601,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
         __syncthreads();
     }
     // Full-resolution residual image at the final pose, mask ignored (:282-284).
-    pass<false>(a, 0, st.pose, false, true, 0.0, scratch, blk, st.trial());
+    pass<false>(a, 0, st.pose(), false, true, 0.0, scratch, blk, st.trial());
 }
 
 // ------------------------------------------------------------------ mask
@@ -1025,8 +1039,8 @@ __device__ double build_mask(const TrackArgs& a, int stages, double* scratch, do
 
 __device__ void write_out(const TrackArgs& a, const RegState& st) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        for (int i = 0; i < 9; ++i) a.out->pose[i] = st.pose.R[i];
-        for (int i = 0; i < 3; ++i) a.out->pose[9 + i] = st.pose.t[i];
+        for (int i = 0; i < 9; ++i) a.out->pose[i] = st.pose().R[i];
+        for (int i = 0; i < 3; ++i) a.out->pose[9 + i] = st.pose().t[i];
     }
 }
 
@@ -1125,7 +1139,7 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
         if (a.dynamics) {
             masked = build_mask(a, 15, scratch, blk, red, &rounds);
             if (masked > 0.0) {
-                Pose p1 = st.pose;
+                Pose p1 = st.pose();
                 build_pyramid(a, false, true);
                 __syncthreads();
                 run_register(a, p1, true, st, scratch, blk);
@@ -1147,8 +1161,8 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
         o->valid = st.lost ? 0ull : (unsigned long long)st.cur()[29];
         o->final_error = st.lost ? 0.0 : st.cur()[27] + a.reg.color_weight * st.cur()[28];
         if (!st.lost) {  // hold the previous pose on loss (pipeline.cpp:117-122)
-            for (int i = 0; i < 9; ++i) a.pose_state[i] = st.pose.R[i];
-            for (int i = 0; i < 3; ++i) a.pose_state[9 + i] = st.pose.t[i];
+            for (int i = 0; i < 9; ++i) a.pose_state[i] = st.pose().R[i];
+            for (int i = 0; i < 3; ++i) a.pose_state[9 + i] = st.pose().t[i];
         }
         for (int i = 0; i < 12; ++i) o->pose[i] = a.pose_state[i];
         if (a.vol_counters) {  // frame bookkeeping for the allocate / cull / fuse launches that follow
