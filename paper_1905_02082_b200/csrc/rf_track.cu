@@ -904,10 +904,11 @@ __device__ int floodfill(const TrackArgs& a, uint8_t* m, const uint32_t* planes,
             g &= valid;
             for (int it = 0;; ++it) {
                 const uint32_t old = g;
-                g = fill_xplus(g, P[0]);
-                g = fill_xminus(g, P[1]);
-                g = fill_yplus(g, P[2], lane);
-                g = fill_yminus(g, P[3], lane);
+                // Along one axis the two directions are independent (a path that
+                // turns back within a row or column only revisits covered pixels),
+                // so each pair runs as two parallel chains on the same input.
+                g = fill_xplus(g, P[0]) | fill_xminus(g, P[1]);
+                g = fill_yplus(g, P[2], lane) | fill_yminus(g, P[3], lane);
                 if (conn == 8) {
                     const uint32_t gu0 = __shfl_up_sync(0xffffffffu, g, 1);
                     const uint32_t gd0 = __shfl_down_sync(0xffffffffu, g, 1);
