@@ -517,3 +517,28 @@ def test_mask_stages_bitexact_ragged(h, w):
     for r in (1, 3):
         assert (O.erode(m, r) == G.erode(m, r)).all()
         assert (O.dilate(m, r) == G.dilate(m, r)).all()
+
+
+def test_mask_floodfill_atomic_worklist_path():
+    """A frame whose floodfill tile flags do not fit in the tracking kernel's
+    dynamic shared memory (8192 x 4608: 36864 tiles) takes the atomic
+    worklist path of the floodfill (ff_flag_mode false); it must give the
+    oracle's mask bit for bit like the flag path does at camera sizes."""
+    rng = np.random.default_rng(21)
+    h, w = 4608, 8192
+    yy, xx = np.mgrid[0:h, 0:w]
+    depth = np.zeros((h, w), np.float32)
+    # depth-continuous bands the growth can run along, with gaps it cannot cross
+    band = ((yy // 64) % 3) != 2
+    depth[band] = (1.0 + 0.0005 * (xx[band] % 512) / 512.0).astype(np.float32)
+    sq = np.zeros((h, w), np.float32)
+    valid = band.astype(np.uint8)
+    for _ in range(60):  # eroded-surviving seed blocks scattered over the bands
+        cy, cx = int(rng.integers(0, h - 8)), int(rng.integers(0, w - 8))
+        sq[cy:cy + 8, cx:cx + 8] = 0.05
+    cfg = O.mask_cfg()
+    gc = G.mask_config()
+    om = O.build_mask(sq, valid, depth, cfg)
+    gm = G.build_mask(sq, valid, depth, gc)
+    assert om.sum() > 100000
+    assert (om == gm).all()
