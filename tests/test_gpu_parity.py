@@ -542,3 +542,20 @@ def test_mask_floodfill_atomic_worklist_path():
     gm = G.build_mask(sq, valid, depth, gc)
     assert om.sum() > 100000
     assert (om == gm).all()
+
+
+def test_mask_wide_morphology_path():
+    """Erosion / dilation radii beyond the tiled path's halo (kMorphMaxR = 8)
+    run as separable passes through global memory; bit-exact as well."""
+    rng = np.random.default_rng(8)
+    h, w = 120, 200
+    depth = (1.0 + 0.5 * (rng.random((h, w)) < 0.2) + 0.002 * rng.standard_normal((h, w))).astype(np.float32)
+    sq = (rng.random((h, w)) * 0.004).astype(np.float32)
+    sq[20:90, 30:150] = 0.02  # a large region that survives a wide erosion
+    valid = (rng.random((h, w)) < 0.95).astype(np.uint8)
+    valid[20:90, 30:150] = 1
+    for er, dr, conn in ((9, 2, 4), (2, 11, 8), (10, 12, 8)):
+        oc = O.mask_cfg(erode_radius=er, dilate_radius=dr, connectivity=conn)
+        gc = G.mask_config(erode_radius=er, dilate_radius=dr, connectivity=conn)
+        om, gm = O.build_mask(sq, valid, depth, oc), G.build_mask(sq, valid, depth, gc)
+        assert om.sum() > 0 and (om == gm).all(), (er, dr, conn)
