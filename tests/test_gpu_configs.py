@@ -100,3 +100,23 @@ def test_c4_1280x720_mesh_export():
     om = op.volume().extract_mesh(2)
     assert len(om[2]) > 50000
     assert_meshes_identical(om, gv.extract_mesh(2))
+
+
+def test_1920x1080_pixel_cache_overflow():
+    """At 1920x1080 a thread meets 37 pixel steps at level 0, more than the
+    pixel cache holds (32 steps in its 96 KB): the steps beyond it reload their
+    inputs every pass. Poses and counts still match the oracle frame by frame."""
+    s = O.Scene(scenes.room_script(with_mover=True, width=1920, height=1080, frames=5))
+    op = O.Pipeline(O.pipe_cfg(refine=False, reg=O.reg_cfg(threads=16), threads=16))
+    gp = G.Pipeline(G.pipeline_config(refine=False))
+    worst, mism = 0.0, {k: 0 for k in COUNTS}
+    for i in range(len(s)):
+        f = s.render(i)
+        so, po = op.process_frame(f["depth"], f["rgb"], s.k, f["timestamp"])
+        sg, pg = gp.process_frame(frame(s.k, f["depth"], f["rgb"], f["timestamp"]))
+        worst = max(worst, *pose_error(po, pg))
+        for k in COUNTS:
+            mism[k] += int(so[k] != sg[k])
+    assert worst <= 1e-4, worst
+    assert mism == {k: 0 for k in COUNTS}, mism
+    assert all(v == 0 for v in gp.volume().check().values())
