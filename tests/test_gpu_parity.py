@@ -238,6 +238,29 @@ def test_register_matches_oracle(corner, cw):
     assert et < 5e-3 and er < 0.5 * math.pi / 180
 
 
+@pytest.mark.parametrize("levels", [1, 2, 4, 5])
+def test_register_pyramid_depths(corner, levels):
+    """Register with other pyramid depths than the default 3 (the per-level
+    ranges, intrinsics and images the kernel stages per level). Five levels of
+    the 64x48 image leave a 4x3 top level: too few residuals, TrackingLost on
+    both sides."""
+    c = corner
+    k = c["s"].k
+    if levels == 5:
+        with pytest.raises(O.TrackingLost):
+            c["ov"].register(c["r"]["depth"], c["r"]["rgb"], k, c["init"], None, O.reg_cfg(pyramid_levels=5))
+        with pytest.raises(G.TrackingLostError):
+            c["gv"].register(frame(k, c["r"]["depth"], c["r"]["rgb"]), c["init"], None,
+                             G.registration_config(pyramid_levels=5))
+        return
+    o = c["ov"].register(c["r"]["depth"], c["r"]["rgb"], k, c["init"], None, O.reg_cfg(pyramid_levels=levels))
+    g = c["gv"].register(frame(k, c["r"]["depth"], c["r"]["rgb"]), c["init"], None,
+                         G.registration_config(pyramid_levels=levels))
+    dt, dr = pose_error(o["pose"], g["pose"])
+    assert dt <= POSE_TOL_T and dr <= POSE_TOL_R
+    assert g["iterations"] == o["iterations"] and g["valid_residuals"] == o["valid_residuals"]
+
+
 def test_register_with_mask_ignores_corruption(corner):  # test_registration.cpp:220-262
     c = corner
     k = c["s"].k
