@@ -217,7 +217,8 @@ rf_status rf_register(const rf_volume* v, const rf_frame* f, const double initia
 
 /* ---- dynamics mask (dynamics_mask.hpp:21-41) ----------------------------
  * stages: bit0 ThresholdResiduals, bit1 Erode, bit2 FloodfillDepth, bit3 Dilate
- * (15 = BuildMask). With bit0 clear, `res_valid` is read as the input mask. */
+ * (15 = BuildMask). With bit0 clear, `res_valid` is read as the input mask;
+ * `res_sq` may be NULL without bit0, `depth` without bit2. */
 rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const float* depth, int32_t width,
                          int32_t height, const rf_mask_config* cfg, int32_t stages, int device, uint8_t* out,
                          uint64_t* masked);

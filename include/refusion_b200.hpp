@@ -666,6 +666,20 @@ inline PixelMask BuildMask(const ResidualImage& r, const DepthImage& depth, cons
     return detail::MaskStages(r.squared.data(), r.valid.data(), depth.data(), depth.width(), depth.height(), config,
                               15);
 }
+// ResidualHistogram (dynamics_mask.hpp:38-41): counts of the valid squared
+// residuals in `bins` equal bins over [0, max_value], values beyond it in the
+// last bin. A diagnostic over a host image, off the per-frame path: computed here.
+inline std::vector<std::size_t> ResidualHistogram(const ResidualImage& r, int bins, double max_value) {
+    if (bins < 1 || !(max_value > 0)) throw std::invalid_argument("bad histogram shape");
+    std::vector<std::size_t> hist(static_cast<std::size_t>(bins), 0);
+    const std::size_t n = std::size_t(r.squared.width()) * r.squared.height();
+    for (std::size_t i = 0; i < n; ++i) {
+        if (!r.valid.data()[i]) continue;
+        const int b = static_cast<int>(double(r.squared.data()[i]) / max_value * bins);
+        ++hist[static_cast<std::size_t>(b < bins - 1 ? b : bins - 1)];
+    }
+    return hist;
+}
 
 // ---------------------------------------------------------------- raycast / mesh
 // Ray-march of RenderVirtualDepth (depth_refinement.cpp:32-79) over `volume`.

@@ -31,6 +31,9 @@ def build() -> str | None:
     """make ref (only where /root/reference exists; the GPU box uses the prebuilt library)."""
     if buildable():
         subprocess.check_call(["make", "-s", "-j8", "-C", _HERE, "ref"])
+        # the reference's own test sources against the B200 host layer (needs the CUDA library)
+        if os.path.exists(os.path.join(os.path.dirname(_HERE), "paper_1905_02082_b200", "librefusion_b200.so")):
+            subprocess.check_call(["make", "-s", "-j8", "-C", _HERE, "refsuite"])
     return LIB_PATH if os.path.exists(LIB_PATH) else None
 
 

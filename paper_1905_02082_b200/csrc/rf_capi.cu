@@ -1256,8 +1256,9 @@ rf_status rf_register(const rf_volume* cv, const rf_frame* f, const double init[
 rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const float* depth, int32_t w, int32_t h,
                          const rf_mask_config* cfg, int32_t stages, int device, uint8_t* out, uint64_t* masked) {
     return guard([&] {
-        require(res_valid && depth && cfg && out && w > 0 && h > 0, RF_INVALID_ARGUMENT, "null argument");
+        require(res_valid && cfg && out && w > 0 && h > 0, RF_INVALID_ARGUMENT, "null argument");
         require(!(stages & 1) || res_sq, RF_INVALID_ARGUMENT, "threshold stage needs residuals");
+        require(!(stages & 4) || depth, RF_INVALID_ARGUMENT, "floodfill stage needs the depth image");
         require(cfg->free_space >= 0, RF_INVALID_ARGUMENT, "free_space must be >= 0");
         require(cfg->connectivity == 4 || cfg->connectivity == 8, RF_INVALID_ARGUMENT,
                 "connectivity must be 4 or 8");
@@ -1267,7 +1268,7 @@ rf_status rf_mask_stages(const float* res_sq, const uint8_t* res_valid, const fl
         const size_t n = size_t(w) * h;
         if (res_sq) CK(cudaMemcpyAsync(ws.res_sq.p, res_sq, n * 4, cudaMemcpyHostToDevice, ws.stream));
         CK(cudaMemcpyAsync(ws.res_valid.p, res_valid, n, cudaMemcpyHostToDevice, ws.stream));
-        CK(cudaMemcpyAsync(ws.depth.p, depth, n * 4, cudaMemcpyHostToDevice, ws.stream));
+        if (depth) CK(cudaMemcpyAsync(ws.depth.p, depth, n * 4, cudaMemcpyHostToDevice, ws.stream));
         if (!(stages & 1))
             CK(cudaMemcpyAsync(ws.mwork.p, res_valid, n, cudaMemcpyHostToDevice, ws.stream));
         TrackArgs a{};
