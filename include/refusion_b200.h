@@ -166,6 +166,7 @@ rf_status rf_volume_create(const rf_volume_config* cfg, int device, rf_volume** 
 void rf_volume_destroy(rf_volume* v);
 rf_status rf_volume_num_blocks(const rf_volume* v, uint64_t* out);                         /* num_blocks() */
 rf_status rf_volume_hash_capacity(const rf_volume* v, uint64_t* out);
+rf_status rf_volume_get_config(const rf_volume* v, rf_volume_config* out);                 /* config() */
 rf_status rf_volume_allocate_blocks(rf_volume* v, const int32_t* coords, uint64_t n,
                                     int32_t* created);                                     /* AllocateBlock (batched) */
 rf_status rf_volume_allocate_for_frame(rf_volume* v, const rf_frame* f, const double pose[12],

@@ -7,7 +7,10 @@
 // meaning and exceptions, so a caller of the reference switches by changing
 // the include and the namespace (`namespace tsdfslam = tsdfslam_b200;`).
 // Eigen is not a dependency: vectors are std::array<double, 3>, rotations
-// row-major std::array<double, 9>.
+// row-major std::array<double, 9>. With REFUSION_B200_EIGEN defined (and
+// Eigen on the include path) the vector, rotation and pose types are the
+// reference's Eigen types instead, so the reference's own sources (its test
+// suites) compile unchanged against this layer (tests/refsuite).
 //
 // Everything computes on the GPU: the methods marshal host images into an
 // rf_frame and call one C entry point. Header-only; link with
@@ -29,6 +32,10 @@
 #include <vector>
 
 #include "refusion_b200.h"
+#ifdef REFUSION_B200_EIGEN
+#include <Eigen/Core>
+#include <Eigen/Geometry>
+#endif
 
 namespace tsdfslam_b200 {
 
@@ -61,9 +68,17 @@ inline void Check(rf_status s) {
     }
 }
 
+#ifdef REFUSION_B200_EIGEN
+using Vec3 = Eigen::Vector3d;
+using Vec3i = Eigen::Vector3i;
+using Vec3f = Eigen::Vector3f;
+using Mat3 = Eigen::Matrix3d;
+#else
 using Vec3 = std::array<double, 3>;
 using Vec3i = std::array<int, 3>;
 using Vec3f = std::array<float, 3>;
+using Mat3 = std::array<double, 9>;  // row-major
+#endif
 
 // ---------------------------------------------------------------- geometry (geometry.hpp:11-108)
 struct CameraIntrinsics {
@@ -93,18 +108,27 @@ struct CameraIntrinsics {
 class Pose {
   public:
     Pose() : m_{1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0} {}
-    Pose(const std::array<double, 9>& rotation, const Vec3& translation) {
-        std::memcpy(m_.data(), rotation.data(), 9 * sizeof(double));
-        std::memcpy(m_.data() + 9, translation.data(), 3 * sizeof(double));
+    Pose(const Mat3& rotation, const Vec3& translation) {
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) m_[3 * i + j] = M(rotation, i, j);
+        for (int i = 0; i < 3; ++i) m_[9 + i] = translation[i];
     }
+#ifdef REFUSION_B200_EIGEN
+    Pose(const Eigen::Quaterniond& q, const Vec3& translation) : Pose(Mat3(q.normalized().toRotationMatrix()), translation) {}
+#endif
     static Pose Identity() { return Pose(); }
     static Pose FromArray(const double p[12]) {
         Pose r;
         std::memcpy(r.m_.data(), p, 12 * sizeof(double));
         return r;
     }
-    std::array<double, 9> rotation() const { return {m_[0], m_[1], m_[2], m_[3], m_[4], m_[5], m_[6], m_[7], m_[8]}; }
-    Vec3 translation() const { return {m_[9], m_[10], m_[11]}; }
+    Mat3 rotation() const {
+        Mat3 r;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) M(r, i, j) = m_[3 * i + j];
+        return r;
+    }
+    Vec3 translation() const { return Vec3{m_[9], m_[10], m_[11]}; }
     const double* data() const { return m_.data(); }
     double* data() { return m_.data(); }
 
@@ -132,8 +156,65 @@ class Pose {
     }
 
   private:
+#ifdef REFUSION_B200_EIGEN
+    static double M(const Mat3& r, int i, int j) { return r(i, j); }
+    static double& M(Mat3& r, int i, int j) { return r(i, j); }
+#else
+    static double M(const Mat3& r, int i, int j) { return r[3 * i + j]; }
+    static double& M(Mat3& r, int i, int j) { return r[3 * i + j]; }
+#endif
     std::array<double, 12> m_;
 };
+
+// Backproject / Project (geometry.hpp:41-48): host-side camera model helpers.
+inline Vec3 Backproject(double u, double v, double depth, const CameraIntrinsics& k) {
+    return Vec3{(u - k.cx) / k.fx * depth, (v - k.cy) / k.fy * depth, depth};
+}
+#ifdef REFUSION_B200_EIGEN
+using Vec2 = Eigen::Vector2d;
+#else
+using Vec2 = std::array<double, 2>;
+#endif
+inline Vec2 Project(const Vec3& x, const CameraIntrinsics& k) {
+    return Vec2{k.fx * x[0] / x[2] + k.cx, k.fy * x[1] / x[2] + k.cy};
+}
+
+// FloorDiv (tsdf_volume.hpp:136-140): integer division rounding toward -inf.
+inline int FloorDiv(int a, int b) {
+    const int q = a / b;
+    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+// WalkGridSegment (tsdf_volume.hpp:147-185): fn(cell) for every cell of size
+// cell_extent the segment [a, b] passes through, in traversal order -- the
+// host twin of the walk k_alloc runs per pixel (same floors, crossing times
+// and tie order), for callers that enumerate cells themselves.
+template <typename Fn>
+void WalkGridSegment(const Vec3& a, const Vec3& b, double cell_extent, Fn&& fn) {
+    const double inf = HUGE_VAL;
+    double p0[3], p1[3], tmax[3], tdel[3];
+    int cell[3], end[3], step[3];
+    for (int i = 0; i < 3; ++i) {
+        p0[i] = a[i] / cell_extent;
+        p1[i] = b[i] / cell_extent;
+        const double d = p1[i] - p0[i];
+        cell[i] = int(std::floor(p0[i]));
+        end[i] = int(std::floor(p1[i]));
+        step[i] = d > 0 ? 1 : (d < 0 ? -1 : 0);
+        tmax[i] = d > 0 ? (std::floor(p0[i]) + 1.0 - p0[i]) / d : (d < 0 ? (p0[i] - std::floor(p0[i])) / -d : inf);
+        tdel[i] = d > 0 ? 1.0 / d : (d < 0 ? 1.0 / -d : inf);
+    }
+    auto visit = [&] { fn(Vec3i{cell[0], cell[1], cell[2]}); };
+    visit();
+    const int max_steps = std::abs(end[0] - cell[0]) + std::abs(end[1] - cell[1]) + std::abs(end[2] - cell[2]) + 3;
+    for (int n = 0; n < max_steps && (cell[0] != end[0] || cell[1] != end[1] || cell[2] != end[2]); ++n) {
+        const int ax = tmax[2] < (tmax[1] < tmax[0] ? tmax[1] : tmax[0]) ? 2 : (tmax[1] < tmax[0] ? 1 : 0);
+        if (tmax[ax] > 1.0) break;
+        tmax[ax] += tdel[ax];
+        cell[ax] += step[ax];
+        visit();
+    }
+}
 
 // ---------------------------------------------------------------- images (image.hpp:13-103)
 template <typename T>
@@ -442,8 +523,18 @@ class TsdfVolume {
         std::uint64_t generation = 0;
     };
     TsdfVolume(rf_volume* h, bool owned) : h_(h), owned_(owned) {
-        // Config travels with the handle only through Save/Load; callers of
-        // Borrow/Load that need it use the pipeline's config.
+        rf_volume_config c{};
+        Check(rf_volume_get_config(h_, &c));  // a loaded or borrowed volume reports its own config
+        config_.voxel_size = c.voxel_size;
+        config_.truncation = c.truncation;
+        config_.block_side = c.block_side;
+        config_.max_weight = c.max_weight;
+        config_.carve_weight = c.carve_weight;
+        config_.min_depth = c.min_depth;
+        config_.max_depth = c.max_depth;
+        config_.carve_clip = c.carve_clip;
+        config_.max_blocks = c.max_blocks;
+        config_.hash_capacity = c.hash_capacity;
     }
     static int FloorDiv8(int a) { return a >= 0 ? a / 8 : -((-a + 7) / 8); }  // FloorDiv (tsdf_volume.hpp:136-140)
     static Vec3i BlockOf(const Vec3i& v) { return {FloorDiv8(v[0]), FloorDiv8(v[1]), FloorDiv8(v[2])}; }
@@ -452,13 +543,14 @@ class TsdfVolume {
         return (std::size_t(v[2] - 8 * b[2]) * 8 + std::size_t(v[1] - 8 * b[1])) * 8 + std::size_t(v[0] - 8 * b[0]);
     }
     Mirror* Fetch(const Vec3i& bc) const {
-        auto it = mirror_.find(bc);
+        const std::array<int, 3> key{bc[0], bc[1], bc[2]};
+        auto it = mirror_.find(key);
         if (it != mirror_.end() && it->second->generation == generation_) return it->second.get();
         std::vector<Voxel> vox(512);
         std::int32_t found = 0;
         Check(rf_volume_find_block(h_, bc.data(), reinterpret_cast<std::uint8_t*>(vox.data()), &found));
         if (!found) return nullptr;
-        if (it == mirror_.end()) it = mirror_.emplace(bc, std::make_unique<Mirror>()).first;
+        if (it == mirror_.end()) it = mirror_.emplace(key, std::make_unique<Mirror>()).first;
         Mirror& m = *it->second;
         m.block.coord = bc;
         if (m.block.voxels.size() != 512) m.block.voxels.resize(512);
@@ -474,7 +566,7 @@ class TsdfVolume {
     VolumeConfig config_;
     rf_volume* h_ = nullptr;
     bool owned_ = false;
-    mutable std::map<Vec3i, std::unique_ptr<Mirror>> mirror_;
+    mutable std::map<std::array<int, 3>, std::unique_ptr<Mirror>> mirror_;
     mutable std::uint64_t generation_ = 1;
 };
 

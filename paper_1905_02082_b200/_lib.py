@@ -80,7 +80,7 @@ RF_MEMORY_HOST, RF_MEMORY_DEVICE = 0, 1
 # Every exported symbol of include/refusion_b200.h (checked by the CPU tests).
 EXPORTS = [
     "rf_last_error", "rf_version", "rf_volume_create", "rf_volume_destroy", "rf_volume_num_blocks",
-    "rf_volume_hash_capacity", "rf_volume_allocate_blocks", "rf_volume_allocate_for_frame", "rf_volume_integrate",
+    "rf_volume_hash_capacity", "rf_volume_get_config", "rf_volume_allocate_blocks", "rf_volume_allocate_for_frame", "rf_volume_integrate",
     "rf_volume_carve", "rf_volume_sample", "rf_volume_get_voxels", "rf_volume_set_voxels", "rf_volume_export_blocks",
     "rf_volume_hash_occupancy", "rf_volume_reset", "rf_volume_save", "rf_volume_load", "rf_linearize",
     "rf_evaluate_depth_error", "rf_evaluate_color_error", "rf_register", "rf_mask_stages", "rf_raycast",

@@ -736,6 +736,13 @@ rf_status rf_volume_hash_capacity(const rf_volume* v, uint64_t* out) {
     });
 }
 
+rf_status rf_volume_get_config(const rf_volume* v, rf_volume_config* out) {
+    return guard([&] {
+        require(v && out, RF_INVALID_ARGUMENT, "null argument");
+        *out = v->cfg;
+    });
+}
+
 rf_status rf_volume_allocate_blocks(rf_volume* v, const int32_t* coords, uint64_t n, int32_t* created) {
     return guard([&] {
         require(v && (coords || n == 0), RF_INVALID_ARGUMENT, "null argument");
