@@ -131,6 +131,20 @@ class Pose {
     Vec3 translation() const { return Vec3{m_[9], m_[10], m_[11]}; }
     const double* data() const { return m_.data(); }
     double* data() { return m_.data(); }
+#ifdef REFUSION_B200_EIGEN
+    Eigen::Matrix4d Matrix() const {  // homogeneous 4x4 (geometry.hpp:96-101)
+        Eigen::Matrix4d T = Eigen::Matrix4d::Identity();
+        for (int i = 0; i < 3; ++i) {
+            for (int j = 0; j < 3; ++j) T(i, j) = m_[3 * i + j];
+            T(i, 3) = m_[9 + i];
+        }
+        return T;
+    }
+#else
+    std::array<double, 16> Matrix() const {  // homogeneous 4x4, row-major
+        return {m_[0], m_[1], m_[2], m_[9], m_[3], m_[4], m_[5], m_[10], m_[6], m_[7], m_[8], m_[11], 0, 0, 0, 1};
+    }
+#endif
 
     Vec3 operator*(const Vec3& x) const {
         Vec3 r;
@@ -165,6 +179,91 @@ class Pose {
 #endif
     std::array<double, 12> m_;
 };
+
+// Twist / ExpMap / LogMap (geometry.hpp:53-121): se(3) increments on the
+// host (the GPU's LM applies its own ExpMap in the tracking kernel).
+#ifdef REFUSION_B200_EIGEN
+using Vec6 = Eigen::Matrix<double, 6, 1>;
+#else
+using Vec6 = std::array<double, 6>;
+#endif
+struct Twist {
+    Vec3 v = Vec3{0.0, 0.0, 0.0};  // translational part (m)
+    Vec3 w = Vec3{0.0, 0.0, 0.0};  // rotational part (rad)
+    Twist() = default;
+    Twist(const Vec3& v_in, const Vec3& w_in) : v(v_in), w(w_in) {}
+    explicit Twist(const Vec6& xi) : v(Vec3{xi[0], xi[1], xi[2]}), w(Vec3{xi[3], xi[4], xi[5]}) {}
+    Vec6 Vector() const {
+        Vec6 xi;
+        for (int i = 0; i < 3; ++i) {
+            xi[i] = v[i];
+            xi[3 + i] = w[i];
+        }
+        return xi;
+    }
+    double Norm() const {
+        double s = 0.0;
+        for (int i = 0; i < 3; ++i) s += v[i] * v[i] + w[i] * w[i];
+        return std::sqrt(s);
+    }
+};
+// exp of the twist: R = I + a W + b W^2, t = (I + b W + c W^2) v with
+// a = sin t / t, b = (1 - cos t) / t^2, c = (t - sin t) / t^3 (series below 1e-6).
+inline Pose ExpMap(const Twist& xi) {
+    const double w0 = xi.w[0], w1 = xi.w[1], w2 = xi.w[2];
+    const double t2 = w0 * w0 + w1 * w1 + w2 * w2, th = std::sqrt(t2);
+    double a, b, c;
+    if (th < 1e-6) {
+        a = 1.0 - t2 / 6.0;
+        b = 0.5 - t2 / 24.0;
+        c = 1.0 / 6.0 - t2 / 120.0;
+    } else {
+        a = std::sin(th) / th;
+        b = (1.0 - std::cos(th)) / t2;
+        c = (th - std::sin(th)) / (t2 * th);
+    }
+    const double W[9] = {0, -w2, w1, w2, 0, -w0, -w1, w0, 0};
+    double W2[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) W2[3 * i + j] = W[3 * i] * W[j] + W[3 * i + 1] * W[3 + j] + W[3 * i + 2] * W[6 + j];
+    double p[12];
+    for (int i = 0; i < 9; ++i) {
+        const double id = (i % 4 == 0) ? 1.0 : 0.0;
+        p[i] = id + a * W[i] + b * W2[i];
+    }
+    for (int i = 0; i < 3; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < 3; ++j) {
+            const double id = i == j ? 1.0 : 0.0;
+            s += (id + b * W[3 * i + j] + c * W2[3 * i + j]) * xi.v[j];
+        }
+        p[9 + i] = s;
+    }
+    return Pose::FromArray(p);
+}
+// log of the pose (rotation angle < pi): w from the skew part of R, v = V^-1 t.
+inline Twist LogMap(const Pose& pose) {
+    const double* m = pose.data();
+    const double cos_t = std::max(-1.0, std::min(1.0, 0.5 * (m[0] + m[4] + m[8] - 1.0)));
+    const double th = std::acos(cos_t), s = std::sin(th);
+    const double k = th < 1e-6 ? 0.5 + th * th / 12.0 : th / (2.0 * s);
+    const Vec3 w{k * (m[7] - m[5]), k * (m[2] - m[6]), k * (m[3] - m[1])};
+    const double t2 = th * th;
+    // V^-1 = I - W / 2 + (1 - (t sin t) / (2 (1 - cos t))) / t^2 W^2
+    const double d = th < 1e-6 ? 1.0 / 12.0 : (1.0 - th * s / (2.0 * (1.0 - cos_t))) / t2;
+    const double W[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
+    Vec3 v{0.0, 0.0, 0.0};
+    for (int i = 0; i < 3; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < 3; ++j) {
+            const double W2 = W[3 * i] * W[j] + W[3 * i + 1] * W[3 + j] + W[3 * i + 2] * W[6 + j];
+            const double id = i == j ? 1.0 : 0.0;
+            acc += (id - 0.5 * W[3 * i + j] + d * W2) * m[9 + j];
+        }
+        v[i] = acc;
+    }
+    return Twist(v, w);
+}
 
 // Backproject / Project (geometry.hpp:41-48): host-side camera model helpers.
 inline Vec3 Backproject(double u, double v, double depth, const CameraIntrinsics& k) {
@@ -590,8 +689,13 @@ struct ResidualImage {
 };
 
 struct LinearizeResult {
+#ifdef REFUSION_B200_EIGEN
+    Eigen::Matrix<double, 6, 6> H = Eigen::Matrix<double, 6, 6>::Zero();
+    Eigen::Matrix<double, 6, 1> b = Eigen::Matrix<double, 6, 1>::Zero();
+#else
     std::array<double, 36> H{};  // row-major 6x6
     std::array<double, 6> b{};
+#endif
     double depth_error = 0.0, color_error = 0.0, error = 0.0;
     std::size_t valid_count = 0;
     bool degenerate = false;
@@ -661,8 +765,16 @@ inline LinearizeResult Linearize(const TsdfVolume& volume, const Frame& frame, c
     Check(rf_linearize(volume.handle(), &f, pose.data(), &c,
                        detail::MaskPtr(mask, frame.intrinsics.width, frame.intrinsics.height), &r));
     LinearizeResult out;
-    std::memcpy(out.H.data(), r.H, sizeof(r.H));
-    std::memcpy(out.b.data(), r.b, sizeof(r.b));
+    for (int i = 0; i < 6; ++i) {
+        for (int j = 0; j < 6; ++j) {
+#ifdef REFUSION_B200_EIGEN
+            out.H(i, j) = r.H[6 * i + j];
+#else
+            out.H[6 * i + j] = r.H[6 * i + j];
+#endif
+        }
+        out.b[i] = r.b[i];
+    }
     out.depth_error = r.depth_error;
     out.color_error = r.color_error;
     out.error = r.error;
@@ -880,6 +992,13 @@ class Pipeline {
     }
     Pipeline(const Pipeline&) = delete;
     Pipeline& operator=(const Pipeline&) = delete;
+    Pipeline(Pipeline&& o) noexcept
+        : config_(std::move(o.config_)), h_(o.h_), volume_(std::move(o.volume_)), trajectory_(std::move(o.trajectory_)),
+          stats_(std::move(o.stats_)), debug_sink_(std::move(o.debug_sink_)),
+          last_refinement_emitted_(o.last_refinement_emitted_), last_w_(o.last_w_), last_h_(o.last_h_) {
+        o.h_ = nullptr;
+        o.volume_.reset();
+    }
 
     FrameStats ProcessFrame(const Frame& frame) {
         if (!frame.depth.SameSize(frame.intrinsics.width, frame.intrinsics.height) ||
