@@ -160,6 +160,19 @@ class Pose {
         }
         return r;
     }
+    // Rotation orthonormal with determinant +1 and all entries finite, to `tol` (geometry.hpp:103).
+    bool IsValid(double tol = 1e-9) const {
+        for (double x : m_)
+            if (!std::isfinite(x)) return false;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) {
+                const double d = m_[3 * i] * m_[3 * j] + m_[3 * i + 1] * m_[3 * j + 1] + m_[3 * i + 2] * m_[3 * j + 2];
+                if (std::abs(d - (i == j ? 1.0 : 0.0)) > tol) return false;
+            }
+        const double det = m_[0] * (m_[4] * m_[8] - m_[5] * m_[7]) - m_[1] * (m_[3] * m_[8] - m_[5] * m_[6]) +
+                           m_[2] * (m_[3] * m_[7] - m_[4] * m_[6]);
+        return std::abs(det - 1.0) <= tol;
+    }
     Pose Inverse() const {
         Pose r;
         for (int i = 0; i < 3; ++i)
@@ -180,6 +193,21 @@ class Pose {
     std::array<double, 12> m_;
 };
 
+inline constexpr double kSmallAngle = 1e-6;  // ExpMap / LogMap series branch (geometry.hpp:123)
+// W with W x = w x x (geometry.hpp:110-114).
+inline Mat3 SkewMatrix(const Vec3& w) {
+    Mat3 s;
+    const double e[9] = {0.0, -w[2], w[1], w[2], 0.0, -w[0], -w[1], w[0], 0.0};
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+#ifdef REFUSION_B200_EIGEN
+            s(i, j) = e[3 * i + j];
+#else
+            s[3 * i + j] = e[3 * i + j];
+#endif
+        }
+    return s;
+}
 // Twist / ExpMap / LogMap (geometry.hpp:53-121): se(3) increments on the
 // host (the GPU's LM applies its own ExpMap in the tracking kernel).
 #ifdef REFUSION_B200_EIGEN
@@ -213,7 +241,7 @@ inline Pose ExpMap(const Twist& xi) {
     const double w0 = xi.w[0], w1 = xi.w[1], w2 = xi.w[2];
     const double t2 = w0 * w0 + w1 * w1 + w2 * w2, th = std::sqrt(t2);
     double a, b, c;
-    if (th < 1e-6) {
+    if (th < kSmallAngle) {
         a = 1.0 - t2 / 6.0;
         b = 0.5 - t2 / 24.0;
         c = 1.0 / 6.0 - t2 / 120.0;
@@ -246,11 +274,11 @@ inline Twist LogMap(const Pose& pose) {
     const double* m = pose.data();
     const double cos_t = std::max(-1.0, std::min(1.0, 0.5 * (m[0] + m[4] + m[8] - 1.0)));
     const double th = std::acos(cos_t), s = std::sin(th);
-    const double k = th < 1e-6 ? 0.5 + th * th / 12.0 : th / (2.0 * s);
+    const double k = th < kSmallAngle ? 0.5 + th * th / 12.0 : th / (2.0 * s);
     const Vec3 w{k * (m[7] - m[5]), k * (m[2] - m[6]), k * (m[3] - m[1])};
     const double t2 = th * th;
     // V^-1 = I - W / 2 + (1 - (t sin t) / (2 (1 - cos t))) / t^2 W^2
-    const double d = th < 1e-6 ? 1.0 / 12.0 : (1.0 - th * s / (2.0 * (1.0 - cos_t))) / t2;
+    const double d = th < kSmallAngle ? 1.0 / 12.0 : (1.0 - th * s / (2.0 * (1.0 - cos_t))) / t2;
     const double W[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
     Vec3 v{0.0, 0.0, 0.0};
     for (int i = 0; i < 3; ++i) {
