@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -942,6 +943,104 @@ inline Mesh ExtractMesh(const TsdfVolume& volume, int min_weight = 2, int /*thre
     rf_mesh_destroy(m);
     Check(s);
     return out;
+}
+
+// WritePly / ReadPly / WritePointCloudPly (mesh.hpp:27-32): binary little-endian
+// PLY, float x/y/z, uchar red/green/blue per vertex when the mesh has colours,
+// uchar-counted int index lists. Host-side I/O of a host mesh (the device mesh
+// writes the same bytes through rf_mesh_write_ply).
+namespace detail {
+inline void WritePlyFile(const std::string& path, const std::vector<Vec3f>& v, const std::vector<Rgb8>* colors,
+                         const std::vector<Vec3i>* faces) {
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot open for writing: " + path);
+    std::string h = "ply\nformat binary_little_endian 1.0\nelement vertex " + std::to_string(v.size()) +
+                    "\nproperty float x\nproperty float y\nproperty float z\n";
+    if (colors) h += "property uchar red\nproperty uchar green\nproperty uchar blue\n";
+    if (faces) h += "element face " + std::to_string(faces->size()) + "\nproperty list uchar int vertex_indices\n";
+    h += "end_header\n";
+    bool ok = std::fwrite(h.data(), 1, h.size(), f) == h.size();
+    for (std::size_t i = 0; ok && i < v.size(); ++i) {
+        const float p[3] = {v[i][0], v[i][1], v[i][2]};
+        ok = std::fwrite(p, 4, 3, f) == 3 && (!colors || std::fwrite(&(*colors)[i].r, 1, 3, f) == 3);
+    }
+    for (std::size_t i = 0; ok && faces && i < faces->size(); ++i) {
+        const unsigned char n = 3;
+        const std::int32_t idx[3] = {(*faces)[i][0], (*faces)[i][1], (*faces)[i][2]};
+        ok = std::fwrite(&n, 1, 1, f) == 1 && std::fwrite(idx, 4, 3, f) == 3;
+    }
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw std::runtime_error("write failed: " + path);
+}
+}  // namespace detail
+
+inline void WritePly(const std::string& path, const Mesh& mesh) {
+    const bool colored = !mesh.vertices.empty() && mesh.colors.size() == mesh.vertices.size();
+    detail::WritePlyFile(path, mesh.vertices, colored ? &mesh.colors : nullptr, &mesh.faces);
+}
+inline void WritePointCloudPly(const std::string& path, const std::vector<Vec3f>& points) {
+    detail::WritePlyFile(path, points, nullptr, nullptr);
+}
+inline Mesh ReadPly(const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("cannot open " + path);
+    auto fail = [&](const std::string& why) {
+        std::fclose(f);
+        return std::runtime_error("malformed PLY " + path + ": " + why);
+    };
+    char line[256];
+    auto next = [&]() -> std::string {
+        if (!std::fgets(line, sizeof(line), f)) return std::string("\x01");  // end of file marker
+        std::string s(line);
+        while (!s.empty() && (s.back() == '\n' || s.back() == '\r')) s.pop_back();
+        return s;
+    };
+    if (next() != "ply") throw fail("missing magic");
+    if (next() != "format binary_little_endian 1.0") throw fail("not binary little endian");
+    std::size_t nv = 0, nf = 0;
+    int vprops = 0;
+    bool colored = false, faces = false, in_vertex = false;
+    for (;;) {
+        const std::string s = next();
+        if (s == "\x01") throw fail("no end_header");
+        if (s == "end_header") break;
+        if (s.rfind("element vertex ", 0) == 0) {
+            nv = std::stoull(s.substr(15));
+            in_vertex = true;
+        } else if (s.rfind("element face ", 0) == 0) {
+            nf = std::stoull(s.substr(13));
+            faces = true;
+            in_vertex = false;
+        } else if (s.rfind("property ", 0) == 0) {
+            if (in_vertex) {
+                if (s == "property uchar red") colored = true;
+                ++vprops;
+            } else if (faces && s != "property list uchar int vertex_indices") {
+                throw fail("unsupported face property");
+            }
+        } else if (s.rfind("comment", 0) != 0) {
+            throw fail("unexpected header line");
+        }
+    }
+    if (vprops != (colored ? 6 : 3)) throw fail("unsupported vertex properties");
+    Mesh m;
+    m.vertices.resize(nv);
+    if (colored) m.colors.resize(nv);
+    for (std::size_t i = 0; i < nv; ++i) {
+        float p[3];
+        if (std::fread(p, 4, 3, f) != 3) throw fail("truncated vertices");
+        m.vertices[i] = Vec3f{p[0], p[1], p[2]};
+        if (colored && std::fread(&m.colors[i].r, 1, 3, f) != 3) throw fail("truncated colours");
+    }
+    m.faces.resize(nf);
+    for (std::size_t i = 0; i < nf; ++i) {
+        unsigned char n = 0;
+        std::int32_t idx[3];
+        if (std::fread(&n, 1, 1, f) != 1 || n != 3 || std::fread(idx, 4, 3, f) != 3) throw fail("bad face");
+        m.faces[i] = Vec3i{idx[0], idx[1], idx[2]};
+    }
+    std::fclose(f);
+    return m;
 }
 
 // ---------------------------------------------------------------- pipeline (pipeline.hpp:18-96, config.hpp:12-24)
