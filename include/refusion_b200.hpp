@@ -344,6 +344,82 @@ void WalkGridSegment(const Vec3& a, const Vec3& b, double cell_extent, Fn&& fn) 
     }
 }
 
+// HashCoord / CoordHashMap (spatial_hash.hpp:10-83): the volume's brick hash
+// (the same multiply-XOR hash and linear probing the GPU table uses,
+// csrc/rf_common.cuh) as a host container from integer 3D coordinates to
+// 32-bit values, for callers that index coordinates themselves. Power-of-two
+// capacity, doubled before an insert would pass load 3/4; no removal.
+inline std::uint64_t HashCoord(const Vec3i& c) {
+    return (std::uint64_t(std::uint32_t(c[0])) * 73856093ull) ^ (std::uint64_t(std::uint32_t(c[1])) * 19349669ull) ^
+           (std::uint64_t(std::uint32_t(c[2])) * 83492791ull);
+}
+class CoordHashMap {
+  public:
+    explicit CoordHashMap(std::size_t initial_capacity = 1024) {
+        std::size_t n = 16;
+        while (n < initial_capacity) n *= 2;
+        Reset(n);
+    }
+    std::size_t size() const { return count_; }
+    std::size_t capacity() const { return used_.size(); }
+    // The slot `coord` probes to: its own, or the empty slot that ends its probe.
+    std::size_t ProbeSlot(const Vec3i& coord) const {
+        const std::size_t mask = used_.size() - 1;
+        std::size_t i = std::size_t(HashCoord(coord)) & mask;
+        while (used_[i] && !Same(keys_[i], coord)) i = (i + 1) & mask;
+        return i;
+    }
+    const std::uint32_t* Find(const Vec3i& coord) const {
+        const std::size_t i = ProbeSlot(coord);
+        return used_[i] ? &values_[i] : nullptr;
+    }
+    // {stored value, true} when inserted; {existing value, false} when present.
+    std::pair<std::uint32_t, bool> Insert(const Vec3i& coord, std::uint32_t value) {
+        if (4 * (count_ + 1) > 3 * used_.size()) Rehash(2 * used_.size());
+        const std::size_t i = ProbeSlot(coord);
+        if (used_[i]) return {values_[i], false};
+        used_[i] = 1;
+        keys_[i] = Key{coord[0], coord[1], coord[2]};
+        values_[i] = value;
+        ++count_;
+        return {value, true};
+    }
+    template <typename Fn>
+    void ForEach(Fn&& fn) const {  // slot order
+        for (std::size_t i = 0; i < used_.size(); ++i)
+            if (used_[i]) fn(Vec3i{keys_[i][0], keys_[i][1], keys_[i][2]}, values_[i]);
+    }
+
+  private:
+    using Key = std::array<int, 3>;
+    static bool Same(const Key& k, const Vec3i& c) { return k[0] == c[0] && k[1] == c[1] && k[2] == c[2]; }
+    void Reset(std::size_t n) {
+        used_.assign(n, 0);
+        keys_.assign(n, Key{0, 0, 0});
+        values_.assign(n, 0u);
+        count_ = 0;
+    }
+    void Rehash(std::size_t n) {  // re-inserts in the old slot order
+        std::vector<std::uint8_t> used = std::move(used_);
+        std::vector<Key> keys = std::move(keys_);
+        std::vector<std::uint32_t> values = std::move(values_);
+        Reset(n);
+        for (std::size_t i = 0; i < used.size(); ++i) {
+            if (!used[i]) continue;
+            const Vec3i c{keys[i][0], keys[i][1], keys[i][2]};
+            const std::size_t j = ProbeSlot(c);
+            used_[j] = 1;
+            keys_[j] = keys[i];
+            values_[j] = values[i];
+            ++count_;
+        }
+    }
+    std::vector<std::uint8_t> used_;
+    std::vector<Key> keys_;
+    std::vector<std::uint32_t> values_;
+    std::size_t count_ = 0;
+};
+
 // ---------------------------------------------------------------- images (image.hpp:13-103)
 template <typename T>
 class Image {
@@ -648,6 +724,7 @@ class TsdfVolume {
     struct Mirror {
         VoxelBlock block;
         bool dirty = false;
+        bool present = false;
         std::uint64_t generation = 0;
     };
     TsdfVolume(rf_volume* h, bool owned) : h_(h), owned_(owned) {
@@ -673,18 +750,20 @@ class TsdfVolume {
     Mirror* Fetch(const Vec3i& bc) const {
         const std::array<int, 3> key{bc[0], bc[1], bc[2]};
         auto it = mirror_.find(key);
-        if (it != mirror_.end() && it->second->generation == generation_) return it->second.get();
+        if (it != mirror_.end() && it->second->generation == generation_)
+            return it->second->present ? it->second.get() : nullptr;
         std::vector<Voxel> vox(512);
         std::int32_t found = 0;
         Check(rf_volume_find_block(h_, bc.data(), reinterpret_cast<std::uint8_t*>(vox.data()), &found));
-        if (!found) return nullptr;
         if (it == mirror_.end()) it = mirror_.emplace(key, std::make_unique<Mirror>()).first;
         Mirror& m = *it->second;
+        m.generation = generation_;
+        m.present = found != 0;  // absence is cached too, until the next GPU operation
+        if (!found) return nullptr;
         m.block.coord = bc;
         if (m.block.voxels.size() != 512) m.block.voxels.resize(512);
         std::memcpy(m.block.voxels.data(), vox.data(), 512 * sizeof(Voxel));  // in place: handed-out pointers stay valid
         m.dirty = false;
-        m.generation = generation_;
         return &m;
     }
     SdfSample Value(int mode, const Vec3& p) const {

@@ -101,6 +101,25 @@ struct ArrayView {
     }
     Matrix<S, R, C> matrix() const { return m; }
 };
+// array() of a non-const matrix: the same view, plus in-place coefficient-wise
+// compound assignment (`v.array() -= s`).
+template <typename S, int R, int C>
+struct ArrayRef {
+    Matrix<S, R, C>& m;
+    Matrix<S, R, C> floor() const { return ArrayView<S, R, C>{m}.floor(); }
+    Matrix<S, R, C> abs() const { return m.cwiseAbs(); }
+    operator Matrix<S, R, C>() const { return m; }
+    ArrayView<S, R, C> operator+(S s) const { return ArrayView<S, R, C>{m} + s; }
+    Matrix<S, R, C> matrix() const { return m; }
+    ArrayRef& operator+=(S s) {
+        for (int i = 0; i < R * C; ++i) m.d[i] += s;
+        return *this;
+    }
+    ArrayRef& operator-=(S s) {
+        for (int i = 0; i < R * C; ++i) m.d[i] -= s;
+        return *this;
+    }
+};
 
 // Comma initialiser: scalars and sub-matrices, filled row block by row block.
 template <typename S, int R, int C>
@@ -350,6 +369,7 @@ class Matrix {
         return r;
     }
     ArrayView<S, R, C> array() const { return {*this}; }
+    ArrayRef<S, R, C> array() { return {*this}; }
     template <typename T>
     Matrix<T, R, C> cast() const {
         Matrix<T, R, C> r;

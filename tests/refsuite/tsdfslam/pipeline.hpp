@@ -3,6 +3,7 @@
 // compile unchanged against the GPU implementation.
 #pragma once
 #include "refusion_b200.hpp"
+#include "tsdfslam/dataset_io.hpp"  // as the reference pipeline.hpp does
 namespace tsdfslam {
 using namespace tsdfslam_b200;
 }  // namespace tsdfslam

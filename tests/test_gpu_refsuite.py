@@ -13,6 +13,17 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SUITES = sorted(glob.glob(os.path.join(ROOT, "oracle", "_ref", "suite_test_*")))
+# The spatial-hash suite exercises the host CoordHashMap only (no device calls).
+HOST_SUITES = [p for p in SUITES if p.endswith("suite_test_spatial_hash")]
+GPU_SUITES = [p for p in SUITES if p not in HOST_SUITES]
+ACCEPTANCE = os.path.join(ROOT, "oracle", "_ref", "suite_acceptance")
+
+
+def _run_doctest_suite(exe):
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    summary = [l for l in r.stdout.splitlines() if l.startswith("[doctest-shim] test cases:")]
+    assert summary and "| 0 failed |" in summary[-1] and summary[-1].endswith("| 0 failed"), r.stdout[-2000:]
 
 
 def test_refsuite_sources_resolve_to_the_host_layer():
@@ -22,10 +33,27 @@ def test_refsuite_sources_resolve_to_the_host_layer():
         assert '#include "refusion_b200.hpp"' in text and "using namespace tsdfslam_b200;" in text, path
 
 
+@pytest.mark.parametrize("exe", HOST_SUITES, ids=[os.path.basename(p) for p in HOST_SUITES])
+def test_reference_host_suite(exe):
+    _run_doctest_suite(exe)
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("exe", SUITES, ids=[os.path.basename(p) for p in SUITES])
+@pytest.mark.parametrize("exe", GPU_SUITES, ids=[os.path.basename(p) for p in GPU_SUITES])
 def test_reference_suite_on_gpu(exe):
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    _run_doctest_suite(exe)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(ACCEPTANCE), reason="acceptance program not built (needs /root/reference)")
+def test_reference_acceptance_on_gpu():
+    """The reference's acceptance program (proj/tests/acceptance.cpp): criteria 1-8
+    must PASS; 9 (TUM sequences) has no data on the box and must SKIP."""
+    env = dict(os.environ)
+    env.pop("TUM_DATA_DIR", None)
+    r = subprocess.run([ACCEPTANCE], capture_output=True, text=True, timeout=900, env=env)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("[")]
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
-    summary = [l for l in r.stdout.splitlines() if l.startswith("[doctest-shim] test cases:")]
-    assert summary and "| 0 failed |" in summary[-1] and summary[-1].endswith("| 0 failed"), r.stdout[-2000:]
+    for n in range(1, 9):
+        assert any(l.startswith("[PASS] criterion %d:" % n) for l in lines), r.stdout[-4000:]
+    assert any(l.startswith("[SKIP] criterion 9:") for l in lines), r.stdout[-4000:]
