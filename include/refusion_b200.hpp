@@ -22,6 +22,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdio>
+#include <deque>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -1129,6 +1130,94 @@ struct RefinementConfig {  // depth_refinement.hpp:12-17
     double far_value = 8.0;
     int bisection_iterations = 8;
 };
+
+// WindowEntry / FrameWindow (depth_refinement.hpp:19-44): the host form of the
+// refinement window. Pipeline keeps its own window on the device; this one is
+// for callers that drive RenderVirtualDepth themselves.
+struct WindowEntry {
+    Frame frame;
+    Pose pose = Pose::Identity();
+    PixelMask mask;  // may be empty
+};
+class FrameWindow {
+  public:
+    explicit FrameWindow(std::size_t capacity) : capacity_(capacity) {}
+    std::size_t capacity() const { return capacity_; }
+    std::size_t size() const { return entries_.size(); }
+    bool Empty() const { return entries_.empty(); }
+    bool Full() const { return entries_.size() >= capacity_; }
+    void Push(WindowEntry entry) {  // depth_refinement.cpp:10-13
+        if (Full()) throw std::logic_error("frame window is full");
+        entries_.push_back(std::move(entry));
+    }
+    WindowEntry PopFront() {  // depth_refinement.cpp:15-20
+        if (entries_.empty()) throw std::logic_error("frame window is empty");
+        WindowEntry e = std::move(entries_.front());
+        entries_.pop_front();
+        return e;
+    }
+    const std::deque<WindowEntry>& entries() const { return entries_; }
+
+  private:
+    std::size_t capacity_;
+    std::deque<WindowEntry> entries_;
+};
+
+// RenderVirtualDepth (depth_refinement.cpp:22-80): the window fused into a
+// throw-away volume on the GPU and ray-marched from view_pose
+// (rf_render_virtual_depth: all entries uploaded and fused in one pass when
+// they share a size; a mixed-size window goes through a TsdfVolume entry by
+// entry). An empty window has no surface: all pixels invalid.
+inline DepthImage RenderVirtualDepth(const FrameWindow& window, const Pose& view_pose, const CameraIntrinsics& k,
+                                     const VolumeConfig& volume_config, const RefinementConfig& config,
+                                     int /*threads*/ = 1) {
+    volume_config.Validate();
+    DepthImage out(k.width, k.height, 0.f);
+    const auto& es = window.entries();
+    if (es.empty()) return out;
+    bool same = true;
+    for (const WindowEntry& e : es) {
+        if (!e.frame.depth.SameSize(e.frame.intrinsics.width, e.frame.intrinsics.height))
+            throw std::invalid_argument("depth size does not match the intrinsics");
+        same = same && e.frame.intrinsics.width == es.front().frame.intrinsics.width &&
+               e.frame.intrinsics.height == es.front().frame.intrinsics.height;
+    }
+    if (!same) {
+        TsdfVolume temp(volume_config);
+        for (const WindowEntry& e : es) {
+            const PixelMask* m = e.mask.Empty() ? nullptr : &e.mask;
+            temp.AllocateForFrame(e.frame.depth, e.frame.intrinsics, e.pose, m);
+            temp.Integrate(e.frame, e.pose, m);
+        }
+        return Raycast(temp, view_pose, k, config.bisection_iterations);
+    }
+    std::vector<rf_frame> frames;
+    std::vector<double> poses;
+    std::vector<const std::uint8_t*> masks;
+    for (const WindowEntry& e : es) {
+        frames.push_back(detail::ToC(e.frame));
+        poses.insert(poses.end(), e.pose.data(), e.pose.data() + 12);
+        masks.push_back(detail::MaskPtr(&e.mask, e.frame.intrinsics.width, e.frame.intrinsics.height));
+    }
+    const rf_intrinsics ck = k.c();
+    const rf_volume_config vc = volume_config.c();
+    Check(rf_render_virtual_depth(frames.data(), poses.data(), masks.data(), std::int32_t(frames.size()),
+                                  view_pose.data(), &ck, &vc, config.bisection_iterations, config.far_value, 0,
+                                  out.data(), nullptr));
+    return out;
+}
+
+// RefineDepth (depth_refinement.cpp:82-93): raw where valid, else virtual
+// where valid, else far_value. Host-side: one pass over one image.
+inline DepthImage RefineDepth(const DepthImage& raw, const DepthImage& virtual_depth, double far_value) {
+    if (!raw.SameSize(virtual_depth)) throw std::invalid_argument("depth size mismatch");
+    DepthImage out = raw;
+    for (int y = 0; y < out.height(); ++y)
+        for (int x = 0; x < out.width(); ++x)
+            if (!DepthValid(out(x, y)))
+                out(x, y) = DepthValid(virtual_depth(x, y)) ? virtual_depth(x, y) : static_cast<float>(far_value);
+    return out;
+}
 
 struct PipelineConfig {
     VolumeConfig volume;
