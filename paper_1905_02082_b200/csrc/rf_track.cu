@@ -477,24 +477,61 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
     for (int l = R.levels - 1; l >= 0; --l) {
         const long long mv = (long long)(max(R.min_valid, 1)) >> (2 * l);
         const double min_valid = double(mv > 16 ? mv : 16);
-        pass<true>(a, l, st.pose(), use_mask, false, cw, scratch, blk, st.cur());
-        if (st.cur()[29] < min_valid) {
-            if (threadIdx.x == 0) st.lost = 1;
-            __syncthreads();
-            return;
-        }
-        __syncthreads();
-        if (threadIdx.x == kLmThread) {  // the LM thread's own state: no barrier needed before it reads it
-            st.lambda = R.lambda_init;
-            st.converged = 0;
-            st.brk = 0;
-            st.level_it = 0;
-        }
-        // One barrier per LM iteration: kLmThread judges the last trial and
-        // solves for the next candidate in one straight-line section on
-        // local copies of its state (registration.cpp:233-272).
-        bool judge = false;  // a trial was evaluated since the last solve
+        // One pass site per level (the level's linearization at the current
+        // pose, then the LM trials), so the level's first pass and its trials
+        // run the same instructions: the trials start with a warm i-cache.
+        bool lin = true;
         for (;;) {
+            pass<true>(a, l, lin ? st.pose() : st.cand(), use_mask, false, cw, scratch, blk, lin ? st.cur() : st.trial(),
+                       [&] {
+                           // everything of the judge but the trial's error, on thread 0 while the
+                           // all-reduce's arrivals propagate (off every critical path)
+                           if (lin) return;
+                           st.cur_err = st.cur()[27] + cw * st.cur()[28];
+                           st.tol = kRelDecreaseTol * st.cur_err;
+                           st.lam_acc = fmax(st.lambda / R.lambda_down, 1e-12);
+                           st.lam_rej = fmin(st.lambda * R.lambda_up, 1e12);
+                           st.small_step = sqrt(st.dn[st.ic]) < R.eps;
+                       },
+                       [&] {
+                           // registration.cpp:265-271 then :240-249 on rejection: lambda
+                           // raised (a level that reaches 1e12 converges instead)
+                           if (lin) return;
+                           const double lam = fmin(st.lambda * R.lambda_up, 1e12);
+                           if (!(lam >= 1e12)) {
+                               double delta[6];
+                               if (lm_solve(st.cur(), lam, delta)) {
+                                   Pose e;
+                                   expmap(delta, e);
+                                   const int fr = 3 - st.ip - st.ic;  // the free slot
+                                   st.P[fr] = pose_mul(e, st.pose());
+                                   double dn = 0.0;
+#pragma unroll
+                                   for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
+                                   st.dn[fr] = dn;
+                                   st.rej_ok = 1;
+                               }
+                           }
+                       });
+            const bool judge = !lin;  // a trial was evaluated since the last solve
+            if (lin) {
+                if (st.cur()[29] < min_valid) {
+                    if (threadIdx.x == 0) st.lost = 1;
+                    __syncthreads();
+                    return;
+                }
+                __syncthreads();
+                if (threadIdx.x == kLmThread) {  // the LM thread's own state: no barrier needed before it reads it
+                    st.lambda = R.lambda_init;
+                    st.converged = 0;
+                    st.brk = 0;
+                    st.level_it = 0;
+                }
+                lin = false;
+            }
+            // One barrier per LM iteration: kLmThread judges the last trial and
+            // solves for the next candidate in one straight-line section on
+            // local copies of its state (registration.cpp:233-272).
             if (threadIdx.x == kLmThread) {
                 double lambda = st.lambda;
                 int brk = st.brk, level_it = st.level_it, total = st.total, converged = st.converged, ci = st.ci;
@@ -569,34 +606,6 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
             }
             __syncthreads();
             if (!st.go) break;
-            // everything of the judge but the trial's error, on thread 0 while the
-            // all-reduce's arrivals propagate (off every critical path)
-            pass<true>(a, l, st.cand(), use_mask, false, cw, scratch, blk, st.trial(), [&] {
-                st.cur_err = st.cur()[27] + cw * st.cur()[28];
-                st.tol = kRelDecreaseTol * st.cur_err;
-                st.lam_acc = fmax(st.lambda / R.lambda_down, 1e-12);
-                st.lam_rej = fmin(st.lambda * R.lambda_up, 1e12);
-                st.small_step = sqrt(st.dn[st.ic]) < R.eps;
-            }, [&] {
-                // registration.cpp:265-271 then :240-249 on rejection: lambda
-                // raised (a level that reaches 1e12 converges instead)
-                const double lam = fmin(st.lambda * R.lambda_up, 1e12);
-                if (!(lam >= 1e12)) {
-                    double delta[6];
-                    if (lm_solve(st.cur(), lam, delta)) {
-                        Pose e;
-                        expmap(delta, e);
-                        const int fr = 3 - st.ip - st.ic;  // the free slot
-                        st.P[fr] = pose_mul(e, st.pose());
-                        double dn = 0.0;
-#pragma unroll
-                        for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
-                        st.dn[fr] = dn;
-                        st.rej_ok = 1;
-                    }
-                }
-            });
-            judge = true;
         }
         __syncthreads();
     }
@@ -1115,7 +1124,23 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
     }
     const bool masked_reg = a.mode == kModeRegister && a.use_mask;
     build_pyramid(a, true, masked_reg);
-    run_register(a, init, masked_reg, st, scratch, blk);
+    // kModeFrame: pipeline.cpp:79-122 (tracking part). Both registrations go
+    // through one run_register site (one copy of the pass code for both).
+    int registrations = 0, iterations = 0, rounds = 0;
+    double masked = 0.0;
+    bool reg_mask = masked_reg;
+    for (int r = 0;; ++r) {
+        run_register(a, r == 0 ? init : st.pose(), reg_mask, st, scratch, blk);  // registration 2 starts at 1's pose
+        if (a.mode == kModeRegister || st.lost) break;
+        registrations = r + 1;
+        iterations += st.total;
+        if (r == 1 || !a.dynamics) break;
+        masked = build_mask(a, 15, scratch, blk, red, &rounds);
+        if (!(masked > 0.0)) break;
+        build_pyramid(a, false, true);
+        __syncthreads();
+        reg_mask = true;
+    }
 
     if (a.mode == kModeRegister) {
         if (lead) {
@@ -1129,27 +1154,6 @@ __device__ __forceinline__ void track_main(const TrackArgs& a, RegState& st, dou
         }
         write_out(a, st);
         return;
-    }
-
-    // kModeFrame: pipeline.cpp:79-122 (tracking part).
-    int registrations = 0, iterations = 0, rounds = 0;
-    double masked = 0.0;
-    if (!st.lost) {
-        registrations = 1;
-        iterations = st.total;
-        if (a.dynamics) {
-            masked = build_mask(a, 15, scratch, blk, red, &rounds);
-            if (masked > 0.0) {
-                Pose p1 = st.pose();
-                build_pyramid(a, false, true);
-                __syncthreads();
-                run_register(a, p1, true, st, scratch, blk);
-                if (!st.lost) {
-                    registrations = 2;
-                    iterations += st.total;
-                }
-            }
-        }
     }
     if (lead) {
         TrackOut* o = a.out;
