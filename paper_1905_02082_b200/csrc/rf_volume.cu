@@ -342,11 +342,15 @@ __device__ __forceinline__ double fuse_rcp(double x) {  // ~1 ulp, branch-free
     r = __fma_rn(r, __fma_rn(-x, r, 1.0), r);
     return __fma_rn(r, __fma_rn(-x, r, 1.0), r);
 }
-__device__ __forceinline__ long project_lround(double num, double z, double rz, double c) {
+// The pixel coordinate, or -1 for any value outside [0, INT_MAX] (the caller
+// only tests 0 <= p < width). Away from half-integers every round-to-nearest
+// agrees with lround, so the fast path converts with one F2I.
+__device__ __forceinline__ int project_lround(double num, double z, double rz, double c) {
     const double xa = num * rz + c;
     const double fr = xa - floor(xa);
-    if (fabs(xa) < 1e6 && fabs(fr - 0.5) > 1e-9) return lround(xa);
-    return lround(num / z + c);  // Project, geometry.hpp:46-48
+    if (fabs(xa) < 1e6 && fabs(fr - 0.5) > 1e-9) return __double2int_rn(xa);
+    const long l = lround(num / z + c);  // Project, geometry.hpp:46-48
+    return (l < 0 || l > 0x7fffffffL) ? -1 : int(l);
 }
 __device__ __forceinline__ float div_f32(double a, double b, double rb) {
     const double q = a * rb;
@@ -354,16 +358,16 @@ __device__ __forceinline__ float div_f32(double a, double b, double rb) {
     return lo == hi ? lo : float(a / b);
 }
 // lround((c * w + in) / (w + 1)) (tsdf_volume.cpp:190-196) = (2n + d) / (2d) with
-// n = c * w + in, d = w + 1, as a multiply by M = ceil(2^40 / (2d)): exact for
-// every numerator < 2^17 (n <= 255 * 255 + 255) and 2d <= 512 (checked
-// exhaustively), with no integer division on the per-voxel path.
-__device__ __forceinline__ uint32_t colour_avg(uint32_t c, uint32_t w, uint32_t in, const unsigned long long* cdiv) {
+// n = c * w + in, d = w + 1, as the high word of a multiply by M = ceil(2^32 /
+// (2d)): exact for every numerator < 2^17 (n <= 255 * 255 + 255) and 2d <= 512
+// (checked exhaustively: tools/micro/colour_magic.c), one IMAD.HI and no integer
+// division on the per-voxel path.
+__device__ __forceinline__ uint32_t colour_avg(uint32_t c, uint32_t w, uint32_t in, const uint32_t* cdiv) {
     const uint32_t d = w + 1u;
-    const unsigned long long num = 2ull * (c * w + in) + d;
-    return uint32_t((num * cdiv[d]) >> 40);
+    return __umulhi(2u * (c * w + in) + d, cdiv[d]);
 }
-__device__ __forceinline__ unsigned long long colour_magic(uint32_t d) {  // ceil(2^40 / (2d)), d >= 1
-    return ((1ull << 40) + 2ull * d - 1ull) / (2ull * d);
+__device__ __forceinline__ uint32_t colour_magic(uint32_t d) {  // ceil(2^32 / (2d)), d >= 1
+    return uint32_t(((1ull << 32) + 2ull * d - 1ull) / (2ull * d));
 }
 
 __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
@@ -372,14 +376,14 @@ __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
     link_new_commit(a.V);  // index the bricks k_cull assigned, for the next frame's tracking
     __shared__ Pose W;
     __shared__ double s_rcp[512];  // RN(1 / i): i = w + 1 (integrate) or w + carve_weight (carve), <= 510
-    __shared__ unsigned long long s_cdiv[257];  // colour_avg multipliers by d = w + 1
+    __shared__ uint32_t s_cdiv[257];  // colour_avg multipliers by d = w + 1
     if (threadIdx.x == 0) {
         Pose P;
         for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = a.pose[i];
         W = pose_inverse(P);
     }
     for (int i = threadIdx.x; i < 512; i += blockDim.x) s_rcp[i] = i ? 1.0 / double(i) : 0.0;
-    for (int i = threadIdx.x; i < 257; i += blockDim.x) s_cdiv[i] = i ? colour_magic(uint32_t(i)) : 0ull;
+    for (int i = threadIdx.x; i < 257; i += blockDim.x) s_cdiv[i] = i ? colour_magic(uint32_t(i)) : 0u;
     __syncthreads();
     const uint32_t nvis = a.V.counters[kVisible];
     const int x = threadIdx.x & 7, y = (threadIdx.x >> 3) & 7, z = threadIdx.x >> 6;
@@ -395,23 +399,26 @@ __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
     uint32_t e_nx2 = i + G < nvis ? __ldcg(a.list + i + G) : 0u;
     int4 c_nx = make_int4(0, 0, 0, 0);
     uint2 v_nx = make_uint2(0, 0);
+    uint2* p_nx = nullptr;  // this thread's voxel of the next brick
     if (i < nvis) {
         c_nx = a.V.coords[e_nx & kIndexMask];
-        v_nx = *reinterpret_cast<const uint2*>(a.V.voxels + size_t(e_nx & kIndexMask) * kBrickVoxels + threadIdx.x);
+        p_nx = reinterpret_cast<uint2*>(a.V.voxels + size_t(e_nx & kIndexMask) * kBrickVoxels + threadIdx.x);
+        v_nx = *p_nx;
     }
+    const bool has_mask = a.mask != nullptr, has_rgb = a.rgb != nullptr;
     RF_ASSERT(nvis <= a.V.max_blocks);
     for (; i < nvis; i += G) {
         const uint32_t e = e_nx;
-        const uint32_t b = e & kIndexMask;
-        RF_ASSERT(b < min(a.V.counters[kNumBlocks], a.V.max_blocks));
+        RF_ASSERT((e & kIndexMask) < min(a.V.counters[kNumBlocks], a.V.max_blocks));
         const int4 c = c_nx;
         uint2 raw = v_nx;
+        uint2* const vp = p_nx;
         e_nx = e_nx2;
         if (i + 2 * G < nvis) e_nx2 = __ldcg(a.list + i + 2 * G);
         if (i + G < nvis) {
             c_nx = a.V.coords[e_nx & kIndexMask];
-            v_nx = *reinterpret_cast<const uint2*>(a.V.voxels + size_t(e_nx & kIndexMask) * kBrickVoxels +
-                                                   threadIdx.x);
+            p_nx = reinterpret_cast<uint2*>(a.V.voxels + size_t(e_nx & kIndexMask) * kBrickVoxels + threadIdx.x);
+            v_nx = *p_nx;
         }
         const double cx = (double(c.x * kSide + x) + 0.5) * s;  // VoxelCenter, tsdf_volume.hpp:117-119
         const double cy = (double(c.y * kSide + y) + 0.5) * s;
@@ -420,20 +427,19 @@ __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
         pose_apply(W, cx, cy, cz, pc);
         if (!(pc[2] <= 1e-9)) {
             const double rz = fuse_rcp(pc[2]);
-            const long pu = project_lround(a.K.fx * pc[0], pc[2], rz, a.K.cx);
-            const long pv = project_lround(a.K.fy * pc[1], pc[2], rz, a.K.cy);
+            const int pu = project_lround(a.K.fx * pc[0], pc[2], rz, a.K.cx);
+            const int pv = project_lround(a.K.fy * pc[1], pc[2], rz, a.K.cy);
             if (pu >= 0 && pu < a.K.w && pv >= 0 && pv < a.K.h) {
-                const int pix = int(pv) * a.K.w + int(pu);
+                const int pix = pv * a.K.w + pu;
                 const float d = __ldg(a.depth + pix);  // depth, mask and colour in one round trip
-                const bool pix_masked = a.mask && __ldg(a.mask + pix);
+                const bool pix_masked = has_mask && __ldg(a.mask + pix);
                 uint32_t cr = 0, cg = 0, cb = 0;
-                if (a.rgb) {
+                if (has_rgb) {
                     const uint8_t* col = a.rgb + 3 * size_t(pix);
                     cr = __ldg(col);
                     cg = __ldg(col + 1);
                     cb = __ldg(col + 2);
                 }
-                Voxel* vp = a.V.voxels + size_t(b) * kBrickVoxels + threadIdx.x;
                 float sdf = __uint_as_float(raw.x);
                 uint32_t wgt = raw.y & 0xFFu, r = (raw.y >> 8) & 0xFFu, g = (raw.y >> 16) & 0xFFu,
                          bl = raw.y >> 24;
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
                         const double clamped = fmin(dist, tau);
                         const double w = double(wgt);
                         sdf = div_f32(double(sdf) * w + clamped, w + 1.0, s_rcp[wgt + 1u]);
-                        if (fabs(dist) <= tau && a.rgb) {
+                        if (fabs(dist) <= tau && has_rgb) {
                             r = colour_avg(r, wgt, cr, s_cdiv);
                             g = colour_avg(g, wgt, cg, s_cdiv);
                             bl = colour_avg(bl, wgt, cb, s_cdiv);
@@ -463,7 +469,7 @@ __global__ void __launch_bounds__(kBrickVoxels) k_fuse(FuseArgs a) {
                 if (dirty) {
                     raw.x = __float_as_uint(sdf);
                     raw.y = (wgt & 0xFFu) | ((r & 0xFFu) << 8) | ((g & 0xFFu) << 16) | ((bl & 0xFFu) << 24);
-                    *reinterpret_cast<uint2*>(vp) = raw;
+                    *vp = raw;
                 }
             }
         }
@@ -691,14 +697,14 @@ __global__ void __launch_bounds__(kBrickVoxels, 2) k_fuse_window(WindowArgs a) {
     commit_links(a.V);
     __shared__ Pose Ws[kMaxWin];
     __shared__ double s_rcp[512];  // RN(1 / i) for the running averages (see div_f32)
-    __shared__ unsigned long long s_cdiv[257];  // colour_avg multipliers by d = w + 1
+    __shared__ uint32_t s_cdiv[257];  // colour_avg multipliers by d = w + 1
     if (threadIdx.x < a.n) {
         Pose P;
         for (int i = 0; i < 12; ++i) (i < 9 ? P.R[i] : P.t[i - 9]) = a.pose[threadIdx.x][i];
         Ws[threadIdx.x] = pose_inverse(P);
     }
     for (int i = threadIdx.x; i < 512; i += blockDim.x) s_rcp[i] = i ? 1.0 / double(i) : 0.0;
-    for (int i = threadIdx.x; i < 257; i += blockDim.x) s_cdiv[i] = i ? colour_magic(uint32_t(i)) : 0ull;
+    for (int i = threadIdx.x; i < 257; i += blockDim.x) s_cdiv[i] = i ? colour_magic(uint32_t(i)) : 0u;
     __syncthreads();
     const uint32_t nvis = a.V.counters[kVisible];
     const int x = threadIdx.x & 7, y = (threadIdx.x >> 3) & 7, z = threadIdx.x >> 6;
