@@ -1,4 +1,4 @@
-P=r02d
+P=${1:-r02e}
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${P}_smoke.txt 2>&1
 timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/${P}_gputests.txt 2>&1
 python bench.py > gpurun_out/${P}_bench_c2_default.json 2> gpurun_out/${P}_bench_c2_default.err
