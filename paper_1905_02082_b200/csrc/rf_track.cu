@@ -75,6 +75,13 @@ struct RegState {
     int rej_ok;
 };
 
+#ifdef RF_LM_CLOCKS  // diagnostics build: LM-thread cycle counters in trace record 251 (CTA 0)
+#define LMC_T(v) const long long v = clock64()
+#define LMC_ADD(k, val) do { if (a.trace && blockIdx.x == 0) a.trace[8 * 251 + (k)] += (unsigned long long)(val); } while (0)
+#else
+#define LMC_T(v)
+#define LMC_ADD(k, val) do {} while (0)
+#endif
 // ------------------------------------------------------------------ math
 // 1/x without the IEEE division's special-case branch: the fp64 reciprocal
 // approximation plus two Newton steps (relative error ~1e-16; pivots of the
@@ -500,6 +507,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                            const double lam = fmin(st.lambda * R.lambda_up, 1e12);
                            if (!(lam >= 1e12)) {
                                double delta[6];
+                               LMC_T(p0);
                                if (lm_solve(st.cur(), lam, delta)) {
                                    Pose e;
                                    expmap(delta, e);
@@ -510,6 +518,9 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                                    for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
                                    st.dn[fr] = dn;
                                    st.rej_ok = 1;
+                                   LMC_T(p1);
+                                   LMC_ADD(5, 1);
+                                   LMC_ADD(6, p1 - p0);
                                }
                            }
                        });
@@ -533,6 +544,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
             // solves for the next candidate in one straight-line section on
             // local copies of its state (registration.cpp:233-272).
             if (threadIdx.x == kLmThread) {
+                LMC_T(c0);
                 double lambda = st.lambda;
                 int brk = st.brk, level_it = st.level_it, total = st.total, converged = st.converged, ci = st.ci;
                 const int ip0 = st.ip, ic0 = st.ic;
@@ -574,9 +586,11 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                 while (!go && !brk && level_it < R.max_iterations) {
                     ++level_it;
                     ++total;
+                    LMC_T(c1);
                     const Pose P0 = st.P[ip];
                     double delta[6];  // in registers: ExpMap and the norm read it straight from the solve
                     const bool solved = lm_solve(st.buf[ci], lambda, delta);
+                    LMC_T(c2);
                     if (!solved) {
                         lambda = fmin(lambda * R.lambda_up, 1e12);  // NumericalIssue: damp more, retry
                         continue;
@@ -588,6 +602,11 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
 #pragma unroll
                     for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
                     st.dn[ic] = dn;  // squared; the sqrt is taken off the critical path below
+                    LMC_T(c3);
+                    LMC_ADD(0, 1);
+                    LMC_ADD(1, c1 - c0);
+                    LMC_ADD(2, c2 - c1);
+                    LMC_ADD(3, c3 - c2);
                     go = 1;
                     break;
                 }
@@ -603,6 +622,9 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                 st.rej_ok = 0;
                 if (a.trace && blockIdx.x == 0 && s_trace_pass < kTracePasses)
                     a.trace[8 * s_trace_pass + 7] = global_ns();  // solve done (next pass's record)
+                LMC_T(c4);
+                LMC_ADD(4, c4 - c0);
+                LMC_ADD(7, 1);
             }
             __syncthreads();
             if (!st.go) break;

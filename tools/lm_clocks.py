@@ -1,0 +1,13 @@
+"""Reads trace record 251 of an RF_TRACE_FILE written by the RF_LM_CLOCKS
+diagnostics build: LM-thread cycle counters of CTA 0 per frame (accept-path
+judge, solve, ExpMap + compose, whole LM section; reject-path pre-solve)."""
+import sys
+
+import numpy as np
+
+raw = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 256, 8)[3:]
+r = raw[:, 251, :].astype(np.float64).sum(0)
+print("accept-path solves %.0f: judge %.0f, lm_solve %.0f, expmap+compose %.0f cycles each" %
+      (r[0], r[1] / max(r[0], 1), r[2] / max(r[0], 1), r[3] / max(r[0], 1)))
+print("LM sections %.0f: %.0f cycles each (all paths)" % (r[7], r[4] / max(r[7], 1)))
+print("pre-solves %.0f: %.0f cycles each (lm_solve + expmap + compose)" % (r[5], r[6] / max(r[5], 1)))
