@@ -95,14 +95,17 @@ __device__ __forceinline__ double rcp_nobranch(double x) {
     return r;
 }
 
-__device__ void expmap(const double xi[6], Pose& out) {  // geometry.cpp:14-38
+// out = ExpMap(xi) * P0 (geometry.cpp:14-38, geometry.hpp:89-91). One thread
+// runs this between the all-reduce and the next pass, and its fp64
+// instructions issue at the warp's fp64 rate, so the closed forms count
+// instructions: hat^2 = w w^T - |w|^2 I (its diagonal as minus the other two
+// squares), R = I + a hat + b hat^2 and V = I + b hat + c hat^2 entry by entry,
+// and the products as FMA chains (about half the instructions of the matrix
+// forms; the same values to within an ulp).
+__device__ __forceinline__ void expmap_compose(const double xi[6], const Pose& P0, Pose& out) {
     const double w0 = xi[3], w1 = xi[4], w2 = xi[5];
-    const double t2 = (w0 * w0 + w1 * w1) + w2 * w2;
-    const double hat[9] = {0.0, -w2, w1, w2, 0.0, -w0, -w1, w0, 0.0};
-    double hat2[9];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j)
-            hat2[3 * i + j] = (hat[3 * i] * hat[j] + hat[3 * i + 1] * hat[3 + j]) + hat[3 * i + 2] * hat[6 + j];
+    const double s0 = w0 * w0, s1 = w1 * w1, s2 = w2 * w2;
+    const double t2 = (s0 + s1) + s2;
     double a, b, c;
     if (t2 < 0.0025) {
         // theta < 0.05 (an LM step is a few milliradians): sin(t)/t,
@@ -124,13 +127,25 @@ __device__ void expmap(const double xi[6], Pose& out) {  // geometry.cpp:14-38
         b = (1.0 - ct) / t2;
         c = (theta - st) / (t2 * theta);
     }
-    double vm[9];
-    for (int i = 0; i < 9; ++i) {
-        const double id = (i % 4 == 0) ? 1.0 : 0.0;
-        out.R[i] = (id + a * hat[i]) + b * hat2[i];
-        vm[i] = (id + b * hat[i]) + c * hat2[i];
+    const double h01 = w0 * w1, h02 = w0 * w2, h12 = w1 * w2;  // off-diagonal of hat^2 (symmetric)
+    const double d0 = -(s1 + s2), d1 = -(s0 + s2), d2 = -(s0 + s1);
+    const double aw0 = a * w0, aw1 = a * w1, aw2 = a * w2, bw0 = b * w0, bw1 = b * w1, bw2 = b * w2;
+    // hat = [0 -w2 w1; w2 0 -w0; -w1 w0 0]
+    const double R[9] = {__fma_rn(b, d0, 1.0), __fma_rn(b, h01, -aw2), __fma_rn(b, h02, aw1),
+                         __fma_rn(b, h01, aw2),  __fma_rn(b, d1, 1.0),  __fma_rn(b, h12, -aw0),
+                         __fma_rn(b, h02, -aw1), __fma_rn(b, h12, aw0), __fma_rn(b, d2, 1.0)};
+    const double V[9] = {__fma_rn(c, d0, 1.0), __fma_rn(c, h01, -bw2), __fma_rn(c, h02, bw1),
+                         __fma_rn(c, h01, bw2),  __fma_rn(c, d1, 1.0),  __fma_rn(c, h12, -bw0),
+                         __fma_rn(c, h02, -bw1), __fma_rn(c, h12, bw0), __fma_rn(c, d2, 1.0)};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double et = __fma_rn(V[3 * i], xi[0], __fma_rn(V[3 * i + 1], xi[1], V[3 * i + 2] * xi[2]));
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            out.R[3 * i + j] =
+                __fma_rn(R[3 * i], P0.R[j], __fma_rn(R[3 * i + 1], P0.R[3 + j], R[3 * i + 2] * P0.R[6 + j]));
+        out.t[i] = __fma_rn(R[3 * i], P0.t[0], __fma_rn(R[3 * i + 1], P0.t[1], __fma_rn(R[3 * i + 2], P0.t[2], et)));
     }
-    for (int i = 0; i < 3; ++i) out.t[i] = (vm[3 * i] * xi[0] + vm[3 * i + 1] * xi[1]) + vm[3 * i + 2] * xi[2];
 }
 
 // One damped LM solve (registration.cpp:236-248): damped = H + lambda *
@@ -509,10 +524,8 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                                double delta[6];
                                LMC_T(p0);
                                if (lm_solve(st.cur(), lam, delta)) {
-                                   Pose e;
-                                   expmap(delta, e);
                                    const int fr = 3 - st.ip - st.ic;  // the free slot
-                                   st.P[fr] = pose_mul(e, st.pose());
+                                   expmap_compose(delta, st.pose(), st.P[fr]);
                                    double dn = 0.0;
 #pragma unroll
                                    for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
@@ -595,9 +608,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                         lambda = fmin(lambda * R.lambda_up, 1e12);  // NumericalIssue: damp more, retry
                         continue;
                     }
-                    Pose e;
-                    expmap(delta, e);
-                    st.P[ic] = pose_mul(e, P0);
+                    expmap_compose(delta, P0, st.P[ic]);
                     double dn = 0.0;
 #pragma unroll
                     for (int i = 0; i < 6; ++i) dn += delta[i] * delta[i];
@@ -1325,9 +1336,8 @@ __global__ void k_lm_bench(int iters, double* out) {
         if (threadIdx.x != 0) continue;
         double d[6];
         for (int i = 0; i < 6; ++i) d[i] = delta[i];
-        Pose e;
-        expmap(d, e);
-        pose = pose_mul(e, pose);
+        const Pose p0 = pose;
+        expmap_compose(d, p0, pose);
         const long long t2 = clock64();
         t_solve += t1 - t0;
         t_rest += t2 - t1;
