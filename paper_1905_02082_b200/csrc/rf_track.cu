@@ -75,12 +75,24 @@ struct RegState {
     int rej_ok;
 };
 
-#ifdef RF_LM_CLOCKS  // diagnostics build: LM-thread cycle counters in trace record 251 (CTA 0)
+#ifdef RF_LM_CLOCKS  // diagnostics build: cycle counters of CTA 0's LM thread, kept in shared
+// memory (no global traffic on the path) and written to trace records 250/251 at exit
+__shared__ unsigned long long s_lmacc[16];
+__shared__ long long s_lmc[2];
 #define LMC_T(v) const long long v = clock64()
-#define LMC_ADD(k, val) do { if (a.trace && blockIdx.x == 0) a.trace[8 * 251 + (k)] += (unsigned long long)(val); } while (0)
+#define RF_PASS_TRACE(a) false  // the per-pass timeline is off: only these counters are written
+#define LMC_ADD(k, val) do { if (blockIdx.x == 0) s_lmacc[(k)] += (unsigned long long)(val); } while (0)
+// pass-side stamps (record 250): barrier release, pass prologue, own pixels,
+// all-reduce, all-reduce end to the next LM section
+#define LMC_MARK(k) do { if (blockIdx.x == 0 && threadIdx.x == kLmThread) { const long long t_ = clock64(); \
+    if (s_lmc[1]) s_lmacc[8 + (k)] += (unsigned long long)(t_ - s_lmc[0]); s_lmc[0] = t_; } } while (0)
+#define LMC_ARM(on) do { if (threadIdx.x == kLmThread) s_lmc[1] = (on); } while (0)
 #else
+#define RF_PASS_TRACE(a) ((a).trace != nullptr)
 #define LMC_T(v)
 #define LMC_ADD(k, val) do {} while (0)
+#define LMC_MARK(k) do {} while (0)
+#define LMC_ARM(on) do {} while (0)
 #endif
 // ------------------------------------------------------------------ math
 // 1/x without the IEEE division's special-case branch: the fp64 reciprocal
@@ -269,6 +281,7 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
 template <bool kJac, bool kColor, bool kRobust, class Hook, class Pre>
 __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
                            double* scratch, double* blk, double* out, const Hook& hook, const Pre& pre) {
+    if (kJac) LMC_MARK(6);  // pass entry -> accumulate entry
     const FrameView& F = a.F;
     const LevelInfo& LI = s_lvl[level];
     const Intr K = LI.K;
@@ -278,13 +291,14 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
     for (int i = 0; i < kAccN; ++i) acc[i] = 0.0;
     const float* depth = LI.depth;
     const uint8_t* mask = use_mask ? LI.mask : nullptr;
-    unsigned long long* tr = (a.trace && s_trace_pass < kTracePasses) ? a.trace + 8 * s_trace_pass : nullptr;
+    unsigned long long* tr = (RF_PASS_TRACE(a) && s_trace_pass < kTracePasses) ? a.trace + 8 * s_trace_pass : nullptr;
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
         tr[0] = global_ns();
         tr[4] = level;
         tr[5] = (unsigned long long)K.w * K.h;
         tr[6] = kJac;
     }
+    if (kJac) LMC_MARK(1);  // pass prologue
     const int pxc_tag = (level + 1) | (use_mask ? 16 : 0);
     const bool pxc_hit = kJac && s_pxc_tag == pxc_tag;
     auto pixel = [&](const int u, const int v, const int it) {
@@ -449,7 +463,9 @@ __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool us
     // read across CTAs by the mask that follows (publish). Warps without
     // pixels (most of them at the coarsest level) skip their transpose.
     const bool warp_has_pixels = (int(threadIdx.x) & ~31) < s_lvl[level].per;
+    if (kJac) LMC_MARK(2);  // the LM thread's own pixels (and pre-solve)
     block_grid_allreduce<kAccN, !kJac>(a.grid, acc, scratch, out, hook, warp_has_pixels);
+    if (kJac) LMC_MARK(3);  // all-reduce
     if (kJac && threadIdx.x == 0) s_pxc_tag = pxc_tag;  // (every thread read it before the barriers above)
     if (tr && blockIdx.x == 0 && threadIdx.x == 0) tr[3] = global_ns();
     if (a.trace && threadIdx.x == 0) ++s_trace_pass;
@@ -461,6 +477,7 @@ template <bool kJac, class Hook = NoHook, class Pre = NoHook>
 __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res,
                                      double cw, double* scratch, double* blk, double* out, const Hook& hook = Hook(),
                                      const Pre& pre = Pre()) {
+    if (kJac) LMC_MARK(5);  // barrier release -> pass entry
     const bool color = cw > 0.0 && a.F.rgb0 != nullptr;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         s_passes += 1;  // CTA 0's tally, published once at kernel exit (no global RMW on the pass path)
@@ -557,6 +574,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
             // solves for the next candidate in one straight-line section on
             // local copies of its state (registration.cpp:233-272).
             if (threadIdx.x == kLmThread) {
+                LMC_MARK(4);  // all-reduce end to the LM section
                 LMC_T(c0);
                 double lambda = st.lambda;
                 int brk = st.brk, level_it = st.level_it, total = st.total, converged = st.converged, ci = st.ci;
@@ -594,7 +612,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                     ic = 3 - ip0 - ic0;
                     go = 1;
                 }
-                if (judge && a.trace && blockIdx.x == 0 && s_trace_pass > 0 && s_trace_pass <= kTracePasses)
+                if (judge && RF_PASS_TRACE(a) && blockIdx.x == 0 && s_trace_pass > 0 && s_trace_pass <= kTracePasses)
                     a.trace[8 * (s_trace_pass - 1) + 6] |= rejected ? 0x200ull : 0x100ull;  // the trial's verdict
                 while (!go && !brk && level_it < R.max_iterations) {
                     ++level_it;
@@ -631,13 +649,17 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                 st.ci = ci;
                 st.go = go;
                 st.rej_ok = 0;
-                if (a.trace && blockIdx.x == 0 && s_trace_pass < kTracePasses)
+                if (RF_PASS_TRACE(a) && blockIdx.x == 0 && s_trace_pass < kTracePasses)
                     a.trace[8 * s_trace_pass + 7] = global_ns();  // solve done (next pass's record)
                 LMC_T(c4);
+                LMC_ARM(0);
+                LMC_MARK(0);
+                LMC_ARM(1);
                 LMC_ADD(4, c4 - c0);
                 LMC_ADD(7, 1);
             }
             __syncthreads();
+            LMC_MARK(0);  // barrier release after the LM section
             if (!st.go) break;
         }
         __syncthreads();
@@ -1248,7 +1270,17 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
         s_luma_lut[i] = w * double(i & 255);
     }
     grid_init(a.grid);
+#ifdef RF_LM_CLOCKS
+    if (threadIdx.x < 16) s_lmacc[threadIdx.x] = 0ull;
+    LMC_ARM(0);
+    __syncthreads();
+#endif
     track_main(a, st, scratch, blk, red, lead);
+#ifdef RF_LM_CLOCKS
+    __syncthreads();
+    if (a.trace && blockIdx.x == 0 && threadIdx.x < 16)
+        a.trace[8 * (threadIdx.x < 8 ? 251 : 250) + (threadIdx.x & 7)] = s_lmacc[threadIdx.x];
+#endif
     if (lead && a.out) {
         a.out->passes = s_passes;
         a.out->pixel_passes = s_pixel_passes;
