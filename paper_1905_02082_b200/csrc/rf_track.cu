@@ -658,6 +658,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
                 LMC_ADD(4, c4 - c0);
                 LMC_ADD(7, 1);
             }
+            LMC_MARK(7);  // LM section end -> reconverged
             __syncthreads();
             LMC_MARK(0);  // barrier release after the LM section
             if (!st.go) break;
