@@ -281,7 +281,6 @@ __device__ void build_pyramid(const TrackArgs& a, bool images, bool masks) {
 template <bool kJac, bool kColor, bool kRobust, class Hook, class Pre>
 __device__ void accumulate(const TrackArgs& a, int level, const Pose& P, bool use_mask, bool write_res, double cw,
                            double* scratch, double* blk, double* out, const Hook& hook, const Pre& pre) {
-    if (kJac) LMC_MARK(6);  // pass entry -> accumulate entry
     const FrameView& F = a.F;
     const LevelInfo& LI = s_lvl[level];
     const Intr K = LI.K;
@@ -662,6 +661,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
             __syncthreads();
             LMC_MARK(0);  // barrier release after the LM section
             if (!st.go) break;
+            LMC_MARK(6);  // go read (before the back-edge)
         }
         __syncthreads();
     }
