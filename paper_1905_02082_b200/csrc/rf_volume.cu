@@ -744,10 +744,10 @@ __global__ void __launch_bounds__(kBrickVoxels, 2) k_fuse_window(WindowArgs a) {
                 pose_apply(Ws[j], cx, cy, cz, pc);
                 if (pc[2] <= 1e-9) continue;
                 const double rz = fuse_rcp(pc[2]);
-                const long pu = project_lround(K.fx * pc[0], pc[2], rz, K.cx);
-                const long pv = project_lround(K.fy * pc[1], pc[2], rz, K.cy);
+                const int pu = project_lround(K.fx * pc[0], pc[2], rz, K.cx);
+                const int pv = project_lround(K.fy * pc[1], pc[2], rz, K.cy);
                 if (!(pu >= 0 && pu < K.w && pv >= 0 && pv < K.h)) continue;
-                const int pix = int(pv) * K.w + int(pu);
+                const int pix = pv * K.w + pu;
                 if (a.mask[j] && __ldg(a.mask[j] + pix)) continue;
                 jj[k] = j;
                 zz[k] = pc[2];
