@@ -35,6 +35,19 @@ def test_host_layer_compiles(tmp_path):
                     os.path.join(ROOT, "include"), str(probe)], check=True)
 
 
+def test_host_containers(tmp_path):
+    """CoordHashMap / HashCoord, FrameWindow and RefineDepth: host-side code of the
+    layer, checked against an ordered map and the reference's rules (no GPU)."""
+    if not os.path.exists(os.path.join(LIBDIR, "librefusion_b200.so")):
+        pytest.skip("CUDA library not built")
+    exe = str(tmp_path / "containers")
+    subprocess.run([CXX, "-std=c++20", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "host_containers.cpp"), "-L", LIBDIR, "-lrefusion_b200",
+                    f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "host containers ok" in r.stdout, r.stderr
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("refine,debug", [(False, True), (True, True), (False, False)])
 def test_host_layer_pipeline_matches(tmp_path, refine, debug):
