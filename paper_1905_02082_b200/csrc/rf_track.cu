@@ -77,8 +77,12 @@ struct RegState {
 
 #ifdef RF_LM_CLOCKS  // diagnostics build: cycle counters of CTA 0's LM thread, kept in shared
 // memory (no global traffic on the path) and written to trace records 250/251 at exit
-__shared__ unsigned long long s_lmacc[16];
+__shared__ unsigned long long s_lmacc[18];
 __shared__ long long s_lmc[2];
+__shared__ long long s_t0c;  // thread 0's own stamp (record 249: its barrier release -> pass entry)
+#define T0_MARK_A() do { if (blockIdx.x == 0 && threadIdx.x == 0) s_t0c = clock64(); } while (0)
+#define T0_MARK_B() do { if (blockIdx.x == 0 && threadIdx.x == 0 && s_t0c) { \
+    s_lmacc[16] += (unsigned long long)(clock64() - s_t0c); s_lmacc[17] += 1; s_t0c = 0; } } while (0)
 #define LMC_T(v) const long long v = clock64()
 #define RF_PASS_TRACE(a) false  // the per-pass timeline is off: only these counters are written
 #define LMC_ADD(k, val) do { if (blockIdx.x == 0) s_lmacc[(k)] += (unsigned long long)(val); } while (0)
@@ -91,6 +95,8 @@ __shared__ long long s_lmc[2];
 #define RF_PASS_TRACE(a) ((a).trace != nullptr)
 #define LMC_T(v)
 #define LMC_ADD(k, val) do {} while (0)
+#define T0_MARK_A() do {} while (0)
+#define T0_MARK_B() do {} while (0)
 #define LMC_MARK(k) do {} while (0)
 #define LMC_ARM(on) do {} while (0)
 #endif
@@ -477,6 +483,7 @@ __device__ __forceinline__ void pass(const TrackArgs& a, int level, const Pose& 
                                      double cw, double* scratch, double* blk, double* out, const Hook& hook = Hook(),
                                      const Pre& pre = Pre()) {
     if (kJac) LMC_MARK(5);  // barrier release -> pass entry
+    if (kJac) T0_MARK_B();
     const bool color = cw > 0.0 && a.F.rgb0 != nullptr;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         s_passes += 1;  // CTA 0's tally, published once at kernel exit (no global RMW on the pass path)
@@ -660,6 +667,7 @@ __device__ __forceinline__ void run_register(const TrackArgs& a, const Pose& ini
             LMC_MARK(7);  // LM section end -> reconverged
             __syncthreads();
             LMC_MARK(0);  // barrier release after the LM section
+            T0_MARK_A();
             if (!st.go) break;
             LMC_MARK(6);  // go read (before the back-edge)
         }
@@ -1272,15 +1280,16 @@ __global__ void __launch_bounds__(kTrackThreads, kTrackMinBlocks) k_track(TrackA
     }
     grid_init(a.grid);
 #ifdef RF_LM_CLOCKS
-    if (threadIdx.x < 16) s_lmacc[threadIdx.x] = 0ull;
+    if (threadIdx.x < 18) s_lmacc[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) s_t0c = 0;
     LMC_ARM(0);
     __syncthreads();
 #endif
     track_main(a, st, scratch, blk, red, lead);
 #ifdef RF_LM_CLOCKS
     __syncthreads();
-    if (a.trace && blockIdx.x == 0 && threadIdx.x < 16)
-        a.trace[8 * (threadIdx.x < 8 ? 251 : 250) + (threadIdx.x & 7)] = s_lmacc[threadIdx.x];
+    if (a.trace && blockIdx.x == 0 && threadIdx.x < 18)
+        a.trace[8 * (threadIdx.x < 8 ? 251 : (threadIdx.x < 16 ? 250 : 249)) + (threadIdx.x & 7)] = s_lmacc[threadIdx.x];
 #endif
     if (lead && a.out) {
         a.out->passes = s_passes;

@@ -16,3 +16,5 @@ n = max(r[7], 1)
 print("per LM iteration on CTA 0's LM thread (cycles): LM-section end -> reconverged %.0f, -> barrier release %.0f, "
       "-> go read %.0f, -> (back-edge) pass entry %.0f, -> prologue done %.0f, own pixels %.0f, all-reduce %.0f, "
       "all-reduce end -> LM section %.0f" % (q[7] / n, q[0] / n, q[6] / n, q[5] / n, q[1] / n, q[2] / n, q[3] / n, q[4] / n))
+t = raw[:, 249, :2].astype(np.float64).sum(0)
+print("thread 0 (warp 0), same span: barrier release -> pass entry %.0f cycles (%d samples)" % (t[0] / max(t[1], 1), t[1]))

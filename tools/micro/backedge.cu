@@ -13,7 +13,10 @@
 #define F64 F8 F8 F8 F8 F8 F8 F8 F8
 #define F512 F64 F64 F64 F64 F64 F64 F64 F64
 
-__global__ void __launch_bounds__(384, 1) k(int iters, float* out, unsigned long long* cyc) {
+#ifndef STREAM_KB
+#define STREAM_KB 0  // per CTA per iteration: global bytes streamed (L2 pressure)
+#endif
+__global__ void __launch_bounds__(384, 1) k(int iters, float* out, unsigned long long* cyc, const float4* buf) {
     float x = threadIdx.x * 1e-3f, y = 0.999f, z = 1e-4f;
     __shared__ float s;
     unsigned long long tot = 0, t_end = 0;
@@ -27,6 +30,18 @@ __global__ void __launch_bounds__(384, 1) k(int iters, float* out, unsigned long
 #if (BODY % 512) >= 64
 #pragma unroll
         for (int r = 0; r < (BODY % 512) / 64; ++r) { F64 }
+#endif
+#if STREAM_KB > 0
+        {
+            const size_t chunk = STREAM_KB * 1024 / 16, nchunks = (size_t(256) << 20) / 16 / chunk;
+            const float4* b = buf + ((size_t(blockIdx.x) * iters + it) % nchunks) * chunk;
+            float4 acc4 = make_float4(0, 0, 0, 0);
+            for (int i = threadIdx.x; i < STREAM_KB * 1024 / 16; i += 384) {
+                const float4 v4 = __ldcg(b + i);
+                acc4.x += v4.x;
+            }
+            x += acc4.x * 1e-30f;
+        }
 #endif
         __syncthreads();
         if (threadIdx.x == 383) {
@@ -49,12 +64,16 @@ int main() {
     unsigned long long* cyc;
     cudaMalloc(&out, sms * 384 * 4);
     cudaMallocManaged(&cyc, sms * 8);
-    k<<<sms, 384>>>(4, out, cyc);
-    k<<<sms, 384>>>(200, out, cyc);
+    float4* buf = nullptr;
+    const size_t bytes = (size_t(256) << 20) + 16;  // streamed cyclically (2x the L2)
+    cudaMalloc(&buf, bytes);
+    cudaMemset(buf, 0, bytes);
+    k<<<sms, 384>>>(4, out, cyc, buf);
+    k<<<sms, 384>>>(200, out, cyc, buf);
     cudaDeviceSynchronize();
     double m = 0;
     for (int i = 0; i < sms; ++i) m += cyc[i];
-    printf("BODY %d instr (%.1f KB): back-edge + loop top %.0f cycles (mean over %d CTAs)\n", BODY, BODY * 16 / 1024.0,
-           m / sms, sms);
+    printf("BODY %d instr (%.1f KB), %d KB streamed per CTA per iteration: back-edge + loop top %.0f cycles (mean over %d CTAs)\n",
+           BODY, BODY * 16 / 1024.0, STREAM_KB, m / sms, sms);
     return 0;
 }
