@@ -5,13 +5,16 @@ import numpy as np
 
 
 def test_colour_average_magic_multiply_is_exact():
-    """colour_avg: lround((c w + in) / (w + 1)) = (2n + d) / (2d) with n = c w + in and
-    d = w + 1, computed as ((2n + d) * ceil(2^40 / 2d)) >> 40. Every numerator
-    < 2^17 and every d in 1..256 is checked."""
+    """colour_avg (rf_volume.cu): lround((c w + in) / (w + 1)) = (2n + d) / (2d) with
+    n = c w + in and d = w + 1, computed as the high word of the 32-bit product
+    (2n + d) * ceil(2^32 / 2d) (one IMAD.HI). Every numerator < 2^17 and every d in
+    1..256 is checked (tools/micro/colour_magic.c runs the same check over the
+    (c, w, in) triples the update can see)."""
     num = np.arange(0, 1 << 17, dtype=np.uint64)
     for d in range(1, 257):
-        m = np.uint64(((1 << 40) + 2 * d - 1) // (2 * d))
-        np.testing.assert_array_equal((num * m) >> np.uint64(40), num // np.uint64(2 * d))
+        m = ((1 << 32) + 2 * d - 1) // (2 * d)
+        assert m < (1 << 32)
+        np.testing.assert_array_equal((num * np.uint64(m)) >> np.uint64(32), num // np.uint64(2 * d))
 
 
 def test_colour_average_matches_rounded_quotient():
