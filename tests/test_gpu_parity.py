@@ -112,6 +112,45 @@ def test_lockstep_carve_allocate_integrate_bitexact(voxel):
         assert_volumes_identical(ov, gv)
 
 
+@pytest.mark.parametrize("shift", [0.01, 0.03, -0.05])
+def test_projection_ties_take_the_exact_path(shift):
+    """Voxels whose projection lands on a pixel boundary (x = fx X / Z + cx at a
+    half-integer, where lround's tie rule decides): with f s = 1, cx = 31.5 and the
+    camera shifted by half a voxel, every voxel of the z = 0.25 m layer projects
+    to within an ulp of a half-integer. k_fuse's reciprocal fast path must hand
+    those to the exact division (rf_volume.cu project_lround), so the voxels stay
+    bit-identical to the oracle's."""
+    k = O.small_intrinsics(64, 48, 50.0)  # cx = 31.5, cy = 23.5
+    cfg = O.vol_cfg(voxel_size=0.02)
+    pose = O.IDENTITY.copy()
+    pose[9:] = (shift, shift, 0.0)
+    d = np.full((k.height, k.width), 0.3, np.float32)
+    rgb = np.full((k.height, k.width, 3), 90, np.uint8)
+    rgb[:, ::2] = 200
+    ov, gv = pair(cfg)
+    for _ in range(3):
+        ov.carve(d, k, pose)
+        gv.carve(frame(k, d), pose)
+        ov.allocate_for_frame(d, k, pose)
+        gv.allocate_for_frame(frame(k, d), pose)
+        ov.integrate(d, rgb, k, pose)
+        gv.integrate(frame(k, d, rgb), pose)
+    assert_volumes_identical(ov, gv)
+    # the layer really sits on ties (the fast path's 1e-9 margin catches them)
+    coords, _ = ov.export()
+    s = cfg.voxel_size
+    ties = 0
+    for c in coords:
+        v = (np.stack(np.meshgrid(np.arange(8), np.arange(8), np.arange(8), indexing="ij"), -1).reshape(-1, 3)
+             + 8 * c[:3])
+        ctr = (v + 0.5) * s
+        z = ctr[:, 2]
+        on = (np.abs(z - 0.25) < 1e-12)
+        x = k.fx * (ctr[on, 0] - shift) / z[on] + k.cx
+        ties += int(np.sum(np.abs(x - np.floor(x) - 0.5) <= 1e-9))
+    assert ties > 0
+
+
 def test_allocation_640x480_keys_and_occupancy():
     """Full-size frame of the bench scene: bit-exact key set and hash occupancy."""
     s = O.Scene(scenes.bench_script(frames=3))
