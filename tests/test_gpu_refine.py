@@ -80,6 +80,30 @@ def test_render_virtual_depth_bitexact():
         assert holes.sum() > 100 and (grf[holes] == 8.0).sum() < holes.sum()  # holes were filled
 
 
+def test_window_fusion_projection_ties_bitexact():
+    """The window re-fusion (k_fuse_window) on poses whose voxel layer at z = 0.25 m
+    projects onto half-integer pixels (f s = 1, cx = 31.5, half-voxel camera
+    shifts; see test_gpu_parity.py::test_projection_ties_take_the_exact_path): the
+    virtual and refined depth stay bit-identical to the oracle's."""
+    k = O.small_intrinsics(64, 48, 50.0)
+    vc = O.vol_cfg(voxel_size=0.02)
+    d = np.full((k.height, k.width), 0.3, np.float32)
+    d[10:20, 20:30] = 0.0  # a hole for RefineDepth to fill
+    rgb = np.full((k.height, k.width, 3), 90, np.uint8)
+    poses = []
+    for shift in (0.01, 0.03, -0.05):
+        p = O.IDENTITY.copy()
+        p[9:] = (shift, shift, 0.0)
+        poses.append(p)
+    entries = [dict(depth=d, rgb=rgb, mask=None, pose=p) for p in poses]
+    ov, orf = O.render_virtual_depth(entries, poses[0], k, vc)
+    gv, grf = G.render_virtual_depth([frame(k, d, rgb) for _ in poses], poses, [None] * len(poses), poses[0], gk(k),
+                                     gcfg(vc))
+    assert (ov > 0).mean() > 0.5
+    assert ov.tobytes() == gv.tobytes(), "virtual depth differs"
+    assert orf.tobytes() == grf.tobytes(), "refined depth differs"
+
+
 @pytest.mark.parametrize("window", [1, 3, 10])
 def test_pipeline_refinement_matches_oracle(window):
     s, frames = room_frames(14, seed=window)
