@@ -60,3 +60,55 @@ def test_walk_division_by_reciprocal_is_correctly_rounded():
         q = a * rb
         r = _fma(-q, b, a)
         assert _fma(r, rb, q) == a / b or (a == 0.0), (a, b)
+
+
+def test_running_average_f32_fast_path_agrees_with_division():
+    """div_f32 (rf_volume.cu): f32((sdf w + u) / (w + k)) from q = RN(a * RN(1/b));
+    when every f64 within 2^-50 relative of q rounds to the same f32 (lo == hi),
+    that f32 is the f32 of the correctly rounded quotient. Checked on 2e6 random
+    updates over the ranges the carve and integrate updates see (numpy float64 is
+    IEEE binary64 without contraction, like the kernels under -fmad=false)."""
+    rng = np.random.default_rng(11)
+    n = 2_000_000
+    tau = 0.1
+    sdf = rng.uniform(-tau, tau, n).astype(np.float32).astype(np.float64)
+    w = rng.integers(0, 65, n).astype(np.float64)
+    k = np.where(rng.random(n) < 0.5, 1.0, rng.integers(1, 5, n).astype(np.float64))
+    u = np.where(rng.random(n) < 0.8, rng.uniform(-tau, tau, n), tau * k)
+    a = sdf * w + u
+    b = w + k
+    rb = 1.0 / b
+    q = a * rb
+    lo = (q * (1.0 - 2.0 ** -50)).astype(np.float32)
+    hi = (q * (1.0 + 2.0 ** -50)).astype(np.float32)
+    fast = lo == hi
+    assert fast.mean() > 0.99
+    np.testing.assert_array_equal(lo[fast], (a[fast] / b[fast]).astype(np.float32))
+
+
+def test_projection_rounding_fast_path_agrees_with_lround():
+    """project_lround (rf_volume.cu): away from half-integers (margin 1e-9) the
+    pixel from num * rz + c, rz within an ulp of 1/z (the kernel's branch-free
+    reciprocal; perturbed by +-1 ulp here), rounds like lround(num / z + c)
+    (Project, geometry.hpp:46-48). 2e6 random camera points in and around a
+    1280x720 view, plus points forced onto exact half-integers, which the
+    margin sends to the exact path."""
+    rng = np.random.default_rng(5)
+    n = 2_000_000
+    z = rng.uniform(1e-3, 6.0, n)
+    f = rng.choice([50.0, 525.0, 1050.0], n)
+    c = rng.choice([31.5, 319.5, 639.5], n)
+    x = rng.uniform(-0.5, 1.5, n) * 1280.0
+    X = (x - c) * z / f
+    X[: n // 10] = (np.round(x[: n // 10]) + 0.5 - c[: n // 10]) * z[: n // 10] / f[: n // 10]  # ties
+    num = f * X
+    rz = 1.0 / z
+    ulp = rng.integers(-1, 2, n)
+    rz = np.where(ulp > 0, np.nextafter(rz, np.inf), np.where(ulp < 0, np.nextafter(rz, 0.0), rz))
+    xa = num * rz + c
+    fr = xa - np.floor(xa)
+    fast = (np.abs(xa) < 1e6) & (np.abs(fr - 0.5) > 1e-9)
+    v = num / z + c
+    lround = np.where(v >= 0, np.floor(v + 0.5), np.ceil(v - 0.5))
+    assert fast.mean() > 0.85 and (~fast).sum() > 0
+    np.testing.assert_array_equal(np.rint(xa[fast]), lround[fast])
