@@ -210,6 +210,40 @@ def test_sampling_bitexact_all_modes():
             assert (ov_g[ov_ok] == gv_g[gv_ok]).all(), mode
 
 
+def test_small_hash_long_probe_chains():
+    """A hash table at load ~0.7 (2^12 slots): most lookups continue past their home
+    slot (gather_corners' collision path, k_alloc's probe and CAS chains, the link
+    records of displaced bricks). Fused voxels, hash occupancy and samples stay
+    bit-identical to the oracle's."""
+    k = O.small_intrinsics(64, 48, 50.0)
+    ocfg = O.vol_cfg(voxel_size=0.005, max_blocks=3200)  # ~2850 bricks
+    gc = gcfg(ocfg)
+    gc.hash_capacity = 1 << 12
+    ov, gv = O.Volume(ocfg), G.TsdfVolume(gc)
+    rng = np.random.default_rng(9)
+    for i in range(4):
+        d, rgb = wavy_frame(k, 20 + i)
+        pose = H.small_pose(rng.uniform(-0.03, 0.03, 3), rng.uniform(-1, 1, 3), rng.uniform(-0.05, 0.05))
+        ov.carve(d, k, pose)
+        gv.carve(frame(k, d), pose)
+        ov.allocate_for_frame(d, k, pose)
+        gv.allocate_for_frame(frame(k, d), pose)
+        ov.integrate(d, rgb, k, pose)
+        gv.integrate(frame(k, d, rgb), pose)
+    assert gv.hash_capacity() == 1 << 12 and gv.num_blocks() > 0.5 * (1 << 12)
+    assert_volumes_identical(ov, gv)
+    assert all(v == 0 for v in gv.check().values())
+    pts = np.stack([rng.uniform(-0.3, 0.3, 4000), rng.uniform(-0.25, 0.25, 4000), rng.uniform(0.2, 0.8, 4000)], 1)
+    for mode in range(5):
+        ov_v, ov_g, ov_ok = ov.sample(pts, mode)
+        gv_v, gv_g, gv_ok = gv.sample(pts, mode)
+        assert (ov_ok == gv_ok).all(), mode
+        assert ov_ok.sum() > 200, mode
+        assert (ov_v[ov_ok] == gv_v[gv_ok]).all(), mode
+        if mode >= 2:
+            assert (ov_g[ov_ok] == gv_g[gv_ok]).all(), mode
+
+
 def test_voxel_handle_roundtrip_and_export():
     ov, gv = wavy_volumes()
     coords = np.array([[0, 0, 10], [-3, 5, 20], [100, 100, 100]], np.int32)
