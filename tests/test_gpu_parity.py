@@ -242,6 +242,12 @@ def test_small_hash_long_probe_chains():
         assert (ov_v[ov_ok] == gv_v[gv_ok]).all(), mode
         if mode >= 2:
             assert (ov_g[ov_ok] == gv_g[gv_ok]).all(), mode
+    # the tracking kernel's gathers through the same chains
+    o = ov.linearize(d, rgb, k, pose, O.reg_cfg(color_weight=0.025))
+    g = gv.linearize(frame(k, d, rgb), pose, G.registration_config(color_weight=0.025))
+    assert o["valid"] == g["valid"] > 500
+    np.testing.assert_allclose(g["H"], o["H"], rtol=1e-9, atol=1e-9 * np.abs(o["H"]).max())
+    np.testing.assert_allclose(g["b"], o["b"], rtol=1e-9, atol=1e-9 * np.abs(o["b"]).max())
 
 
 def test_voxel_handle_roundtrip_and_export():
